@@ -1,0 +1,169 @@
+/*
+ * fempack_b200 — C ABI of the B200-native FE assembly + solver-vector path.
+ *
+ * Drop-in boundary for the reference mini-app `fempack`
+ * (/root/reference/pkg/src/fempack).  The reference is Python/Numba and binds
+ * no FFI; each entry point below replaces one reference kernel or setup
+ * routine (cited per function).  The Python host package
+ * `paper_2107_11541_b200` binds these through ctypes.
+ *
+ * Conventions (mirroring the reference kernel contract, _kernels.py:1-15):
+ *  - every pointer argument is a DEVICE pointer unless the name ends in _h;
+ *  - outputs are caller-allocated; assembly kernels ACCUMULATE into them
+ *    (callers zero them, as assembly.py:167/:206 do);
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *  - calls are stream-ordered and asynchronous unless documented otherwise;
+ *  - return FPB_OK (0) or an error code; fpb_last_error() describes it.
+ *
+ * Index types: node ids, connectivity, CSR column indices, row pointers and
+ * element->CSR positions are int32 on the device (every BASELINE config has
+ * nnz < 2^31; larger meshes are rejected with FPB_ECONFIG).
+ */
+#ifndef FEMPACK_B200_H
+#define FEMPACK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define FPB_OK 0
+#define FPB_ECONFIG 1   /* ConfigurationError (errors.py:4-5) */
+#define FPB_EINVERTED 2 /* InvertedElementError (errors.py:8-22) */
+#define FPB_EPATTERN 3  /* ScatterPatternError (errors.py:33-34) */
+#define FPB_ECUDA 4     /* CUDA runtime failure */
+
+/* element types, ElementType (elements.py:28-33) */
+typedef enum { FPB_TRI03 = 0, FPB_QUAD04 = 1, FPB_TET04 = 2, FPB_PYR05 = 3, FPB_HEX08 = 4 } fpb_etype;
+
+/* kernel kinds, KernelKind (assembly.py:32-41), plus the fused continuity
+ * kind FPB_GRADIENT_XYZ (= CONVECTION with unit e_k for k < dim in one pass,
+ * timeloop.py:159-171) */
+typedef enum {
+  FPB_MASS = 0,
+  FPB_LAPLACIAN = 1,
+  FPB_CONVECTION = 2,
+  FPB_MOMENTUM_RHS = 3,
+  FPB_SCALAR_RHS = 4,
+  FPB_GRADIENT_XYZ = 5
+} fpb_kind;
+
+const char* fpb_last_error(void);
+int fpb_version(void);
+
+/* Upload one reference element's tables (host pointers) to device constant
+ * memory: N[nn][ng], dN[dim][nn][ng], w[ng] — the constant inputs of every
+ * reference kernel (elements.py:258-274). */
+int fpb_set_reference_element(int etype, int nn, int ng, int dim, const double* N_h,
+                              const double* dN_h, const double* w_h);
+
+/* ---- setup (mesh.py, packing.py, sparse.py, assembly.py) -------------- */
+
+/* Structured-grid node coordinates, i fastest, np.linspace-exact
+ * (mesh.py:158-187).  coords[(nx+1)(ny+1)(nz+1)][3] (2-D: [(nx+1)(ny+1)][2],
+ * nz ignored). */
+int fpb_grid_coords(int dim, int nx, int ny, int nz, double lx, double ly, double lz,
+                    double* coords, void* stream);
+
+/* Single-type box connectivity, cells k-major (mesh.py:227-289):
+ * TET04 = 6 Kuhn tets/cell, HEX08 = 1/cell, QUAD04 = 1/cell, TRI03 = 2/cell.
+ * conn[nelem][nn] int32. */
+int fpb_box_conn(int etype, int nx, int ny, int nz, int32_t* conn, void* stream);
+
+/* Mixed pyramid/hex box (mesh.py:292-336): cells with i < nlayers become 6
+ * pyramids around an appended centre node.  Writes pyramid connectivity
+ * pyr_conn[6*npyrcells][5], hex_conn[nhexcells][8] and the centre
+ * coordinates into coords[ngrid + c][3] (coords[0:ngrid] must already hold
+ * the grid from fpb_grid_coords). */
+int fpb_mixed_conn(int nx, int ny, int nz, int nlayers, double* coords, int32_t* pyr_conn,
+                   int32_t* hex_conn, void* stream);
+
+/* Lane packs (packing.py:85-127): lane_conn[npacks][nn][vs] with the tail
+ * replicating the last element.  npacks = ceil(nelem/vs). */
+int fpb_build_packs(int64_t nelem, int nn, int vs, const int32_t* conn, int32_t* lane_conn,
+                    void* stream);
+
+/* Node-adjacency CSR graph (sparse.py:59-75).  Two calls: with colind==NULL
+ * it fills rowptr[n+1] and returns nnz through nnz_h (synchronous); with
+ * colind!=NULL it fills colind[nnz] (ascending within rows, diagonal always
+ * present).  groups: ngroups connectivity arrays conns[g][nelem[g]][nn[g]]
+ * given as host arrays of device pointers. */
+int fpb_build_pattern(int32_t n, int ngroups, const int32_t* const* conns_h,
+                      const int64_t* nelem_h, const int* nn_h, int32_t* rowptr, int32_t* colind,
+                      int64_t* nnz_h, void* stream);
+
+/* Element->CSR value index (assembly.py:44-52, :89-93).  layout 0 = scalar
+ * pos[e][i][j]; layout 1 = packed pos[p][i][j][vs] (padded lanes replicate
+ * the last element).  Returns FPB_EPATTERN (synchronously) if a node pair is
+ * missing from the pattern. */
+int fpb_matrix_positions(int64_t nelem, int nn, const int32_t* conn, int32_t n,
+                         const int32_t* rowptr, const int32_t* colind, int layout, int vs,
+                         int32_t* pos, void* stream);
+
+/* Geometry (_kernels.py:78-147) in the reference packed layout at pack width
+ * vs: detjw[npacks][ng][vs], gradn[npacks][dim][nn][ng][vs] (gradn may be
+ * NULL).  Padded lanes get detjw = 0.  Returns FPB_EINVERTED (synchronously)
+ * with *bad_elem_h / *bad_gauss_h set to the first non-positive determinant
+ * in the reference's (pack, gauss, lane) scan order. */
+int fpb_geometry(int etype, int64_t nelem, int vs, const int32_t* conn, const double* coords,
+                 double* detjw, double* gradn, int64_t* bad_elem_h, int* bad_gauss_h,
+                 void* stream);
+
+/* ---- assembly (assembly.py:209-270, _kernels.py:150-519) -------------- */
+
+/* One element group, packed at 32 lanes (one warp per pack).
+ *  lane_conn[npacks][nn][32]   (fpb_build_packs with vs = 32)
+ *  coords[nnode][dim], vel[nnode][dim] (CONVECTION / *_RHS), phi[nnode]
+ *  pos[npacks][nn][nn][32]     (matrix kinds; fpb_matrix_positions layout 1, vs 32)
+ *  out: matrix kinds -> vals[nnz]; FPB_GRADIENT_XYZ -> dim arrays vals[k*nnz]
+ *       MOMENTUM_RHS -> rhs[nnode][dim]; SCALAR_RHS -> rhs[nnode]
+ * Contributions are added with FP64 reductions (scatter). */
+int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
+                 const double* coords, const double* vel, const double* phi, double rho,
+                 double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
+                 void* stream);
+
+/* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
+
+/* y = A x (sparse.py:78-84).  nnz = rowptr[n] sizes the lanes per row. */
+int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+             const double* vals, const double* x, double* y, void* stream);
+/* out = alpha*x + y (sparse.py:96-99) */
+int fpb_axpy(int64_t n, double alpha, const double* x, const double* y, double* out,
+             void* stream);
+/* result[0] = sum x_i y_i, deterministic fixed-order two-level reduction.
+ * work must hold fpb_dot_work_size() doubles. */
+int64_t fpb_dot_work_size(void);
+int fpb_dot(int64_t n, const double* x, const double* y, double* result, double* work,
+            void* stream);
+/* d[i] = stored diagonal of row i or 0 (sparse.py:48-56) */
+int fpb_diagonal(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                 double* d, void* stream);
+/* row sums: lumped[i] = sum_k vals[k], k in row i (timeloop.py:174-181) */
+int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* out, void* stream);
+
+/* ---- device-resident Jacobi-PCG (krylov.py:27-89) ----------------------
+ * One call runs up to `iters` iterations of the reference recurrence with
+ * every scalar kept on the device.  state[] (device, 8 doubles) carries
+ * {rz, bnorm, tol, status, iterations, relres, pq, spare}; status 0 =
+ * running, 1 = converged, 2 = breakdown (pq <= 0).  hist[] receives relres
+ * per completed iteration at hist[iterations - hist_first]
+ * (fpb_pcg_init writes hist[0]).  Once status != 0 the
+ * remaining iterations are no-ops, so batches can be launched without a host
+ * round trip per iteration.  vectors: x, r, p, q, z and the Jacobi diagonal d
+ * (z = r / d, krylov.py:65,84), all of length n. */
+int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                 const double* b, const double* x0, double* x, double* r, double* p,
+                 double* z, const double* d, double* state, double* hist, double tol,
+                 double* work, void* stream);
+int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind,
+                    const double* vals, double* x, double* r, double* p, double* q, double* z,
+                    const double* d, double* state, double* hist, int64_t hist_first, int iters,
+                    double* work, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEMPACK_B200_H */

@@ -1,0 +1,107 @@
+"""ctypes binding of the C ABI in include/fempack_b200.h.
+
+The shared library is built in-tree (`libfempack_b200.so` next to this file,
+see `__graft_entry__.build()`).  There is no CPU fallback: if the library or a
+CUDA device is missing, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfempack_b200.so")
+
+FPB_OK, FPB_ECONFIG, FPB_EINVERTED, FPB_EPATTERN, FPB_ECUDA = 0, 1, 2, 3, 4
+
+_i32, _i64, _int, _dbl, _vp = C.c_int32, C.c_int64, C.c_int, C.c_double, C.c_void_p
+_pi64, _pint = C.POINTER(C.c_int64), C.POINTER(C.c_int)
+
+# name -> (restype, argtypes); mirrors include/fempack_b200.h
+SIGNATURES = {
+    "fpb_last_error": (C.c_char_p, []),
+    "fpb_version": (_int, []),
+    "fpb_set_reference_element": (_int, [_int, _int, _int, _int, _vp, _vp, _vp]),
+    "fpb_grid_coords": (_int, [_int, _int, _int, _int, _dbl, _dbl, _dbl, _vp, _vp]),
+    "fpb_box_conn": (_int, [_int, _int, _int, _int, _vp, _vp]),
+    "fpb_mixed_conn": (_int, [_int, _int, _int, _int, _vp, _vp, _vp, _vp]),
+    "fpb_build_packs": (_int, [_i64, _int, _int, _vp, _vp, _vp]),
+    "fpb_build_pattern": (_int, [_i32, _int, _vp, _vp, _vp, _vp, _vp, _pi64, _vp]),
+    "fpb_matrix_positions": (_int, [_i64, _int, _vp, _i32, _vp, _vp, _int, _int, _vp, _vp]),
+    "fpb_geometry": (_int, [_int, _i64, _int, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
+    "fpb_assemble": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _i64, _vp, _vp]),
+    "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),
+    "fpb_dot_work_size": (_i64, []),
+    "fpb_dot": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_diagonal": (_int, [_i32, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_row_sums": (_int, [_i32, _vp, _vp, _vp, _vp]),
+    "fpb_pcg_init": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
+    "fpb_pcg_iterate": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
+}
+
+_lib = None
+
+
+def load(require_gpu: bool = True):
+    """Load the library once; raise loudly when it or the GPU is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)"
+            )
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    if require_gpu and not torch.cuda.is_available():
+        raise RuntimeError("fempack_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return _lib
+
+
+def last_error() -> str:
+    return load(require_gpu=False).fpb_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == FPB_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == FPB_ECONFIG:
+        raise ConfigurationError(msg)
+    if rc == FPB_EPATTERN:
+        raise ScatterPatternError(msg)
+    if rc == FPB_EINVERTED:
+        raise InvertedElementError(-1, -1, float("nan"))
+    raise RuntimeError(f"CUDA failure in fempack_b200: {msg}")
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def device() -> torch.device:
+    load()
+    return torch.device("cuda", torch.cuda.current_device())

@@ -1,0 +1,143 @@
+// Shared definitions of the fempack_b200 CUDA library (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/fempack_b200.h"
+
+namespace fpb {
+
+// ---- error plumbing (fpb_last_error) ------------------------------------
+void set_error(const char* fmt, ...);
+
+#define FPB_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ::fpb::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+      return FPB_ECUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+#define FPB_LAUNCH_CHECK() FPB_CUDA(cudaGetLastError())
+
+#define FPB_REQUIRE(cond, ...)   \
+  do {                           \
+    if (!(cond)) {               \
+      ::fpb::set_error(__VA_ARGS__); \
+      return FPB_ECONFIG;        \
+    }                            \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+constexpr int kNumSMs = 148;  // B200; grids are sized in multiples of this
+
+// ---- element traits -------------------------------------------------------
+// NN nodes, NG Gauss points, DIM; AFFINE: dN is constant over Gauss points
+// (TRI03/TET04, elements.py:118-145), so J, det and gradN are identical at
+// every point and are computed once — bit-identical to recomputing them.
+template <int ET> struct Elem;
+template <> struct Elem<FPB_TRI03> { static constexpr int NN = 3, NG = 3, DIM = 2; static constexpr bool AFFINE = true; };
+template <> struct Elem<FPB_QUAD04> { static constexpr int NN = 4, NG = 4, DIM = 2; static constexpr bool AFFINE = false; };
+template <> struct Elem<FPB_TET04> { static constexpr int NN = 4, NG = 4, DIM = 3; static constexpr bool AFFINE = true; };
+template <> struct Elem<FPB_PYR05> { static constexpr int NN = 5, NG = 8, DIM = 3; static constexpr bool AFFINE = false; };
+template <> struct Elem<FPB_HEX08> { static constexpr int NN = 8, NG = 8, DIM = 3; static constexpr bool AFFINE = false; };
+
+inline int etype_nn(int et) { const int t[5] = {3, 4, 4, 5, 8}; return (et >= 0 && et < 5) ? t[et] : 0; }
+inline int etype_ng(int et) { const int t[5] = {3, 4, 4, 8, 8}; return (et >= 0 && et < 5) ? t[et] : 0; }
+inline int etype_dim(int et) { const int t[5] = {2, 2, 3, 3, 3}; return (et >= 0 && et < 5) ? t[et] : 0; }
+
+// Reference tables in constant memory, uploaded once by
+// fpb_set_reference_element.  Layouts follow elements.py: N[a][g],
+// dN[l][a][g], w[g]; with every loop fully unrolled the indices are
+// compile-time constants and the values become constant-bank operands.
+struct RefTables {
+  double N[8 * 8];
+  double dN[3 * 8 * 8];
+  double w[8];
+};
+extern __constant__ RefTables c_ref[5];
+extern bool g_ref_loaded[5];
+
+template <int ET> __device__ __forceinline__ double refN(int a, int g) {
+  return c_ref[ET].N[a * Elem<ET>::NG + g];
+}
+template <int ET> __device__ __forceinline__ double refdN(int l, int a, int g) {
+  return c_ref[ET].dN[(l * Elem<ET>::NN + a) * Elem<ET>::NG + g];
+}
+template <int ET> __device__ __forceinline__ double refW(int g) { return c_ref[ET].w[g]; }
+
+// ---- geometry -------------------------------------------------------------
+// J[d][l] = sum_a x[a][d] dN[l][a][g]; det; gradN[d][a] = sum_l Ji[l][d] dN[l][a][g]
+// (_kernels.py:88-146).  Returns det.
+template <int ET>
+__device__ __forceinline__ double jacobian(const double (&xe)[Elem<ET>::NN][Elem<ET>::DIM], int g,
+                                           double (&J)[Elem<ET>::DIM][Elem<ET>::DIM]) {
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d)
+#pragma unroll
+    for (int l = 0; l < DIM; ++l) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) acc += xe[a][d] * refdN<ET>(l, a, g);
+      J[d][l] = acc;
+    }
+  if constexpr (DIM == 2) {
+    return J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  } else {
+    return J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
+           J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+           J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+  }
+}
+
+template <int ET>
+__device__ __forceinline__ void grad_shape(const double (&J)[Elem<ET>::DIM][Elem<ET>::DIM], double det,
+                                           int g, double (&gN)[Elem<ET>::DIM][Elem<ET>::NN]) {
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+  double Ji[DIM][DIM];
+  const double inv = 1.0 / det;
+  if constexpr (DIM == 2) {
+    Ji[0][0] = J[1][1] * inv;
+    Ji[0][1] = -J[0][1] * inv;
+    Ji[1][0] = -J[1][0] * inv;
+    Ji[1][1] = J[0][0] * inv;
+  } else {
+    Ji[0][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * inv;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * inv;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * inv;
+    Ji[1][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * inv;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * inv;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * inv;
+    Ji[2][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * inv;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * inv;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * inv;
+  }
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < DIM; ++l) acc += Ji[l][d] * refdN<ET>(l, a, g);
+      gN[d][a] = acc;
+    }
+}
+
+// ---- misc -------------------------------------------------------------------
+__device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
+
+inline int grid_for(int64_t work, int block, int per_sm = 16) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)kNumSMs * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace fpb

@@ -1,0 +1,391 @@
+// Solver vector kernels (sparse.py:78-130) and a device-resident Jacobi-PCG
+// (krylov.py:27-89).  All reductions are deterministic: a fixed grid of
+// kDotBlocks blocks reduces fixed strided slices in a fixed tree order, and
+// the last block to finish (atomic ticket) folds the per-block partials in
+// index order.  Repeated calls are therefore bitwise reproducible, like the
+// reference's sequential loops (test_sparse.py:93-107).
+#include "common.cuh"
+
+namespace fpb {
+
+constexpr int kDotBlocks = 2 * kNumSMs;  // 296
+constexpr int kDotThreads = 512;
+// work layout (doubles): [0, 4*kDotBlocks) partials for up to 4 fused dots,
+// then 4 ticket counters (as unsigned int in the low word).
+constexpr int kWorkDoubles = 4 * kDotBlocks + 8;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide fixed-order sum of NV values per thread; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV]) {
+  __shared__ double sh[NV][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[q][wid] = v[q];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double t = lane < nw ? sh[q][lane] : 0.0;
+      v[q] = warp_sum(t);
+    }
+  }
+}
+
+// Publish this block's NV partials; returns true in thread 0 of the last
+// block, with the grand totals in tot[] (summed in block-index order).
+template <int NV>
+__device__ __forceinline__ bool grid_finish(double (&v)[NV], double* work, int slot, double (&tot)[NV]) {
+  __shared__ bool last;
+  double* part = work;  // [NV][gridDim.x]
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(work + 4 * kDotBlocks) + 2 * slot;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) part[q * gridDim.x + blockIdx.x] = v[q];
+    __threadfence();
+    unsigned int t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  // last block: fold partials in fixed order with the whole block
+  __threadfence();
+  double s[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) s[q] = 0.0;
+  // fixed assignment: thread t sums partials t, t+blockDim, ... in order
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) s[q] += __ldcg(part + q * gridDim.x + b);
+  block_sum<NV>(s);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) tot[q] = s[q];
+    *ticket = 0u;  // re-arm for the next launch
+  }
+  return threadIdx.x == 0;
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV, G lanes per row (G = 4/8/16 picked from the mean row length).
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
+                                          const int32_t* __restrict__ colind,
+                                          const double* __restrict__ vals,
+                                          const double* __restrict__ x, int64_t row, bool valid,
+                                          int sub) {
+  double acc = 0.0;
+  if (valid) {
+    const int lo = __ldg(rowptr + row), hi = __ldg(rowptr + row + 1);
+    for (int k = lo + sub; k < hi; k += G) acc += __ldcs(vals + k) * __ldg(x + __ldcs(colind + k));
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+  return acc;
+}
+
+// Warp-uniform row loop: each warp covers 32/G consecutive rows per trip, so
+// every lane of a warp runs the same number of trips (the shuffles above need
+// the full warp).
+#define FPB_ROW_LOOP(G, n)                                                               \
+  const int sub = threadIdx.x & ((G) - 1);                                              \
+  const int64_t wid_ = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;           \
+  const int64_t nwarps_ = ((int64_t)gridDim.x * blockDim.x) >> 5;                       \
+  for (int64_t base_ = wid_ * (32 / (G)); base_ < (n); base_ += nwarps_ * (32 / (G)))  \
+    for (int64_t row = base_ + (threadIdx.x & 31) / (G), once_ = 0; once_ < 1; ++once_)
+
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv(int32_t n, const int32_t* __restrict__ rowptr,
+                                              const int32_t* __restrict__ colind,
+                                              const double* __restrict__ vals,
+                                              const double* __restrict__ x, double* __restrict__ y) {
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    double acc = row_dot<G>(rowptr, colind, vals, x, row, valid, sub);
+    if (valid && sub == 0) y[row] = acc;
+  }
+}
+
+__global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x,
+                       const double* __restrict__ y, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = alpha * x[i] + y[i];
+}
+
+__global__ void k_axpy2(int64_t n2, double alpha, const double2* __restrict__ x,
+                        const double2* __restrict__ y, double2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = __ldcs(x + i), b = __ldcs(y + i);
+    __stcs(out + i, make_double2(alpha * a.x + b.x, alpha * a.y + b.y));
+  }
+}
+
+__global__ void __launch_bounds__(kDotThreads) k_dot(int64_t n, const double* __restrict__ x,
+                                                     const double* __restrict__ y,
+                                                     double* __restrict__ result, double* work) {
+  double v[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    v[0] += __ldcs(x + i) * __ldcs(y + i);
+  block_sum<1>(v);
+  double tot[1];
+  if (grid_finish<1>(v, work, 0, tot)) *result = tot[0];
+}
+
+__global__ void k_diagonal(int32_t n, const int32_t* __restrict__ rowptr,
+                           const int32_t* __restrict__ colind, const double* __restrict__ vals,
+                           double* __restrict__ d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = rowptr[i], hi = rowptr[i + 1], end = hi;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (colind[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    d[i] = (lo < end && colind[lo] == i) ? vals[lo] : 0.0;
+  }
+}
+
+__global__ void k_row_sums(int32_t n, const int32_t* __restrict__ rowptr,
+                           const double* __restrict__ vals, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) s += vals[k];
+    out[i] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident PCG.  state: [0] rz, [1] bnorm, [2] tol, [3] status,
+// [4] iterations, [5] relres, [6] pq, [7] beta
+// ---------------------------------------------------------------------------
+enum { S_RZ = 0, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA };
+
+// init part 1: x = x0 | 0, r = b - A x0 | b, partial ||b||^2, ||r||^2
+template <int G>
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_init(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+           const double* __restrict__ vals, const double* __restrict__ b,
+           const double* __restrict__ x0, double* __restrict__ x, double* __restrict__ r,
+           double* state, double* hist, double tol, double* work) {
+  double v[2] = {0.0, 0.0};
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    double ri = 0.0;
+    if (x0) {
+      double ax = row_dot<G>(rowptr, colind, vals, x0, row, valid, sub);
+      if (valid) ri = -1.0 * ax + b[row];  // axpy(-1.0, spmv(A, x), b) (krylov.py:59)
+      if (valid && sub == 0) x[row] = x0[row];
+    } else {
+      if (valid) ri = b[row];
+      if (valid && sub == 0) x[row] = 0.0;
+    }
+    if (valid && sub == 0) {
+      r[row] = ri;
+      v[0] += b[row] * b[row];
+      v[1] += ri * ri;
+    }
+  }
+  block_sum<2>(v);
+  double tot[2];
+  if (grid_finish<2>(v, work, 0, tot)) {
+    double bnorm = sqrt(tot[0]);
+    double relres = bnorm == 0.0 ? 0.0 : sqrt(tot[1]) / bnorm;
+    state[S_BNORM] = bnorm;
+    state[S_TOL] = tol;
+    state[S_IT] = 0.0;
+    state[S_RELRES] = relres;
+    state[S_PQ] = 0.0;
+    state[S_STATUS] = (bnorm == 0.0 || relres <= tol) ? 1.0 : 0.0;
+    hist[0] = relres;
+  }
+}
+
+// init part 2: z = r / d, p = z, rz = r.z
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_init2(int64_t n, const double* __restrict__ r, const double* __restrict__ d,
+            double* __restrict__ z, double* __restrict__ p, double* state, double* work) {
+  double v[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double zi = r[i] / d[i];
+    z[i] = zi;
+    p[i] = zi;
+    v[0] += r[i] * zi;
+  }
+  block_sum<1>(v);
+  double tot[1];
+  if (grid_finish<1>(v, work, 1, tot)) state[S_RZ] = tot[0];
+}
+
+// iteration step 1: q = A p, pq = p.q; breakdown if pq <= 0
+template <int G>
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_spmv(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+           const double* __restrict__ vals, const double* __restrict__ p, double* __restrict__ q,
+           double* state, double* work) {
+  if (state[S_STATUS] != 0.0) return;
+  double v[1] = {0.0};
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    double qi = row_dot<G>(rowptr, colind, vals, p, row, valid, sub);
+    if (valid && sub == 0) {
+      q[row] = qi;
+      v[0] += p[row] * qi;
+    }
+  }
+  block_sum<1>(v);
+  double tot[1];
+  if (grid_finish<1>(v, work, 2, tot)) {
+    state[S_PQ] = tot[0];
+    if (tot[0] <= 0.0) state[S_STATUS] = 2.0;
+  }
+}
+
+// iteration step 2: x += alpha p; r -= alpha q; relres; z = r/d; rz_new = r.z
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
+             const double* __restrict__ p, const double* __restrict__ q,
+             const double* __restrict__ d, double* __restrict__ z, double* state, double* hist,
+             int64_t hist_first, double* work) {
+  if (state[S_STATUS] != 0.0) return;
+  const double alpha = state[S_RZ] / state[S_PQ];
+  double v[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double pi = p[i];
+    x[i] = alpha * pi + x[i];
+    const double ri = -alpha * q[i] + r[i];
+    r[i] = ri;
+    const double zi = ri / d[i];
+    z[i] = zi;
+    v[0] += ri * ri;
+    v[1] += ri * zi;
+  }
+  block_sum<2>(v);
+  double tot[2];
+  if (grid_finish<2>(v, work, 3, tot)) {
+    const double relres = sqrt(tot[0]) / state[S_BNORM];
+    const double it = state[S_IT] + 1.0;
+    state[S_IT] = it;
+    state[S_RELRES] = relres;
+    hist[(int64_t)it - hist_first] = relres;
+    if (relres <= state[S_TOL]) {
+      state[S_STATUS] = 1.0;
+    } else {
+      state[S_BETA] = tot[1] / state[S_RZ];
+      state[S_RZ] = tot[1];
+    }
+  }
+}
+
+// iteration step 3: p = beta p + z
+__global__ void k_pcg_direction(int64_t n, double* __restrict__ p, const double* __restrict__ z,
+                                const double* state) {
+  if (state[S_STATUS] != 0.0) return;
+  const double beta = state[S_BETA];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = beta * p[i] + z[i];
+}
+
+}  // namespace fpb
+
+using namespace fpb;
+
+extern "C" {
+
+int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+             const double* vals, const double* x, double* y, void* stream) {
+  if (n <= 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  // lanes per row from the mean row length (tet ~15 -> 8, hex ~27 -> 16)
+  const double mean = (double)nnz / n;
+  const int G = mean <= 6.0 ? 4 : (mean <= 20.0 ? 8 : 16);
+  int grid = grid_for((int64_t)n * G, 256, 16);
+  if (G == 4) k_spmv<4><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  else if (G == 8) k_spmv<8><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  else k_spmv<16><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_axpy(int64_t n, double alpha, const double* x, const double* y, double* out, void* stream) {
+  if (n <= 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && ((uintptr_t)out % 16 == 0);
+  if (aligned && n % 2 == 0) {
+    k_axpy2<<<grid_for(n / 2, 256, 8), 256, 0, s>>>(n / 2, alpha, (const double2*)x, (const double2*)y,
+                                                    (double2*)out);
+  } else {
+    k_axpy<<<grid_for(n, 256, 8), 256, 0, s>>>(n, alpha, x, y, out);
+  }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int64_t fpb_dot_work_size(void) { return kWorkDoubles; }
+
+int fpb_dot(int64_t n, const double* x, const double* y, double* result, double* work, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_dot<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, y, result, work);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_diagonal(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                 double* d, void* stream) {
+  if (n <= 0) return FPB_OK;
+  k_diagonal<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, rowptr, colind, vals, d);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* out, void* stream) {
+  if (n <= 0) return FPB_OK;
+  k_row_sums<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, rowptr, vals, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                 const double* b, const double* x0, double* x, double* r, double* p, double* z,
+                 const double* d, double* state, double* hist, double tol, double* work,
+                 void* stream) {
+  cudaStream_t s = as_stream(stream);
+  k_pcg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state,
+                                                   hist, tol, work);
+  FPB_LAUNCH_CHECK();
+  k_pcg_init2<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, d, z, p, state, work);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                    double* x, double* r, double* p, double* q, double* z, const double* d,
+                    double* state, double* hist, int64_t hist_first, int iters, double* work,
+                    void* stream) {
+  cudaStream_t s = as_stream(stream);
+  for (int it = 0; it < iters; ++it) {
+    k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
+    k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_first, work);
+    k_pcg_direction<<<grid_for(n, 256, 8), 256, 0, s>>>(n, p, z, state);
+  }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+"""CSR matrices and the solver vector kernels on the device (sparse.py:1-130).
+
+Drop-in for the reference's `CsrMatrix`, `build_node_pattern`, `spmv`,
+`axpy`, `dot`, `norm2`: numpy arguments are copied to HBM and results come
+back as numpy (the reference's return types); torch CUDA tensors stay on the
+device and results are returned as CUDA tensors without a host round trip.
+
+Storage: rowptr / colind are int32 in HBM (nnz < 2^31 is enforced), vals
+float64.  The numpy views `rowptr` / `colind` are int64 like the
+reference's; `vals` is a fresh host copy of the device values.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_INT32_MAX = np.iinfo(np.int32).max
+
+
+def to_device(x, dtype=torch.float64) -> tuple[torch.Tensor, bool]:
+    """(contiguous CUDA tensor, came_from_host)."""
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            return x.to(_lib.device(), dtype=dtype).contiguous(), True
+        if x.dtype != dtype:
+            x = x.to(dtype)
+        return x.contiguous(), False
+    arr = np.ascontiguousarray(x, dtype=np.float64 if dtype == torch.float64 else np.int32)
+    return torch.from_numpy(arr).to(_lib.device()), True
+
+
+def _to_i32(x) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        if x.numel() and int(x.max()) > _INT32_MAX:
+            raise ValueError("index exceeds int32")
+        return x.to(_lib.device(), dtype=torch.int32).contiguous()
+    a = np.asarray(x)
+    if a.size and a.max() > _INT32_MAX:
+        raise ValueError("index exceeds int32")
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(_lib.device())
+
+
+class CsrMatrix:
+    """n x n CSR matrix in HBM (sparse.py:20-56)."""
+
+    def __init__(self, n, rowptr, colind, vals, _host=None):
+        self.n = int(n)
+        self.rowptr_d = rowptr if isinstance(rowptr, torch.Tensor) and rowptr.is_cuda and rowptr.dtype == torch.int32 else _to_i32(rowptr)
+        self.colind_d = colind if isinstance(colind, torch.Tensor) and colind.is_cuda and colind.dtype == torch.int32 else _to_i32(colind)
+        self.vals_d = to_device(vals)[0]
+        self._host = _host if _host is not None else {}
+
+    @property
+    def nnz(self) -> int:
+        return int(self.colind_d.shape[0])
+
+    @property
+    def rowptr(self) -> np.ndarray:
+        if "rowptr" not in self._host:
+            self._host["rowptr"] = self.rowptr_d.cpu().numpy().astype(np.int64)
+        return self._host["rowptr"]
+
+    @property
+    def colind(self) -> np.ndarray:
+        if "colind" not in self._host:
+            self._host["colind"] = self.colind_d.cpu().numpy().astype(np.int64)
+        return self._host["colind"]
+
+    @property
+    def vals(self) -> np.ndarray:
+        return self.vals_d.cpu().numpy()
+
+    def copy(self) -> "CsrMatrix":
+        return CsrMatrix(self.n, self.rowptr_d, self.colind_d, self.vals_d.clone(), self._host)
+
+    def with_vals(self, vals) -> "CsrMatrix":
+        return CsrMatrix(self.n, self.rowptr_d, self.colind_d, vals, self._host)
+
+    def row_indices(self) -> np.ndarray:
+        return np.repeat(np.arange(self.n, dtype=np.int64), np.diff(self.rowptr))
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.n, self.n))
+        out[self.row_indices(), self.colind] = self.vals
+        return out
+
+    def diagonal_d(self) -> torch.Tensor:
+        d = torch.empty(self.n, dtype=torch.float64, device=self.vals_d.device)
+        _lib.call("fpb_diagonal", self.n, self.rowptr_d.data_ptr(), self.colind_d.data_ptr(),
+                  self.vals_d.data_ptr(), d.data_ptr(), _lib.stream())
+        return d
+
+    def diagonal(self) -> np.ndarray:
+        return self.diagonal_d().cpu().numpy()
+
+    def row_sums_d(self) -> torch.Tensor:
+        out = torch.empty(self.n, dtype=torch.float64, device=self.vals_d.device)
+        _lib.call("fpb_row_sums", self.n, self.rowptr_d.data_ptr(), self.vals_d.data_ptr(),
+                  out.data_ptr(), _lib.stream())
+        return out
+
+
+def build_node_pattern(mesh) -> CsrMatrix:
+    """Zero-valued CSR graph of node adjacency plus diagonal (sparse.py:59-75)."""
+    from .mesh import as_device_mesh
+
+    mesh = as_device_mesh(mesh)
+    n = mesh.nnode
+    if n > _INT32_MAX:
+        raise ValueError("node count exceeds int32")
+    groups = [g for g in mesh.groups if g.nelem]
+    ng = len(groups)
+    conns = (ctypes.c_void_p * max(ng, 1))(*[g.conn_d.data_ptr() for g in groups])
+    nelem = np.array([g.nelem for g in groups] or [0], dtype=np.int64)
+    nn = np.array([g.conn_d.shape[1] for g in groups] or [0], dtype=np.int32)
+    dev = mesh.coords_d.device
+    rowptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    nnz = np.zeros(1, dtype=np.int64)
+    lib = _lib.load()
+    nnz_p = nnz.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    _lib.check(lib.fpb_build_pattern(n, ng, ctypes.cast(conns, ctypes.c_void_p), nelem.ctypes.data,
+                                     nn.ctypes.data, rowptr.data_ptr(), None, nnz_p, _lib.stream()),
+               "fpb_build_pattern")
+    colind = torch.empty(int(nnz[0]), dtype=torch.int32, device=dev)
+    _lib.check(lib.fpb_build_pattern(n, ng, ctypes.cast(conns, ctypes.c_void_p), nelem.ctypes.data,
+                                     nn.ctypes.data, rowptr.data_ptr(), colind.data_ptr(), nnz_p,
+                                     _lib.stream()),
+               "fpb_build_pattern")
+    vals = torch.zeros(int(nnz[0]), dtype=torch.float64, device=dev)
+    return CsrMatrix(n, rowptr, colind, vals)
+
+
+# ---- vector kernels --------------------------------------------------------
+
+_work: dict = {}
+
+
+def dot_work() -> torch.Tensor:
+    """Per-(device, stream) scratch for the deterministic reductions."""
+    key = (torch.cuda.current_device(), _lib.stream())
+    w = _work.get(key)
+    if w is None:
+        size = int(_lib.load().fpb_dot_work_size())
+        w = torch.zeros(size, dtype=torch.float64, device=_lib.device())
+        _work[key] = w
+    return w
+
+
+def spmv_d(A: CsrMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    y = out if out is not None else torch.empty(A.n, dtype=torch.float64, device=x.device)
+    _lib.call("fpb_spmv", A.n, A.nnz, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(),
+              A.vals_d.data_ptr(), x.data_ptr(), y.data_ptr(), _lib.stream())
+    return y
+
+
+def spmv(A: CsrMatrix, x, parallel: bool = False):
+    """y = A x (sparse.py:110-116); `parallel` is accepted for API parity —
+    the device kernel is always parallel and deterministic."""
+    xd, host = to_device(x)
+    y = spmv_d(A, xd)
+    return y.cpu().numpy() if host else y
+
+
+def axpy_d(alpha: float, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None):
+    o = out if out is not None else torch.empty_like(x)
+    _lib.call("fpb_axpy", x.numel(), float(alpha), x.data_ptr(), y.data_ptr(), o.data_ptr(),
+              _lib.stream())
+    return o
+
+
+def axpy(alpha: float, x, y):
+    """out = alpha x + y, a new array (sparse.py:119-122)."""
+    xd, hx = to_device(x)
+    yd, hy = to_device(y)
+    o = axpy_d(alpha, xd, yd)
+    return o.cpu().numpy() if (hx or hy) else o
+
+
+def dot_d(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Device scalar (0-d tensor) = x . y, no host synchronisation."""
+    r = out if out is not None else torch.empty((), dtype=torch.float64, device=x.device)
+    _lib.call("fpb_dot", x.numel(), x.data_ptr(), y.data_ptr(), r.data_ptr(),
+              dot_work().data_ptr(), _lib.stream())
+    return r
+
+
+def dot(x, y) -> float:
+    """x . y (sparse.py:125-126); fixed-order tree, bitwise reproducible."""
+    xd, _ = to_device(x)
+    yd, _ = to_device(y)
+    return float(dot_d(xd, yd).item())
+
+
+def norm2(x) -> float:
+    xd, _ = to_device(x)
+    return float(np.sqrt(dot_d(xd, xd).item()))

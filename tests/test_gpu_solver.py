@@ -1,0 +1,96 @@
+"""Solver vector kernels and PCG on the B200 vs the reference goldens."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import fempack_np as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=["tet_6", "hex_8", "mixed_8", "tet_c1"])
+def case(request, cuda_ok):
+    import paper_2107_11541_b200 as P
+    from gpu_cases import CASES
+
+    return request.param, P.AssemblyContext.build(CASES[request.param](), 8), load_golden(request.param)
+
+
+def test_spmv_axpy_dot(case):
+    import paper_2107_11541_b200 as P
+
+    name, ctx, g = case
+    M = ctx.assemble_matrix(P.KernelKind.MASS)
+    y = P.spmv(M, g["spmv_x"])
+    assert O.rel_diff(y, g["spmv_y"]) < 1e-12
+    assert P.spmv(M, g["spmv_x"]).tobytes() == y.tobytes()  # deterministic
+    out = P.axpy(2.5, g["bench_scalar0"], g["bench_scalar1"])
+    assert out.tobytes() == g["axpy_out"].tobytes()  # one rounding per entry, as the reference
+    x, yy = g["bench_scalar0"], g["bench_scalar1"]
+    d = P.dot(x, yy)
+    assert abs(d - math.fsum(x * yy)) <= 1e-12 * float(np.abs(x * yy).sum())
+    assert P.dot(x, yy) == d  # bitwise reproducible
+    assert P.norm2(x) == pytest.approx(float(g["norm2"]), rel=1e-13)
+
+
+def test_pcg_matches_reference(case):
+    import paper_2107_11541_b200 as P
+
+    name, ctx, g = case
+    if "cg_b" not in g:
+        pytest.skip("no PCG fixture")
+    A = ctx.pattern.with_vals(g["cg_vals"])
+    x, st = P.pcg_solve(A, g["cg_b"], tol=1e-8)
+    it_ref = int(g["cg_iterations"])
+    assert st.converged
+    assert abs(st.iterations - it_ref) <= 1
+    assert len(st.residual_history) == st.iterations + 1
+    n = min(len(st.residual_history), len(g["cg_history"]))
+    np.testing.assert_allclose(st.residual_history[: n - 1], g["cg_history"][: n - 1], rtol=1e-6)
+    # same solution to the solver tolerance
+    assert O.rel_diff(x, g["cg_x"]) < 1e-6
+    assert st.true_residual <= 1e-8 * 1.01 or st.true_residual == pytest.approx(float(g["cg_true_residual"]), rel=1e-3)
+
+
+def _csr(D):
+    import paper_2107_11541_b200 as P
+
+    n = D.shape[0]
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    cols, vals = [], []
+    for i in range(n):
+        nz = np.nonzero(D[i])[0]
+        rowptr[i + 1] = rowptr[i] + nz.size
+        cols.append(nz)
+        vals.append(D[i, nz])
+    return P.CsrMatrix(n, rowptr, np.concatenate(cols), np.concatenate(vals))
+
+
+def test_pcg_known_answers(cuda_ok):
+    """krylov known answers (test_krylov.py:16-110)."""
+    import paper_2107_11541_b200 as P
+
+    x, st = P.pcg_solve(_csr(np.eye(6)), np.arange(1.0, 7.0), tol=1e-12)
+    np.testing.assert_allclose(x, np.arange(1.0, 7.0), atol=1e-15)
+    assert st.iterations == 1 and st.converged and st.residual_history[0] == 1.0
+    x, st = P.pcg_solve(_csr(np.array([[4.0, 1.0], [1.0, 3.0]])), np.array([1.0, 2.0]), tol=1e-14)
+    np.testing.assert_allclose(x, [1 / 11, 7 / 11], atol=1e-13)
+    rng = np.random.default_rng(21)
+    B = rng.standard_normal((50, 50))
+    x, st = P.pcg_solve(_csr(B @ B.T + 50 * np.eye(50)), rng.standard_normal(50), tol=1e-10)
+    assert st.converged and st.iterations <= 55 and st.true_residual <= 2e-10
+    with pytest.raises(P.SolverBreakdownError, match="curvature"):
+        P.pcg_solve(_csr(np.array([[1.0, 2.0], [2.0, 1.0]])), np.array([1.0, -1.0]), tol=1e-12)
+    with pytest.raises(P.SolverBreakdownError, match="diagonal"):
+        P.pcg_solve(_csr(np.array([[1.0, 0.5], [0.5, -2.0]])), np.ones(2))
+    x, st = P.pcg_solve(_csr(np.eye(4) * 3.0), np.zeros(4))
+    assert not x.any() and st.converged and st.iterations == 0 and st.residual_history == [0.0]
+    x, st = P.pcg_solve(_csr(np.diag([2.0, 4.0])), np.array([2.0, 8.0]), x0=np.array([1.0, 2.0]), tol=1e-12)
+    assert st.iterations == 0 and st.converged
+    rng = np.random.default_rng(24)
+    B = rng.standard_normal((30, 30))
+    x, st = P.pcg_solve(_csr(B @ B.T + 1e-2 * np.eye(30)), rng.standard_normal(30), tol=1e-14, max_iter=3)
+    assert not st.converged and st.iterations == 3 and len(st.residual_history) == 4

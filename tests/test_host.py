@@ -1,0 +1,86 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared
+symbol, the ctypes table matches the header, host-side tables and config
+validation behave like the reference."""
+
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden
+
+HEADER = os.path.join(ROOT, "include", "fempack_b200.h")
+LIB = os.path.join(ROOT, "paper_2107_11541_b200", "libfempack_b200.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|int)\s+(fpb_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    assert os.path.exists(LIB), "run __graft_entry__.build() first"
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (fpb_\w+)", out))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+
+
+def test_ctypes_table_covers_header():
+    from paper_2107_11541_b200 import _lib
+
+    assert sorted(_lib.SIGNATURES) == declared_functions()
+    lib = _lib.load(require_gpu=False)
+    assert lib.fpb_version() == 1
+    assert lib.fpb_dot_work_size() > 0
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_config_errors_without_gpu():
+    from paper_2107_11541_b200 import _lib
+    from paper_2107_11541_b200.errors import ConfigurationError
+
+    lib = _lib.load(require_gpu=False)
+    # invalid vector size is rejected before touching the device
+    rc = lib.fpb_build_packs(10, 4, 3, None, None, None)
+    assert rc == _lib.FPB_ECONFIG
+    assert "vector_size" in _lib.last_error()
+    with pytest.raises(ConfigurationError):
+        _lib.check(rc)
+    assert lib.fpb_set_reference_element(7, 4, 4, 3, None, None, None) == _lib.FPB_ECONFIG
+
+
+def test_tables_match_reference_bitwise():
+    from paper_2107_11541_b200.elements import ElementType, reference_element
+
+    g = load_golden("elements")
+    for et in ElementType:
+        r = reference_element(et)
+        assert r.N.tobytes() == g[f"{et.value}_N"].tobytes(), et
+        assert r.dN.tobytes() == g[f"{et.value}_dN"].tobytes(), et
+        assert r.weights.tobytes() == g[f"{et.value}_w"].tobytes(), et
+
+
+def test_pack_config_validation():
+    from paper_2107_11541_b200 import ConfigurationError, PackConfig
+
+    for vs in (1, 2, 4, 8, 16, 32):
+        PackConfig(vs)
+    with pytest.raises(ConfigurationError):
+        PackConfig(3)
+
+
+def test_no_oracle_import_in_product():
+    pkg = os.path.join(ROOT, "paper_2107_11541_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*", "", src).replace('"""', ""), f
