@@ -1,0 +1,322 @@
+"""Headline bench: assembled elements/s for BASELINE.json config 2 —
+NS momentum RHS + continuity (B_x, B_y, B_z) assembly on the 5,036,520-tet
+box mesh (94 x 94 x 95 cells, unit cube), SIMD-packed layout, one B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+One step = zero the outputs, MOMENTUM_RHS (rho=1, mu=1e-2, velocity
+= default_rng(0).standard_normal((nnode, 3)), bench.py:196-207 of the
+reference) and the fused gradient/continuity matrices B_k over every element.
+`value` = elements assembled per second (each element contributes its
+momentum block and all three B_k blocks) with inputs resident in HBM, timed
+with CUDA events per step, L2 flushed (512 MiB write) between steps.
+`e2e` = the same step through the public API with host (numpy) inputs and
+outputs: velocity H2D in, RHS + three matrices' values D2H out.
+
+Multi-GPU (torchrun, N > 1): weak scaling — rank r assembles z-slab r of an
+(94, 94, 95 N) mesh, and interface-plane RHS/matrix contributions are summed
+by an NCCL halo exchange (paper_2107_11541_b200/distributed.py).
+
+`--impl reference`: the reference's CPU algorithm (C restatement of the
+packed kernels, oracle/fempack_ref.c, all host threads) on a bounded sample of
+the same workload; prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "assembled elements/s (Melem/s) & FP64/HBM roofline fraction at 1/2/4/8 B200"
+UNIT = "Melem/s"
+# measured DFMA rate on this pool's B200 (tools/microbench/peaks.cu,
+# profiles/r01_microbench.txt); MEASURED_PEAKS.json carries no FP64 figure
+FP64_PEAK_TFLOPS = 34.1
+HBM_FALLBACK_GBS = 6650.0
+# SURVEY 8(d) algorithmic work per TET04 element (flops, compulsory bytes)
+WORK = {"momentum_rhs": (1492.0, 28.0), "gradient_xyz": (676.0, 145.0)}
+L2_FLUSH_BYTES = 512 << 20
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_baseline(nx, ny, nz_sample, steps=3, warmup=1):
+    from oracle import cport
+    from oracle.baseline import CpuWorkload
+
+    threads = cport.max_threads()
+    wl = CpuWorkload(nx, ny, nz_sample, nthreads=threads)
+    ts = wl.time_steps(steps, warmup)
+    t = statistics.median(ts)
+    return {"value": wl.nelem / t / 1e6, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"TET04 {nx}x{ny}x{nz_sample} slab of the config-2 mesh ({wl.nelem} elements), "
+                      f"momentum RHS + 3x CONVECTION(e_k) + scatters, reference packed kernels "
+                      f"(oracle/fempack_ref.c, vs=8, geometry cached as in the reference bench), "
+                      f"median of {steps}"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: reference CPU algorithm on the host cores (rank 0)."""
+    if rank != 0:
+        return
+    from oracle import cport
+    from oracle.baseline import CpuWorkload
+
+    threads = cport.max_threads()
+    wl = CpuWorkload(args.nx, args.ny, args.cpu_nz, nthreads=threads)
+    ts = wl.time_steps(args.steps, args.warmup)
+    t = statistics.mean(ts)
+    value = wl.nelem / t / 1e6
+    sample = (f"TET04 {args.nx}x{args.ny}x{args.cpu_nz} slab of the config-2 mesh ({wl.nelem} elements) "
+              f"per step, reference packed kernels in C (oracle/fempack_ref.c), {threads} threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "config 2: TET04 94x94x95 box (5,036,520 elements), NS momentum RHS + "
+                               "continuity B_x,B_y,B_z, packed layout", "sample_elements": wl.nelem},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=94)
+    ap.add_argument("--ny", type=int, default=94)
+    ap.add_argument("--nz", type=int, default=95)
+    ap.add_argument("--cpu-nz", type=int, default=24, help="z-layers of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds under load before timing")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2107_11541_b200 as P
+
+    dev = torch.device("cuda", local)
+    if world > 1:
+        from paper_2107_11541_b200 import distributed as D
+
+        sub = D.SlabDomain.build(args.nx, args.ny, args.nz * world, rank, world)
+        mesh, ctx = sub.mesh, sub.ctx
+    else:
+        sub = None
+        mesh = P.generate_box_mesh(P.ElementType.TET04, args.nx, args.ny, args.nz)
+        ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    ctx.refresh_geometry("packed", need_grad=False)
+    nelem, nnode, nnz = mesh.nelem, mesh.nnode, ctx.pattern.nnz
+    rng = np.random.default_rng(0)
+    vel_h = rng.standard_normal((nnode, 3))
+    vel = torch.as_tensor(vel_h, device=dev)
+    rhs = torch.zeros((nnode, 3), dtype=torch.float64, device=dev)
+    mats = torch.zeros(3 * nnz, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        rhs.zero_()
+        mats.zero_()
+        if ev:
+            ev[0].record(stream)
+        ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs)
+        if ev:
+            ev[1].record(stream)
+        ctx.assemble_gradients_d(mats)
+        if ev:
+            ev[2].record(stream)
+        if sub is not None:
+            sub.halo_sum_rhs(rhs)
+            sub.halo_sum_matrix(mats, 3)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    # soak (untimed) so the clock sampler sees the loaded state
+    t_end = time.perf_counter() + args.soak
+    while time.perf_counter() < t_end:
+        step()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, k_mom, k_grad = [], [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush outside the timed window
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e_start.record(stream)
+        step(ev)
+        e_end.record(stream)
+        torch.cuda.synchronize()
+        step_ms.append(e_start.elapsed_time(e_end))
+        k_mom.append(ev[0].elapsed_time(ev[1]))
+        k_grad.append(ev[1].elapsed_time(ev[2]))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    total_elems = nelem * world
+    value = total_elems / (ms_per_step / 1e3) / 1e6
+
+    # roofline of the dominant kernel (mean launch duration on its stream)
+    kern = {"momentum_rhs": statistics.mean(k_mom), "gradient_xyz": statistics.mean(k_grad)}
+    dom = max(kern, key=kern.get)
+    F, B = WORK[dom]
+    t_s = kern[dom] / 1e3
+    flops_rate = F * nelem / t_s / 1e12
+    bytes_rate = B * nelem / t_s / 1e9
+    hbm, hbm_src = hbm_peak()
+    if F / B > FP64_PEAK_TFLOPS * 1e3 / hbm:  # compute-bound by the ridge point
+        roof = {"bound": "fp64", "achieved": flops_rate, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": flops_rate / FP64_PEAK_TFLOPS,
+                "peak_source": "measured DFMA microbenchmark (profiles/r01_microbench.txt)"}
+    else:
+        roof = {"bound": "hbm", "achieved": bytes_rate, "peak": hbm, "unit": "GB/s",
+                "frac": bytes_rate / hbm, "peak_source": hbm_src}
+    roof.update({"kernel": dom, "traffic": None,
+                 "work_per_element": {"flops": F, "bytes": B, "source": "SURVEY.md 8(d)"}})
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        grads = None
+        e2e_ms = []
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel_h, None, 1.0, 1e-2, 0.0)
+            grads = P.gradient_matrices(ctx)
+            vals = [B.vals for B in grads]
+            torch.cuda.synchronize()
+            if i > 0:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert r.shape == (nnode, 3) and all(v.shape == (nnz,) for v in vals)
+        t = statistics.mean(e2e_ms)
+        if dist:
+            tt = torch.tensor([t], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        e2e = {"value": total_elems / (t / 1e3) / 1e6, "unit": UNIT, "ms_per_step": t,
+               "h2d_bytes_per_step": int(vel_h.nbytes),
+               "d2h_bytes_per_step": int(r.nbytes + sum(v.nbytes for v in vals)),
+               "api": "AssemblyContext.assemble_rhs(MOMENTUM_RHS, numpy) + gradient_matrices(ctx) + .vals"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.nx, args.ny, args.cpu_nz)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"error": repr(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"config 2: TET04 box {args.nx}x{args.ny}x{args.nz} per GPU "
+                                   f"({nelem} elements, {nnode} nodes, nnz {nnz}), NS momentum RHS + "
+                                   "continuity B_x,B_y,B_z, SIMD-packed (32-lane) layout",
+                       "elements_per_step": total_elems, "l2": "flushed (512 MiB write) between steps",
+                       "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
+            "roofline": roof,
+            "kernels_ms": kern,
+            "gpu_launches": args.steps * 2 * len(ctx.groups),
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,12 @@ constexpr int kDotThreads = 512;
 // then 4 ticket counters (as unsigned int in the low word).
 constexpr int kWorkDoubles = 4 * kDotBlocks + 8;
 
+// alpha*x + y with the reference's two roundings (no DFMA contraction), so
+// axpy is bitwise identical to sparse.py:96-99
+__device__ __forceinline__ double axpy1(double a, double x, double y) {
+  return __dadd_rn(__dmul_rn(a, x), y);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -120,7 +126,7 @@ __global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x,
                        const double* __restrict__ y, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = alpha * x[i] + y[i];
+    out[i] = axpy1(alpha, x[i], y[i]);
 }
 
 __global__ void k_axpy2(int64_t n2, double alpha, const double2* __restrict__ x,
@@ -128,7 +134,7 @@ __global__ void k_axpy2(int64_t n2, double alpha, const double2* __restrict__ x,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
        i += (int64_t)gridDim.x * blockDim.x) {
     double2 a = __ldcs(x + i), b = __ldcs(y + i);
-    __stcs(out + i, make_double2(alpha * a.x + b.x, alpha * a.y + b.y));
+    __stcs(out + i, make_double2(axpy1(alpha, a.x, b.x), axpy1(alpha, a.y, b.y)));
   }
 }
 
@@ -187,7 +193,7 @@ k_pcg_init(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restr
     double ri = 0.0;
     if (x0) {
       double ax = row_dot<G>(rowptr, colind, vals, x0, row, valid, sub);
-      if (valid) ri = -1.0 * ax + b[row];  // axpy(-1.0, spmv(A, x), b) (krylov.py:59)
+      if (valid) ri = axpy1(-1.0, ax, b[row]);  // axpy(-1.0, spmv(A, x), b) (krylov.py:59)
       if (valid && sub == 0) x[row] = x0[row];
     } else {
       if (valid) ri = b[row];
@@ -267,8 +273,8 @@ k_pcg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const double pi = p[i];
-    x[i] = alpha * pi + x[i];
-    const double ri = -alpha * q[i] + r[i];
+    x[i] = axpy1(alpha, pi, x[i]);
+    const double ri = axpy1(-alpha, q[i], r[i]);
     r[i] = ri;
     const double zi = ri / d[i];
     z[i] = zi;
@@ -299,7 +305,7 @@ __global__ void k_pcg_direction(int64_t n, double* __restrict__ p, const double*
   const double beta = state[S_BETA];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = beta * p[i] + z[i];
+    p[i] = axpy1(beta, p[i], z[i]);
 }
 
 }  // namespace fpb

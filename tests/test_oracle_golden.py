@@ -133,3 +133,27 @@ def test_pcg(case):
     assert it == int(g["cg_iterations"])
     assert np.array(hist).tobytes() == g["cg_history"].tobytes()
     assert x.tobytes() == g["cg_x"].tobytes()
+
+
+def test_c_port_bitwise_vs_reference():
+    """The C restatement (bench cpu_baseline) reproduces the reference
+    packed path bit for bit when run on one thread."""
+    from oracle import cport
+
+    for name in ("tet_6", "hex_8", "tet_c1"):
+        g = load_golden(name)
+        m = CASES[name]()
+        (et, conn), = m.groups
+        pg = cport.PackedGroup(et, conn, m.coords, vs=8, nthreads=1)
+        rhs = pg.momentum_rhs(g["bench_vel"], 1.0, 1e-2, np.zeros((m.nnode, 3)))
+        assert rhs.tobytes() == g["rhs_momentum"].tobytes(), name
+        rowptr, colind = O.build_node_pattern(m.nnode, [conn])
+        pos = O.packed_positions(O.matrix_positions(conn, rowptr, colind), pg.elem_index)
+        vals = pg.convection(g["bench_vel"], np.ascontiguousarray(pos), np.zeros(colind.size))
+        assert vals.tobytes() == g["mat_convection"].tobytes(), name
+        y = cport.spmv(rowptr, colind, O.assemble_matrix(m, "mass")[2], g["spmv_x"])
+        assert y.tobytes() == g["spmv_y"].tobytes()
+        # threaded run: same values up to summation order
+        pg4 = cport.PackedGroup(et, conn, m.coords, vs=8, nthreads=4)
+        r4 = pg4.momentum_rhs(g["bench_vel"], 1.0, 1e-2, np.zeros((m.nnode, 3)))
+        assert O.rel_diff(r4, g["rhs_momentum"]) < 1e-13
