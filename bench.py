@@ -4,7 +4,7 @@ box mesh (94 x 94 x 95 cells, unit cube), SIMD-packed layout, one B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-One step = zero the outputs, MOMENTUM_RHS (rho=1, mu=1e-2, velocity
+One step = MOMENTUM_RHS (rho=1, mu=1e-2, velocity
 = default_rng(0).standard_normal((nnode, 3)), bench.py:196-207 of the
 reference) and the fused gradient/continuity matrices B_k over every element.
 `value` = elements assembled per second (each element contributes its
@@ -152,6 +152,8 @@ def main():
     ap.add_argument("--cpu-nz", type=int, default=24, help="z-layers of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--scatter", default="auto", choices=["auto", "rows", "atomic"],
+                    help="global-assembly strategy (AssemblyContext.build)")
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds under load before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -183,7 +185,7 @@ def main():
     else:
         sub = None
         mesh = P.generate_box_mesh(P.ElementType.TET04, args.nx, args.ny, args.nz)
-        ctx = P.AssemblyContext.build(mesh, vector_size=8)
+        ctx = P.AssemblyContext.build(mesh, vector_size=8, scatter=args.scatter)
     ctx.refresh_geometry("packed", need_grad=False)
     nelem, nnode, nnz = mesh.nelem, mesh.nnode, ctx.pattern.nnz
     rng = np.random.default_rng(0)
@@ -195,8 +197,6 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
-        rhs.zero_()
-        mats.zero_()
         if ev:
             ev[0].record(stream)
         ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs)
@@ -304,7 +304,7 @@ def main():
             "config": {"workload": f"config 2: TET04 box {args.nx}x{args.ny}x{args.nz} per GPU "
                                    f"({nelem} elements, {nnode} nodes, nnz {nnz}), NS momentum RHS + "
                                    "continuity B_x,B_y,B_z, SIMD-packed (32-lane) layout",
-                       "elements_per_step": total_elems, "l2": "flushed (512 MiB write) between steps",
+                       "elements_per_step": total_elems, "l2": "flushed (512 MiB write) between steps", "scatter": args.scatter,
                        "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
             "kernels_ms": kern,

@@ -125,6 +125,57 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
                  double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
                  void* stream);
 
+/* ---- row-owned assembly for affine simplices (TRI03, TET04) -------------
+ * Each CSR row / node is owned by one thread that walks its incident
+ * elements in ascending order and writes its outputs once: no atomics, no
+ * zero fill, bitwise reproducible (see rows.cu).  Incidence lists are SELL-32:
+ * slice s = rows [32s, 32s+32) holds columns [slice_ptr[s], slice_ptr[s+1]),
+ * entry (m, lane) at inc[32 m + lane] (element id, -1 padding).
+ *
+ * fpb_incidence_build: slice_ptr[ceil(n/32)+1]; with inc == NULL only sizes
+ * (returns the column count through ncols_h, synchronous); otherwise also
+ * fills inc[32 * ncols].
+ * fpb_incidence_slots: for matrices, slots[32 * ncols] packs the 8-bit
+ * offsets of each incident element's nodes inside the row's column list;
+ * returns the longest row through rowcap_h (synchronous).
+ * fpb_assemble_rows: out is overwritten (accumulate = 0) or added to
+ * (accumulate = 1); layouts of out as in fpb_assemble. */
+int fpb_incidence_build(int32_t n, int64_t nelem, int nn, const int32_t* conn, int32_t* slice_ptr,
+                        int32_t* inc, int64_t* ncols_h, void* stream);
+int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_ptr,
+                        const int32_t* inc, const int32_t* conn, const int32_t* rowptr,
+                        const int32_t* colind, uint32_t* slots, int* rowcap_h, void* stream);
+int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+                      const uint32_t* slots, const int32_t* conn, const double* coords,
+                      const double* vel, const double* phi, double rho, double mu, double kappa,
+                      const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate, double* out,
+                      void* stream);
+
+/* ---- element-block RHS assembly (deterministic, atomic-free) ------------
+ * Blocks of fpb_block_elems() consecutive elements; phase 1 integrates each
+ * element once and reduces inside the block (sorted gather lists), phase 2
+ * sums the per-(block, node) partials per node in ascending block order.
+ * fpb_blocks_build: with blk_nodes == NULL fills blk_ptr[nblocks+1] and
+ * returns the partial count P through npartial_h (synchronous); otherwise
+ * and the largest block's distinct-node count through maxnu_h; otherwise
+ * (npartial_h holding P) fills blk_nodes[P], blk_gptr[P + nblocks],
+ * blk_gslot and blk_lidx [nblocks * block_elems * nn], node_pptr[n+1],
+ * node_plist[P].  Phase 1 stages each block's distinct nodes through shared
+ * memory (blk_lidx = local node of every element slot).
+ * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; partial[P * nv] is
+ * scratch; out overwritten (accumulate = 0) or added to. */
+int fpb_block_elems(void);
+int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int32_t* blk_ptr,
+                     int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
+                     int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
+                     void* stream);
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* coords, const double* vel,
+                        const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+                        const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
+                        const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
+                        const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,
+                        void* stream);
+
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 
 /* y = A x (sparse.py:78-84).  nnz = rowptr[n] sizes the lanes per row. */

@@ -14,7 +14,8 @@ import torch
 
 from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfempack_b200.so")
+LIB_PATH = os.environ.get("FPB_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libfempack_b200.so")
 
 FPB_OK, FPB_ECONFIG, FPB_EINVERTED, FPB_EPATTERN, FPB_ECUDA = 0, 1, 2, 3, 4
 
@@ -34,6 +35,14 @@ SIGNATURES = {
     "fpb_matrix_positions": (_int, [_i64, _int, _vp, _i32, _vp, _vp, _int, _int, _vp, _vp]),
     "fpb_geometry": (_int, [_int, _i64, _int, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
     "fpb_assemble": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _i64, _vp, _vp]),
+    "fpb_incidence_build": (_int, [_i32, _i64, _int, _vp, _vp, _vp, _pi64, _vp]),
+    "fpb_incidence_slots": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
+    "fpb_assemble_rows": (_int, [_int, _int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl,
+                                 _vp, _i64, _int, _int, _vp, _vp]),
+    "fpb_block_elems": (_int, []),
+    "fpb_blocks_build": (_int, [_i64, _int, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
+    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
+                                   _vp, _int, _vp, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),
     "fpb_dot_work_size": (_i64, []),

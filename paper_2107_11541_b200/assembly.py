@@ -30,7 +30,7 @@ from .elements import ETYPE_ID, ReferenceElement, reference_element, upload_tabl
 from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
 from .mesh import Mesh, as_device_mesh
 from .packing import KERNEL_LANES, PackConfig, PackSet, pack_lanes
-from .sparse import CsrMatrix, build_node_pattern, to_device
+from .sparse import CsrMatrix, build_node_pattern, to_device, to_host
 
 LAYOUTS = ("scalar", "packed")
 
@@ -78,6 +78,84 @@ def matrix_positions(conn, pattern: CsrMatrix) -> np.ndarray:
     return pos.cpu().numpy().astype(np.int64).reshape(lead + pos.shape[1:])
 
 
+ROW_OWNED = ("TRI03", "TET04")  # affine simplices: row-owned kernels (rows.cu)
+
+
+class RowPlan:
+    """SELL-32 node->element incidence of one affine group, plus (for
+    matrices) the row-local column offsets of every incidence (rows.cu)."""
+
+    def __init__(self, conn_d: torch.Tensor, n: int):
+        nn = int(conn_d.shape[1])
+        nsl = -(-n // 32)
+        self.n, self.nn = n, nn
+        self.slice_ptr = torch.empty(nsl + 1, dtype=torch.int32, device=conn_d.device)
+        ncols = np.zeros(1, dtype=np.int64)
+        lib = _lib.load()
+        pn = ncols.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        args = (n, int(conn_d.shape[0]), nn, conn_d.data_ptr(), self.slice_ptr.data_ptr())
+        _lib.check(lib.fpb_incidence_build(*args, None, pn, _lib.stream()), "fpb_incidence_build")
+        self.ncols = int(ncols[0])
+        self.inc = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
+        _lib.check(lib.fpb_incidence_build(*args, self.inc.data_ptr(), pn, _lib.stream()),
+                   "fpb_incidence_build")
+        self.slots = None
+        self.rowcap = 0
+
+    def ensure_slots(self, conn_d: torch.Tensor, pattern: "CsrMatrix") -> None:
+        if self.slots is not None:
+            return
+        slots = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
+        cap = np.zeros(1, dtype=np.int32)
+        _lib.check(_lib.load().fpb_incidence_slots(
+            self.n, self.nn, self.ncols, self.slice_ptr.data_ptr(), self.inc.data_ptr(),
+            conn_d.data_ptr(), pattern.rowptr_d.data_ptr(), pattern.colind_d.data_ptr(),
+            slots.data_ptr(), cap.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _lib.stream()),
+            "fpb_incidence_slots")
+        self.slots, self.rowcap = slots, int(cap[0])
+
+
+class BlockPlan:
+    """Element blocks of one group for the deterministic two-phase RHS
+    assembly (blocks.cu): per-block distinct nodes + sorted gather slots,
+    and per-node lists of block partials."""
+
+    def __init__(self, conn_d: torch.Tensor, n: int):
+        lib = _lib.load()
+        ne, nn = int(conn_d.shape[0]), int(conn_d.shape[1])
+        be = int(lib.fpb_block_elems())
+        nblocks = -(-ne // be)
+        dev = conn_d.device
+        self.n, self.nelem = n, ne
+        self.blk_ptr = torch.empty(nblocks + 1, dtype=torch.int32, device=dev)
+        P = np.zeros(1, dtype=np.int64)
+        mx = np.zeros(1, dtype=np.int32)
+        pp = P.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        pm = mx.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+        s = _lib.stream()
+        _lib.check(lib.fpb_blocks_build(ne, nn, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(), None, None,
+                                        None, None, None, None, pp, pm, s), "fpb_blocks_build")
+        self.npartial, self.maxnu = int(P[0]), int(mx[0])
+        self.blk_nodes = torch.empty(max(self.npartial, 1), dtype=torch.int32, device=dev)
+        self.blk_gptr = torch.empty(self.npartial + nblocks + 1, dtype=torch.int16, device=dev)
+        self.blk_gslot = torch.empty(max(nblocks * be * nn, 1), dtype=torch.int16, device=dev)
+        self.blk_lidx = torch.empty(max(nblocks * be * nn, 4), dtype=torch.int16, device=dev)
+        self.node_pptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        self.node_plist = torch.empty(max(self.npartial, 1), dtype=torch.int32, device=dev)
+        _lib.check(lib.fpb_blocks_build(ne, nn, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(),
+                                        self.blk_nodes.data_ptr(), self.blk_gptr.data_ptr(),
+                                        self.blk_gslot.data_ptr(), self.blk_lidx.data_ptr(),
+                                        self.node_pptr.data_ptr(), self.node_plist.data_ptr(), pp, pm, s),
+                   "fpb_blocks_build")
+        self._partial: dict = {}
+
+    def partial(self, nv: int, dev) -> torch.Tensor:
+        buf = self._partial.get(nv)
+        if buf is None:
+            buf = self._partial[nv] = torch.empty(max(self.npartial, 1) * nv, dtype=torch.float64, device=dev)
+        return buf
+
+
 @dataclass
 class GroupData:
     """Per element-type device state (assembly.py:55-70)."""
@@ -88,6 +166,8 @@ class GroupData:
     packset: PackSet          # packs at the context's vector_size (parity view)
     lane_conn32: torch.Tensor  # kernel packs, 32 lanes
     pattern: CsrMatrix
+    rows: RowPlan | None = None
+    blocks: BlockPlan | None = None
     _pos32: torch.Tensor | None = None
     _cache: dict = field(default_factory=dict)
 
@@ -139,7 +219,15 @@ class AssemblyContext:
         self._checked = False
 
     @classmethod
-    def build(cls, mesh, vector_size: int = 8) -> "AssemblyContext":
+    def build(cls, mesh, vector_size: int = 8, scatter: str = "auto") -> "AssemblyContext":
+        """scatter selects the global-assembly strategy (scatter):
+        "auto"   — matrices of affine simplices (TRI03, TET04): row-owned
+                   kernels; RHS of every type: element blocks; matrices of
+                   PYR05/HEX08/QUAD04: element kernels + FP64 reductions;
+        "rows"   — row-owned kernels for every affine kind (RHS included);
+        "atomic" — element kernels + FP64 reductions for everything."""
+        if scatter not in ("auto", "rows", "atomic"):
+            raise ConfigurationError(f"scatter must be 'auto', 'rows' or 'atomic', got {scatter!r}")
         cfg = PackConfig(vector_size)  # validates like the reference
         mesh = as_device_mesh(mesh)
         if not mesh.is_grouped_by_type():
@@ -153,8 +241,13 @@ class AssemblyContext:
             ps = PackSet(g.etype, cfg.vector_size, g.nelem, offset, pack_lanes(g.conn_d, cfg.vector_size))
             lane32 = ps.lane_conn_d if cfg.vector_size == KERNEL_LANES else pack_lanes(g.conn_d, KERNEL_LANES)
             gd = GroupData(reference_element(g.etype), g.conn_d, offset, ps, lane32, pattern)
-            # ScatterPatternError surfaces at build time, as in the reference
-            _ = gd.pos32
+            if scatter == "auto":
+                gd.blocks = BlockPlan(g.conn_d, mesh.nnode)
+            if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED:
+                gd.rows = RowPlan(g.conn_d, mesh.nnode)
+                gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time
+            else:
+                _ = gd.pos32  # ScatterPatternError at build time, as in the reference
             groups.append(gd)
             offset += g.nelem
         return cls(mesh, pattern, groups, cfg.vector_size)
@@ -197,7 +290,7 @@ class AssemblyContext:
         if key not in self._geometry or self._geometry[key][1] is None:
             self.refresh_geometry(layout, need_grad=True)
         d, gr = self._geometry[key]
-        return d.cpu().numpy(), gr.cpu().numpy()
+        return to_host(d), to_host(gr)
 
     def _ensure_checked(self) -> None:
         if not self._checked:
@@ -209,46 +302,67 @@ class AssemblyContext:
         nnz = self.pattern.nnz
         dev = self.mesh.coords_d.device
         if not reuse:
-            return torch.zeros(nmat * nnz, dtype=torch.float64, device=dev)
+            return torch.empty(nmat * nnz, dtype=torch.float64, device=dev)
         key = (layout, nmat)
         buf = self._vals.get(key)
         if buf is None:
-            buf = self._vals[key] = torch.zeros(nmat * nnz, dtype=torch.float64, device=dev)
-        else:
-            buf.zero_()
-        return buf
+            buf = self._vals[key] = torch.empty(nmat * nnz, dtype=torch.float64, device=dev)
+        return buf  # overwritten by the next assembly
+
+    def _run(self, kind_id: int, vel, phi, rho: float, mu: float, kappa: float,
+             out: torch.Tensor) -> torch.Tensor:
+        """Overwrite `out` with one assembly over every group."""
+        self._ensure_checked()
+        matrix = kind_id in (0, 1, 2, GRADIENT_XYZ)
+        # owner-writes paths (row-owned matrices, element-block RHS) overwrite
+        # their output; anything else accumulates into a zeroed buffer
+        owner = [(g.rows is not None) if matrix else (g.blocks is not None or g.rows is not None)
+                 for g in self.groups]
+        single_rows = len(self.groups) == 1 and owner[0]
+        if not single_rows:
+            out.zero_()
+        nnz = self.pattern.nnz
+        coords = self.mesh.coords_d.data_ptr()
+        vp = vel.data_ptr() if vel is not None else None
+        pp = phi.data_ptr() if phi is not None else None
+        for g, own in zip(self.groups, owner):
+            if own and not matrix and g.blocks is not None:
+                bp = g.blocks
+                nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
+                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, coords, vp,
+                          pp, float(rho), float(mu), float(kappa), bp.blk_ptr.data_ptr(),
+                          bp.blk_nodes.data_ptr(), bp.blk_gptr.data_ptr(), bp.blk_gslot.data_ptr(),
+                          bp.blk_lidx.data_ptr(), bp.maxnu,
+                          bp.partial(nv, out.device).data_ptr(), self.mesh.nnode, bp.node_pptr.data_ptr(),
+                          bp.node_plist.data_ptr(), 0 if single_rows else 1, out.data_ptr(), _lib.stream())
+            elif own:
+                r = g.rows
+                _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
+                          r.inc.data_ptr(), r.slots.data_ptr() if matrix else None, g.conn_d.data_ptr(),
+                          coords, vp, pp, float(rho), float(mu), float(kappa),
+                          self.pattern.rowptr_d.data_ptr(), nnz, r.rowcap, 0 if single_rows else 1,
+                          out.data_ptr(), _lib.stream())
+            else:
+                _lib.call("fpb_assemble", kind_id, g.etype_id, g.nelem, g.lane_conn32.data_ptr(),
+                          coords, vp, pp, float(rho), float(mu), float(kappa),
+                          g.pos32.data_ptr() if matrix else None, nnz, out.data_ptr(), _lib.stream())
+        return out
 
     def assemble_matrix_d(self, kind: KernelKind, velocity_d: torch.Tensor | None,
                           out: torch.Tensor) -> torch.Tensor:
-        """Device fast path: accumulate `kind` into out[nnz] (caller zeroes it)."""
-        self._ensure_checked()
-        vel = velocity_d.data_ptr() if velocity_d is not None else None
-        for g in self.groups:
-            _lib.call("fpb_assemble", KIND_ID[kind], g.etype_id, g.nelem, g.lane_conn32.data_ptr(),
-                      self.mesh.coords_d.data_ptr(), vel, None, 1.0, 0.0, 0.0,
-                      g.pos32.data_ptr(), self.pattern.nnz, out.data_ptr(), _lib.stream())
-        return out
+        """Device fast path: overwrite out[nnz] with the global `kind` matrix values."""
+        vel = velocity_d if kind is KernelKind.CONVECTION else None
+        return self._run(KIND_ID[kind], vel, None, 1.0, 0.0, 0.0, out)
 
     def assemble_gradients_d(self, out: torch.Tensor) -> torch.Tensor:
-        """Fused continuity assembly: out[k*nnz:(k+1)*nnz] += B_k, k < dim,
+        """Fused continuity assembly: out[k*nnz:(k+1)*nnz] = B_k, k < dim,
         where B_k = CONVECTION with unit velocity e_k (timeloop.py:159-171)."""
-        self._ensure_checked()
-        for g in self.groups:
-            _lib.call("fpb_assemble", GRADIENT_XYZ, g.etype_id, g.nelem, g.lane_conn32.data_ptr(),
-                      self.mesh.coords_d.data_ptr(), None, None, 1.0, 0.0, 0.0,
-                      g.pos32.data_ptr(), self.pattern.nnz, out.data_ptr(), _lib.stream())
-        return out
+        return self._run(GRADIENT_XYZ, None, None, 1.0, 0.0, 0.0, out)
 
     def assemble_rhs_d(self, kind: KernelKind, velocity_d: torch.Tensor, scalar_d, rho: float,
                        mu: float, kappa: float, out: torch.Tensor) -> torch.Tensor:
-        """Device fast path: accumulate an RHS into out (caller zeroes it)."""
-        self._ensure_checked()
-        phi = scalar_d.data_ptr() if scalar_d is not None else None
-        for g in self.groups:
-            _lib.call("fpb_assemble", KIND_ID[kind], g.etype_id, g.nelem, g.lane_conn32.data_ptr(),
-                      self.mesh.coords_d.data_ptr(), velocity_d.data_ptr(), phi, float(rho),
-                      float(mu), float(kappa), None, 0, out.data_ptr(), _lib.stream())
-        return out
+        """Device fast path: overwrite out with the global RHS."""
+        return self._run(KIND_ID[kind], velocity_d, scalar_d, rho, mu, kappa, out)
 
     def assemble_matrix(self, kind: KernelKind, layout: str = "packed", velocity=None,
                         reuse: bool = False) -> CsrMatrix:
@@ -277,9 +391,9 @@ class AssemblyContext:
         vel = self._field(velocity, dim)
         phi = self._field(scalar, 1) if kind is KernelKind.SCALAR_RHS else None
         shape = (n, dim) if kind is KernelKind.MOMENTUM_RHS else (n,)
-        out = torch.zeros(shape, dtype=torch.float64, device=vel.device)
+        out = torch.empty(shape, dtype=torch.float64, device=vel.device)
         self.assemble_rhs_d(kind, vel, phi, rho, mu, kappa, out)
-        return out.cpu().numpy() if host else out
+        return to_host(out) if host else out
 
     def _field(self, x, width: int) -> torch.Tensor:
         t, _ = to_device(x)
@@ -322,7 +436,7 @@ def gradient_matrices(ctx: AssemblyContext, layout: str = "packed") -> list[CsrM
     (timeloop.py:159-171)."""
     _check_layout(layout)
     dim, nnz = ctx.mesh.dim, ctx.pattern.nnz
-    out = torch.zeros(dim * nnz, dtype=torch.float64, device=ctx.mesh.coords_d.device)
+    out = torch.empty(dim * nnz, dtype=torch.float64, device=ctx.mesh.coords_d.device)
     ctx.assemble_gradients_d(out)
     return [ctx.pattern.with_vals(out[k * nnz:(k + 1) * nnz]) for k in range(dim)]
 
@@ -330,7 +444,7 @@ def gradient_matrices(ctx: AssemblyContext, layout: str = "packed") -> list[CsrM
 def lumped_mass(ctx: AssemblyContext, layout: str = "packed") -> np.ndarray:
     """Row-sum lumped mass (timeloop.py:174-181)."""
     M = ctx.assemble_matrix(KernelKind.MASS, layout)
-    lumped = M.row_sums_d().cpu().numpy()
+    lumped = to_host(M.row_sums_d())
     if not (lumped > 0.0).all():
         raise ConfigurationError("lumped mass has non-positive entries")
     return lumped

@@ -1,0 +1,389 @@
+// Element-block RHS assembly: element-centric integration with a
+// deterministic, atomic-free two-level reduction.
+//
+// Elements are cut into blocks of kBlockElems consecutive elements (4 packs
+// of 32 lanes — consecutive elements of the reference's k-major cell order
+// share nodes heavily: ~0.72 distinct nodes per element inside a 128-element
+// block versus 4 node references per element).  128-element blocks with
+// 6 CTAs/SM measured fastest on B200 (profiles/r01_blocks_variants.txt).  One CTA per block:
+//   phase 1 (k_blk_rhs): every thread integrates one element in registers
+//     (closed form for affine simplices, the reference Gauss loop otherwise),
+//     parks its NN x NV contributions in shared memory, and after one barrier
+//     each distinct node of the block sums its contributions in ascending
+//     element order (pre-sorted gather list) into a per-(block, node) partial;
+//   phase 2 (k_blk_gather): one thread per mesh node sums its partials in
+//     ascending block order and writes the RHS entry once.
+// Each element is integrated exactly once, nothing is zero-filled, and the
+// summation order is fixed — the output is bitwise reproducible.
+//
+// Setup (k_blk_setup): a CTA radix-sorts its block's (node, slot) pairs with
+// CUB's BlockRadixSort (stable, so equal nodes keep ascending slot order),
+// giving the distinct node list, the per-node gather ranges and the gather
+// slots in one pass; the node -> partial lists for phase 2 are a counting
+// sort plus a per-node insertion sort.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <climits>
+
+#include "simplex.cuh"
+
+namespace fpb {
+
+#ifndef FPB_BLK_ELEMS
+#define FPB_BLK_ELEMS 128
+#endif
+#ifndef FPB_BLK_MINB
+#define FPB_BLK_MINB 6
+#endif
+constexpr int kBlockElems = FPB_BLK_ELEMS;
+
+// ---- setup -------------------------------------------------------------------
+template <int NN>
+__global__ void __launch_bounds__(kBlockElems)
+k_blk_setup(int64_t nelem, const int32_t* __restrict__ conn, int pass, int32_t* __restrict__ blk_count,
+            const int32_t* __restrict__ blk_ptr, int32_t* __restrict__ blk_nodes,
+            uint16_t* __restrict__ blk_gptr, uint16_t* __restrict__ blk_gslot,
+            uint16_t* __restrict__ blk_lidx) {
+  using Sort = cub::BlockRadixSort<int, kBlockElems, NN, unsigned short>;
+  using Scan = cub::BlockScan<int, kBlockElems>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ int sorted[kBlockElems * NN + 1];
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const int64_t e = b * kBlockElems + tid;
+  int keys[NN];
+  unsigned short vals[NN];
+#pragma unroll
+  for (int q = 0; q < NN; ++q) {
+    keys[q] = e < nelem ? conn[e * NN + q] : INT_MAX;
+    vals[q] = (unsigned short)(tid * NN + q);  // slot = local element * NN + local node
+  }
+  Sort(tmp.sort).Sort(keys, vals);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NN; ++q) sorted[tid * NN + q] = keys[q];
+  __syncthreads();
+  int head[NN], nhead = 0;
+#pragma unroll
+  for (int q = 0; q < NN; ++q) {
+    const int pos = tid * NN + q;
+    head[q] = keys[q] != INT_MAX && (pos == 0 || sorted[pos - 1] != keys[q]);
+    nhead += head[q];
+  }
+  int first, total;
+  Scan(tmp.scan).ExclusiveSum(nhead, first, total);
+  if (pass == 0) {
+    if (tid == 0) blk_count[b] = total;
+    return;
+  }
+  const int64_t base = blk_ptr[b];
+  uint16_t* gptr = blk_gptr + base + b;  // total + 1 entries
+  int u = first;
+#pragma unroll
+  for (int q = 0; q < NN; ++q) {
+    const int pos = tid * NN + q;
+    if (head[q]) {
+      blk_nodes[base + u] = keys[q];
+      gptr[u] = (uint16_t)pos;
+      ++u;
+    }
+    blk_gslot[b * kBlockElems * NN + pos] = vals[q];
+    // slot -> local node (u - 1 is the run this sorted item belongs to)
+    if (keys[q] != INT_MAX) blk_lidx[b * kBlockElems * NN + vals[q]] = (uint16_t)(u - 1);
+  }
+  // end of the last gather range = number of valid (node, slot) pairs
+  int64_t nvalid = nelem - b * kBlockElems;
+  if (nvalid > kBlockElems) nvalid = kBlockElems;
+  if (tid == 0) gptr[total] = (uint16_t)(nvalid * NN);
+}
+
+__global__ void k_max_count(int64_t m, const int32_t* cnt, int32_t* out) {
+  int best = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    best = max(best, cnt[i]);
+  best = __reduce_max_sync(0xffffffffu, best);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+__global__ void k_p2_count(int64_t P, const int32_t* blk_nodes, int32_t* cnt) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[blk_nodes[p]], 1);
+}
+
+__global__ void k_p2_fill(int64_t P, const int32_t* blk_nodes, const int32_t* ptr, int32_t* cursor,
+                          int32_t* list) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const int node = blk_nodes[p];
+    list[ptr[node] + atomicAdd(&cursor[node], 1)] = (int32_t)p;
+  }
+}
+
+__global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t* l = list + ptr[i];
+    const int len = ptr[i + 1] - ptr[i];
+    for (int x = 1; x < len; ++x) {
+      const int v = l[x];
+      int y = x - 1;
+      while (y >= 0 && l[y] > v) {
+        l[y + 1] = l[y];
+        --y;
+      }
+      l[y + 1] = v;
+    }
+  }
+}
+
+// ---- phase 1: stage nodes, integrate, in-block gather ---------------------------
+// Shared memory: [node data of the block's distinct nodes: maxnu x NDAT]
+// followed by [contributions: NN * NV x kBlockElems].
+template <int ET, int KIND>
+__global__ void __launch_bounds__(kBlockElems, FPB_BLK_MINB)
+k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ coords,
+          const double* __restrict__ vel, const double* __restrict__ phi, double rho, double mu,
+          double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
+          const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
+          double* __restrict__ partial) {
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+  constexpr int NV = Out<ET, KIND>::NV;
+  constexpr int NDAT = 2 * DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);  // x, u (, phi)
+  extern __shared__ double smem[];
+  double* snode = smem;                        // [maxnu][NDAT]
+  double* sm = smem + (int64_t)maxnu * NDAT;   // [NN * NV][kBlockElems]
+  const int tid = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  const int64_t base = blk_ptr[b];
+  const int nu = blk_ptr[b + 1] - (int)base;
+  // stage the block's distinct nodes (each node's data read from HBM once)
+  for (int u = tid; u < nu; u += kBlockElems) {
+    const int64_t node = __ldg(blk_nodes + base + u);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      snode[u * NDAT + d] = __ldg(coords + node * DIM + d);
+      snode[u * NDAT + DIM + d] = __ldg(vel + node * DIM + d);
+    }
+    if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = __ldg(phi + node);
+  }
+  const int64_t e = b * kBlockElems + tid;
+  int li[NN];
+  if (e < nelem) {
+    const uint16_t* lp = blk_lidx + e * NN;
+    if constexpr (NN == 4) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(lp));
+      li[0] = v.x & 0xffff; li[1] = v.x >> 16; li[2] = v.y & 0xffff; li[3] = v.y >> 16;
+    } else {
+#pragma unroll
+      for (int a = 0; a < NN; ++a) li[a] = __ldg(lp + a);
+    }
+  }
+  __syncthreads();
+  if (e < nelem) {
+    double xe[NN][DIM], ue[Out<ET, KIND>::NU][DIM], fe[Out<ET, KIND>::NF];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        xe[a][d] = snode[li[a] * NDAT + d];
+        ue[a][d] = snode[li[a] * NDAT + DIM + d];
+      }
+      if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = snode[li[a] * NDAT + 2 * DIM];
+    }
+    double acc[Out<ET, KIND>::NOUT];
+    if constexpr (Elem<ET>::AFFINE) {
+      simplex_rhs_all<ET, KIND>(xe, ue, fe, rho, mu, kappa, acc);
+    } else {
+      element_integrate<ET, KIND>(xe, ue, fe, rho, mu, kappa, 0, acc);
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int k = 0; k < NV; ++k) sm[(a * NV + k) * kBlockElems + tid] = acc[a * NV + k];
+  }
+  __syncthreads();
+  const uint16_t* gptr = blk_gptr + base + b;
+  const uint16_t* gslot = blk_gslot + b * kBlockElems * NN;
+  for (int u = tid; u < nu; u += kBlockElems) {
+    double s[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] = 0.0;
+    const int lo = gptr[u], hi = gptr[u + 1];
+    for (int q = lo; q < hi; ++q) {
+      const int slot = gslot[q];
+      const int el = slot / NN, a = slot - el * NN;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] += sm[(a * NV + k) * kBlockElems + el];
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) partial[(base + u) * NV + k] = s[k];
+  }
+}
+
+// ---- phase 2: per-node gather of block partials ---------------------------------
+template <int NV>
+__global__ void k_blk_gather(int32_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ list,
+                             const double* __restrict__ partial, int accumulate, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) s[k] = 0.0;
+    const int lo = __ldg(ptr + i), hi = __ldg(ptr + i + 1);
+    for (int q = lo; q < hi; ++q) {
+      const int64_t p = __ldg(list + q);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] += __ldg(partial + p * NV + k);
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[i * NV + k] = accumulate ? out[i * NV + k] + s[k] : s[k];
+  }
+}
+
+template <int ET, int KIND>
+static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* coords, const double* vel,
+                      const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+                      const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
+                      int maxnu, double* partial, cudaStream_t s) {
+  constexpr int NV = Out<ET, KIND>::NV;
+  constexpr int NDAT = 2 * Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);
+  const size_t smem = ((size_t)Elem<ET>::NN * NV * kBlockElems + (size_t)maxnu * NDAT) * sizeof(double);
+  FPB_REQUIRE(smem <= 227 * 1024, "element block needs %zu bytes of shared memory", smem);
+  if (smem > 48 * 1024)
+    FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
+  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockElems, smem, s>>>(nelem, lidx, coords, vel, phi, rho, mu, kappa,
+                                                                   blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
+                                                                   partial);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+template <int ET>
+static int blk_kind(int kind, int64_t nelem, const uint16_t* lidx, const double* coords, const double* vel,
+                    const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+                    const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot, int maxnu,
+                    double* partial, cudaStream_t s) {
+  if (kind == FPB_MOMENTUM_RHS)
+    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+                                            blk_gptr, blk_gslot, maxnu, partial, s);
+  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+                                        blk_gptr, blk_gslot, maxnu, partial, s);
+}
+
+}  // namespace fpb
+
+using namespace fpb;
+
+extern "C" {
+
+int fpb_block_elems(void) { return kBlockElems; }
+
+int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int32_t* blk_ptr,
+                     int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
+                     int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
+                     void* stream) {
+  FPB_REQUIRE(nn == 3 || nn == 4 || nn == 5 || nn == 8, "unsupported node count %d", nn);
+  FPB_REQUIRE(nelem >= 0 && n >= 0, "bad sizes");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  if (blk_nodes == nullptr) {  // pass 0: sizes
+    int32_t* cnt = nullptr;
+    FPB_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * (nblocks + 1), s));
+    FPB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nblocks + 1), s));
+    if (nblocks > 0) {
+      switch (nn) {
+        case 3: k_blk_setup<3><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 4: k_blk_setup<4><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 5: k_blk_setup<5><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+        case 8: k_blk_setup<8><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
+      }
+      FPB_LAUNCH_CHECK();
+    }
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, blk_ptr, nblocks + 1, s);
+    FPB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+    FPB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, blk_ptr, nblocks + 1, s));
+    int32_t P = 0;
+    FPB_CUDA(cudaMemcpyAsync(&P, blk_ptr + nblocks, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    int32_t* mx = nullptr;
+    FPB_CUDA(cudaMallocAsync(&mx, sizeof(int32_t), s));
+    FPB_CUDA(cudaMemsetAsync(mx, 0, sizeof(int32_t), s));
+    if (nblocks > 0) k_max_count<<<grid_for(nblocks, 256), 256, 0, s>>>(nblocks, cnt, mx);
+    int32_t mxh = 0;
+    FPB_CUDA(cudaMemcpyAsync(&mxh, mx, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FPB_CUDA(cudaFreeAsync(mx, s));
+    FPB_CUDA(cudaFreeAsync(tmp, s));
+    FPB_CUDA(cudaFreeAsync(cnt, s));
+    FPB_CUDA(cudaStreamSynchronize(s));
+    *npartial_h = P;
+    *maxnu_h = mxh;
+    return FPB_OK;
+  }
+  const int64_t P = *npartial_h;
+  if (nblocks > 0) {
+    switch (nn) {
+      case 3: k_blk_setup<3><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
+      case 4: k_blk_setup<4><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
+      case 5: k_blk_setup<5><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
+      case 8: k_blk_setup<8><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
+    }
+    FPB_LAUNCH_CHECK();
+  }
+  int32_t* cnt = nullptr;
+  FPB_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * (n + 1), s));
+  FPB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), s));
+  if (P > 0) k_p2_count<<<grid_for(P, 256), 256, 0, s>>>(P, blk_nodes, cnt);
+  FPB_LAUNCH_CHECK();
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, node_pptr, n + 1, s);
+  FPB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+  FPB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, node_pptr, n + 1, s));
+  FPB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), s));
+  if (P > 0) k_p2_fill<<<grid_for(P, 256), 256, 0, s>>>(P, blk_nodes, node_pptr, cnt, node_plist);
+  if (n > 0) k_p2_sort<<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist);
+  FPB_LAUNCH_CHECK();
+  FPB_CUDA(cudaFreeAsync(tmp, s));
+  FPB_CUDA(cudaFreeAsync(cnt, s));
+  return FPB_OK;
+}
+
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* coords, const double* vel,
+                        const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+                        const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
+                        const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
+                        const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,
+                        void* stream) {
+  FPB_REQUIRE(etype >= 0 && etype < 5 && g_ref_loaded[etype],
+              "reference tables for element type %d not uploaded", etype);
+  FPB_REQUIRE(kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS,
+              "element-block assembly covers the RHS kinds (got %d)", kind);
+  FPB_REQUIRE(vel != nullptr, "kind %d needs a velocity field", kind);
+  FPB_REQUIRE(kind != FPB_SCALAR_RHS || phi, "SCALAR_RHS needs a scalar field");
+  cudaStream_t s = as_stream(stream);
+  if (nelem > 0) {
+    int rc = FPB_OK;
+    switch (etype) {
+      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+    }
+    if (rc) return rc;
+  }
+  if (n > 0) {
+    if (kind == FPB_MOMENTUM_RHS && etype_dim(etype) == 3)
+      k_blk_gather<3><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+    else if (kind == FPB_MOMENTUM_RHS)
+      k_blk_gather<2><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+    else
+      k_blk_gather<1><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+    FPB_LAUNCH_CHECK();
+  }
+  return FPB_OK;
+}
+
+}  // extern "C"

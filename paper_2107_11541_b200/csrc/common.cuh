@@ -59,6 +59,11 @@ struct RefTables {
   double N[8 * 8];
   double dN[3 * 8 * 8];
   double w[8];
+  // derived once on the host from N and w (fpb_set_reference_element), used
+  // by the closed-form affine-simplex kernels (rows.cu):
+  double M[8 * 8];  // M[a][b] = sum_g w_g N_b(g) N_a(g)        (mass integrand / det)
+  double mN[8];     // mN[a]   = sum_g w_g (sum_c N_c(g)) N_a(g) (unit-velocity convection)
+  double W;         // sum_g w_g
 };
 extern __constant__ RefTables c_ref[5];
 extern bool g_ref_loaded[5];
@@ -70,6 +75,11 @@ template <int ET> __device__ __forceinline__ double refdN(int l, int a, int g) {
   return c_ref[ET].dN[(l * Elem<ET>::NN + a) * Elem<ET>::NG + g];
 }
 template <int ET> __device__ __forceinline__ double refW(int g) { return c_ref[ET].w[g]; }
+template <int ET> __device__ __forceinline__ double refM(int a, int b) {
+  return c_ref[ET].M[a * Elem<ET>::NN + b];
+}
+template <int ET> __device__ __forceinline__ double refmN(int a) { return c_ref[ET].mN[a]; }
+template <int ET> __device__ __forceinline__ double refWsum() { return c_ref[ET].W; }
 
 // ---- geometry -------------------------------------------------------------
 // J[d][l] = sum_a x[a][d] dN[l][a][g]; det; gradN[d][a] = sum_l Ji[l][d] dN[l][a][g]

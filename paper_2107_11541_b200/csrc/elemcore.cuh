@@ -1,0 +1,180 @@
+// Per-element Gauss-point integration shared by the element kernels
+// (assemble.cu: FP64-reduction scatter) and the element-block kernels
+// (blocks.cu: deterministic in-block gather).  Arithmetic follows the
+// reference packed kernels (_kernels.py:150-461) term by term.
+#pragma once
+#include "common.cuh"
+
+namespace fpb {
+
+constexpr int KIND_GRADIENT_K = 100;  // CONVECTION with unit e_k, one direction k
+
+template <int ET, int KIND>
+struct Out {
+  static constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+  static constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
+                              KIND == KIND_GRADIENT_K;
+  static constexpr bool GRADXYZ = KIND == FPB_GRADIENT_XYZ;
+  static constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS;
+  static constexpr int NU = NEED_VEL ? NN : 1;
+  static constexpr int NF = KIND == FPB_SCALAR_RHS ? NN : 1;
+  // values per node for RHS kinds
+  static constexpr int NV = KIND == FPB_MOMENTUM_RHS ? DIM : 1;
+  static constexpr int NOUT = MAT ? NN * NN : GRADXYZ ? DIM * NN * NN : KIND == FPB_MOMENTUM_RHS ? NN * DIM : NN;
+};
+
+// acc: matrices [i][j] (GRADIENT_XYZ: [k][i][j]); MOMENTUM [a][k]; SCALAR [a]
+template <int ET, int KIND>
+__device__ __forceinline__ void element_integrate(
+    const double (&xe)[Elem<ET>::NN][Elem<ET>::DIM], const double (&ue)[Out<ET, KIND>::NU][Elem<ET>::DIM],
+    const double (&fe)[Out<ET, KIND>::NF], double rho, double mu, double kappa, int kdir,
+    double (&acc)[Out<ET, KIND>::NOUT]) {
+  constexpr int NN = Elem<ET>::NN, NG = Elem<ET>::NG, DIM = Elem<ET>::DIM;
+  constexpr int NOUT = Out<ET, KIND>::NOUT;
+  constexpr bool NEED_GRAD = KIND != FPB_MASS;
+#pragma unroll
+  for (int q = 0; q < NOUT; ++q) acc[q] = 0.0;
+
+  double J[DIM][DIM], gN[DIM][NN], det = 0.0;
+  if constexpr (Elem<ET>::AFFINE) {
+    det = jacobian<ET>(xe, 0, J);
+    if constexpr (NEED_GRAD) grad_shape<ET>(J, det, 0, gN);
+  }
+
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    if constexpr (!Elem<ET>::AFFINE) {
+      det = jacobian<ET>(xe, g, J);
+      if constexpr (NEED_GRAD) grad_shape<ET>(J, det, g, gN);
+    }
+    const double w = det * refW<ET>(g);  // detJw
+
+    if constexpr (KIND == FPB_MASS) {  // _kernels.py:163-172
+#pragma unroll
+      for (int j = 0; j < NN; ++j)
+#pragma unroll
+        for (int i = 0; i < NN; ++i) acc[i * NN + j] += w * refN<ET>(j, g) * refN<ET>(i, g);
+    } else if constexpr (KIND == FPB_LAPLACIAN) {  // _kernels.py:191-207
+#pragma unroll
+      for (int j = 0; j < NN; ++j)
+#pragma unroll
+        for (int i = 0; i < NN; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) s += gN[d][i] * gN[d][j];
+          acc[i * NN + j] += w * s;
+        }
+    } else if constexpr (KIND == FPB_CONVECTION) {  // _kernels.py:238-266
+      double ug[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) s += ue[a][d] * refN<ET>(a, g);
+        ug[d] = s;
+      }
+#pragma unroll
+      for (int j = 0; j < NN; ++j) {
+        double adv = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) adv += ug[d] * gN[d][j];
+#pragma unroll
+        for (int i = 0; i < NN; ++i) acc[i * NN + j] += w * adv * refN<ET>(i, g);
+      }
+    } else if constexpr (KIND == KIND_GRADIENT_K || KIND == FPB_GRADIENT_XYZ) {
+      // CONVECTION with u = e_k at every node: u_g = (sum_a N_a) e_k
+      // (timeloop.py:159-171)
+      double sN = 0.0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) sN += refN<ET>(a, g);
+      if constexpr (KIND == KIND_GRADIENT_K) {
+#pragma unroll
+        for (int j = 0; j < NN; ++j) {
+          double gk = kdir == 0 ? gN[0][j] : (kdir == 1 ? gN[1][j] : gN[DIM - 1][j]);
+          double adv = sN * gk;
+#pragma unroll
+          for (int i = 0; i < NN; ++i) acc[i * NN + j] += w * adv * refN<ET>(i, g);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < DIM; ++k)
+#pragma unroll
+          for (int j = 0; j < NN; ++j) {
+            double adv = sN * gN[k][j];
+#pragma unroll
+            for (int i = 0; i < NN; ++i) acc[(k * NN + i) * NN + j] += w * adv * refN<ET>(i, g);
+          }
+      }
+    } else if constexpr (KIND == FPB_MOMENTUM_RHS) {  // _kernels.py:320-382
+      double ug[DIM], G[DIM][DIM], S[DIM][DIM], c[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) s += ue[a][d] * refN<ET>(a, g);
+        ug[d] = s;
+      }
+#pragma unroll
+      for (int l = 0; l < DIM; ++l)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < NN; ++a) s += ue[a][k] * gN[l][a];
+          G[l][k] = s;
+        }
+      double divu = 0.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) divu += G[d][d];
+#pragma unroll
+      for (int l = 0; l < DIM; ++l)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) S[l][k] = 0.5 * (G[l][k] + G[k][l]);
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        double us = 0.0, gk = 0.0;
+#pragma unroll
+        for (int l = 0; l < DIM; ++l) {
+          us += ug[l] * S[l][k];
+          gk += ug[l] * G[k][l];
+        }
+        c[k] = 2.0 * us + divu * ug[k] - gk;
+      }
+#pragma unroll
+      for (int i = 0; i < NN; ++i)
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+          double visc = 0.0;
+#pragma unroll
+          for (int l = 0; l < DIM; ++l) visc += S[k][l] * gN[l][i];
+          acc[i * DIM + k] -= w * (rho * refN<ET>(i, g) * c[k] + 2.0 * mu * visc);
+        }
+    } else if constexpr (KIND == FPB_SCALAR_RHS) {  // _kernels.py:420-461
+      double ug[DIM], gphi[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double au = 0.0, ap = 0.0;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          au += ue[a][d] * refN<ET>(a, g);
+          ap += fe[a] * gN[d][a];
+        }
+        ug[d] = au;
+        gphi[d] = ap;
+      }
+      double adv = 0.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) adv += ug[d] * gphi[d];
+#pragma unroll
+      for (int i = 0; i < NN; ++i) {
+        double diff = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) diff += gphi[d] * gN[d][i];
+        acc[i] -= w * (refN<ET>(i, g) * adv + kappa * diff);
+      }
+    }
+  }
+
+}
+
+}  // namespace fpb

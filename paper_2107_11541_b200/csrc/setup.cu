@@ -354,6 +354,23 @@ int fpb_set_reference_element(int etype, int nn, int ng, int dim, const double* 
   memcpy(t.N, N_h, sizeof(double) * nn * ng);
   memcpy(t.dN, dN_h, sizeof(double) * dim * nn * ng);
   memcpy(t.w, w_h, sizeof(double) * ng);
+  // derived tables, summed over Gauss points in the reference's order
+  for (int a = 0; a < nn; ++a) {
+    double m1 = 0.0;
+    for (int b = 0; b < nn; ++b) {
+      double acc = 0.0;
+      for (int g = 0; g < ng; ++g) acc += w_h[g] * N_h[b * ng + g] * N_h[a * ng + g];
+      t.M[a * nn + b] = acc;
+    }
+    for (int g = 0; g < ng; ++g) {
+      double sN = 0.0;
+      for (int c = 0; c < nn; ++c) sN += N_h[c * ng + g];
+      m1 += w_h[g] * (sN * N_h[a * ng + g]);
+    }
+    t.mN[a] = m1;
+  }
+  t.W = 0.0;
+  for (int g = 0; g < ng; ++g) t.W += w_h[g];
   FPB_CUDA(cudaMemcpyToSymbol(c_ref, &t, sizeof(t), sizeof(RefTables) * etype));
   g_ref_loaded[etype] = true;
   return FPB_OK;

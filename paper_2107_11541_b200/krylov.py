@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .errors import SolverBreakdownError
-from .sparse import CsrMatrix, axpy_d, dot_d, dot_work, spmv_d, to_device
+from .sparse import CsrMatrix, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
 
 S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 
@@ -57,7 +57,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
               x.data_ptr(), r.data_ptr(), p.data_ptr(), z.data_ptr(), d.data_ptr(), state.data_ptr(),
               hist_d.data_ptr(), float(tol), work.data_ptr(), s)
     st = state.cpu().numpy()
-    out = (lambda t: t.cpu().numpy()) if host else (lambda t: t)
+    out = to_host if host else (lambda t: t)
     if st[S_BNORM] == 0.0:
         return out(torch.zeros(n, dtype=torch.float64, device=dev)), SolverStats(0, True, [0.0], 0.0)
     history = [float(hist_d[0].item())]

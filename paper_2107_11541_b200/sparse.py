@@ -34,6 +34,16 @@ def to_device(x, dtype=torch.float64) -> tuple[torch.Tensor, bool]:
     return torch.from_numpy(arr).to(_lib.device()), True
 
 
+def to_host(t: torch.Tensor) -> np.ndarray:
+    """Device -> numpy through a pinned staging buffer (torch's caching host
+    allocator recycles it once the returned array is dropped), so D2H runs
+    at PCIe DMA speed instead of the pageable-copy path."""
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out.numpy()
+
+
 def _to_i32(x) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         if x.numel() and int(x.max()) > _INT32_MAX:
@@ -73,7 +83,7 @@ class CsrMatrix:
 
     @property
     def vals(self) -> np.ndarray:
-        return self.vals_d.cpu().numpy()
+        return to_host(self.vals_d)
 
     def copy(self) -> "CsrMatrix":
         return CsrMatrix(self.n, self.rowptr_d, self.colind_d, self.vals_d.clone(), self._host)
@@ -96,7 +106,7 @@ class CsrMatrix:
         return d
 
     def diagonal(self) -> np.ndarray:
-        return self.diagonal_d().cpu().numpy()
+        return to_host(self.diagonal_d())
 
     def row_sums_d(self) -> torch.Tensor:
         out = torch.empty(self.n, dtype=torch.float64, device=self.vals_d.device)
@@ -163,7 +173,7 @@ def spmv(A: CsrMatrix, x, parallel: bool = False):
     the device kernel is always parallel and deterministic."""
     xd, host = to_device(x)
     y = spmv_d(A, xd)
-    return y.cpu().numpy() if host else y
+    return to_host(y) if host else y
 
 
 def axpy_d(alpha: float, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None):
@@ -178,7 +188,7 @@ def axpy(alpha: float, x, y):
     xd, hx = to_device(x)
     yd, hy = to_device(y)
     o = axpy_d(alpha, xd, yd)
-    return o.cpu().numpy() if (hx or hy) else o
+    return to_host(o) if (hx or hy) else o
 
 
 def dot_d(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -17,13 +17,19 @@ TOL = 1e-12
 NAMES = ["tri_4x3", "quad_4x3", "tet_6", "pyr_6", "hex_8", "mixed_8", "mixed_3x2x2", "tet_c1"]
 
 
-@pytest.fixture(scope="module", params=NAMES)
+@pytest.fixture(scope="module", params=[(n, s) for n in NAMES for s in ("auto", "rows", "atomic")
+                                        if s == "auto" or n in ("tri_4x3", "tet_6", "tet_c1", "mixed_8")],
+                ids=lambda p: f"{p[0]}-{p[1]}")
 def case(request, cuda_ok):
+    """Every golden mesh through the default dispatch (row-owned kernels for
+    TRI03/TET04, element kernels + FP64 reductions otherwise), and the
+    simplex meshes once more through the element/atomic kernels."""
     import paper_2107_11541_b200 as P
     from gpu_cases import CASES
 
-    mesh = CASES[request.param]()
-    return request.param, P.AssemblyContext.build(mesh, vector_size=8), load_golden(request.param)
+    name, scatter = request.param
+    mesh = CASES[name]()
+    return name, P.AssemblyContext.build(mesh, vector_size=8, scatter=scatter), load_golden(name)
 
 
 def test_matrices_match_reference(case):
@@ -136,8 +142,9 @@ def test_missing_fields_raise(cuda_ok):
 
 
 def test_repeat_assembly_reproducible_to_rounding(cuda_ok):
-    """The reference packed path is bitwise repeatable (test_assembly.py:270-276);
-    FP64 reductions at L2 reorder additions, so repeats agree to rounding."""
+    """The reference packed path is bitwise repeatable (test_assembly.py:270-276).
+    Element kernels with FP64 reductions at L2 (PYR05/HEX08) reorder
+    additions, so their repeats agree to rounding."""
     import paper_2107_11541_b200 as P
 
     mesh = P.generate_mixed_mesh(2, 2, 2, fraction=0.5)
@@ -146,6 +153,50 @@ def test_repeat_assembly_reproducible_to_rounding(cuda_ok):
     a = ctx.assemble_matrix(P.KernelKind.CONVECTION, "packed", velocity=vel).vals
     b = ctx.assemble_matrix(P.KernelKind.CONVECTION, "packed", velocity=vel).vals
     assert O.rel_diff(a, b) < 1e-15
+
+
+@pytest.mark.parametrize("et", ["TET04", "TRI03"])
+def test_row_owned_assembly_is_bitwise_deterministic(cuda_ok, et):
+    """Row-owned kernels (TRI03/TET04) sum each row in a fixed element
+    order: repeated assemblies are byte-identical, as in the reference
+    (test_assembly.py:270-276, test_sparse.py:93-97)."""
+    import paper_2107_11541_b200 as P
+
+    dims = (9, 7, 5) if et == "TET04" else (9, 7)
+    mesh = P.generate_box_mesh(P.ElementType[et], *dims)
+    ctx = P.AssemblyContext.build(mesh, 8)
+    assert ctx.groups[0].rows is not None
+    vel, phi = O.smooth_fields(mesh.coords)
+    for kind, kw in ((P.KernelKind.CONVECTION, dict(velocity=vel)), (P.KernelKind.LAPLACIAN, {})):
+        a = ctx.assemble_matrix(kind, "packed", **kw).vals
+        b = ctx.assemble_matrix(kind, "packed", **kw).vals
+        assert a.tobytes() == b.tobytes()
+    r1 = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.2, 1e-2)
+    r2 = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.2, 1e-2)
+    assert r1.tobytes() == r2.tobytes()
+    g1 = [B.vals for B in P.gradient_matrices(ctx)]
+    g2 = [B.vals for B in P.gradient_matrices(ctx)]
+    assert all(x.tobytes() == y.tobytes() for x, y in zip(g1, g2))
+
+
+@pytest.mark.parametrize("strategy", ["auto", "rows"])
+def test_owner_kernels_match_atomic_kernels(cuda_ok, strategy):
+    """Independent device formulations agree to rounding on a 90k-tet mesh."""
+    import paper_2107_11541_b200 as P
+
+    mesh = P.generate_box_mesh(P.ElementType.TET04, 25, 24, 25)
+    rows = P.AssemblyContext.build(mesh, 8, scatter=strategy)
+    atom = P.AssemblyContext.build(mesh, 8, scatter="atomic")
+    vel, phi = O.smooth_fields(mesh.coords)
+    for kind in (P.KernelKind.MASS, P.KernelKind.LAPLACIAN, P.KernelKind.CONVECTION):
+        a = rows.assemble_matrix(kind, velocity=vel).vals
+        b = atom.assemble_matrix(kind, velocity=vel).vals
+        assert O.rel_diff(a, b) < 1e-13, kind
+    for kind, kw in ((P.KernelKind.MOMENTUM_RHS, dict(rho=1.1, mu=0.02)),
+                     (P.KernelKind.SCALAR_RHS, dict(scalar=phi, kappa=0.03))):
+        a = rows.assemble_rhs(kind, "packed", vel, **kw)
+        b = atom.assemble_rhs(kind, "packed", vel, **kw)
+        assert O.rel_diff(a, b) < 1e-13, kind
 
 
 def test_c2_momentum_and_continuity_vs_oracle(cuda_ok):
@@ -172,3 +223,21 @@ def test_c2_momentum_and_continuity_vs_oracle(cuda_ok):
     for B in grads:
         assert float(B.row_sums_d().abs().max()) < 1e-12 * float(B.vals_d.abs().max())
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name", ["mixed_8", "hex_8", "pyr_6"])
+def test_block_rhs_is_bitwise_deterministic(cuda_ok, name):
+    """Element-block RHS (every element type) reduces in a fixed order:
+    repeated assemblies are byte-identical."""
+    import paper_2107_11541_b200 as P
+    from gpu_cases import CASES
+
+    mesh = CASES[name]()
+    ctx = P.AssemblyContext.build(mesh, 8)
+    vel, phi = O.smooth_fields(mesh.coords)
+    r1 = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.2, 1e-2)
+    r2 = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.2, 1e-2)
+    assert r1.tobytes() == r2.tobytes()
+    s1 = ctx.assemble_rhs(P.KernelKind.SCALAR_RHS, "packed", vel, phi, kappa=0.3)
+    s2 = ctx.assemble_rhs(P.KernelKind.SCALAR_RHS, "packed", vel, phi, kappa=0.3)
+    assert s1.tobytes() == s2.tobytes()

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -q -x -m gpu -p no:cacheprovider -k "assembly" > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python tools/kbench.py --scatters auto > gpurun_out/kbench.json 2>&1; cat gpurun_out/kbench.json
+timeout 300 python tools/kbench.py --etype HEX08 --nx 60 --ny 60 --nz 60 --scatters auto > gpurun_out/kbench_hex.json 2>&1; cat gpurun_out/kbench_hex.json
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_blk_rhs -s 2 -c 1 -o gpurun_out/prof_blk2 python bench.py --steps 1 --warmup 3 --soak 0 --no-cpu-baseline --e2e-steps 0 > gpurun_out/ncu_blk.log 2>&1; tail -1 gpurun_out/ncu_blk.log
