@@ -67,6 +67,12 @@ int fpb_set_reference_element(int etype, int nn, int ng, int dim, const double* 
 int fpb_grid_coords(int dim, int nx, int ny, int nz, double lx, double ly, double lz,
                     double* coords, void* stream);
 
+/* Planes k0 .. k0+nplanes-1 of the (nx, ny, nz) grid (z-slab of a larger
+ * mesh for domain decomposition); coords[(nx+1)(ny+1) nplanes][3], values
+ * identical to the corresponding rows of fpb_grid_coords on the full grid. */
+int fpb_grid_coords_slab(int nx, int ny, int nz, int k0, int nplanes, double lx, double ly, double lz,
+                         double* coords, void* stream);
+
 /* Single-type box connectivity, cells k-major (mesh.py:227-289):
  * TET04 = 6 Kuhn tets/cell, HEX08 = 1/cell, QUAD04 = 1/cell, TRI03 = 2/cell.
  * conn[nelem][nn] int32. */

@@ -28,6 +28,7 @@ SIGNATURES = {
     "fpb_version": (_int, []),
     "fpb_set_reference_element": (_int, [_int, _int, _int, _int, _vp, _vp, _vp]),
     "fpb_grid_coords": (_int, [_int, _int, _int, _int, _dbl, _dbl, _dbl, _vp, _vp]),
+    "fpb_grid_coords_slab": (_int, [_int, _int, _int, _int, _int, _dbl, _dbl, _dbl, _vp, _vp]),
     "fpb_box_conn": (_int, [_int, _int, _int, _int, _vp, _vp]),
     "fpb_mixed_conn": (_int, [_int, _int, _int, _int, _vp, _vp, _vp, _vp]),
     "fpb_build_packs": (_int, [_i64, _int, _int, _vp, _vp, _vp]),

@@ -219,20 +219,27 @@ class AssemblyContext:
         self._checked = False
 
     @classmethod
-    def build(cls, mesh, vector_size: int = 8, scatter: str = "auto") -> "AssemblyContext":
+    def build(cls, mesh, vector_size: int = 8, scatter: str = "auto",
+              pattern: CsrMatrix | None = None) -> "AssemblyContext":
         """scatter selects the global-assembly strategy (scatter):
         "auto"   — matrices of affine simplices (TRI03, TET04): row-owned
                    kernels; RHS of every type: element blocks; matrices of
                    PYR05/HEX08/QUAD04: element kernels + FP64 reductions;
         "rows"   — row-owned kernels for every affine kind (RHS included);
-        "atomic" — element kernels + FP64 reductions for everything."""
+        "atomic" — element kernels + FP64 reductions for everything.
+        pattern: an externally built CSR graph that contains every element
+        node pair (e.g. a slab's graph including ghost elements,
+        distributed.py); default: the mesh's own node graph."""
         if scatter not in ("auto", "rows", "atomic"):
             raise ConfigurationError(f"scatter must be 'auto', 'rows' or 'atomic', got {scatter!r}")
         cfg = PackConfig(vector_size)  # validates like the reference
         mesh = as_device_mesh(mesh)
         if not mesh.is_grouped_by_type():
             raise ConfigurationError("mesh has repeated element-type blocks; renumber_by_type first")
-        pattern = build_node_pattern(mesh)
+        if pattern is None:
+            pattern = build_node_pattern(mesh)
+        elif pattern.n != mesh.nnode:
+            raise ConfigurationError("pattern size does not match the mesh node count")
         groups, offset = [], 0
         for g in mesh.groups:
             if not g.nelem:

@@ -38,14 +38,17 @@ __device__ __forceinline__ double lin(int i, int n, double L) {
   return (double)i * step + 0.0;
 }
 
-__global__ void k_grid3(int nx, int ny, int nz, double lx, double ly, double lz, double* coords) {
-  int64_t total = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+// nz: global cell count along z; planes k0 .. k0 + nplanes - 1 are generated
+// (slab of a larger grid, for z-slab domain decomposition)
+__global__ void k_grid3(int nx, int ny, int nz, int k0, int nplanes, double lx, double ly, double lz,
+                        double* coords) {
+  int64_t total = (int64_t)(nx + 1) * (ny + 1) * nplanes;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     int i = (int)(t % (nx + 1));
     int64_t r = t / (nx + 1);
     int j = (int)(r % (ny + 1));
-    int k = (int)(r / (ny + 1));
+    int k = (int)(r / (ny + 1)) + k0;
     coords[3 * t + 0] = lin(i, nx, lx);
     coords[3 * t + 1] = lin(j, ny, ly);
     coords[3 * t + 2] = lin(k, nz, lz);
@@ -385,8 +388,19 @@ int fpb_grid_coords(int dim, int nx, int ny, int nz, double lx, double ly, doubl
   } else {
     int64_t total = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
     FPB_REQUIRE(total < INT_MAX, "mesh too large for int32 node ids");
-    k_grid3<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(nx, ny, nz, lx, ly, lz, coords);
+    k_grid3<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(nx, ny, nz, 0, nz + 1, lx, ly, lz, coords);
   }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_grid_coords_slab(int nx, int ny, int nz, int k0, int nplanes, double lx, double ly, double lz,
+                         double* coords, void* stream) {
+  FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "cell counts must be at least 1");
+  FPB_REQUIRE(k0 >= 0 && nplanes >= 1 && k0 + nplanes <= nz + 1, "slab planes outside the grid");
+  int64_t total = (int64_t)(nx + 1) * (ny + 1) * nplanes;
+  FPB_REQUIRE(total < INT_MAX, "slab too large for int32 node ids");
+  k_grid3<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(nx, ny, nz, k0, nplanes, lx, ly, lz, coords);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
