@@ -52,6 +52,11 @@ typedef enum {
 
 const char* fpb_last_error(void);
 int fpb_version(void);
+/* Performance knobs with no effect on results (for measured design
+ * choices): "gradient_split" = 1 assembles the continuity
+ * matrices B_x, B_y, B_z with one row-owned pass each instead of one fused
+ * pass. */
+int fpb_set_tuning(const char* name, int value);
 
 /* Upload one reference element's tables (host pointers) to device constant
  * memory: N[nn][ng], dN[dim][nn][ng], w[ng] — the constant inputs of every
@@ -131,6 +136,11 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
                  double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
                  void* stream);
 
+/* 32-byte node records for 256-bit loads: rec[i] = (a[i][0..dim), 0.., extra[i]
+ * or 0); rec must be 32-byte aligned.  Coordinates are packed once per mesh,
+ * velocity (+ the transported scalar in the 4th slot) once per call. */
+int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* rec, void* stream);
+
 /* ---- row-owned assembly for affine simplices (TRI03, TET04) -------------
  * Each CSR row / node is owned by one thread that walks its incident
  * elements in ascending order and writes its outputs once: no atomics, no
@@ -144,18 +154,24 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
  * fpb_incidence_slots: for matrices, slots[32 * ncols] packs the 8-bit
  * offsets of each incident element's nodes inside the row's column list;
  * returns the longest row through rowcap_h (synchronous).
- * fpb_assemble_rows: out is overwritten (accumulate = 0) or added to
- * (accumulate = 1); layouts of out as in fpb_assemble. */
+ * fpb_incidence_nodes: incn[32 * ncols][4] = node ids of each entry's element
+ * (inline copy of conn, -1 padding) — the hot loop reads it instead of inc.
+ * fpb_assemble_rows: element nodes come from incn when non-NULL, else
+ * from inc + conn; node data come as 32-byte records (fpb_pack4):
+ * xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0, phi|0); out is
+ * overwritten (accumulate = 0) or added to (accumulate = 1); layouts of out
+ * as in fpb_assemble. */
 int fpb_incidence_build(int32_t n, int64_t nelem, int nn, const int32_t* conn, int32_t* slice_ptr,
                         int32_t* inc, int64_t* ncols_h, void* stream);
 int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_ptr,
                         const int32_t* inc, const int32_t* conn, const int32_t* rowptr,
                         const int32_t* colind, uint32_t* slots, int* rowcap_h, void* stream);
+int fpb_incidence_nodes(int64_t ncols, int nn, const int32_t* inc, const int32_t* conn, int32_t* incn,
+                        void* stream);
 int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
-                      const uint32_t* slots, const int32_t* conn, const double* coords,
-                      const double* vel, const double* phi, double rho, double mu, double kappa,
-                      const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate, double* out,
-                      void* stream);
+                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
+                      double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
+                      double* out, void* stream);
 
 /* ---- element-block RHS assembly (deterministic, atomic-free) ------------
  * Blocks of fpb_block_elems() consecutive elements; phase 1 integrates each
@@ -168,15 +184,16 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, 
  * blk_gslot and blk_lidx [nblocks * block_elems * nn], node_pptr[n+1],
  * node_plist[P].  Phase 1 stages each block's distinct nodes through shared
  * memory (blk_lidx = local node of every element slot).
- * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; partial[P * nv] is
- * scratch; out overwritten (accumulate = 0) or added to. */
+ * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; node records as for
+ * fpb_assemble_rows; partial[P * nv] is scratch; out overwritten
+ * (accumulate = 0) or added to. */
 int fpb_block_elems(void);
 int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int32_t* blk_ptr,
                      int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
                      int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
                      void* stream);
-int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* coords, const double* vel,
-                        const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
+                        double rho, double mu, double kappa, const int32_t* blk_ptr,
                         const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                         const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
                         const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,

@@ -26,6 +26,7 @@ _pi64, _pint = C.POINTER(C.c_int64), C.POINTER(C.c_int)
 SIGNATURES = {
     "fpb_last_error": (C.c_char_p, []),
     "fpb_version": (_int, []),
+    "fpb_set_tuning": (_int, [C.c_char_p, _int]),
     "fpb_set_reference_element": (_int, [_int, _int, _int, _int, _vp, _vp, _vp]),
     "fpb_grid_coords": (_int, [_int, _int, _int, _int, _dbl, _dbl, _dbl, _vp, _vp]),
     "fpb_grid_coords_slab": (_int, [_int, _int, _int, _int, _int, _dbl, _dbl, _dbl, _vp, _vp]),
@@ -38,11 +39,13 @@ SIGNATURES = {
     "fpb_assemble": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _i64, _vp, _vp]),
     "fpb_incidence_build": (_int, [_i32, _i64, _int, _vp, _vp, _vp, _pi64, _vp]),
     "fpb_incidence_slots": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
+    "fpb_pack4": (_int, [_i64, _int, _vp, _vp, _vp, _vp]),
+    "fpb_incidence_nodes": (_int, [_i64, _int, _vp, _vp, _vp, _vp]),
     "fpb_assemble_rows": (_int, [_int, _int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl,
                                  _vp, _i64, _int, _int, _vp, _vp]),
     "fpb_block_elems": (_int, []),
     "fpb_blocks_build": (_int, [_i64, _int, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
-    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
+    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
                                    _vp, _int, _vp, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),

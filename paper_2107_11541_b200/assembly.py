@@ -19,6 +19,7 @@ are built once per context on the device.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -99,6 +100,13 @@ class RowPlan:
         self.inc = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
         _lib.check(lib.fpb_incidence_build(*args, self.inc.data_ptr(), pn, _lib.stream()),
                    "fpb_incidence_build")
+        # inline node ids per entry (int4): one dependent load level less in
+        # the hot loop (profiles/r01_rows_variants.txt); FPB_ROWS_INLINE=0
+        # reads inc + conn instead
+        self.inline_nodes = os.environ.get("FPB_ROWS_INLINE", "1") == "1"
+        self.incn = torch.empty(max(self.ncols, 1) * 32 * 4, dtype=torch.int32, device=conn_d.device)
+        _lib.check(lib.fpb_incidence_nodes(self.ncols, nn, self.inc.data_ptr(), conn_d.data_ptr(),
+                                           self.incn.data_ptr(), _lib.stream()), "fpb_incidence_nodes")
         self.slots = None
         self.rowcap = 0
 
@@ -214,6 +222,11 @@ class AssemblyContext:
         self.pattern = pattern
         self.groups = groups
         self.vector_size = vector_size
+        # 32-byte node records for the owner-writes kernels (256-bit loads)
+        n = mesh.nnode
+        self.xyz4 = torch.empty((n, 4), dtype=torch.float64, device=mesh.coords_d.device)
+        _lib.call("fpb_pack4", n, mesh.dim, mesh.coords_d.data_ptr(), None, self.xyz4.data_ptr(), _lib.stream())
+        self._uvw4 = torch.empty((n, 4), dtype=torch.float64, device=mesh.coords_d.device)
         self._vals: dict = {}
         self._geometry: dict = {}
         self._checked = False
@@ -332,12 +345,17 @@ class AssemblyContext:
         coords = self.mesh.coords_d.data_ptr()
         vp = vel.data_ptr() if vel is not None else None
         pp = phi.data_ptr() if phi is not None else None
+        uvw4 = None
+        if vel is not None and any(owner):
+            _lib.call("fpb_pack4", self.mesh.nnode, self.mesh.dim, vp, pp, self._uvw4.data_ptr(), _lib.stream())
+            uvw4 = self._uvw4.data_ptr()
+        xyz4 = self.xyz4.data_ptr()
         for g, own in zip(self.groups, owner):
             if own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
-                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, coords, vp,
-                          pp, float(rho), float(mu), float(kappa), bp.blk_ptr.data_ptr(),
+                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, xyz4, uvw4,
+                          float(rho), float(mu), float(kappa), bp.blk_ptr.data_ptr(),
                           bp.blk_nodes.data_ptr(), bp.blk_gptr.data_ptr(), bp.blk_gslot.data_ptr(),
                           bp.blk_lidx.data_ptr(), bp.maxnu,
                           bp.partial(nv, out.device).data_ptr(), self.mesh.nnode, bp.node_pptr.data_ptr(),
@@ -345,8 +363,10 @@ class AssemblyContext:
             elif own:
                 r = g.rows
                 _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
-                          r.inc.data_ptr(), r.slots.data_ptr() if matrix else None, g.conn_d.data_ptr(),
-                          coords, vp, pp, float(rho), float(mu), float(kappa),
+                          r.inc.data_ptr(), g.conn_d.data_ptr(),
+                          r.incn.data_ptr() if r.inline_nodes else None,
+                          r.slots.data_ptr() if matrix else None, xyz4, uvw4,
+                          float(rho), float(mu), float(kappa),
                           self.pattern.rowptr_d.data_ptr(), nnz, r.rowcap, 0 if single_rows else 1,
                           out.data_ptr(), _lib.stream())
             else:

@@ -144,9 +144,8 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 // followed by [contributions: NN * NV x kBlockElems].
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kBlockElems, FPB_BLK_MINB)
-k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ coords,
-          const double* __restrict__ vel, const double* __restrict__ phi, double rho, double mu,
-          double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
+k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
+          const double* __restrict__ uvw4, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
           double* __restrict__ partial) {
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
@@ -159,15 +158,18 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   const int64_t b = blockIdx.x;
   const int64_t base = blk_ptr[b];
   const int nu = blk_ptr[b + 1] - (int)base;
-  // stage the block's distinct nodes (each node's data read from HBM once)
+  // stage the block's distinct nodes: two 256-bit loads per node record
   for (int u = tid; u < nu; u += kBlockElems) {
     const int64_t node = __ldg(blk_nodes + base + u);
+    double rx[4], ru[4];
+    ld256(xyz4 + 4 * node, rx);
+    ld256(uvw4 + 4 * node, ru);
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-      snode[u * NDAT + d] = __ldg(coords + node * DIM + d);
-      snode[u * NDAT + DIM + d] = __ldg(vel + node * DIM + d);
+      snode[u * NDAT + d] = rx[d];
+      snode[u * NDAT + DIM + d] = ru[d];
     }
-    if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = __ldg(phi + node);
+    if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = ru[3];
   }
   const int64_t e = b * kBlockElems + tid;
   int li[NN];
@@ -243,8 +245,8 @@ __global__ void k_blk_gather(int32_t n, const int32_t* __restrict__ ptr, const i
 }
 
 template <int ET, int KIND>
-static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* coords, const double* vel,
-                      const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+                      double rho, double mu, double kappa, const int32_t* blk_ptr,
                       const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                       int maxnu, double* partial, cudaStream_t s) {
   constexpr int NV = Out<ET, KIND>::NV;
@@ -254,7 +256,7 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* coords,
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
-  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockElems, smem, s>>>(nelem, lidx, coords, vel, phi, rho, mu, kappa,
+  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockElems, smem, s>>>(nelem, lidx, xyz4, uvw4, rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
   FPB_LAUNCH_CHECK();
@@ -262,14 +264,14 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* coords,
 }
 
 template <int ET>
-static int blk_kind(int kind, int64_t nelem, const uint16_t* lidx, const double* coords, const double* vel,
-                    const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+static int blk_kind(int kind, int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+                    double rho, double mu, double kappa, const int32_t* blk_ptr,
                     const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot, int maxnu,
                     double* partial, cudaStream_t s) {
   if (kind == FPB_MOMENTUM_RHS)
-    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes,
                                             blk_gptr, blk_gslot, maxnu, partial, s);
-  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes,
                                         blk_gptr, blk_gslot, maxnu, partial, s);
 }
 
@@ -350,8 +352,8 @@ int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int3
   return FPB_OK;
 }
 
-int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* coords, const double* vel,
-                        const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
+                        double rho, double mu, double kappa, const int32_t* blk_ptr,
                         const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                         const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
                         const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,
@@ -360,17 +362,16 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* coords
               "reference tables for element type %d not uploaded", etype);
   FPB_REQUIRE(kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS,
               "element-block assembly covers the RHS kinds (got %d)", kind);
-  FPB_REQUIRE(vel != nullptr, "kind %d needs a velocity field", kind);
-  FPB_REQUIRE(kind != FPB_SCALAR_RHS || phi, "SCALAR_RHS needs a scalar field");
+  FPB_REQUIRE(xyz4 != nullptr && uvw4 != nullptr, "kind %d needs node records", kind);
   cudaStream_t s = as_stream(stream);
   if (nelem > 0) {
     int rc = FPB_OK;
     switch (etype) {
-      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, coords, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
     }
     if (rc) return rc;
   }

@@ -140,6 +140,13 @@ __device__ __forceinline__ void grad_shape(const double (&J)[Elem<ET>::DIM][Elem
 }
 
 // ---- misc -------------------------------------------------------------------
+// one 256-bit read-only load (sm_100a: LDG.E.ENL2.256) of a 32-byte record
+__device__ __forceinline__ void ld256(const double* p, double (&r)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+}
+
 __device__ __forceinline__ void red_add(double* p, double v) { atomicAdd(p, v); }
 
 inline int grid_for(int64_t work, int block, int per_sm = 16) {

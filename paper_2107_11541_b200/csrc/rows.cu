@@ -30,23 +30,31 @@
 //   SCALAR      r_a = -det (ubar_a . gphi + kappa W gphi . gN_a)
 #include <cub/device/device_scan.cuh>
 
+#include <cstring>
+
 #include "simplex.cuh"
 
 namespace fpb {
 
 constexpr int kRowsBlock = 128;
+int g_tuning_gradient_split = 0;  // fpb_set_tuning("gradient_split", 0|1)
+#ifndef FPB_ROWS_LD256
+#define FPB_ROWS_LD256 1
+#endif
+
+constexpr int KIND_GRAD1 = 101;  // one gradient direction (kdir) per launch
 
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kRowsBlock)
-k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ inc,
-       const uint32_t* __restrict__ slots, const int32_t* __restrict__ conn,
-       const double* __restrict__ coords, const double* __restrict__ vel,
-       const double* __restrict__ phi, double rho, double mu, double kappa,
-       const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate,
+k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ incn,
+       const int32_t* __restrict__ inc, const int32_t* __restrict__ conn,
+       const uint32_t* __restrict__ slots, const double* __restrict__ xyz4,
+       const double* __restrict__ uvw4, double rho, double mu, double kappa,
+       const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate, int kdir,
        double* __restrict__ out) {
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
   constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
-                       KIND == FPB_GRADIENT_XYZ;
+                       KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? DIM : 1;
   constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS;
   constexpr int NACC = KIND == FPB_MOMENTUM_RHS ? DIM : 1;
@@ -70,65 +78,84 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
   const double W = refWsum<ET>();
 
-  // Software pipeline over the incidence list (depth 3): while element m is
-  // integrated, the node data of m+1, the connectivity of m+2 and the id of
-  // m+3 are in flight, so each trip waits on one load latency, not three.
-  auto ld_e = [&](int mm) -> int { return mm < m1 ? __ldg(inc + (int64_t)mm * 32 + lane) : -1; };
-  auto ld_c = [&](int e, int (&c)[NN]) {
-    if (e < 0) return;
-    if constexpr (NN == 4) {
-      const int4 c4 = __ldg(reinterpret_cast<const int4*>(conn) + e);
-      c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-    } else {
+  // Software pipeline over the incidence list: while element m is
+  // integrated, the node records of m+1 and the node ids of m+2 are in
+  // flight.  Incidences carry the element's node ids inline (int4 SELL
+  // entries), and node data are 32-byte records read with one 256-bit load
+  // (LDG.E.ENL2.256) each: xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0, phi).
+  auto ld_c = [&](int mm, int (&c)[4]) {
+    if (mm < m1) {
+      if (incn) {  // inline node ids (one dependent load level less)
+        const int4 c4 = __ldg(reinterpret_cast<const int4*>(incn) + (int64_t)mm * 32 + lane);
+        c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+        return;
+      }
+      const int e = __ldg(inc + (int64_t)mm * 32 + lane);
+      if (e < 0) {
+        c[0] = -1;
+      } else if constexpr (NN == 4) {
+        const int4 c4 = __ldg(reinterpret_cast<const int4*>(conn) + e);
+        c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
+      } else {
 #pragma unroll
-      for (int b = 0; b < NN; ++b) c[b] = __ldg(conn + (int64_t)e * NN + b);
+        for (int b = 0; b < NN; ++b) c[b] = __ldg(conn + (int64_t)e * NN + b);
+      }
+    } else {
+      c[0] = -1;
     }
   };
   constexpr int NU = NEED_VEL ? NN : 1;
   constexpr int NF = KIND == FPB_SCALAR_RHS ? NN : 1;
-  auto ld_x = [&](int e, const int (&c)[NN], double (&x)[NN][DIM], double (&u)[NU][DIM], double (&f)[NF]) {
-    if (e < 0) return;
+  auto ld_x = [&](const int (&c)[4], double (&x)[NN][DIM], double (&u)[NU][DIM], double (&f)[NF]) {
+    if (c[0] < 0) return;
 #pragma unroll
-    for (int b = 0; b < NN; ++b)
+    for (int b = 0; b < NN; ++b) {
+#if FPB_ROWS_LD256
+      double r[4];
+      ld256(xyz4 + 4 * (int64_t)c[b], r);
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) x[b][d] = __ldg(coords + (int64_t)c[b] * DIM + d);
+      for (int d = 0; d < DIM; ++d) x[b][d] = r[d];
+#else
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) x[b][d] = __ldg(xyz4 + 4 * (int64_t)c[b] + d);
+#endif
+    }
     if constexpr (NEED_VEL) {
 #pragma unroll
-      for (int b = 0; b < NN; ++b)
+      for (int b = 0; b < NN; ++b) {
+        double r[4];
+        ld256(uvw4 + 4 * (int64_t)c[b], r);
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) u[b][d] = __ldg(vel + (int64_t)c[b] * DIM + d);
-    }
-    if constexpr (KIND == FPB_SCALAR_RHS) {
-#pragma unroll
-      for (int b = 0; b < NN; ++b) f[b] = __ldg(phi + c[b]);
+        for (int d = 0; d < DIM; ++d) u[b][d] = r[d];
+        if constexpr (KIND == FPB_SCALAR_RHS) f[b] = r[3];
+      }
     }
   };
-  int eA = ld_e(m0), eB = ld_e(m0 + 1), eC = ld_e(m0 + 2);
-  int cA[NN] = {}, cB[NN] = {}, cC[NN] = {};
+  int cA[4], cB[4], cC[4];
   double xA[NN][DIM] = {}, xB[NN][DIM] = {}, uA[NU][DIM] = {}, uB[NU][DIM] = {}, fA[NF] = {}, fB[NF] = {};
-  ld_c(eA, cA);
-  ld_c(eB, cB);
-  ld_x(eA, cA, xA, uA, fA);
+  ld_c(m0, cA);
+  ld_c(m0 + 1, cB);
+  ld_x(cA, xA, uA, fA);
 
   for (int m = m0; m < m1; ++m) {
-    if (eA < 0) break;  // row lists are padded with -1 at the end
-    ld_x(eB, cB, xB, uB, fB);
-    ld_c(eC, cC);
-    const int eD = ld_e(m + 3);
-    const int e = eA;
-    (void)e;
+    if (cA[0] < 0) break;  // row lists are padded at the end
+    ld_x(cB, xB, uB, fB);
+    ld_c(m + 2, cC);
     int c[NN];
     double xe[NN][DIM], ue[NU][DIM], fe[NF];
 #pragma unroll
     for (int b = 0; b < NN; ++b) {
       c[b] = cA[b];
-      cA[b] = cB[b];
-      cB[b] = cC[b];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         xe[b][d] = xA[b][d];
         xA[b][d] = xB[b][d];
       }
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      cA[b] = cB[b];
+      cB[b] = cC[b];
     }
 #pragma unroll
     for (int b = 0; b < NU; ++b)
@@ -142,9 +169,6 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
       fe[b] = fA[b];
       fA[b] = fB[b];
     }
-    eA = eB;
-    eB = eC;
-    eC = eD;
     int a = 0;
 #pragma unroll
     for (int b = 1; b < NN; ++b) a = (c[b] == row) ? b : a;
@@ -201,15 +225,20 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
           for (int d = 0; d < DIM; ++d) s += ubar[d] * gN[d][b];
           val[0][b] = det * s;
         }
-      } else {  // GRADIENT_XYZ
+      } else {  // GRADIENT_XYZ / GRAD1
         double t[NN];
 #pragma unroll
         for (int b = 0; b < NN; ++b) t[b] = refmN<ET>(b);
         const double f = det * pick<NN>(t, a);
+        if constexpr (KIND == KIND_GRAD1) {
 #pragma unroll
-        for (int k = 0; k < NMAT; ++k)
+          for (int b = 0; b < NN; ++b) val[0][b] = f * (kdir == 0 ? gN[0][b] : (kdir == 1 ? gN[1][b] : gN[DIM - 1][b]));
+        } else {
 #pragma unroll
-          for (int b = 0; b < NN; ++b) val[k][b] = f * gN[k][b];
+          for (int k = 0; k < NMAT; ++k)
+#pragma unroll
+            for (int b = 0; b < NN; ++b) val[k][b] = f * gN[k][b];
+        }
       }
       const uint32_t sl = __ldg(slots + (int64_t)m * 32 + lane);
 #pragma unroll
@@ -364,6 +393,31 @@ __global__ void k_inc_slots(int32_t n, int nn, int64_t total, const int32_t* sli
   }
 }
 
+// inline node ids of every SELL entry (padding: -1)
+__global__ void k_inc_nodes(int64_t total, int nn, const int32_t* inc, const int32_t* conn, int4* incn) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int e = inc[t];
+    int4 v = make_int4(-1, -1, -1, -1);
+    if (e >= 0) {
+      const int32_t* c = conn + (int64_t)e * nn;
+      v.x = c[0]; v.y = c[1]; v.z = c[2];
+      v.w = nn > 3 ? c[3] : -1;
+    }
+    incn[t] = v;
+  }
+}
+
+// 32-byte node records: rec[i] = (a[i][0..dim), 0..., extra[i] | 0)
+__global__ void k_pack4(int64_t n, int dim, const double* a, const double* extra, double* rec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int d = 0; d < dim; ++d) r[d] = a[i * dim + d];
+    if (extra) r[3] = extra[i];
+    reinterpret_cast<double4*>(rec)[i] = make_double4(r[0], r[1], r[2], r[3]);
+  }
+}
+
 __global__ void k_max_rowlen(int32_t n, const int32_t* rowptr, int* out) {
   int best = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -374,32 +428,33 @@ __global__ void k_max_rowlen(int32_t n, const int32_t* rowptr, int* out) {
 }
 
 template <int ET, int KIND>
-static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* inc, const uint32_t* slots,
-                       const int32_t* conn, const double* coords, const double* vel, const double* phi,
-                       double rho, double mu, double kappa, const int32_t* rowptr, int64_t nnz,
-                       int rowcap, int accumulate, double* out, cudaStream_t s) {
+static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn, const int32_t* inc,
+                       const int32_t* conn, const uint32_t* slots,
+                       const double* xyz4, const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr, int64_t nnz,
+                       int rowcap, int accumulate, double* out, cudaStream_t s, int kdir = 0) {
   constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
-                       KIND == FPB_GRADIENT_XYZ;
+                       KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? Elem<ET>::DIM : 1;
   size_t smem = MAT ? (size_t)NMAT * rowcap * kRowsBlock * sizeof(double) : 0;
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = (n + kRowsBlock - 1) / kRowsBlock;
-  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, inc, slots, conn, coords, vel, phi,
-                                                    rho, mu, kappa, rowptr, nnz, rowcap, accumulate, out);
+  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, incn, inc, conn, slots, xyz4,
+                                                    uvw4, rho, mu, kappa,
+                                                    rowptr, nnz, rowcap, accumulate, kdir, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
 
 template <int ET>
-static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
-                     const uint32_t* slots, const int32_t* conn, const double* coords,
-                     const double* vel, const double* phi, double rho, double mu, double kappa,
+static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_t* incn,
+                     const int32_t* inc, const int32_t* conn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
+                     double kappa,
                      const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate, double* out,
                      cudaStream_t s) {
 #define FPB_ROWS_CASE(K)                                                                       \
   case K:                                                                                      \
-    return launch_rows<ET, K>(n, slice_ptr, inc, slots, conn, coords, vel, phi, rho, mu, kappa, \
+    return launch_rows<ET, K>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, \
                               rowptr, nnz, rowcap, accumulate, out, s);
   switch (kind) {
     FPB_ROWS_CASE(FPB_MASS)
@@ -407,7 +462,17 @@ static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_
     FPB_ROWS_CASE(FPB_CONVECTION)
     FPB_ROWS_CASE(FPB_MOMENTUM_RHS)
     FPB_ROWS_CASE(FPB_SCALAR_RHS)
-    FPB_ROWS_CASE(FPB_GRADIENT_XYZ)
+    case FPB_GRADIENT_XYZ:
+      if (g_tuning_gradient_split) {
+        for (int k = 0; k < Elem<ET>::DIM; ++k) {
+          int rc = launch_rows<ET, KIND_GRAD1>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa,
+                                               rowptr, nnz, rowcap, accumulate, out + k * nnz, s, k);
+          if (rc) return rc;
+        }
+        return FPB_OK;
+      }
+      return launch_rows<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa,
+                                               rowptr, nnz, rowcap, accumulate, out, s);
   }
 #undef FPB_ROWS_CASE
   set_error("unknown kernel kind %d", kind);
@@ -419,6 +484,15 @@ static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_
 using namespace fpb;
 
 extern "C" {
+
+int fpb_set_tuning(const char* name, int value) {
+  if (name && strcmp(name, "gradient_split") == 0) {
+    g_tuning_gradient_split = value;
+    return FPB_OK;
+  }
+  set_error("unknown tuning knob %s", name ? name : "(null)");
+  return FPB_ECONFIG;
+}
 
 int fpb_incidence_build(int32_t n, int64_t nelem, int nn, const int32_t* conn, int32_t* slice_ptr,
                         int32_t* inc, int64_t* ncols_h, void* stream) {
@@ -485,27 +559,45 @@ int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_p
   return FPB_OK;
 }
 
+int fpb_incidence_nodes(int64_t ncols, int nn, const int32_t* inc, const int32_t* conn, int32_t* incn,
+                        void* stream) {
+  FPB_REQUIRE(nn == 3 || nn == 4, "inline incidence records hold at most 4 nodes");
+  if (ncols <= 0) return FPB_OK;
+  k_inc_nodes<<<grid_for(ncols * 32, 256), 256, 0, as_stream(stream)>>>(ncols * 32, nn, inc, conn,
+                                                                        reinterpret_cast<int4*>(incn));
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* rec, void* stream) {
+  FPB_REQUIRE(dim >= 1 && dim <= 3, "pack4 holds at most 3 components plus one extra");
+  FPB_REQUIRE(((uintptr_t)rec & 31) == 0, "node records must be 32-byte aligned");
+  if (n <= 0) return FPB_OK;
+  k_pack4<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(n, dim, a, extra, rec);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
 int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
-                      const uint32_t* slots, const int32_t* conn, const double* coords,
-                      const double* vel, const double* phi, double rho, double mu, double kappa,
-                      const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate, double* out,
-                      void* stream) {
+                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
+                      double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
+                      double* out, void* stream) {
   FPB_REQUIRE(etype == FPB_TRI03 || etype == FPB_TET04,
               "row-owned assembly is for affine simplices (TRI03, TET04)");
   FPB_REQUIRE(g_ref_loaded[etype], "reference tables for element type %d not uploaded", etype);
   bool mat = kind == FPB_MASS || kind == FPB_LAPLACIAN || kind == FPB_CONVECTION || kind == FPB_GRADIENT_XYZ;
   FPB_REQUIRE(!mat || (slots && rowptr && rowcap > 0), "matrix kinds need slots, rowptr and rowcap");
-  FPB_REQUIRE(!(kind == FPB_CONVECTION || kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS) || vel,
+  FPB_REQUIRE(!(kind == FPB_CONVECTION || kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS) || uvw4,
               "kind %d needs a velocity field", kind);
-  FPB_REQUIRE(kind != FPB_SCALAR_RHS || phi, "SCALAR_RHS needs a scalar field");
   FPB_REQUIRE(rowcap <= 256, "row too long for row-owned assembly");
+  FPB_REQUIRE(incn || (inc && conn), "need inline node records or incidence + connectivity");
   if (n <= 0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   if (etype == FPB_TET04)
-    return rows_kind<FPB_TET04>(kind, n, slice_ptr, inc, slots, conn, coords, vel, phi, rho, mu, kappa,
-                                rowptr, nnz, rowcap, accumulate, out, s);
-  return rows_kind<FPB_TRI03>(kind, n, slice_ptr, inc, slots, conn, coords, vel, phi, rho, mu, kappa,
-                              rowptr, nnz, rowcap, accumulate, out, s);
+    return rows_kind<FPB_TET04>(kind, n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz,
+                                rowcap, accumulate, out, s);
+  return rows_kind<FPB_TRI03>(kind, n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,
+                              accumulate, out, s);
 }
 
 }  // extern "C"

@@ -37,7 +37,12 @@ def main():
     ap.add_argument("--etype", default="TET04")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--scatters", default="auto,rows,atomic")
+    ap.add_argument("--tune", default="", help="name=value[,name=value] passed to fpb_set_tuning")
     args = ap.parse_args()
+    from paper_2107_11541_b200 import _lib
+    for kv in filter(None, args.tune.split(",")):
+        name, val = kv.split("=")
+        _lib.check(_lib.load().fpb_set_tuning(name.encode(), int(val)))
     et = P.ElementType[args.etype]
     mesh = P.generate_box_mesh(et, args.nx, args.ny, args.nz)
     n, ne = mesh.nnode, mesh.nelem
