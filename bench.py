@@ -154,6 +154,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--scatter", default="auto", choices=["auto", "rows", "atomic"],
                     help="global-assembly strategy (AssemblyContext.build)")
+    ap.add_argument("--no-solver", action="store_true", help="skip the solver vector-kernel block")
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds under load before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -290,6 +291,15 @@ def main():
                "d2h_bytes_per_step": int(r.nbytes + sum(v.nbytes for v in vals)),
                "api": "AssemblyContext.assemble_rhs(MOMENTUM_RHS, numpy) + gradient_matrices(ctx) + .vals"}
 
+    solver = None
+    if rank == 0 and not args.no_solver:
+        # config 3 companions: SpMV on the MASS matrix, axpy / dot on vectors
+        # larger than L2 (C5's node count), Jacobi-PCG on the pinned LAPLACIAN
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from solver_bench import solver_metrics
+
+        solver = solver_metrics(ctx, 16_974_593, hbm=hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -312,6 +322,7 @@ def main():
             "gpu_launches": args.steps * 2 * len(ctx.groups),
             "clocks": clk,
             "e2e": e2e,
+            "solver": solver,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

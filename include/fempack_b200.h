@@ -223,8 +223,9 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
  * every scalar kept on the device.  state[] (device, 8 doubles) carries
  * {rz, bnorm, tol, status, iterations, relres, pq, spare}; status 0 =
  * running, 1 = converged, 2 = breakdown (pq <= 0).  hist[] receives relres
- * per completed iteration at hist[iterations - hist_first]
- * (fpb_pcg_init writes hist[0]).  Once status != 0 the
+ * per completed iteration at hist[iterations % hist_cap] (fpb_pcg_init
+ * writes hist[0]); launch arguments are the same for every batch, so a
+ * batch can be captured once in a CUDA graph and replayed.  Once status != 0 the
  * remaining iterations are no-ops, so batches can be launched without a host
  * round trip per iteration.  vectors: x, r, p, q, z and the Jacobi diagonal d
  * (z = r / d, krylov.py:65,84), all of length n. */
@@ -234,7 +235,7 @@ int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const 
                  double* work, void* stream);
 int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind,
                     const double* vals, double* x, double* r, double* p, double* q, double* z,
-                    const double* d, double* state, double* hist, int64_t hist_first, int iters,
+                    const double* d, double* state, double* hist, int64_t hist_cap, int iters,
                     double* work, void* stream);
 
 #ifdef __cplusplus

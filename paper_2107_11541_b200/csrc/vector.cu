@@ -84,7 +84,12 @@ __device__ __forceinline__ bool grid_finish(double (&v)[NV], double* work, int s
 // ---------------------------------------------------------------------------
 // CSR SpMV, G lanes per row (G = 4/8/16 picked from the mean row length).
 // ---------------------------------------------------------------------------
-template <int G>
+// G lanes per row; each lane owns entries lo+sub, lo+sub+G, ...  The first
+// ITEMS of them are loaded together (all index/value loads issued before the
+// dependent x gathers) — rows up to G*ITEMS entries (tet ~15, hex ~27) take
+// one round trip; longer rows continue in a remainder loop.  Each lane sums
+// its entries in ascending order, then a fixed xor-tree: deterministic.
+template <int G, int ITEMS = 2>
 __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
                                           const int32_t* __restrict__ colind,
                                           const double* __restrict__ vals,
@@ -93,7 +98,18 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
   double acc = 0.0;
   if (valid) {
     const int lo = __ldg(rowptr + row), hi = __ldg(rowptr + row + 1);
-    for (int k = lo + sub; k < hi; k += G) acc += __ldcs(vals + k) * __ldg(x + __ldcs(colind + k));
+    int col[ITEMS];
+    double v[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int k = lo + sub + it * G;
+      col[it] = k < hi ? __ldcs(colind + k) : -1;
+      v[it] = k < hi ? __ldcs(vals + k) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it)
+      if (col[it] >= 0) acc += v[it] * __ldg(x + col[it]);
+    for (int k = lo + sub + ITEMS * G; k < hi; k += G) acc += __ldcs(vals + k) * __ldg(x + __ldcs(colind + k));
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
@@ -266,7 +282,7 @@ __global__ void __launch_bounds__(kDotThreads)
 k_pcg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
              const double* __restrict__ p, const double* __restrict__ q,
              const double* __restrict__ d, double* __restrict__ z, double* state, double* hist,
-             int64_t hist_first, double* work) {
+             int64_t hist_cap, double* work) {
   if (state[S_STATUS] != 0.0) return;
   const double alpha = state[S_RZ] / state[S_PQ];
   double v[2] = {0.0, 0.0};
@@ -288,7 +304,7 @@ k_pcg_update(int64_t n, double* __restrict__ x, double* __restrict__ r,
     const double it = state[S_IT] + 1.0;
     state[S_IT] = it;
     state[S_RELRES] = relres;
-    hist[(int64_t)it - hist_first] = relres;
+    hist[(int64_t)it % hist_cap] = relres;
     if (relres <= state[S_TOL]) {
       state[S_STATUS] = 1.0;
     } else {
@@ -382,12 +398,12 @@ int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const 
 
 int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
                     double* x, double* r, double* p, double* q, double* z, const double* d,
-                    double* state, double* hist, int64_t hist_first, int iters, double* work,
+                    double* state, double* hist, int64_t hist_cap, int iters, double* work,
                     void* stream) {
   cudaStream_t s = as_stream(stream);
   for (int it = 0; it < iters; ++it) {
     k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
-    k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_first, work);
+    k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_cap, work);
     k_pcg_direction<<<grid_for(n, 256, 8), 256, 0, s>>>(n, p, z, state);
   }
   FPB_LAUNCH_CHECK();

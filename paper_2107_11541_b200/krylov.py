@@ -32,7 +32,7 @@ class SolverStats:
 
 
 def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None = None,
-              jacobi: bool = True, batch: int = 32):
+              jacobi: bool = True, batch: int = 32, graph: bool = True):
     """Solve A x = b; returns (x, SolverStats).  numpy b -> numpy x."""
     bd, host = to_device(b)
     n = A.n
@@ -49,7 +49,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     x, r, p, q, z = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(5))
     state = torch.zeros(8, dtype=torch.float64, device=dev)
     cap = max(1, min(batch, max_iter))
-    hist_d = torch.zeros(cap + 1, dtype=torch.float64, device=dev)
+    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)  # hist[it % cap]
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
@@ -63,22 +63,34 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     history = [float(hist_d[0].item())]
     if st[S_STATUS] == 1.0:
         return out(x), SolverStats(0, True, history, history[0])
-    done, step = 0, 4
+    args = (n, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
+            d.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
+    cuda_graph = None
+    done = 0
     while done < max_iter:
-        k = min(step, cap, max_iter - done)
-        _lib.call("fpb_pcg_iterate", n, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(),
-                  q.data_ptr(), z.data_ptr(), d.data_ptr(), state.data_ptr(), hist_d.data_ptr(),
-                  done + 1, k, work.data_ptr(), s)
+        k = min(cap, max_iter - done)
+        if graph and k == cap and done > 0:
+            # every full batch launches identical arguments: capture it once
+            # and replay (3 kernels x cap iterations, no per-launch overhead)
+            if cuda_graph is None:
+                cuda_graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(cuda_graph, stream=side):
+                    _lib.call("fpb_pcg_iterate", *args, k, work.data_ptr(), _lib.stream())
+            cuda_graph.replay()
+        else:
+            _lib.call("fpb_pcg_iterate", *args, k, work.data_ptr(), s)
         st = state.cpu().numpy()
         it = int(st[S_IT])
         if it > done:
-            history.extend(float(v) for v in hist_d[: it - done].cpu().numpy())
+            h = hist_d.cpu().numpy()
+            history.extend(float(h[i % cap]) for i in range(done + 1, it + 1))
         done = it
         if st[S_STATUS] == 2.0:
             raise SolverBreakdownError(f"non-positive curvature p^T A p = {st[S_PQ]:.6e}")
         if st[S_STATUS] == 1.0:
             break
-        step = min(step * 2, cap)
     converged = bool(st[S_STATUS] == 1.0)
     res = axpy_d(-1.0, spmv_d(A, x), bd)
     bnorm = float(st[S_BNORM])
