@@ -151,27 +151,32 @@ int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* 
  * fpb_incidence_build: slice_ptr[ceil(n/32)+1]; with inc == NULL only sizes
  * (returns the column count through ncols_h, synchronous); otherwise also
  * fills inc[32 * ncols].
- * fpb_incidence_slots: for matrices, slots[32 * ncols] packs the 8-bit
- * offsets of each incident element's nodes inside the row's column list;
- * returns the longest row through rowcap_h (synchronous).
- * fpb_incidence_nodes: incn[32 * ncols][4] = node ids of each entry's element
- * (inline copy of conn, -1 padding) — the hot loop reads it instead of inc.
- * fpb_assemble_rows: element nodes come from incn when non-NULL, else
- * from inc + conn; node data come as 32-byte records (fpb_pack4):
- * xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0, phi|0); out is
- * overwritten (accumulate = 0) or added to (accumulate = 1); layouts of out
+ * fpb_incidence_nodes: incn[32 * ncols][4] = node ids of each entry's element,
+ * rotated by an even permutation so the row's own node is first (XOR with
+ * its local index for tets, rotation for triangles; orientation and det
+ * are unchanged), -1 padding.  The hot loop reads these instead of inc.
+ * fpb_incidence_slots: for matrices, slots[32 * ncols] packs one byte per
+ * node of the rotated record: byte 0 = offset of the diagonal in the row's
+ * column list, bytes 1.. = offsets with the diagonal skipped (the kernel
+ * keeps the diagonal in registers); returns the longest row through
+ * rowcap_h (synchronous).
+ * fpb_assemble_rows: element nodes come from incn (required; inc and conn
+ * are accepted for ABI stability and unused); node data come as 32-byte
+ * records (fpb_pack4): xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0,
+ * phi|0); out is overwritten (accumulate = 0) or added to (accumulate = 1);
+ * layouts of out
  * as in fpb_assemble. */
 int fpb_incidence_build(int32_t n, int64_t nelem, int nn, const int32_t* conn, int32_t* slice_ptr,
                         int32_t* inc, int64_t* ncols_h, void* stream);
 int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_ptr,
                         const int32_t* inc, const int32_t* conn, const int32_t* rowptr,
                         const int32_t* colind, uint32_t* slots, int* rowcap_h, void* stream);
-int fpb_incidence_nodes(int64_t ncols, int nn, const int32_t* inc, const int32_t* conn, int32_t* incn,
-                        void* stream);
+int fpb_incidence_nodes(int32_t n, int64_t ncols, int nn, const int32_t* slice_ptr, const int32_t* inc,
+                        const int32_t* conn, int32_t* incn, void* stream);
 int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
-                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
-                      double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
-                      double* out, void* stream);
+                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4,
+                      const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
+                      const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream);
 
 /* ---- element-block RHS assembly (deterministic, atomic-free) ------------
  * Blocks of fpb_block_elems() consecutive elements; phase 1 integrates each

@@ -100,13 +100,13 @@ class RowPlan:
         self.inc = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
         _lib.check(lib.fpb_incidence_build(*args, self.inc.data_ptr(), pn, _lib.stream()),
                    "fpb_incidence_build")
-        # inline node ids per entry (int4): one dependent load level less in
-        # the hot loop (profiles/r01_rows_variants.txt); FPB_ROWS_INLINE=0
-        # reads inc + conn instead
-        self.inline_nodes = os.environ.get("FPB_ROWS_INLINE", "1") == "1"
+        # inline node ids per entry (int4), rotated so the row's node is
+        # local node 0: one dependent load level less in the hot loop
+        # (profiles/r01_rows_variants.txt) and no per-element node search
         self.incn = torch.empty(max(self.ncols, 1) * 32 * 4, dtype=torch.int32, device=conn_d.device)
-        _lib.check(lib.fpb_incidence_nodes(self.ncols, nn, self.inc.data_ptr(), conn_d.data_ptr(),
-                                           self.incn.data_ptr(), _lib.stream()), "fpb_incidence_nodes")
+        _lib.check(lib.fpb_incidence_nodes(n, self.ncols, nn, self.slice_ptr.data_ptr(), self.inc.data_ptr(),
+                                           conn_d.data_ptr(), self.incn.data_ptr(), _lib.stream()),
+                   "fpb_incidence_nodes")
         self.slots = None
         self.rowcap = 0
 
@@ -364,10 +364,11 @@ class AssemblyContext:
                 r = g.rows
                 _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
                           r.inc.data_ptr(), g.conn_d.data_ptr(),
-                          r.incn.data_ptr() if r.inline_nodes else None,
+                          r.incn.data_ptr(),
                           r.slots.data_ptr() if matrix else None, xyz4, uvw4,
                           float(rho), float(mu), float(kappa),
-                          self.pattern.rowptr_d.data_ptr(), nnz, r.rowcap, 0 if single_rows else 1,
+                          self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
+                          0 if single_rows else 1,
                           out.data_ptr(), _lib.stream())
             else:
                 _lib.call("fpb_assemble", kind_id, g.etype_id, g.nelem, g.lane_conn32.data_ptr(),

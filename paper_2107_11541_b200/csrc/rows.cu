@@ -37,7 +37,12 @@
 namespace fpb {
 
 constexpr int kRowsBlock = 128;
+#ifndef FPB_ROWS_MINB
+#define FPB_ROWS_MINB 4  // matrix kinds: CTAs per SM the register budget is sized for
+#endif
+constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
 int g_tuning_gradient_split = 0;  // fpb_set_tuning("gradient_split", 0|1)
+int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
 #ifndef FPB_ROWS_LD256
 #define FPB_ROWS_LD256 1
 #endif
@@ -45,9 +50,8 @@ int g_tuning_gradient_split = 0;  // fpb_set_tuning("gradient_split", 0|1)
 constexpr int KIND_GRAD1 = 101;  // one gradient direction (kdir) per launch
 
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kRowsBlock)
-k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ incn,
-       const int32_t* __restrict__ inc, const int32_t* __restrict__ conn,
+__global__ void __launch_bounds__(kRowsBlock, (KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS) ? 1 : (KIND == FPB_CONVECTION ? 4 : FPB_ROWS_MINB))
+k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict__ incn,
        const uint32_t* __restrict__ slots, const double* __restrict__ xyz4,
        const double* __restrict__ uvw4, double rho, double mu, double kappa,
        const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate, int kdir,
@@ -57,164 +61,148 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
                        KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? DIM : 1;
   constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS;
-  constexpr int NACC = KIND == FPB_MOMENTUM_RHS ? DIM : 1;
-  extern __shared__ double sacc[];  // [NMAT][rowcap][kRowsBlock] (matrix kinds)
+  constexpr int NACC = KIND == FPB_MOMENTUM_RHS ? DIM : (MAT ? NMAT : 1);
+  // MASS / CONVECTION / GRADIENT are linear in det*gN: adjugate form, no
+  // reciprocal (gN then holds det*gN and det_s is 1)
+  constexpr bool ADJ = KIND == FPB_MASS || KIND == FPB_CONVECTION || KIND == FPB_GRADIENT_XYZ ||
+                       KIND == KIND_GRAD1;
+  // off-diagonal accumulators [NMAT][rowcap-1][kRowsBlock]; the diagonal
+  // entry (local node 0 of every record) lives in registers
+  extern __shared__ double sacc[];
 
   const int tid = threadIdx.x;
   const int row = blockIdx.x * kRowsBlock + tid;
-  if (row >= n) return;  // no block-wide synchronisation below
+  // matrix kinds keep every lane alive for the warp-cooperative write-out;
+  // rows past n get an empty incidence range
+  if (!MAT && row >= n) return;
+  const bool live = row < n;
   const int lane = row & 31;
-  const int m0 = __ldg(slice_ptr + (row >> 5)), m1 = __ldg(slice_ptr + (row >> 5) + 1);
+  const int m0 = live ? __ldg(slice_ptr + (row >> 5)) : 0;
+  const int m1 = live ? __ldg(slice_ptr + (row >> 5) + 1) : 0;
 
   int rlo = 0, rlen = 0;
   if constexpr (MAT) {
-    rlo = __ldg(rowptr + row);
-    rlen = __ldg(rowptr + row + 1) - rlo;
-    for (int k = 0; k < NMAT; ++k)
-      for (int r = 0; r < rlen; ++r) sacc[(k * rowcap + r) * kRowsBlock + tid] = 0.0;
+    if (live) {
+      rlo = __ldg(rowptr + row);
+      rlen = __ldg(rowptr + row + 1) - rlo;
+    }
+    for (int r = 0; r + 1 < rlen; ++r)
+#pragma unroll
+      for (int k = 0; k < NMAT; ++k) sacc[(r * NMAT + k) * kRowsBlock + tid] = 0.0;
   }
   double acc[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
   const double W = refWsum<ET>();
 
-  // Software pipeline over the incidence list: while element m is
-  // integrated, the node records of m+1 and the node ids of m+2 are in
-  // flight.  Incidences carry the element's node ids inline (int4 SELL
-  // entries), and node data are 32-byte records read with one 256-bit load
-  // (LDG.E.ENL2.256) each: xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0, phi).
-  auto ld_c = [&](int mm, int (&c)[4]) {
-    if (mm < m1) {
-      if (incn) {  // inline node ids (one dependent load level less)
-        const int4 c4 = __ldg(reinterpret_cast<const int4*>(incn) + (int64_t)mm * 32 + lane);
-        c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-        return;
-      }
-      const int e = __ldg(inc + (int64_t)mm * 32 + lane);
-      if (e < 0) {
-        c[0] = -1;
-      } else if constexpr (NN == 4) {
-        const int4 c4 = __ldg(reinterpret_cast<const int4*>(conn) + e);
-        c[0] = c4.x; c[1] = c4.y; c[2] = c4.z; c[3] = c4.w;
-      } else {
-#pragma unroll
-        for (int b = 0; b < NN; ++b) c[b] = __ldg(conn + (int64_t)e * NN + b);
-      }
-    } else {
-      c[0] = -1;
-    }
-  };
+  // Records are rotated at setup (fpb_incidence_nodes) so the row's own node
+  // is local node 0 (even permutation: orientation and det unchanged); its
+  // data are loaded once per row.  Node data are 32-byte records read with
+  // one 256-bit load each: xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0, phi).
+  //
+  // Software pipeline without register rotation: two buffer sets alternate
+  // roles (the loop body is unrolled by two), so a load's destination is not
+  // read until its consumer step.  Step m integrates set m&1 while the
+  // nodes of m+1 (other set) and the ids / slot bytes of m+2 (this set,
+  // after use) are in flight.
   constexpr int NU = NEED_VEL ? NN : 1;
   constexpr int NF = KIND == FPB_SCALAR_RHS ? NN : 1;
-  auto ld_x = [&](const int (&c)[4], double (&x)[NN][DIM], double (&u)[NU][DIM], double (&f)[NF]) {
-    if (c[0] < 0) return;
-#pragma unroll
-    for (int b = 0; b < NN; ++b) {
-#if FPB_ROWS_LD256
-      double r[4];
-      ld256(xyz4 + 4 * (int64_t)c[b], r);
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) x[b][d] = r[d];
-#else
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) x[b][d] = __ldg(xyz4 + 4 * (int64_t)c[b] + d);
-#endif
-    }
-    if constexpr (NEED_VEL) {
-#pragma unroll
-      for (int b = 0; b < NN; ++b) {
-        double r[4];
-        ld256(uvw4 + 4 * (int64_t)c[b], r);
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) u[b][d] = r[d];
-        if constexpr (KIND == FPB_SCALAR_RHS) f[b] = r[3];
-      }
+  struct Stage {
+    int c[4];
+    uint32_t sl;
+    double x[NN][DIM], u[NU][DIM], f[NF];
+  };
+  auto ld_c = [&](int mm, Stage& S) {
+    if (mm < m1) {
+      if constexpr (MAT) S.sl = __ldg(slots + (int64_t)mm * 32 + lane);
+      const int4 c4 = __ldg(incn + (int64_t)mm * 32 + lane);
+      S.c[0] = c4.x; S.c[1] = c4.y; S.c[2] = c4.z; S.c[3] = c4.w;
+    } else {
+      S.c[0] = -1;
     }
   };
-  int cA[4], cB[4], cC[4];
-  double xA[NN][DIM] = {}, xB[NN][DIM] = {}, uA[NU][DIM] = {}, uB[NU][DIM] = {}, fA[NF] = {}, fB[NF] = {};
-  ld_c(m0, cA);
-  ld_c(m0 + 1, cB);
-  ld_x(cA, xA, uA, fA);
+  auto ld_node = [&](int node, double (&x)[DIM], double (&u)[DIM], double& f) {
+    double r[4];
+    ld256(xyz4 + 4 * (int64_t)node, r);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x[d] = r[d];
+    if constexpr (NEED_VEL) {
+      ld256(uvw4 + 4 * (int64_t)node, r);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) u[d] = r[d];
+      f = r[3];
+    }
+  };
+  auto ld_x = [&](Stage& S) {
+    if (S.c[0] < 0) return;
+#pragma unroll
+    for (int b = 1; b < NN; ++b) {
+      double fu = 0.0;
+      ld_node(S.c[b], S.x[b], S.u[NEED_VEL ? b : 0], fu);
+      if constexpr (KIND == FPB_SCALAR_RHS) S.f[b] = fu;
+    }
+  };
+  // row node (local node 0 of every record)
+  double x0[DIM] = {}, u0[DIM] = {}, f0 = 0.0;
+  if (live) ld_node(row, x0, u0, f0);
 
-  for (int m = m0; m < m1; ++m) {
-    if (cA[0] < 0) break;  // row lists are padded at the end
-    ld_x(cB, xB, uB, fB);
-    ld_c(m + 2, cC);
-    int c[NN];
+  // row 0 of the reference tables (local node 0 is the row node)
+  double M0[NN];
+#pragma unroll
+  for (int b = 0; b < NN; ++b) M0[b] = refM<ET>(0, b);
+  const double mN0 = refmN<ET>(0);
+
+  auto step = [&](Stage& S) {
+    const uint32_t sl = S.sl;
     double xe[NN][DIM], ue[NU][DIM], fe[NF];
 #pragma unroll
-    for (int b = 0; b < NN; ++b) {
-      c[b] = cA[b];
+    for (int d = 0; d < DIM; ++d) xe[0][d] = x0[d];
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        xe[b][d] = xA[b][d];
-        xA[b][d] = xB[b][d];
-      }
+    for (int b = 1; b < NN; ++b)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) xe[b][d] = S.x[b][d];
+    if constexpr (NEED_VEL) {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) ue[0][d] = u0[d];
+#pragma unroll
+      for (int b = 1; b < NN; ++b)
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) ue[b][d] = S.u[b][d];
     }
+    if constexpr (KIND == FPB_SCALAR_RHS) {
+      fe[0] = f0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      cA[b] = cB[b];
-      cB[b] = cC[b];
+      for (int b = 1; b < NN; ++b) fe[b] = S.f[b];
     }
-#pragma unroll
-    for (int b = 0; b < NU; ++b)
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        ue[b][d] = uA[b][d];
-        uA[b][d] = uB[b][d];
-      }
-#pragma unroll
-    for (int b = 0; b < NF; ++b) {
-      fe[b] = fA[b];
-      fA[b] = fB[b];
-    }
-    int a = 0;
-#pragma unroll
-    for (int b = 1; b < NN; ++b) a = (c[b] == row) ? b : a;
+    (void)fe;
+    (void)ue;
     double gN[DIM][NN];
-    const double det = simplex_geometry<ET>(xe, gN);
+    const double det = ADJ ? simplex_adj<ET>(xe, gN) : simplex_geometry<ET>(xe, gN);
+    const double det_s = ADJ ? 1.0 : det;
 
-    // row a of the element mass table, M[a][0..NN)
-    double Ma[NN];
-#pragma unroll
-    for (int b = 0; b < NN; ++b) {
-      double t[NN];
-#pragma unroll
-      for (int q = 0; q < NN; ++q) t[q] = refM<ET>(q, b);
-      Ma[b] = pick<NN>(t, a);
-    }
     double ubar[DIM];
     if constexpr (NEED_VEL) {
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         double s = 0.0;
 #pragma unroll
-        for (int b = 0; b < NN; ++b) s += Ma[b] * ue[b][d];
+        for (int b = 0; b < NN; ++b) s += M0[b] * ue[b][d];
         ubar[d] = s;
       }
-    }
-    double gNa[DIM];
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      double t[NN];
-#pragma unroll
-      for (int b = 0; b < NN; ++b) t[b] = gN[d][b];
-      gNa[d] = pick<NN>(t, a);
     }
 
     if constexpr (MAT) {
       double val[NMAT][NN];
       if constexpr (KIND == FPB_MASS) {
 #pragma unroll
-        for (int b = 0; b < NN; ++b) val[0][b] = det * Ma[b];
+        for (int b = 0; b < NN; ++b) val[0][b] = det * M0[b];
       } else if constexpr (KIND == FPB_LAPLACIAN) {
         const double dw = det * W;
 #pragma unroll
         for (int b = 0; b < NN; ++b) {
           double s = 0.0;
 #pragma unroll
-          for (int d = 0; d < DIM; ++d) s += gNa[d] * gN[d][b];
+          for (int d = 0; d < DIM; ++d) s += gN[d][0] * gN[d][b];
           val[0][b] = dw * s;
         }
       } else if constexpr (KIND == FPB_CONVECTION) {
@@ -223,13 +211,10 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
           double s = 0.0;
 #pragma unroll
           for (int d = 0; d < DIM; ++d) s += ubar[d] * gN[d][b];
-          val[0][b] = det * s;
+          val[0][b] = det_s * s;
         }
       } else {  // GRADIENT_XYZ / GRAD1
-        double t[NN];
-#pragma unroll
-        for (int b = 0; b < NN; ++b) t[b] = refmN<ET>(b);
-        const double f = det * pick<NN>(t, a);
+        const double f = det_s * mN0;
         if constexpr (KIND == KIND_GRAD1) {
 #pragma unroll
           for (int b = 0; b < NN; ++b) val[0][b] = f * (kdir == 0 ? gN[0][b] : (kdir == 1 ? gN[1][b] : gN[DIM - 1][b]));
@@ -240,13 +225,24 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
             for (int b = 0; b < NN; ++b) val[k][b] = f * gN[k][b];
         }
       }
-      const uint32_t sl = __ldg(slots + (int64_t)m * 32 + lane);
 #pragma unroll
-      for (int b = 0; b < NN; ++b) {
-        const int s = (sl >> (8 * b)) & 0xff;
+      for (int k = 0; k < NMAT; ++k) acc[k] += val[k][0];
+      // off-diagonal columns are distinct, so all loads are issued before the
+      // stores (the compiler cannot prove the slots differ and would
+      // otherwise serialise the read-modify-writes)
+      double* p[NN];
+      double old[NN][NMAT];
 #pragma unroll
-        for (int k = 0; k < NMAT; ++k) sacc[(k * rowcap + s) * kRowsBlock + tid] += val[k][b];
+      for (int b = 1; b < NN; ++b) {
+        const int s = (sl >> (8 * b)) & 0xff;  // off-diagonal index (diagonal skipped)
+        p[b] = sacc + s * (NMAT * kRowsBlock) + tid;
+#pragma unroll
+        for (int k = 0; k < NMAT; ++k) old[b][k] = p[b][k * kRowsBlock];
       }
+#pragma unroll
+      for (int b = 1; b < NN; ++b)
+#pragma unroll
+        for (int k = 0; k < NMAT; ++k) p[b][k * kRowsBlock] = old[b][k] + val[k][b];
     } else if constexpr (KIND == FPB_MOMENTUM_RHS) {
       double G[DIM][DIM];  // G[l][k] = d u_k / d x_l
 #pragma unroll
@@ -270,7 +266,7 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
           const double S_lk = 0.5 * (G[l][k] + G[k][l]);
           const double Mc = 2.0 * S_lk + (l == k ? divu : 0.0) - G[k][l];
           conv += ubar[l] * Mc;
-          visc += S_lk * gNa[l];
+          visc += S_lk * gN[l][0];
         }
         acc[k] -= drho * conv + dw2mu * visc;
       }
@@ -287,26 +283,329 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restri
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         adv += ubar[d] * gphi[d];
-        diff += gphi[d] * gNa[d];
+        diff += gphi[d] * gN[d][0];
       }
       acc[0] -= det * adv + kappa * det * W * diff;
     }
+  };
+
+  Stage SA, SB;
+  SA.sl = SB.sl = 0;
+  ld_c(m0, SA);
+  ld_c(m0 + 1, SB);
+  ld_x(SA);
+  int dslot = rlen - 1;  // diagonal position in the row (slot byte 0)
+  if constexpr (MAT) {
+    if (m0 < m1 && SA.c[0] >= 0) dslot = SA.sl & 0xff;
+  }
+  for (int m = m0; m < m1; m += 2) {
+    if (SA.c[0] < 0) break;  // row lists are padded at the end
+    ld_x(SB);
+    step(SA);
+    ld_c(m + 2, SA);
+    if (SB.c[0] < 0) break;
+    ld_x(SA);
+    step(SB);
+    ld_c(m + 3, SB);
   }
 
   if constexpr (MAT) {
+    // Warp-cooperative, coalesced write-out: the warp's 32 consecutive rows
+    // are one contiguous CSR range [base, base + span).  Each lane marks its
+    // row's positions with its lane id in a per-warp byte map, then lane l
+    // writes positions base + l, base + l + 32, ... taking the value from
+    // the owner's accumulators (shared memory) or diagonal (shuffle).
+    __shared__ uint8_t owner_map[kRowsBlock / 32][kOwnerSpan];
+    uint8_t* om = owner_map[tid >> 5];
+    const int wlane = tid & 31;
+    const int base = __shfl_sync(0xffffffffu, rlo, 0);
+    int wend = live ? rlo + rlen : 0;
 #pragma unroll
-    for (int k = 0; k < NMAT; ++k) {
-      double* o = out + k * nnz + rlo;
-      for (int r = 0; r < rlen; ++r) {
-        const double v = sacc[(k * rowcap + r) * kRowsBlock + tid];
-        o[r] = accumulate ? o[r] + v : v;
+    for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+    const int span = wend - base;
+    const int dpos = rlo + dslot;
+    for (int c0 = 0; c0 < span; c0 += kOwnerSpan) {
+      const int c1 = min(span, c0 + kOwnerSpan);
+      for (int q = max(rlo - base, c0); q < min(rlo - base + rlen, c1); ++q) om[q - c0] = (uint8_t)wlane;
+      __syncwarp();
+      for (int q = c0 + wlane; q < c0 + ((c1 - c0 + 31) & ~31); q += 32) {
+        const bool ok = q < c1;
+        const int own = ok ? om[q - c0] : wlane;
+        const int own_rlo = __shfl_sync(0xffffffffu, rlo, own);
+        const int own_d = __shfl_sync(0xffffffffu, dpos, own);
+        const int pos = base + q;
+        const int r = pos - own_rlo;
+        const int sidx = max(0, min(r - (pos > own_d), rowcap - 2));
+        const double* src = sacc + sidx * (NMAT * kRowsBlock) + (tid & ~31) + own;
+#pragma unroll
+        for (int k = 0; k < NMAT; ++k) {
+          const double dg = __shfl_sync(0xffffffffu, acc[k], own);
+          if (ok) {
+            const double v = pos == own_d ? dg : src[k * kRowsBlock];
+            double* o = out + k * nnz + pos;
+            *o = accumulate ? *o + v : v;
+          }
+        }
       }
+      __syncwarp();
     }
   } else {
 #pragma unroll
     for (int q = 0; q < NACC; ++q) {
       double* o = out + (int64_t)row * NACC + q;
       *o = accumulate ? *o + acc[q] : acc[q];
+    }
+  }
+}
+
+// ---- neighbour-staged row kernel (matrix kinds) --------------------------------
+// The row's column list IS the set of nodes its incident elements touch, so
+// each thread first stages its neighbours' records in shared memory (one
+// gather per distinct neighbour instead of one per (element, node)), then
+// walks its incidences reading nothing from global memory but the 32-bit
+// slot word: byte b (b = 1..NN-1) is the off-diagonal index s of rotated
+// record node b, which addresses both the staged neighbour record and the
+// accumulator of column s.  Shared memory per thread, per off-diagonal
+// slot: DIM coordinates (+ DIM velocities for CONVECTION) + NMAT sums, laid
+// out [s][field][thread] so every access is conflict-free.
+constexpr int kNbBlock = 64;
+
+template <int ET, int KIND>
+struct NbLayout {
+  static constexpr int DIM = Elem<ET>::DIM;
+  static constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? DIM : 1;
+  static constexpr int NV = KIND == FPB_CONVECTION ? DIM : 0;
+  static constexpr int FIELDS = DIM + NV + NMAT;  // doubles per (slot, thread)
+  static constexpr int OX = 0, OU = DIM, OA = DIM + NV;
+};
+
+template <int ET, int KIND>
+__global__ void __launch_bounds__(kNbBlock)
+k_rows_nb(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
+          const double* __restrict__ xyz4, const double* __restrict__ uvw4,
+          const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz, int rowcap,
+          int accumulate, double* __restrict__ out) {
+  using L = NbLayout<ET, KIND>;
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM, NMAT = L::NMAT, F = L::FIELDS;
+  constexpr bool VEL = L::NV > 0;
+  constexpr int SS = F * kNbBlock;  // doubles per off-diagonal slot
+  extern __shared__ double sm[];
+
+  const int tid = threadIdx.x;
+  const int row = blockIdx.x * kNbBlock + tid;
+  const bool live = row < n;
+  const int lane = row & 31;
+  const int m0 = live ? __ldg(slice_ptr + (row >> 5)) : 0;
+  const int m1 = live ? __ldg(slice_ptr + (row >> 5) + 1) : 0;
+  int rlo = 0, rlen = 0;
+  if (live) {
+    rlo = __ldg(rowptr + row);
+    rlen = __ldg(rowptr + row + 1) - rlo;
+  }
+  double* const my = sm + tid;
+
+  // ---- stage the neighbours (and find the diagonal) ----
+  // batches of kStage columns: all gathers of a batch are in flight before
+  // the first shared-memory store
+  constexpr int kStage = 8;
+  double x0[DIM] = {}, u0[DIM] = {};
+  int dslot = rlen - 1;
+  {
+    int s = 0;
+    for (int r0 = 0; r0 < rlen; r0 += kStage) {
+      int col[kStage];
+      double rx[kStage][4], ru[kStage][4];
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) col[j] = r0 + j < rlen ? __ldg(colind + rlo + r0 + j) : -1;
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) {
+        if (col[j] >= 0) {
+          ld256(xyz4 + 4 * (int64_t)col[j], rx[j]);
+          if constexpr (VEL) ld256(uvw4 + 4 * (int64_t)col[j], ru[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) {
+        if (col[j] < 0) continue;
+        if (col[j] == row) {
+          dslot = r0 + j;
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            x0[d] = rx[j][d];
+            if constexpr (VEL) u0[d] = ru[j][d];
+          }
+          continue;
+        }
+        double* q = my + s * SS;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) q[(L::OX + d) * kNbBlock] = rx[j][d];
+        if constexpr (VEL) {
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) q[(L::OU + d) * kNbBlock] = ru[j][d];
+        }
+#pragma unroll
+        for (int k = 0; k < NMAT; ++k) q[(L::OA + k) * kNbBlock] = 0.0;
+        ++s;
+      }
+    }
+  }
+  (void)u0;
+
+  double M0[NN];
+#pragma unroll
+  for (int b = 0; b < NN; ++b) M0[b] = refM<ET>(0, b);
+  const double mN0 = refmN<ET>(0);
+  const double W = refWsum<ET>();
+  double dacc[NMAT];
+#pragma unroll
+  for (int k = 0; k < NMAT; ++k) dacc[k] = 0.0;
+
+  // ---- walk the incidences: slot words only (prefetched two ahead) ----
+  struct Nodes {
+    double x[NN][DIM];
+    double u[NN][DIM];
+    int s[NN];
+  };
+  auto ld_nodes = [&](uint32_t w, Nodes& Q) {
+#pragma unroll
+    for (int b = 1; b < NN; ++b) {
+      const int s = (w >> (8 * b)) & 0xff;
+      Q.s[b] = s;
+      const double* q = my + s * SS;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) Q.x[b][d] = q[(L::OX + d) * kNbBlock];
+      if constexpr (VEL) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) Q.u[b][d] = q[(L::OU + d) * kNbBlock];
+      }
+    }
+  };
+  auto step = [&](Nodes& Q) {
+    double xe[NN][DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) xe[0][d] = x0[d];
+#pragma unroll
+    for (int b = 1; b < NN; ++b)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) xe[b][d] = Q.x[b][d];
+    constexpr bool ADJ = KIND != FPB_LAPLACIAN;
+    double gN[DIM][NN];
+    const double det = ADJ ? simplex_adj<ET>(xe, gN) : simplex_geometry<ET>(xe, gN);
+    double val[NMAT][NN];
+    if constexpr (KIND == FPB_MASS) {
+#pragma unroll
+      for (int b = 0; b < NN; ++b) val[0][b] = det * M0[b];
+    } else if constexpr (KIND == FPB_LAPLACIAN) {
+      const double dw = det * W;
+#pragma unroll
+      for (int b = 0; b < NN; ++b) {
+        double t = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) t += gN[d][0] * gN[d][b];
+        val[0][b] = dw * t;
+      }
+    } else if constexpr (KIND == FPB_CONVECTION) {
+      double ubar[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double t = M0[0] * u0[d];
+#pragma unroll
+        for (int b = 1; b < NN; ++b) t += M0[b] * Q.u[b][d];
+        ubar[d] = t;
+      }
+#pragma unroll
+      for (int b = 0; b < NN; ++b) {
+        double t = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) t += ubar[d] * gN[d][b];
+        val[0][b] = t;
+      }
+    } else {  // GRADIENT_XYZ: det gN scaled by mN[0]
+#pragma unroll
+      for (int k = 0; k < NMAT; ++k)
+#pragma unroll
+        for (int b = 0; b < NN; ++b) val[k][b] = mN0 * gN[k][b];
+    }
+#pragma unroll
+    for (int k = 0; k < NMAT; ++k) dacc[k] += val[k][0];
+    double old[NN][NMAT];
+#pragma unroll
+    for (int b = 1; b < NN; ++b)
+#pragma unroll
+      for (int k = 0; k < NMAT; ++k) old[b][k] = my[Q.s[b] * SS + (L::OA + k) * kNbBlock];
+#pragma unroll
+    for (int b = 1; b < NN; ++b)
+#pragma unroll
+      for (int k = 0; k < NMAT; ++k) my[Q.s[b] * SS + (L::OA + k) * kNbBlock] = old[b][k] + val[k][b];
+  };
+
+  // slot words in groups of kW, double-buffered: group g+1 is in flight
+  // while group g is integrated (one register copy per step)
+  constexpr int kW = 8;
+  uint32_t wc[kW], wn[kW];
+  auto ld_w = [&](int mm, uint32_t (&w)[kW]) {
+#pragma unroll
+    for (int j = 0; j < kW; ++j) w[j] = mm + j < m1 ? __ldg(slots + (int64_t)(mm + j) * 32 + lane) : 0xffffffffu;
+  };
+  ld_w(m0, wc);
+  ld_w(m0 + kW, wn);
+  Nodes QA, QB;
+  bool done = m0 >= m1 || wc[0] == 0xffffffffu;
+  if (!done) ld_nodes(wc[0], QA);
+  for (int m = m0; !done && m < m1; m += kW) {
+#pragma unroll
+    for (int j = 0; j < kW; j += 2) {
+      // QA holds entry j; stage j+1 into QB, integrate j, stage j+2 into QA
+      const bool h1 = wc[j + 1] != 0xffffffffu;
+      if (h1) ld_nodes(wc[j + 1], QB);
+      step(QA);
+      if (!h1) {
+        done = true;
+        break;
+      }
+      const uint32_t w2 = j + 2 < kW ? wc[j + 2] : wn[0];
+      const bool h2 = w2 != 0xffffffffu;
+      if (h2) ld_nodes(w2, QA);
+      step(QB);
+      if (!h2) {
+        done = true;
+        break;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kW; ++j) wc[j] = wn[j];
+    ld_w(m + 2 * kW, wn);
+  }
+
+  // ---- warp-cooperative coalesced write-out ----
+  // The warp's 32 consecutive rows are one contiguous CSR range
+  // [base, base + span).  Per matrix, every lane copies its row (diagonal
+  // from registers) into a per-warp linear buffer laid over the warp's
+  // now-dead coordinate fields (chunks of 32 doubles: slot s, field d), then
+  // the warp streams the buffer out with fully coalesced stores.
+  const int wbase = tid & ~31;
+  const int wlane = tid & 31;
+  const int base = __shfl_sync(0xffffffffu, rlo, 0);
+  int wend = live ? rlo + rlen : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+  const int span = wend - base;  // <= 32 rowcap <= 32 DIM (rowcap - 1): fits
+  auto buf = [&](int i) -> double& {
+    const int c = i >> 5;  // chunk -> (slot, coordinate field)
+    return sm[(c / DIM) * SS + (L::OX + c % DIM) * kNbBlock + wbase + (i & 31)];
+  };
+#pragma unroll
+  for (int k = 0; k < NMAT; ++k) {
+    __syncwarp();
+    for (int r = 0; r < rlen; ++r) {
+      const double v = r == dslot ? dacc[k] : my[(r - (r > dslot)) * SS + (L::OA + k) * kNbBlock];
+      buf(rlo - base + r) = v;
+    }
+    __syncwarp();
+    double* o = out + k * nnz + base;
+    for (int q = wlane; q < span; q += 32) {
+      const double v = buf(q);
+      o[q] = accumulate ? o[q] + v : v;
     }
   }
 }
@@ -357,52 +656,75 @@ __global__ void k_inc_sort(int32_t n, const int32_t* cnt, const int32_t* slice_p
   }
 }
 
+// Even permutation that brings local node a to position 0: XOR with a for
+// 4-node simplices (identity or a double transposition), rotation for 3.
+__device__ __forceinline__ int rot_node(int nn, int a, int b) { return nn == 4 ? (b ^ a) : (a + b) % 3; }
+
+// row of SELL entry (column m, lane): largest s with slice_ptr[s] <= m
+__device__ __forceinline__ int sell_row(int64_t nsl, const int32_t* slice_ptr, int64_t m, int lane) {
+  int64_t lo = 0, hi = nsl;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (slice_ptr[mid] <= m) lo = mid; else hi = mid;
+  }
+  return (int)(lo * 32 + lane);
+}
+
+// Slot bytes in record order (node b of the rotated record): byte 0 = the
+// diagonal's offset in the row, bytes 1.. = off-diagonal index (row offset
+// with the diagonal skipped, so the row kernel keeps rowcap-1 accumulators).
 __global__ void k_inc_slots(int32_t n, int nn, int64_t total, const int32_t* slice_ptr,
                             const int32_t* inc, const int32_t* conn, const int32_t* rowptr,
                             const int32_t* colind, uint32_t* slots, int* err) {
-  // entry t = (column m, lane); row = 32 * slice(m) + lane is recovered by
-  // binary search of m over slice_ptr
-  int64_t nsl = ((int64_t)n + 31) / 32;
+  const int64_t nsl = ((int64_t)n + 31) / 32;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t m = t >> 5;
-    int lane = (int)(t & 31);
-    int e = inc[t];
-    uint32_t packed = 0;
+    const int e = inc[t];
+    uint32_t packed = 0xffffffffu;  // padding entry
     if (e >= 0) {
-      int64_t lo = 0, hi = nsl;  // largest s with slice_ptr[s] <= m
-      while (hi - lo > 1) {
-        int64_t mid = (lo + hi) >> 1;
-        if (slice_ptr[mid] <= m) lo = mid; else hi = mid;
-      }
-      int row = (int)(lo * 32 + lane);
-      int r0 = rowptr[row], r1 = rowptr[row + 1];
+      const int row = sell_row(nsl, slice_ptr, t >> 5, (int)(t & 31));
+      const int r0 = rowptr[row], r1 = rowptr[row + 1];
+      int a = 0;
+      for (int b = 0; b < nn; ++b) a = conn[(int64_t)e * nn + b] == row ? b : a;
+      int off[4] = {0, 0, 0, 0};
       for (int b = 0; b < nn; ++b) {
-        int col = conn[(int64_t)e * nn + b];
+        const int col = conn[(int64_t)e * nn + rot_node(nn, a, b)];
         int l = r0, h = r1;
         while (l < h) {
           int mid = (l + h) >> 1;
           if (colind[mid] < col) l = mid + 1; else h = mid;
         }
-        int off = l - r0;
-        if (l >= r1 || colind[l] != col || off > 255) atomicExch(err, 1);
-        packed |= (uint32_t)(off & 0xff) << (8 * b);
+        off[b] = l - r0;
+        if (l >= r1 || colind[l] != col || off[b] > 255) atomicExch(err, 1);
+      }
+      packed = (uint32_t)(off[0] & 0xff);
+      for (int b = 1; b < nn; ++b) {
+        const int o = off[b] - (off[b] > off[0]);
+        packed |= (uint32_t)(o & 0xff) << (8 * b);
       }
     }
     slots[t] = packed;
   }
 }
 
-// inline node ids of every SELL entry (padding: -1)
-__global__ void k_inc_nodes(int64_t total, int nn, const int32_t* inc, const int32_t* conn, int4* incn) {
+// inline node ids of every SELL entry, rotated so the row's node comes
+// first (padding: -1)
+__global__ void k_inc_nodes(int32_t n, int64_t total, int nn, const int32_t* slice_ptr, const int32_t* inc,
+                            const int32_t* conn, int4* incn) {
+  const int64_t nsl = ((int64_t)n + 31) / 32;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int e = inc[t];
     int4 v = make_int4(-1, -1, -1, -1);
     if (e >= 0) {
+      const int row = sell_row(nsl, slice_ptr, t >> 5, (int)(t & 31));
       const int32_t* c = conn + (int64_t)e * nn;
-      v.x = c[0]; v.y = c[1]; v.z = c[2];
-      v.w = nn > 3 ? c[3] : -1;
+      int a = 0;
+      for (int b = 0; b < nn; ++b) a = c[b] == row ? b : a;
+      v.x = c[rot_node(nn, a, 0)];
+      v.y = c[rot_node(nn, a, 1)];
+      v.z = c[rot_node(nn, a, 2)];
+      v.w = nn > 3 ? c[rot_node(nn, a, 3)] : -1;
     }
     incn[t] = v;
   }
@@ -428,53 +750,79 @@ __global__ void k_max_rowlen(int32_t n, const int32_t* rowptr, int* out) {
 }
 
 template <int ET, int KIND>
-static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn, const int32_t* inc,
-                       const int32_t* conn, const uint32_t* slots,
-                       const double* xyz4, const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr, int64_t nnz,
-                       int rowcap, int accumulate, double* out, cudaStream_t s, int kdir = 0) {
+static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
+                       const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
+                       double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
+                       double* out, cudaStream_t s, int kdir = 0) {
   constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
                        KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? Elem<ET>::DIM : 1;
-  size_t smem = MAT ? (size_t)NMAT * rowcap * kRowsBlock * sizeof(double) : 0;
+  size_t smem = MAT ? (size_t)NMAT * (rowcap > 1 ? rowcap - 1 : 1) * kRowsBlock * sizeof(double) : 0;
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int blocks = (n + kRowsBlock - 1) / kRowsBlock;
-  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, incn, inc, conn, slots, xyz4,
-                                                    uvw4, rho, mu, kappa,
-                                                    rowptr, nnz, rowcap, accumulate, kdir, out);
+  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, reinterpret_cast<const int4*>(incn), slots,
+                                                    xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,
+                                                    accumulate, kdir, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+template <int ET, int KIND>
+static int launch_rows_nb(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const double* xyz4,
+                          const double* uvw4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
+                          int rowcap, int accumulate, double* out, cudaStream_t s) {
+  using L = NbLayout<ET, KIND>;
+  const size_t smem = (size_t)L::FIELDS * (rowcap > 1 ? rowcap - 1 : 1) * kNbBlock * sizeof(double);
+  if (smem > 48 * 1024)
+    FPB_CUDA(cudaFuncSetAttribute(k_rows_nb<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int blocks = (n + kNbBlock - 1) / kNbBlock;
+  k_rows_nb<ET, KIND><<<blocks, kNbBlock, smem, s>>>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz,
+                                                     rowcap, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
 
 template <int ET>
 static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_t* incn,
-                     const int32_t* inc, const int32_t* conn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
-                     double kappa,
-                     const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate, double* out,
-                     cudaStream_t s) {
-#define FPB_ROWS_CASE(K)                                                                       \
-  case K:                                                                                      \
-    return launch_rows<ET, K>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, \
-                              rowptr, nnz, rowcap, accumulate, out, s);
+                     const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
+                     double kappa, const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap,
+                     int accumulate, double* out, cudaStream_t s) {
+  const bool nb = g_tuning_rows_nb && colind && rowcap >= 2 && rowcap <= 256;
+#define FPB_ROWS_CASE(K)                                                                                 \
+  case K:                                                                                                \
+    return launch_rows<ET, K>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap, \
+                              accumulate, out, s);
+#define FPB_ROWS_NB_CASE(K)                                                                                  \
+  case K:                                                                                                    \
+    if (nb)                                                                                                  \
+      return launch_rows_nb<ET, K>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, \
+                                   out, s);                                                                  \
+    return launch_rows<ET, K>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,     \
+                              accumulate, out, s);
   switch (kind) {
-    FPB_ROWS_CASE(FPB_MASS)
-    FPB_ROWS_CASE(FPB_LAPLACIAN)
-    FPB_ROWS_CASE(FPB_CONVECTION)
+    FPB_ROWS_NB_CASE(FPB_MASS)
+    FPB_ROWS_NB_CASE(FPB_LAPLACIAN)
+    FPB_ROWS_NB_CASE(FPB_CONVECTION)
     FPB_ROWS_CASE(FPB_MOMENTUM_RHS)
     FPB_ROWS_CASE(FPB_SCALAR_RHS)
     case FPB_GRADIENT_XYZ:
+      if (nb)
+        return launch_rows_nb<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap,
+                                                    accumulate, out, s);
       if (g_tuning_gradient_split) {
         for (int k = 0; k < Elem<ET>::DIM; ++k) {
-          int rc = launch_rows<ET, KIND_GRAD1>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa,
-                                               rowptr, nnz, rowcap, accumulate, out + k * nnz, s, k);
+          int rc = launch_rows<ET, KIND_GRAD1>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
+                                               nnz, rowcap, accumulate, out + k * nnz, s, k);
           if (rc) return rc;
         }
         return FPB_OK;
       }
-      return launch_rows<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa,
-                                               rowptr, nnz, rowcap, accumulate, out, s);
+      return launch_rows<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
+                                               nnz, rowcap, accumulate, out, s);
   }
 #undef FPB_ROWS_CASE
+#undef FPB_ROWS_NB_CASE
   set_error("unknown kernel kind %d", kind);
   return FPB_ECONFIG;
 }
@@ -488,6 +836,10 @@ extern "C" {
 int fpb_set_tuning(const char* name, int value) {
   if (name && strcmp(name, "gradient_split") == 0) {
     g_tuning_gradient_split = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "rows_nb") == 0) {
+    g_tuning_rows_nb = value;
     return FPB_OK;
   }
   set_error("unknown tuning knob %s", name ? name : "(null)");
@@ -559,11 +911,11 @@ int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_p
   return FPB_OK;
 }
 
-int fpb_incidence_nodes(int64_t ncols, int nn, const int32_t* inc, const int32_t* conn, int32_t* incn,
-                        void* stream) {
+int fpb_incidence_nodes(int32_t n, int64_t ncols, int nn, const int32_t* slice_ptr, const int32_t* inc,
+                        const int32_t* conn, int32_t* incn, void* stream) {
   FPB_REQUIRE(nn == 3 || nn == 4, "inline incidence records hold at most 4 nodes");
   if (ncols <= 0) return FPB_OK;
-  k_inc_nodes<<<grid_for(ncols * 32, 256), 256, 0, as_stream(stream)>>>(ncols * 32, nn, inc, conn,
+  k_inc_nodes<<<grid_for(ncols * 32, 256), 256, 0, as_stream(stream)>>>(n, ncols * 32, nn, slice_ptr, inc, conn,
                                                                         reinterpret_cast<int4*>(incn));
   FPB_LAUNCH_CHECK();
   return FPB_OK;
@@ -579,25 +931,27 @@ int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* 
 }
 
 int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
-                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
-                      double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
-                      double* out, void* stream) {
+                      const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4,
+                      const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
+                      const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream) {
+  (void)inc;
+  (void)conn;
   FPB_REQUIRE(etype == FPB_TRI03 || etype == FPB_TET04,
               "row-owned assembly is for affine simplices (TRI03, TET04)");
   FPB_REQUIRE(g_ref_loaded[etype], "reference tables for element type %d not uploaded", etype);
   bool mat = kind == FPB_MASS || kind == FPB_LAPLACIAN || kind == FPB_CONVECTION || kind == FPB_GRADIENT_XYZ;
-  FPB_REQUIRE(!mat || (slots && rowptr && rowcap > 0), "matrix kinds need slots, rowptr and rowcap");
+  FPB_REQUIRE(!mat || (slots && rowptr && colind && rowcap > 0), "matrix kinds need slots, rowptr, colind and rowcap");
   FPB_REQUIRE(!(kind == FPB_CONVECTION || kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS) || uvw4,
               "kind %d needs a velocity field", kind);
   FPB_REQUIRE(rowcap <= 256, "row too long for row-owned assembly");
-  FPB_REQUIRE(incn || (inc && conn), "need inline node records or incidence + connectivity");
+  FPB_REQUIRE(incn, "row-owned assembly needs the rotated inline node records (fpb_incidence_nodes)");
   if (n <= 0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   if (etype == FPB_TET04)
-    return rows_kind<FPB_TET04>(kind, n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz,
+    return rows_kind<FPB_TET04>(kind, n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
                                 rowcap, accumulate, out, s);
-  return rows_kind<FPB_TRI03>(kind, n, slice_ptr, incn, inc, conn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,
-                              accumulate, out, s);
+  return rows_kind<FPB_TRI03>(kind, n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
+                              rowcap, accumulate, out, s);
 }
 
 }  // extern "C"

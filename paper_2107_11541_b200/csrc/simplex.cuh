@@ -55,6 +55,51 @@ __device__ __forceinline__ double simplex_geometry(const double (&xe)[Elem<ET>::
   return det;
 }
 
+// det * gN (the adjugate form) without the reciprocal: for integrands that
+// are linear in gN and carry one factor det (MASS, CONVECTION, GRADIENT_k)
+// the row kernels use dg = det gN directly, which rounds within an ulp of
+// det * (adj / det) and saves the FP64 reciprocal sequence per element.
+template <int ET>
+__device__ __forceinline__ double simplex_adj(const double (&xe)[Elem<ET>::NN][Elem<ET>::DIM],
+                                              double (&dg)[Elem<ET>::DIM][Elem<ET>::NN]) {
+  constexpr int DIM = Elem<ET>::DIM;
+  double J[DIM][DIM], A[DIM][DIM];  // A = det * J^-1
+#pragma unroll
+  for (int d = 0; d < DIM; ++d)
+#pragma unroll
+    for (int l = 0; l < DIM; ++l) J[d][l] = xe[l + 1][d] - xe[0][d];
+  double det;
+  if constexpr (DIM == 2) {
+    det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    A[0][0] = J[1][1];
+    A[0][1] = -J[0][1];
+    A[1][0] = -J[1][0];
+    A[1][1] = J[0][0];
+  } else {
+    A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    const double c10 = J[1][0] * J[2][2] - J[1][2] * J[2][0];
+    A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    det = J[0][0] * A[0][0] - J[0][1] * c10 + J[0][2] * A[2][0];
+    A[1][0] = -c10;
+    A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  }
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    double s = -A[0][d];
+#pragma unroll
+    for (int l = 1; l < DIM; ++l) s -= A[l][d];
+    dg[d][0] = s;
+#pragma unroll
+    for (int l = 0; l < DIM; ++l) dg[d][l + 1] = A[l][d];
+  }
+  return det;
+}
+
 // v[a] for a runtime a, without dynamic register indexing (selects)
 template <int NN>
 __device__ __forceinline__ double pick(const double (&v)[NN], int a) {
