@@ -25,17 +25,29 @@
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <climits>
 
 #include "simplex.cuh"
 
 namespace fpb {
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+
 #ifndef FPB_BLK_ELEMS
 #define FPB_BLK_ELEMS 128
 #endif
 #ifndef FPB_BLK_MINB
 #define FPB_BLK_MINB 6
+#endif
+#ifndef FPB_BLK_MINB_NONAFFINE
+#define FPB_BLK_MINB_NONAFFINE 2  // Gauss-loop elements (QUAD04, PYR05, HEX08): registers, not spills
 #endif
 constexpr int kBlockElems = FPB_BLK_ELEMS;
 
@@ -143,7 +155,7 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 // Shared memory: [node data of the block's distinct nodes: maxnu x NDAT]
 // followed by [contributions: NN * NV x kBlockElems].
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kBlockElems, FPB_BLK_MINB)
+__global__ void __launch_bounds__(kBlockElems, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
 k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
@@ -151,13 +163,31 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
   constexpr int NV = Out<ET, KIND>::NV;
   constexpr int NDAT = 2 * DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);  // x, u (, phi)
-  extern __shared__ double smem[];
-  double* snode = smem;                        // [maxnu][NDAT]
-  double* sm = smem + (int64_t)maxnu * NDAT;   // [NN * NV][kBlockElems]
+  extern __shared__ __align__(16) double smem[];
+  double* sm = smem;                                                    // [NN * NV][kBlockElems]
+  uint16_t* sgslot = reinterpret_cast<uint16_t*>(sm + NN * NV * kBlockElems);  // [NN * kBlockElems]
+  double* snode = sm + NN * NV * kBlockElems + NN * kBlockElems / 4;  // [maxnu][NDAT]
   const int tid = threadIdx.x;
   const int64_t b = blockIdx.x;
+  // gather metadata of phase 3 is fetched now so its latency hides behind
+  // staging and integration: slots via cp.async, range bounds in registers
+  {
+    const uint16_t* g = blk_gslot + b * kBlockElems * NN;
+    for (int c = tid; c < NN * kBlockElems / 8; c += kBlockElems) cp_async16(sgslot + 8 * c, g + 8 * c);
+    cp_async_commit();
+  }
   const int64_t base = blk_ptr[b];
   const int nu = blk_ptr[b + 1] - (int)base;
+  const uint16_t* gptr = blk_gptr + base + b;
+  int glo[2] = {0, 0}, ghi[2] = {0, 0};
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int u = tid + j * kBlockElems;
+    if (u < nu) {
+      glo[j] = __ldg(gptr + u);
+      ghi[j] = __ldg(gptr + u + 1);
+    }
+  }
   // stage the block's distinct nodes: two 256-bit loads per node record
   for (int u = tid; u < nu; u += kBlockElems) {
     const int64_t node = __ldg(blk_nodes + base + u);
@@ -206,16 +236,15 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
 #pragma unroll
       for (int k = 0; k < NV; ++k) sm[(a * NV + k) * kBlockElems + tid] = acc[a * NV + k];
   }
+  cp_async_wait_all();
   __syncthreads();
-  const uint16_t* gptr = blk_gptr + base + b;
-  const uint16_t* gslot = blk_gslot + b * kBlockElems * NN;
-  for (int u = tid; u < nu; u += kBlockElems) {
+  for (int u = tid, j = 0; u < nu; u += kBlockElems, ++j) {
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    const int lo = gptr[u], hi = gptr[u + 1];
+    const int lo = j < 2 ? glo[j] : __ldg(gptr + u), hi = j < 2 ? ghi[j] : __ldg(gptr + u + 1);
     for (int q = lo; q < hi; ++q) {
-      const int slot = gslot[q];
+      const int slot = sgslot[q];
       const int el = slot / NN, a = slot - el * NN;
 #pragma unroll
       for (int k = 0; k < NV; ++k) s[k] += sm[(a * NV + k) * kBlockElems + el];
@@ -251,11 +280,13 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
                       int maxnu, double* partial, cudaStream_t s) {
   constexpr int NV = Out<ET, KIND>::NV;
   constexpr int NDAT = 2 * Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);
-  const size_t smem = ((size_t)Elem<ET>::NN * NV * kBlockElems + (size_t)maxnu * NDAT) * sizeof(double);
+  const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
+  const size_t contrib = (size_t)Elem<ET>::NN * NV * kBlockElems * sizeof(double) +
+                         (size_t)Elem<ET>::NN * kBlockElems * sizeof(uint16_t);
+  const size_t smem = contrib + (size_t)maxnu * NDAT * sizeof(double);
   FPB_REQUIRE(smem <= 227 * 1024, "element block needs %zu bytes of shared memory", smem);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
   k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockElems, smem, s>>>(nelem, lidx, xyz4, uvw4, rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
