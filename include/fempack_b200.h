@@ -243,6 +243,29 @@ int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind,
                     const double* d, double* state, double* hist, int64_t hist_cap, int iters,
                     double* work, void* stream);
 
+/* ---- device-resident Jacobi-BiCGSTAB (BASELINE config 5) ----------------
+ * Not in the reference: the van der Vorst
+ * recurrence as scipy.sparse.linalg.bicgstab states it, operation for
+ * operation (rtilde = r0; p = r + beta (p - omega v); phat = p / d;
+ * v = A phat; alpha = rho / (rtilde, v); s = r - alpha v; shat = s / d;
+ * t = A shat; omega = (t, s) / (t, t); x += alpha phat; x += omega shat;
+ * r = s - omega t; stop when ||r|| < tol ||b||, or ||s|| < tol ||b|| after
+ * the half step).  d = NULL runs unpreconditioned.  state[] holds
+ * fpb_bicgstab_state_size() doubles: [0] rho, [1] rho_prev, [2] alpha,
+ * [3] omega, [4] ||b||, [5] tol ||b||, [6] status (0 running, 1 converged,
+ * 2 rho breakdown, 3 (rtilde, v) = 0, 4 omega breakdown), [7] iterations,
+ * [8] ||r|| / ||b||.  Five fused kernels per iteration; iterations after
+ * status != 0 are no-ops, so batches need no host round trip and replay
+ * from a CUDA graph like the PCG's. */
+int fpb_bicgstab_state_size(void);
+int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                      const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
+                      double* state, double* hist, double tol, double* work, void* stream);
+int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                         const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                         double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
+                         int64_t hist_cap, int iters, double* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

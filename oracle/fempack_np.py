@@ -651,6 +651,67 @@ def pcg_solve(rowptr, colind, vals, b, x0=None, tol=1e-8, max_iter=None, jacobi=
     return x, it, conv, hist, tr
 
 
+def bicgstab(rowptr, colind, vals, b, x0=None, tol=1e-8, max_iter=None, jacobi=True):
+    """Jacobi-BiCGSTAB, restated operation for operation from
+    scipy.sparse.linalg.bicgstab (scipy 1.18.1, _isolve/iterative.py; the
+    reference has no BiCGSTAB — SURVEY.md 8(f) rank 1) with this module's
+    sequential spmv / dot.  Returns (x, iterations, status, history) with
+    status 0 converged, 2 rho breakdown, 3 (r~, v) = 0, 4 omega breakdown,
+    -1 iteration cap; history[i] = ||r_i|| / ||b||.  Pinned against scipy in
+    tests/test_bicgstab.py."""
+    n = rowptr.size - 1
+    if max_iter is None:
+        max_iter = 10 * n
+    d = diagonal(rowptr, colind, vals) if jacobi else None
+    psolve = (lambda v: v / d) if jacobi else (lambda v: v.copy())
+    eps2 = np.finfo(float).eps ** 2
+    bnorm = norm2(b)
+    if bnorm == 0.0:
+        return np.zeros(n), 0, 0, [0.0]
+    atol = tol * bnorm
+    x = np.zeros(n) if x0 is None else x0.copy()
+    r = b.copy() if x0 is None else b - spmv(rowptr, colind, vals, x)
+    rt = r.copy()
+    hist = [norm2(r) / bnorm]
+    rho_prev = alpha = omega = 1.0
+    p = v = None
+    for it in range(max_iter):
+        if norm2(r) < atol:
+            return x, it, 0, hist
+        rho = dot(rt, r)
+        if abs(rho) < eps2:
+            return x, it, 2, hist
+        if it > 0:
+            if abs(omega) < eps2:
+                return x, it, 4, hist
+            beta = (rho / rho_prev) * (alpha / omega)
+            p = (p - omega * v) * beta + r
+        else:
+            p = r.copy()
+        ph = psolve(p)
+        v = spmv(rowptr, colind, vals, ph)
+        rv = dot(rt, v)
+        if rv == 0.0:
+            return x, it, 3, hist
+        alpha = rho / rv
+        s = r - alpha * v
+        if norm2(s) < atol:
+            x = x + alpha * ph
+            hist.append(norm2(s) / bnorm)
+            return x, it + 1, 0, hist
+        sh = psolve(s)
+        t = spmv(rowptr, colind, vals, sh)
+        omega = dot(t, s) / dot(t, t)
+        x = x + alpha * ph
+        x = x + omega * sh
+        r = s - omega * t
+        hist.append(norm2(r) / bnorm)
+        rho_prev = rho
+    if norm2(r) < atol:
+        return x, max_iter, 0, hist
+    return x, max_iter, -1, hist
+
+
 # --------------------------------------------------------------------------
 # bench fields  (bench.py:178-179, :196-197; test_assembly.py:199-213)
 # --------------------------------------------------------------------------

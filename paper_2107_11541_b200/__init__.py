@@ -13,7 +13,7 @@ from .assembly import AssemblyContext, KernelKind, gradient_matrices, lumped_mas
 from .elements import ElementType, ReferenceElement, reference_element
 from .errors import (ChecksumMismatchError, ConfigurationError, InvertedElementError,
                      ScatterPatternError, SolverBreakdownError, StepFailureError)
-from .krylov import SolverStats, pcg_solve
+from .krylov import SolverStats, bicgstab_solve, pcg_solve
 from .mesh import ElementGroup, Mesh, generate_box_mesh, generate_mixed_mesh, renumber_by_type
 from .packing import PackConfig, PackSet, build_packs
 from .sparse import CsrMatrix, axpy, build_node_pattern, dot, norm2, spmv
@@ -23,7 +23,7 @@ __all__ = [
     "ElementType", "ReferenceElement", "reference_element",
     "ChecksumMismatchError", "ConfigurationError", "InvertedElementError", "ScatterPatternError",
     "SolverBreakdownError", "StepFailureError",
-    "SolverStats", "pcg_solve",
+    "SolverStats", "pcg_solve", "bicgstab_solve",
     "ElementGroup", "Mesh", "generate_box_mesh", "generate_mixed_mesh", "renumber_by_type",
     "PackConfig", "PackSet", "build_packs",
     "CsrMatrix", "axpy", "build_node_pattern", "dot", "norm2", "spmv",

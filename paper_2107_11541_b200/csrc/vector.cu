@@ -324,6 +324,220 @@ __global__ void k_pcg_direction(int64_t n, double* __restrict__ p, const double*
     p[i] = axpy1(beta, p[i], z[i]);
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident Jacobi-preconditioned BiCGSTAB (config 5's solver; not in
+// the reference, so it follows the published van der Vorst recurrence as
+// scipy.sparse.linalg.bicgstab states it, operation for operation: rtilde =
+// r0, p = r + beta (p - omega v), phat = M^-1 p, v = A phat, alpha =
+// rho / (rtilde, v), s = r - alpha v, shat = M^-1 s, t = A shat,
+// omega = (t, s) / (t, t), x += alpha phat; x += omega shat, r = s - omega t,
+// stop when ||r|| < tol ||b||).  Five fused kernels per iteration, scalars
+// and status on the device, like the PCG above.
+// state: see the B_* enum; status 0 running, 1 converged, 2 rho breakdown,
+// 3 (rtilde, v) = 0, 4 omega breakdown, 5 converged on s (half step pending)
+// ---------------------------------------------------------------------------
+enum {
+  B_RHO = 0, B_RHO_PREV, B_ALPHA, B_OMEGA, B_BNORM, B_ATOL, B_STATUS, B_IT, B_RELRES, B_BETA, B_RV,
+  B_TS, B_TT, B_FIRST, B_NSTATE = 16
+};
+constexpr double kBreakTol = 4.930380657631324e-32;  // eps^2 (scipy's rhotol / omegatol)
+
+template <int G>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_init(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+            const double* __restrict__ vals, const double* __restrict__ b, const double* __restrict__ x0,
+            double* __restrict__ x, double* __restrict__ r, double* __restrict__ rt, double* __restrict__ p,
+            double* __restrict__ v, double* state, double* hist, double tol, double* work) {
+  double acc[3] = {0.0, 0.0, 0.0};
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    double ri = 0.0;
+    if (x0) {
+      const double ax = row_dot<G>(rowptr, colind, vals, x0, row, valid, sub);
+      if (valid) ri = __dsub_rn(b[row], ax);  // r = b - A x0
+    } else if (valid) {
+      ri = b[row];
+    }
+    if (valid && sub == 0) {
+      x[row] = x0 ? x0[row] : 0.0;
+      r[row] = ri;
+      rt[row] = ri;
+      p[row] = 0.0;
+      v[row] = 0.0;
+      acc[0] += b[row] * b[row];
+      acc[1] += ri * ri;
+    }
+  }
+  block_sum<3>(acc);
+  double tot[3];
+  if (grid_finish<3>(acc, work, 0, tot)) {
+    const double bnorm = sqrt(tot[0]), rnorm = sqrt(tot[1]);
+    const double atol = tol * bnorm;
+    state[B_BNORM] = bnorm;
+    state[B_ATOL] = atol;
+    state[B_IT] = 0.0;
+    state[B_RELRES] = bnorm == 0.0 ? 0.0 : rnorm / bnorm;
+    state[B_RHO] = tot[1];  // (rtilde, r) with rtilde = r
+    state[B_RHO_PREV] = 1.0;
+    state[B_ALPHA] = 1.0;
+    state[B_OMEGA] = 1.0;
+    state[B_BETA] = 0.0;  // first spin: p = r
+    state[B_FIRST] = 1.0;
+    hist[0] = state[B_RELRES];
+    double st = 0.0;
+    if (bnorm == 0.0 || rnorm < atol) st = 1.0;
+    else if (fabs(tot[1]) < kBreakTol) st = 2.0;
+    state[B_STATUS] = st;
+  }
+}
+
+// K1: p = r + beta (p - omega v) (first spin: p = r); phat = p / d
+__global__ void k_bicg_dir(int64_t n, const double* __restrict__ r, const double* __restrict__ v,
+                           const double* __restrict__ d, double* __restrict__ p, double* __restrict__ ph,
+                           const double* state) {
+  if (state[B_STATUS] != 0.0) return;
+  const bool first = state[B_FIRST] != 0.0;
+  const double beta = state[B_BETA], omega = state[B_OMEGA];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double pi;
+    if (first) {
+      pi = r[i];
+    } else {  // p -= omega*v; p *= beta; p += r
+      pi = __dadd_rn(__dmul_rn(__dsub_rn(p[i], __dmul_rn(omega, v[i])), beta), r[i]);
+    }
+    p[i] = pi;
+    ph[i] = d ? __ddiv_rn(pi, d[i]) : pi;
+  }
+}
+
+// K2: v = A phat; rv = (rtilde, v); alpha = rho / rv
+template <int G>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_av(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+          const double* __restrict__ vals, const double* __restrict__ ph, const double* __restrict__ rt,
+          double* __restrict__ v, double* state, double* work) {
+  if (state[B_STATUS] != 0.0) return;
+  double acc[1] = {0.0};
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    const double vi = row_dot<G>(rowptr, colind, vals, ph, row, valid, sub);
+    if (valid && sub == 0) {
+      v[row] = vi;
+      acc[0] += rt[row] * vi;
+    }
+  }
+  block_sum<1>(acc);
+  double tot[1];
+  if (grid_finish<1>(acc, work, 1, tot)) {
+    state[B_RV] = tot[0];
+    if (tot[0] == 0.0) state[B_STATUS] = 3.0;
+    else state[B_ALPHA] = state[B_RHO] / tot[0];
+  }
+}
+
+// K3: s = r - alpha v; shat = s / d; ||s|| < atol -> converged on s
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_s(int64_t n, const double* __restrict__ r, const double* __restrict__ v, const double* __restrict__ d,
+         double* __restrict__ sv, double* __restrict__ sh, double* state, double* work) {
+  if (state[B_STATUS] != 0.0) return;
+  const double alpha = state[B_ALPHA];
+  double acc[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double si = __dsub_rn(r[i], __dmul_rn(alpha, v[i]));
+    sv[i] = si;
+    sh[i] = d ? __ddiv_rn(si, d[i]) : si;
+    acc[0] += si * si;
+  }
+  block_sum<1>(acc);
+  double tot[1];
+  if (grid_finish<1>(acc, work, 2, tot)) {
+    if (sqrt(tot[0]) < state[B_ATOL]) {
+      state[B_STATUS] = 5.0;
+      state[B_RELRES] = sqrt(tot[0]) / state[B_BNORM];
+    }
+  }
+}
+
+// K4: t = A shat; (t, s), (t, t); omega = ts / tt
+template <int G>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_at(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+          const double* __restrict__ vals, const double* __restrict__ sh, const double* __restrict__ sv,
+          double* __restrict__ t, double* state, double* work) {
+  if (state[B_STATUS] != 0.0) return;
+  double acc[2] = {0.0, 0.0};
+  FPB_ROW_LOOP(G, n) {
+    const bool valid = row < n;
+    const double ti = row_dot<G>(rowptr, colind, vals, sh, row, valid, sub);
+    if (valid && sub == 0) {
+      t[row] = ti;
+      acc[0] += ti * sv[row];
+      acc[1] += ti * ti;
+    }
+  }
+  block_sum<2>(acc);
+  double tot[2];
+  if (grid_finish<2>(acc, work, 3, tot)) {
+    state[B_TS] = tot[0];
+    state[B_TT] = tot[1];
+    state[B_OMEGA] = tot[0] / tot[1];
+  }
+}
+
+// K5: x += alpha phat; x += omega shat; r = s - omega t; ||r||, rho_new =
+// (rtilde, r); stopping and breakdown tests, beta for the next spin.  With
+// status 5 (converged on s) only x += alpha phat and r = s are applied.
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_update(int64_t n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ ph,
+              const double* __restrict__ sh, const double* __restrict__ sv, const double* __restrict__ t,
+              const double* __restrict__ rt, double* state, double* hist, int64_t hist_cap, double* work) {
+  const double status = state[B_STATUS];
+  if (status != 0.0 && status != 5.0) return;
+  const bool half = status == 5.0;
+  const double alpha = state[B_ALPHA], omega = state[B_OMEGA];
+  double acc[2] = {0.0, 0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double xi = axpy1(alpha, ph[i], x[i]);
+    double ri = sv[i];
+    if (!half) {
+      xi = axpy1(omega, sh[i], xi);
+      ri = __dsub_rn(ri, __dmul_rn(omega, t[i]));
+    }
+    x[i] = xi;
+    r[i] = ri;
+    acc[0] += ri * ri;
+    acc[1] += rt[i] * ri;
+  }
+  block_sum<2>(acc);
+  double tot[2];
+  if (grid_finish<2>(acc, work, 0, tot)) {
+    const double it = state[B_IT] + 1.0;
+    const double rnorm = sqrt(tot[0]);
+    state[B_IT] = it;
+    state[B_RELRES] = rnorm / state[B_BNORM];
+    hist[(int64_t)it % hist_cap] = state[B_RELRES];
+    state[B_FIRST] = 0.0;
+    if (half || rnorm < state[B_ATOL]) {
+      state[B_STATUS] = 1.0;
+    } else if (fabs(tot[1]) < kBreakTol) {
+      state[B_STATUS] = 2.0;
+    } else if (fabs(omega) < kBreakTol) {
+      state[B_STATUS] = 4.0;
+    } else {
+      state[B_BETA] = (tot[1] / state[B_RHO]) * (alpha / omega);
+      state[B_RHO_PREV] = state[B_RHO];
+      state[B_RHO] = tot[1];
+    }
+  }
+}
+
+inline int lanes_per_row(int32_t n, int64_t nnz) {
+  const double mean = n > 0 ? (double)nnz / n : 0.0;
+  return mean <= 6.0 ? 4 : (mean <= 20.0 ? 8 : 16);
+}
+
 }  // namespace fpb
 
 using namespace fpb;
@@ -405,6 +619,44 @@ int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind, con
     k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_cap, work);
     k_pcg_direction<<<grid_for(n, 256, 8), 256, 0, s>>>(n, p, z, state);
+  }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+
+int fpb_bicgstab_state_size(void) { return B_NSTATE; }
+
+int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                      const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
+                      double* state, double* hist, double tol, double* work, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  switch (lanes_per_row(n, nnz)) {
+    case 4: k_bicg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
+    case 8: k_bicg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
+    default: k_bicg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
+  }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                         const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                         double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
+                         int64_t hist_cap, int iters, double* work, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const int G = lanes_per_row(n, nnz);
+  const int vgrid = grid_for(n, 256, 8);
+  for (int it = 0; it < iters; ++it) {
+    k_bicg_dir<<<vgrid, 256, 0, s>>>(n, r, v, d, p, ph, state);
+    if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
+    else if (G == 8) k_bicg_av<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
+    else k_bicg_av<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
+    k_bicg_s<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, v, d, sv, sh, state, work);
+    if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
+    else if (G == 8) k_bicg_at<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
+    else k_bicg_at<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
+    k_bicg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, ph, sh, sv, t, rt, state, hist, hist_cap, work);
   }
   FPB_LAUNCH_CHECK();
   return FPB_OK;

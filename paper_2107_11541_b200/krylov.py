@@ -96,3 +96,88 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     bnorm = float(st[S_BNORM])
     true_residual = float(np.sqrt(dot_d(res, res).item())) / bnorm
     return out(x), SolverStats(done, converged, history, true_residual)
+
+
+# --------------------------------------------------------------------------
+# BiCGSTAB (BASELINE config 5).  Not in the reference: the recurrence is the
+# published van der Vorst algorithm as scipy.sparse.linalg.bicgstab states it
+# (see include/fempack_b200.h); parity is pinned per vector op and against
+# scipy through the oracle's restatement (tests/test_bicgstab.py).
+# --------------------------------------------------------------------------
+
+B_RHO, B_RHO_PREV, B_ALPHA, B_OMEGA, B_BNORM, B_ATOL, B_STATUS, B_IT, B_RELRES = range(9)
+_BICG_BREAKDOWN = {2.0: "rho = (r~, r) vanished", 3.0: "(r~, A p^) vanished", 4.0: "omega vanished"}
+
+
+def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None = None,
+                   jacobi: bool = True, batch: int = 32, graph: bool = True):
+    """Solve A x = b for a general (non-symmetric) A; returns (x, SolverStats).
+
+    Same calling convention as pcg_solve: numpy b -> numpy x, CUDA tensor b
+    -> CUDA tensor x.  Breakdowns raise SolverBreakdownError like the PCG's
+    curvature test (krylov.py:46-49).  history[i] = ||r_i|| / ||b||.
+    """
+    bd, host = to_device(b)
+    n = A.n
+    dev = bd.device
+    if max_iter is None:
+        max_iter = 10 * n
+    if jacobi:
+        d = A.diagonal_d()
+        if bool((d == 0.0).any()):
+            raise SolverBreakdownError("Jacobi preconditioner needs a nonzero diagonal")
+    else:
+        d = None
+    x0d = to_device(x0)[0] if x0 is not None else None
+    x, r, rt, p, ph, v, sv, sh, t = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(9))
+    lib = _lib.load()
+    state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
+    cap = max(1, min(batch, max_iter))
+    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
+    work = dot_work()
+    s = _lib.stream()
+    rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
+    nnz = A.nnz
+    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, bd.data_ptr(),
+              x0d.data_ptr() if x0d is not None else None, x.data_ptr(), r.data_ptr(), rt.data_ptr(),
+              p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol), work.data_ptr(), s)
+    st = state.cpu().numpy()
+    out = to_host if host else (lambda q: q)
+    if st[B_BNORM] == 0.0:
+        return out(torch.zeros(n, dtype=torch.float64, device=dev)), SolverStats(0, True, [0.0], 0.0)
+    history = [float(hist_d[0].item())]
+    if st[B_STATUS] == 1.0:
+        return out(x), SolverStats(0, True, history, history[0])
+    if st[B_STATUS] in _BICG_BREAKDOWN:
+        raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
+    args = (n, nnz, rp, ci, va, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
+            rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
+            t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
+    cuda_graph = None
+    done = 0
+    while done < max_iter:
+        k = min(cap, max_iter - done)
+        if graph and k == cap and done > 0:
+            if cuda_graph is None:
+                cuda_graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(cuda_graph, stream=side):
+                    _lib.call("fpb_bicgstab_iterate", *args, k, work.data_ptr(), _lib.stream())
+            cuda_graph.replay()
+        else:
+            _lib.call("fpb_bicgstab_iterate", *args, k, work.data_ptr(), s)
+        st = state.cpu().numpy()
+        it = int(st[B_IT])
+        if it > done:
+            h = hist_d.cpu().numpy()
+            history.extend(float(h[i % cap]) for i in range(done + 1, it + 1))
+        done = it
+        if st[B_STATUS] in _BICG_BREAKDOWN:
+            raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
+        if st[B_STATUS] == 1.0:
+            break
+    converged = bool(st[B_STATUS] == 1.0)
+    res = axpy_d(-1.0, spmv_d(A, x), bd)
+    true_residual = float(np.sqrt(dot_d(res, res).item())) / float(st[B_BNORM])
+    return out(x), SolverStats(done, converged, history, true_residual)
