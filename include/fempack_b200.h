@@ -258,13 +258,30 @@ int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind,
  * status != 0 are no-ops, so batches need no host round trip and replay
  * from a CUDA graph like the PCG's. */
 int fpb_bicgstab_state_size(void);
+/* x = x0 | 0, r = rtilde = b - A x0 | b, p = v = 0; reductions over the
+ * owned rows [own_lo, own_hi) (0, n on one GPU).  defer = 0 finishes the
+ * scalars on the device; defer = 1 leaves {||b||^2, ||r||^2} (partial, this
+ * rank) in state[16..17] for an allreduce followed by fpb_bicgstab_finish(0). */
 int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
                       const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
-                      double* state, double* hist, double tol, double* work, void* stream);
+                      double* state, double* hist, double tol, int64_t own_lo, int64_t own_hi, int defer,
+                      double* work, void* stream);
+/* `iters` whole iterations on one GPU (all rows owned, scalars on device). */
 int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
                          const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
                          double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                          int64_t hist_cap, int iters, double* work, void* stream);
+/* One reduction step of an iteration, for domain decomposition: step 1 =
+ * direction + v = A phat with (rtilde, v); 2 = s, shat with ||s||^2; 3 =
+ * t = A shat with (t, s), (t, t); 4 = x, r update with ||r||^2, (rtilde, r).
+ * With defer = 1 the partial sums land in state[16..17]; the caller
+ * allreduces them (and refreshes ghost entries of v / t after steps 1 / 3)
+ * before fpb_bicgstab_finish(step). */
+int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                      const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                      double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
+                      int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream);
+int fpb_bicgstab_finish(int step, double* state, double* hist, int64_t hist_cap, double tol, void* stream);
 
 #ifdef __cplusplus
 }

@@ -56,8 +56,10 @@ SIGNATURES = {
     "fpb_pcg_init": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
     "fpb_pcg_iterate": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
     "fpb_bicgstab_state_size": (_int, []),
-    "fpb_bicgstab_init": (_int, [_i32, _i64] + [_vp] * 12 + [_dbl, _vp, _vp]),
+    "fpb_bicgstab_init": (_int, [_i32, _i64] + [_vp] * 12 + [_dbl, _i64, _i64, _int, _vp, _vp]),
     "fpb_bicgstab_iterate": (_int, [_i32, _i64] + [_vp] * 15 + [_i64, _int, _vp, _vp]),
+    "fpb_bicgstab_step": (_int, [_int, _i32, _i64] + [_vp] * 15 + [_i64, _i64, _i64, _int, _vp, _vp]),
+    "fpb_bicgstab_finish": (_int, [_int, _vp, _vp, _i64, _dbl, _vp]),
 }
 
 _lib = None

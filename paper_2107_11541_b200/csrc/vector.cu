@@ -333,22 +333,123 @@ __global__ void k_pcg_direction(int64_t n, double* __restrict__ p, const double*
 // omega = (t, s) / (t, t), x += alpha phat; x += omega shat, r = s - omega t,
 // stop when ||r|| < tol ||b||).  Five fused kernels per iteration, scalars
 // and status on the device, like the PCG above.
+//
+// Domain decomposition (distributed.py): elementwise updates run over all n
+// local entries, reductions only over the owned range [own_lo, own_hi).
+// With defer = 0 the last block finishes the scalars in place (one GPU);
+// with defer = 1 it leaves the partial sums in state[B_RED..] for a
+// cross-rank allreduce, after which fpb_bicgstab_finish applies the same
+// scalar step.
 // state: see the B_* enum; status 0 running, 1 converged, 2 rho breakdown,
 // 3 (rtilde, v) = 0, 4 omega breakdown, 5 converged on s (half step pending)
 // ---------------------------------------------------------------------------
 enum {
   B_RHO = 0, B_RHO_PREV, B_ALPHA, B_OMEGA, B_BNORM, B_ATOL, B_STATUS, B_IT, B_RELRES, B_BETA, B_RV,
-  B_TS, B_TT, B_FIRST, B_NSTATE = 16
+  B_TS, B_TT, B_FIRST, B_RED = 16, B_NSTATE = 20
 };
+enum { BSTEP_INIT = 0, BSTEP_AV, BSTEP_S, BSTEP_AT, BSTEP_UPDATE };
 constexpr double kBreakTol = 4.930380657631324e-32;  // eps^2 (scipy's rhotol / omegatol)
+
+// scalar step after reduction `step` with totals tot[] (identical on every rank)
+__device__ void bicg_finish(int step, const double* tot, double* state, double* hist, int64_t hist_cap,
+                            double tol) {
+  switch (step) {
+    case BSTEP_INIT: {
+      const double bnorm = sqrt(tot[0]), rnorm = sqrt(tot[1]);
+      const double atol = tol * bnorm;
+      state[B_BNORM] = bnorm;
+      state[B_ATOL] = atol;
+      state[B_IT] = 0.0;
+      state[B_RELRES] = bnorm == 0.0 ? 0.0 : rnorm / bnorm;
+      state[B_RHO] = tot[1];  // (rtilde, r) with rtilde = r
+      state[B_RHO_PREV] = 1.0;
+      state[B_ALPHA] = 1.0;
+      state[B_OMEGA] = 1.0;
+      state[B_BETA] = 0.0;  // first spin: p = r
+      state[B_FIRST] = 1.0;
+      hist[0] = state[B_RELRES];
+      double st = 0.0;
+      if (bnorm == 0.0 || rnorm < atol) st = 1.0;
+      else if (fabs(tot[1]) < kBreakTol) st = 2.0;
+      state[B_STATUS] = st;
+      break;
+    }
+    case BSTEP_AV:
+      if (state[B_STATUS] != 0.0) break;
+      state[B_RV] = tot[0];
+      if (tot[0] == 0.0) state[B_STATUS] = 3.0;
+      else state[B_ALPHA] = state[B_RHO] / tot[0];
+      break;
+    case BSTEP_S:
+      if (state[B_STATUS] != 0.0) break;
+      if (sqrt(tot[0]) < state[B_ATOL]) {
+        state[B_STATUS] = 5.0;
+        state[B_RELRES] = sqrt(tot[0]) / state[B_BNORM];
+      }
+      break;
+    case BSTEP_AT:
+      if (state[B_STATUS] != 0.0) break;
+      state[B_TS] = tot[0];
+      state[B_TT] = tot[1];
+      state[B_OMEGA] = tot[0] / tot[1];
+      break;
+    case BSTEP_UPDATE: {
+      const double status = state[B_STATUS];
+      if (status != 0.0 && status != 5.0) break;
+      const bool half = status == 5.0;
+      const double alpha = state[B_ALPHA], omega = state[B_OMEGA];
+      const double it = state[B_IT] + 1.0;
+      const double rnorm = sqrt(tot[0]);
+      state[B_IT] = it;
+      state[B_RELRES] = rnorm / state[B_BNORM];
+      hist[(int64_t)it % hist_cap] = state[B_RELRES];
+      state[B_FIRST] = 0.0;
+      if (half || rnorm < state[B_ATOL]) {
+        state[B_STATUS] = 1.0;
+      } else if (fabs(tot[1]) < kBreakTol) {
+        state[B_STATUS] = 2.0;
+      } else if (fabs(omega) < kBreakTol) {
+        state[B_STATUS] = 4.0;
+      } else {
+        state[B_BETA] = (tot[1] / state[B_RHO]) * (alpha / omega);
+        state[B_RHO_PREV] = state[B_RHO];
+        state[B_RHO] = tot[1];
+      }
+      break;
+    }
+  }
+}
+
+struct BicgRed {  // where a kernel's totals go
+  int64_t own_lo, own_hi;
+  int defer;
+  double* hist;
+  int64_t hist_cap;
+  double tol;
+};
+
+template <int NV>
+__device__ __forceinline__ void bicg_reduce(double (&acc)[NV], int step, double* state, double* work,
+                                            int slot, const BicgRed& R) {
+  block_sum<NV>(acc);
+  double tot[NV];
+  if (grid_finish<NV>(acc, work, slot, tot)) {
+    if (R.defer) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q) state[B_RED + q] = tot[q];
+    } else {
+      bicg_finish(step, tot, state, R.hist, R.hist_cap, R.tol);
+    }
+  }
+}
 
 template <int G>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_init(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
             const double* __restrict__ vals, const double* __restrict__ b, const double* __restrict__ x0,
             double* __restrict__ x, double* __restrict__ r, double* __restrict__ rt, double* __restrict__ p,
-            double* __restrict__ v, double* state, double* hist, double tol, double* work) {
-  double acc[3] = {0.0, 0.0, 0.0};
+            double* __restrict__ v, double* state, double* work, BicgRed R) {
+  double acc[2] = {0.0, 0.0};
   FPB_ROW_LOOP(G, n) {
     const bool valid = row < n;
     double ri = 0.0;
@@ -364,31 +465,13 @@ k_bicg_init(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __rest
       rt[row] = ri;
       p[row] = 0.0;
       v[row] = 0.0;
-      acc[0] += b[row] * b[row];
-      acc[1] += ri * ri;
+      if (row >= R.own_lo && row < R.own_hi) {
+        acc[0] += b[row] * b[row];
+        acc[1] += ri * ri;
+      }
     }
   }
-  block_sum<3>(acc);
-  double tot[3];
-  if (grid_finish<3>(acc, work, 0, tot)) {
-    const double bnorm = sqrt(tot[0]), rnorm = sqrt(tot[1]);
-    const double atol = tol * bnorm;
-    state[B_BNORM] = bnorm;
-    state[B_ATOL] = atol;
-    state[B_IT] = 0.0;
-    state[B_RELRES] = bnorm == 0.0 ? 0.0 : rnorm / bnorm;
-    state[B_RHO] = tot[1];  // (rtilde, r) with rtilde = r
-    state[B_RHO_PREV] = 1.0;
-    state[B_ALPHA] = 1.0;
-    state[B_OMEGA] = 1.0;
-    state[B_BETA] = 0.0;  // first spin: p = r
-    state[B_FIRST] = 1.0;
-    hist[0] = state[B_RELRES];
-    double st = 0.0;
-    if (bnorm == 0.0 || rnorm < atol) st = 1.0;
-    else if (fabs(tot[1]) < kBreakTol) st = 2.0;
-    state[B_STATUS] = st;
-  }
+  bicg_reduce<2>(acc, BSTEP_INIT, state, work, 0, R);
 }
 
 // K1: p = r + beta (p - omega v) (first spin: p = r); phat = p / d
@@ -415,7 +498,7 @@ template <int G>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_av(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
           const double* __restrict__ vals, const double* __restrict__ ph, const double* __restrict__ rt,
-          double* __restrict__ v, double* state, double* work) {
+          double* __restrict__ v, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[1] = {0.0};
   FPB_ROW_LOOP(G, n) {
@@ -423,22 +506,16 @@ k_bicg_av(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restri
     const double vi = row_dot<G>(rowptr, colind, vals, ph, row, valid, sub);
     if (valid && sub == 0) {
       v[row] = vi;
-      acc[0] += rt[row] * vi;
+      if (row >= R.own_lo && row < R.own_hi) acc[0] += rt[row] * vi;
     }
   }
-  block_sum<1>(acc);
-  double tot[1];
-  if (grid_finish<1>(acc, work, 1, tot)) {
-    state[B_RV] = tot[0];
-    if (tot[0] == 0.0) state[B_STATUS] = 3.0;
-    else state[B_ALPHA] = state[B_RHO] / tot[0];
-  }
+  bicg_reduce<1>(acc, BSTEP_AV, state, work, 1, R);
 }
 
 // K3: s = r - alpha v; shat = s / d; ||s|| < atol -> converged on s
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_s(int64_t n, const double* __restrict__ r, const double* __restrict__ v, const double* __restrict__ d,
-         double* __restrict__ sv, double* __restrict__ sh, double* state, double* work) {
+         double* __restrict__ sv, double* __restrict__ sh, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   const double alpha = state[B_ALPHA];
   double acc[1] = {0.0};
@@ -447,16 +524,9 @@ k_bicg_s(int64_t n, const double* __restrict__ r, const double* __restrict__ v, 
     const double si = __dsub_rn(r[i], __dmul_rn(alpha, v[i]));
     sv[i] = si;
     sh[i] = d ? __ddiv_rn(si, d[i]) : si;
-    acc[0] += si * si;
+    if (i >= R.own_lo && i < R.own_hi) acc[0] += si * si;
   }
-  block_sum<1>(acc);
-  double tot[1];
-  if (grid_finish<1>(acc, work, 2, tot)) {
-    if (sqrt(tot[0]) < state[B_ATOL]) {
-      state[B_STATUS] = 5.0;
-      state[B_RELRES] = sqrt(tot[0]) / state[B_BNORM];
-    }
-  }
+  bicg_reduce<1>(acc, BSTEP_S, state, work, 2, R);
 }
 
 // K4: t = A shat; (t, s), (t, t); omega = ts / tt
@@ -464,7 +534,7 @@ template <int G>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_at(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
           const double* __restrict__ vals, const double* __restrict__ sh, const double* __restrict__ sv,
-          double* __restrict__ t, double* state, double* work) {
+          double* __restrict__ t, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[2] = {0.0, 0.0};
   FPB_ROW_LOOP(G, n) {
@@ -472,17 +542,13 @@ k_bicg_at(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restri
     const double ti = row_dot<G>(rowptr, colind, vals, sh, row, valid, sub);
     if (valid && sub == 0) {
       t[row] = ti;
-      acc[0] += ti * sv[row];
-      acc[1] += ti * ti;
+      if (row >= R.own_lo && row < R.own_hi) {
+        acc[0] += ti * sv[row];
+        acc[1] += ti * ti;
+      }
     }
   }
-  block_sum<2>(acc);
-  double tot[2];
-  if (grid_finish<2>(acc, work, 3, tot)) {
-    state[B_TS] = tot[0];
-    state[B_TT] = tot[1];
-    state[B_OMEGA] = tot[0] / tot[1];
-  }
+  bicg_reduce<2>(acc, BSTEP_AT, state, work, 3, R);
 }
 
 // K5: x += alpha phat; x += omega shat; r = s - omega t; ||r||, rho_new =
@@ -491,7 +557,7 @@ k_bicg_at(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restri
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_update(int64_t n, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ ph,
               const double* __restrict__ sh, const double* __restrict__ sv, const double* __restrict__ t,
-              const double* __restrict__ rt, double* state, double* hist, int64_t hist_cap, double* work) {
+              const double* __restrict__ rt, double* state, double* work, BicgRed R) {
   const double status = state[B_STATUS];
   if (status != 0.0 && status != 5.0) return;
   const bool half = status == 5.0;
@@ -507,30 +573,17 @@ k_bicg_update(int64_t n, double* __restrict__ x, double* __restrict__ r, const d
     }
     x[i] = xi;
     r[i] = ri;
-    acc[0] += ri * ri;
-    acc[1] += rt[i] * ri;
-  }
-  block_sum<2>(acc);
-  double tot[2];
-  if (grid_finish<2>(acc, work, 0, tot)) {
-    const double it = state[B_IT] + 1.0;
-    const double rnorm = sqrt(tot[0]);
-    state[B_IT] = it;
-    state[B_RELRES] = rnorm / state[B_BNORM];
-    hist[(int64_t)it % hist_cap] = state[B_RELRES];
-    state[B_FIRST] = 0.0;
-    if (half || rnorm < state[B_ATOL]) {
-      state[B_STATUS] = 1.0;
-    } else if (fabs(tot[1]) < kBreakTol) {
-      state[B_STATUS] = 2.0;
-    } else if (fabs(omega) < kBreakTol) {
-      state[B_STATUS] = 4.0;
-    } else {
-      state[B_BETA] = (tot[1] / state[B_RHO]) * (alpha / omega);
-      state[B_RHO_PREV] = state[B_RHO];
-      state[B_RHO] = tot[1];
+    if (i >= R.own_lo && i < R.own_hi) {
+      acc[0] += ri * ri;
+      acc[1] += rt[i] * ri;
     }
   }
+  bicg_reduce<2>(acc, BSTEP_UPDATE, state, work, 0, R);
+}
+
+__global__ void k_bicg_finish(int step, double* state, double* hist, int64_t hist_cap, double tol) {
+  double tot[2] = {state[B_RED], state[B_RED + 1]};
+  bicg_finish(step, tot, state, hist, hist_cap, tol);
 }
 
 inline int lanes_per_row(int32_t n, int64_t nnz) {
@@ -629,12 +682,14 @@ int fpb_bicgstab_state_size(void) { return B_NSTATE; }
 
 int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
                       const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
-                      double* state, double* hist, double tol, double* work, void* stream) {
+                      double* state, double* hist, double tol, int64_t own_lo, int64_t own_hi, int defer,
+                      double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
+  const BicgRed R{own_lo, own_hi, defer, hist, 1, tol};
   switch (lanes_per_row(n, nnz)) {
-    case 4: k_bicg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
-    case 8: k_bicg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
-    default: k_bicg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, hist, tol, work); break;
+    case 4: k_bicg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
+    case 8: k_bicg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
+    default: k_bicg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
   }
   FPB_LAUNCH_CHECK();
   return FPB_OK;
@@ -645,19 +700,52 @@ int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const in
                          double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                          int64_t hist_cap, int iters, double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
+  for (int it = 0; it < iters; ++it)
+    for (int step = BSTEP_AV; step <= BSTEP_UPDATE; ++step) {
+      int rc = fpb_bicgstab_step(step, n, nnz, rowptr, colind, vals, d, x, r, rt, p, ph, v, sv, sh, t, state,
+                                 hist, hist_cap, 0, n, 0, work, stream);
+      if (rc) return rc;
+    }
+  (void)s;
+  return FPB_OK;
+}
+
+int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
+                      const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                      double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
+                      int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream) {
+  cudaStream_t s = as_stream(stream);
   const int G = lanes_per_row(n, nnz);
-  const int vgrid = grid_for(n, 256, 8);
-  for (int it = 0; it < iters; ++it) {
-    k_bicg_dir<<<vgrid, 256, 0, s>>>(n, r, v, d, p, ph, state);
-    if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
-    else if (G == 8) k_bicg_av<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
-    else k_bicg_av<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work);
-    k_bicg_s<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, v, d, sv, sh, state, work);
-    if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
-    else if (G == 8) k_bicg_at<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
-    else k_bicg_at<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work);
-    k_bicg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, ph, sh, sv, t, rt, state, hist, hist_cap, work);
+  const BicgRed R{own_lo, own_hi, defer, hist, hist_cap, 0.0};
+  switch (step) {
+    case BSTEP_AV:  // K1 + K2
+      k_bicg_dir<<<grid_for(n, 256, 8), 256, 0, s>>>(n, r, v, d, p, ph, state);
+      if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
+      else if (G == 8) k_bicg_av<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
+      else k_bicg_av<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
+      break;
+    case BSTEP_S:
+      k_bicg_s<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, v, d, sv, sh, state, work, R);
+      break;
+    case BSTEP_AT:
+      if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
+      else if (G == 8) k_bicg_at<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
+      else k_bicg_at<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
+      break;
+    case BSTEP_UPDATE:
+      k_bicg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, ph, sh, sv, t, rt, state, work, R);
+      break;
+    default:
+      set_error("bad BiCGSTAB step %d", step);
+      return FPB_ECONFIG;
   }
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_bicgstab_finish(int step, double* state, double* hist, int64_t hist_cap, double tol, void* stream) {
+  FPB_REQUIRE(step >= BSTEP_INIT && step <= BSTEP_UPDATE, "bad BiCGSTAB step %d", step);
+  k_bicg_finish<<<1, 1, 0, as_stream(stream)>>>(step, state, hist, hist_cap, tol);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }

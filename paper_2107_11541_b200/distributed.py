@@ -121,16 +121,23 @@ class SlabLayout:
 
 
 def _exchange(sends: list[tuple[int, torch.Tensor]], group=None) -> list[torch.Tensor]:
-    """Grouped point-to-point exchange; returns one received buffer per send."""
+    """Grouped point-to-point exchange; returns one received buffer per send
+    (on the send buffers' device).  NCCL moves device memory directly; gloo
+    (CPU tests, or several ranks sharing one GPU) is staged through the host."""
+    if not sends:
+        return []
+    dev = sends[0][1].device
+    staged = dev.type == "cuda" and dist.get_backend(group) != "nccl"
+    if staged:
+        sends = [(peer, t.cpu()) for peer, t in sends]
     recvs = [torch.empty_like(t) for _, t in sends]
     ops = []
     for (peer, t), r in zip(sends, recvs):
         ops.append(dist.P2POp(dist.isend, t, peer, group))
         ops.append(dist.P2POp(dist.irecv, r, peer, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    return recvs
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return [r.to(dev) for r in recvs] if staged else recvs
 
 
 def halo_sum_nodes(layout: SlabLayout, x: torch.Tensor, group=None) -> torch.Tensor:
@@ -215,3 +222,150 @@ class SlabDomain:
     def halo_sum_matrix(self, vals: torch.Tensor, nmat: int = 1) -> torch.Tensor:
         return halo_sum_rows(self.layout, self.ctx.pattern.rowptr_d, vals, nmat, self.ctx.pattern.nnz,
                              self.group, self.segs)
+
+
+# --------------------------------------------------------------------------
+# Distributed solver plumbing ("Solver: x-halo of one plane
+# per interface per SpMV, plus an allreduce of 1-3 doubles per dot")
+# --------------------------------------------------------------------------
+
+def _staged(t: torch.Tensor, group=None) -> bool:
+    """gloo moves host memory: CUDA tensors are staged through the host."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """In-place SUM over ranks (NCCL on device; gloo through the host)."""
+    if dist.get_world_size(group) == 1:
+        return t
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def ghost_planes(layout: SlabLayout) -> list[tuple[int, int, int]]:
+    """(peer, plane to send, ghost plane to receive) per neighbour: the lower
+    neighbour gets my plane k0 + 1 for its ghost plane k1' + 1, the upper one
+    my plane k1 - 1 for its ghost plane k0' - 1 (both are planes the sender
+    computes exactly — owned rows or the shared interface)."""
+    out = []
+    if layout.rank > 0:
+        out.append((layout.rank - 1, layout.k0 + 1, layout.kA))
+    if layout.rank < layout.world - 1:
+        out.append((layout.rank + 1, layout.k1 - 1, layout.kB))
+    return out
+
+
+def refresh_ghosts(layout: SlabLayout, x: torch.Tensor, group=None) -> torch.Tensor:
+    """Overwrite the ghost node planes of a node vector with the neighbours'
+    values, so every local entry holds its global value again."""
+    plan = ghost_planes(layout)
+    if not plan:
+        return x
+    sends = []
+    for peer, ks, _ in plan:
+        lo, hi = layout.plane_rows(ks)
+        sends.append((peer, x[lo:hi].contiguous()))
+    recvs = _exchange(sends, group)
+    for (peer, _, kg), r in zip(plan, recvs):
+        lo, hi = layout.plane_rows(kg)
+        x[lo:hi].copy_(r)
+    return x
+
+
+def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 1e-8,
+                  max_iter: int | None = None, jacobi: bool = True, group=None, check_every: int = 8):
+    """Jacobi-BiCGSTAB over the z-slab decomposition (config 5).
+
+    A is this rank's extended-slab CSR with halo-summed values (rows of
+    planes k0..k1 are global rows), b a node vector consistent on every local
+    plane.  Every iteration runs the one-GPU fused kernels with reductions
+    restricted to the owned rows, allreduces the 2-double partials (four
+    times) and refreshes the ghost planes of v = A phat and t = A shat.
+    Returns (x, SolverStats) with x consistent on every local plane; the
+    iterates are those of krylov.bicgstab_solve on the global system up to
+    the order of the cross-rank sums.
+    """
+    import numpy as np
+
+    from . import _lib
+    from .errors import SolverBreakdownError
+    from .krylov import _BICG_BREAKDOWN, B_BNORM, B_IT, B_STATUS, SolverStats
+    from .sparse import axpy_d, dot_d, dot_work, spmv_d
+
+    n, nnz = A.n, A.nnz
+    dev = b.device
+    own_lo, own_hi = layout.owned_rows
+    if max_iter is None:  # 10 x the global unknown count, identical on every rank
+        nglob = torch.tensor([float(own_hi - own_lo)], dtype=torch.float64, device=dev)
+        max_iter = 10 * int(allreduce_sum_(nglob, group).item())
+    d = None
+    if jacobi:
+        # ghost-plane rows are partial locally: their diagonal comes from the
+        # neighbour, so phat = p / d and shat = s / d are global on every plane
+        d = refresh_ghosts(layout, A.diagonal_d(), group)
+        own_zero = (d[own_lo:own_hi] == 0.0).any().to(torch.float64).reshape(1)
+        if allreduce_sum_(own_zero, group).item() > 0:
+            raise SolverBreakdownError("Jacobi preconditioner needs a nonzero diagonal")
+    x, r, rt, p, ph, v, sv, sh, t = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(9))
+    lib = _lib.load()
+    state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
+    red = state[16:18]
+    cap = max(1, min(64, max_iter))
+    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
+    work = dot_work()
+    s = _lib.stream()
+    rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
+    x0p = x0.data_ptr() if x0 is not None else None
+    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
+              rt.data_ptr(), p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol),
+              own_lo, own_hi, 1, work.data_ptr(), s)
+    if x0 is not None:  # r = b - A x0 is exact on computed rows only
+        refresh_ghosts(layout, r, group)
+        rt.copy_(r)
+    allreduce_sum_(red, group)
+    _lib.call("fpb_bicgstab_finish", 0, state.data_ptr(), hist_d.data_ptr(), 1, float(tol), s)
+    st = state.cpu().numpy()
+    if st[B_BNORM] == 0.0:
+        return torch.zeros(n, dtype=torch.float64, device=dev), SolverStats(0, True, [0.0], 0.0)
+    history = [float(hist_d[0].item())]
+    if st[B_STATUS] == 1.0:
+        return x, SolverStats(0, True, history, history[0])
+    if st[B_STATUS] in _BICG_BREAKDOWN:
+        raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
+    args = (n, nnz, rp, ci, va, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
+            rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
+            t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap, own_lo, own_hi, 1, work.data_ptr(), s)
+    done = 0
+    while done < max_iter:
+        k = min(check_every, max_iter - done)
+        for _ in range(k):
+            for step, ghost in ((1, v), (2, None), (3, t), (4, None)):
+                _lib.call("fpb_bicgstab_step", step, *args)
+                if ghost is not None:
+                    refresh_ghosts(layout, ghost, group)
+                allreduce_sum_(red, group)
+                _lib.call("fpb_bicgstab_finish", step, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+        st = state.cpu().numpy()
+        it = int(st[B_IT])
+        if it > done:
+            h = hist_d.cpu().numpy()
+            history.extend(float(h[i % cap]) for i in range(done + 1, it + 1))
+        progressed = it > done
+        done = it
+        if st[B_STATUS] in _BICG_BREAKDOWN:
+            raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
+        if st[B_STATUS] == 1.0 or not progressed:
+            break
+    converged = bool(st[B_STATUS] == 1.0)
+    # true residual over the owned rows, summed across ranks
+    refresh_ghosts(layout, x, group)
+    res = axpy_d(-1.0, spmv_d(A, x), b)
+    rr = dot_d(res[own_lo:own_hi].contiguous(), res[own_lo:own_hi].contiguous()).reshape(1).clone()
+    allreduce_sum_(rr, group)
+    true_residual = float(np.sqrt(rr.item())) / float(st[B_BNORM])
+    return x, SolverStats(done, converged, history, true_residual)

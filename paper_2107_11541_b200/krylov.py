@@ -140,7 +140,8 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
     nnz = A.nnz
     _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, bd.data_ptr(),
               x0d.data_ptr() if x0d is not None else None, x.data_ptr(), r.data_ptr(), rt.data_ptr(),
-              p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol), work.data_ptr(), s)
+              p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol), 0, n, 0,
+              work.data_ptr(), s)
     st = state.cpu().numpy()
     out = to_host if host else (lambda q: q)
     if st[B_BNORM] == 0.0:

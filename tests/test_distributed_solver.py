@@ -1,0 +1,176 @@
+"""Distributed solver plumbing: ghost-plane refresh, owned-
+row reductions and the slab BiCGSTAB.
+
+CPU (gloo, world 2 and 3): the host logic on torch CPU tensors — after
+refresh_ghosts every local entry equals the global vector's, the owned-row
+partials of all ranks sum to the global dot, allreduce_sum_ is a sum.
+GPU (gloo through the host, 2 ranks sharing the box's one B200): the real
+slab BiCGSTAB (device kernels, owned-row reductions, deferred scalar
+finishes) reproduces the single-domain device solve."""
+
+import datetime
+import os
+import tempfile
+import traceback
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import fempack_np as O
+from paper_2107_11541_b200.distributed import (SlabLayout, allreduce_sum_, ghost_planes, refresh_ghosts)
+
+NX, NY, NZ = 4, 3, 7
+
+
+def _run(world, target, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with tempfile.TemporaryDirectory() as d:
+        initfile = os.path.join(d, "init")
+        procs = [ctx.Process(target=target, args=(r, world, initfile, q) + args) for r in range(world)]
+        for p in procs:
+            p.start()
+        out = q.get(timeout=240)
+        for p in procs:
+            p.join(timeout=60)
+            if p.exitcode is None:
+                p.kill()
+        if isinstance(out, str):
+            raise AssertionError(out)
+        for p in procs:
+            assert p.exitcode == 0
+    return out
+
+
+def _plumbing_worker(rank, world, initfile, q):
+    dist.init_process_group("gloo", init_method=f"file://{initfile}", rank=rank, world_size=world)
+    try:
+        L = SlabLayout.make(NX, NY, NZ, rank, world)
+        nglob = (NX + 1) * (NY + 1) * (NZ + 1)
+        g = torch.as_tensor(np.random.default_rng(7).standard_normal(nglob))
+        loc = g[L.node_offset:L.node_offset + L.nnode].clone()
+        for _, _, kg in ghost_planes(L):  # poison the ghost planes
+            lo, hi = L.plane_rows(kg)
+            loc[lo:hi] = float("nan")
+        refresh_ghosts(L, loc)
+        ok_refresh = bool(torch.equal(loc, g[L.node_offset:L.node_offset + L.nnode]))
+        lo, hi = L.owned_rows
+        part = torch.tensor([float((loc[lo:hi] * loc[lo:hi]).sum()), float(rank + 1)], dtype=torch.float64)
+        allreduce_sum_(part)
+        res = {"refresh": ok_refresh, "dot": float(part[0]), "ranks": float(part[1]),
+               "want": float((g * g).sum())}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, res)
+        if rank == 0:
+            q.put(gathered)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ghost_refresh_and_owned_reductions(world):
+    parts = _run(world, _plumbing_worker)
+    for p in parts:
+        assert p["refresh"]
+        assert p["ranks"] == world * (world + 1) / 2
+        assert p["dot"] == pytest.approx(p["want"], rel=1e-13)
+
+
+def test_ghost_plan_covers_neighbours():
+    for world in (2, 3, 4):
+        for r in range(world):
+            L = SlabLayout.make(NX, NY, NZ, r, world)
+            plan = ghost_planes(L)
+            assert len(plan) == (r > 0) + (r < world - 1)
+            for peer, ks, kg in plan:
+                P = SlabLayout.make(NX, NY, NZ, peer, world)
+                # what the peer sends is what I receive: its plane ks is my ghost plane kg
+                (_, ks2, kg2), = [t for t in ghost_planes(P) if t[0] == r]
+                assert ks2 == kg and kg2 == ks
+                # and the sent plane lies in the sender's exactly computed range
+                assert L.k0 <= ks <= L.k1
+
+
+# ------------------------------------------------------------------ device
+def _system_slab(P, dom, vel_g, b_g, dt=0.05, kappa=0.01):
+    L = dom.layout
+    ctx = dom.ctx
+    v = torch.as_tensor(vel_g[L.node_offset:L.node_offset + L.nnode], device="cuda")
+    nnz = ctx.pattern.nnz
+    mats = []
+    for kind, vel in ((P.KernelKind.MASS, None), (P.KernelKind.CONVECTION, v), (P.KernelKind.LAPLACIAN, None)):
+        m = torch.empty(nnz, dtype=torch.float64, device="cuda")
+        ctx.assemble_matrix_d(kind, vel, m)
+        dom.halo_sum_matrix(m)
+        mats.append(m)
+    vals = mats[0] + dt * (mats[1] + kappa * mats[2])
+    A = ctx.pattern.with_vals(vals)
+    b = torch.as_tensor(b_g[L.node_offset:L.node_offset + L.nnode], device="cuda")
+    return A, b
+
+
+def _solver_worker(rank, world, initfile, q, dims):
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200.distributed import SlabDomain, bicgstab_slab
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"file://{initfile}", rank=rank, world_size=world,
+                            timeout=datetime.timedelta(seconds=120))
+    try:
+        nx, ny, nz = dims
+        nglob = (nx + 1) * (ny + 1) * (nz + 1)
+        vel_g, sc = O.bench_fields(nglob, 3)
+        dom = SlabDomain.build(nx, ny, nz, rank, world)
+        A, b = _system_slab(P, dom, vel_g, sc[0])
+        x, st = bicgstab_slab(dom.layout, A, b, tol=1e-10, check_every=4)
+        L = dom.layout
+        x0 = torch.as_tensor(np.linspace(-1.0, 1.0, nglob)[L.node_offset:L.node_offset + L.nnode], device="cuda")
+        x2, st2 = bicgstab_slab(L, A, b, x0=x0, tol=1e-10, check_every=4)
+        lo, hi = L.owned_rows
+        res = {"x": x[lo:hi].cpu().numpy(), "it": st.iterations, "conv": st.converged,
+               "hist": st.residual_history, "tr": st.true_residual,
+               "consistent": bool(torch.isfinite(x).all()),
+               "x2": x2[lo:hi].cpu().numpy(), "it2": st2.iterations, "conv2": st2.converged}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, res)
+        if rank == 0:
+            q.put(gathered)
+    except Exception:
+        q.put(f"rank {rank}: " + traceback.format_exc())
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_bicgstab_reproduces_single_domain(cuda_ok, world):
+    import paper_2107_11541_b200 as P
+
+    dims = (9, 8, 11)
+    parts = _run(world, _solver_worker, dims)
+    nx, ny, nz = dims
+    full = P.AssemblyContext.build(P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz), 8)
+    n = full.mesh.nnode
+    vel_g, sc = O.bench_fields(n, 3)
+    M = full.assemble_matrix(P.KernelKind.MASS)
+    C = full.assemble_matrix(P.KernelKind.CONVECTION, velocity=vel_g)
+    Lp = full.assemble_matrix(P.KernelKind.LAPLACIAN)
+    A = M.with_vals(M.vals_d + 0.05 * (C.vals_d + 0.01 * Lp.vals_d))
+    x, st = P.bicgstab_solve(A, sc[0], tol=1e-10)
+    got = np.concatenate([p["x"] for p in parts])
+    assert got.shape == x.shape
+    for p in parts:
+        assert p["conv"] and p["consistent"]
+        assert abs(p["it"] - st.iterations) <= 1
+        assert p["tr"] < 1.01e-10
+        k = min(len(p["hist"]), len(st.residual_history), 6)
+        np.testing.assert_allclose(p["hist"][:k], st.residual_history[:k], rtol=1e-9)
+    assert O.rel_diff(got, x) < 1e-8
+    xb, stb = P.bicgstab_solve(A, sc[0], x0=np.linspace(-1.0, 1.0, n), tol=1e-10)
+    for p in parts:
+        assert p["conv2"] and abs(p["it2"] - stb.iterations) <= 1
+    assert O.rel_diff(np.concatenate([p["x2"] for p in parts]), xb) < 1e-8
