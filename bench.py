@@ -45,6 +45,19 @@ FP64_PEAK_TFLOPS = 34.1
 HBM_FALLBACK_GBS = 6650.0
 # SURVEY 8(d) algorithmic work per TET04 element (flops, compulsory bytes)
 WORK = {"momentum_rhs": (1492.0, 28.0), "gradient_xyz": (676.0, 145.0)}
+# SURVEY 8(d) per-element work for the config-3 / config-4 kernels: F =
+# G_min + K + S (instrumented reference flop counts), B = compulsory HBM
+# bytes (int32 conn, f64 node data at rho_n = nnode/nelem, CSR values at
+# rho_z = nnz/nelem plus the int32 element->CSR map for matrices).  TET04
+# values are SURVEY's (config-2 mesh); HEX08 F from SURVEY's bounds at
+# 37.2 TF/s nominal, B from the same formula at config 4 (rho_n 1.011,
+# rho_z 27.10).
+WORK_C = {
+    ("TET04", "scalar_rhs"): (592.0, 27.0),
+    ("HEX08", "momentum_rhs"): (7328.0, 105.0),
+    ("HEX08", "scalar_rhs"): (4248.0, 97.0),
+    ("HEX08", "gradient_xyz"): (6169.0, 962.0),
+}
 L2_FLUSH_BYTES = 512 << 20
 
 
@@ -96,6 +109,98 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
                 "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _roof(F, B, ms, nelem, hbm):
+    """Roofline of one kernel at F flops / B bytes per element."""
+    t = ms / 1e3
+    fl, by = F * nelem / t / 1e12, B * nelem / t / 1e9
+    if F / B > FP64_PEAK_TFLOPS * 1e3 / hbm:
+        return {"bound": "fp64", "achieved": fl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": fl / FP64_PEAK_TFLOPS}
+    return {"bound": "hbm", "achieved": by, "peak": hbm, "unit": "GB/s", "frac": by / hbm}
+
+
+def _time_ms(fn, reps, flush):
+    import torch
+
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def config3_block(ctx, vel, flush, hbm, reps=10):
+    """Config 3: scalar transport (enthalpy + 2 species) on the config-2 mesh;
+    the solver vector ops are in the "solver" block."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+
+    n, ne = ctx.mesh.nnode, ctx.mesh.nelem
+    rng = np.random.default_rng(0)
+    rng.standard_normal((n, 3))
+    phis = [torch.as_tensor(rng.standard_normal(n), device=vel.device) for _ in range(3)]
+    outs = [torch.empty(n, dtype=torch.float64, device=vel.device) for _ in range(3)]
+    kap = (1e-2, 1e-2, 1e-2)  # kappa, D, D (timeloop.py:76-79)
+
+    def three():
+        for phi, o, k in zip(phis, outs, kap):
+            ctx.assemble_rhs_d(P.KernelKind.SCALAR_RHS, vel, phi, 1.0, 0.0, k, o)
+
+    ms = _time_ms(three, reps, flush)
+    F, B = WORK_C[("TET04", "scalar_rhs")]
+    return {"workload": "config 3: TET04 94x94x95, SCALAR_RHS x3 (heat kappa, 2 species D), velocity + scalars "
+                        "default_rng(0) draws", "elements": ne, "ms_per_step": ms,
+            "value": 3 * ne / (ms / 1e3) / 1e6, "unit": "Melem/s (element-scalar assemblies)",
+            "roofline": dict(_roof(F, B, ms / 3, ne, hbm), kernel="scalar_rhs", work_per_element={"flops": F, "bytes": B})}
+
+
+def config4_block(flush, hbm, n=272, reps=5):
+    """Config 4: 20,123,648-element HEX08 (Q1, 8 Gauss points) box, full NS +
+    scalar assembly: momentum RHS, continuity B_x,B_y,B_z and three scalar
+    RHS per step."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+
+    mesh = P.generate_box_mesh(P.ElementType.HEX08, n, n, n)
+    ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    ctx.refresh_geometry("packed", need_grad=False)
+    nn_, ne, nnz = mesh.nnode, mesh.nelem, ctx.pattern.nnz
+    dev = flush.device
+    rng = np.random.default_rng(0)
+    vel = torch.as_tensor(rng.standard_normal((nn_, 3)), device=dev)
+    phis = [torch.as_tensor(rng.standard_normal(nn_), device=dev) for _ in range(3)]
+    rhs = torch.empty((nn_, 3), dtype=torch.float64, device=dev)
+    srhs = torch.empty(nn_, dtype=torch.float64, device=dev)
+    mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
+    K = P.KernelKind
+    parts = {
+        "momentum_rhs": lambda: ctx.assemble_rhs_d(K.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs),
+        "gradient_xyz": lambda: ctx.assemble_gradients_d(mats),
+        "scalar_rhs": lambda: [ctx.assemble_rhs_d(K.SCALAR_RHS, vel, ph, 1.0, 0.0, 1e-2, srhs) for ph in phis],
+    }
+    ms = {k: _time_ms(f, reps, flush) for k, f in parts.items()}
+    roof = {}
+    for k, t in ms.items():
+        F, B = WORK_C[("HEX08", k)]
+        per = t / (3 if k == "scalar_rhs" else 1)
+        roof[k] = dict(_roof(F, B, per, ne, hbm), ms=per)
+    total = sum(ms.values())
+    del ctx, mats
+    torch.cuda.empty_cache()
+    return {"workload": f"config 4: HEX08 box {n}^3 ({ne} elements, {nn_} nodes, nnz {nnz}), momentum RHS + "
+                        "B_x,B_y,B_z + 3 scalar RHS", "elements": ne, "ms_per_step": total,
+            "value": ne / (total / 1e3) / 1e6, "unit": "Melem/s", "kernels": roof}
 
 
 def cpu_baseline(nx, ny, nz_sample, steps=3, warmup=1):
@@ -155,6 +260,7 @@ def main():
     ap.add_argument("--scatter", default="auto", choices=["auto", "rows", "atomic"],
                     help="global-assembly strategy (AssemblyContext.build)")
     ap.add_argument("--no-solver", action="store_true", help="skip the solver vector-kernel block")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-3 / config-4 blocks")
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds under load before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -262,7 +368,14 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": bytes_rate, "peak": hbm, "unit": "GB/s",
                 "frac": bytes_rate / hbm, "peak_source": hbm_src}
-    roof.update({"kernel": dom, "traffic": None,
+    traffic = None
+    try:  # measured DRAM bytes per launch of this kernel (ncu --set full, profiles/traffic.json)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh)[dom]["bytes"]
+    except Exception:
+        traffic = None
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_unit": "bytes per launch",
+                 "algorithmic_bytes": B * nelem,
                  "work_per_element": {"flops": F, "bytes": B, "source": "SURVEY.md 8(d)"}})
 
     # e2e through the public API with host buffers
@@ -300,6 +413,13 @@ def main():
 
         solver = solver_metrics(ctx, 16_974_593, hbm=hbm)
 
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = {"c3": config3_block(ctx, vel, flush, hbm)}
+        del mats
+        torch.cuda.empty_cache()
+        configs["c4"] = config4_block(flush, hbm)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -319,10 +439,14 @@ def main():
                        "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
             "kernels_ms": kern,
-            "gpu_launches": args.steps * 2 * len(ctx.groups),
+            # per step: pack the velocity records, element-block momentum RHS
+            # (integrate + partial gather), row-owned B_x,B_y,B_z — 4 launches
+            # (profiles/r01e_step/launches.csv); + halo has no kernels of ours
+            "gpu_launches": args.steps * 4,
             "clocks": clk,
             "e2e": e2e,
             "solver": solver,
+            "configs": configs,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
