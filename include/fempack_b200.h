@@ -178,6 +178,24 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, 
                       const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
                       const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream);
 
+/* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
+ * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices
+ * (fpb_incidence_build, element ids); fpb_incidence_slots8 fills
+ * slots[2 * 32 * ncols] (one uint2 per entry): byte b = 0xff for the row's
+ * own node, else node b's offset in the row's column list with the diagonal
+ * skipped; missing pairs -> FPB_EPATTERN; longest row through rowcap_h
+ * (synchronous).  fpb_assemble_rows_gl overwrites (accumulate = 0) or adds
+ * to (1) out (FPB_GRADIENT_XYZ: dim arrays of nnz); each row thread
+ * evaluates its incident elements' Gauss loops itself — no atomics, bitwise
+ * reproducible. */
+int fpb_incidence_slots8(int32_t n, int nn, int64_t ncols, const int32_t* slice_ptr, const int32_t* inc,
+                         const int32_t* conn, const int32_t* rowptr, const int32_t* colind, uint32_t* slots,
+                         int* rowcap_h, void* stream);
+int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+                         const int32_t* conn, const uint32_t* slots, const double* xyz4, const double* uvw4,
+                         const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap, int accumulate,
+                         double* out, void* stream);
+
 /* ---- element-block RHS assembly (deterministic, atomic-free) ------------
  * Blocks of fpb_block_elems() consecutive elements; phase 1 integrates each
  * element once and reduces inside the block (sorted gather lists), phase 2

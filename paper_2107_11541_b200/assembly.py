@@ -80,16 +80,17 @@ def matrix_positions(conn, pattern: CsrMatrix) -> np.ndarray:
 
 
 ROW_OWNED = ("TRI03", "TET04")  # affine simplices: row-owned kernels (rows.cu)
+ROW_OWNED_GAUSS = ("QUAD04", "PYR05", "HEX08")  # Gauss-loop elements: row-owned matrices (rowsq.cu)
 
 
 class RowPlan:
     """SELL-32 node->element incidence of one affine group, plus (for
     matrices) the row-local column offsets of every incidence (rows.cu)."""
 
-    def __init__(self, conn_d: torch.Tensor, n: int):
+    def __init__(self, conn_d: torch.Tensor, n: int, gauss: bool = False):
         nn = int(conn_d.shape[1])
         nsl = -(-n // 32)
-        self.n, self.nn = n, nn
+        self.n, self.nn, self.gauss = n, nn, gauss
         self.slice_ptr = torch.empty(nsl + 1, dtype=torch.int32, device=conn_d.device)
         ncols = np.zeros(1, dtype=np.int64)
         lib = _lib.load()
@@ -100,26 +101,29 @@ class RowPlan:
         self.inc = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
         _lib.check(lib.fpb_incidence_build(*args, self.inc.data_ptr(), pn, _lib.stream()),
                    "fpb_incidence_build")
-        # inline node ids per entry (int4), rotated so the row's node is
-        # local node 0: one dependent load level less in the hot loop
-        # (profiles/r01_rows_variants.txt) and no per-element node search
-        self.incn = torch.empty(max(self.ncols, 1) * 32 * 4, dtype=torch.int32, device=conn_d.device)
-        _lib.check(lib.fpb_incidence_nodes(n, self.ncols, nn, self.slice_ptr.data_ptr(), self.inc.data_ptr(),
-                                           conn_d.data_ptr(), self.incn.data_ptr(), _lib.stream()),
-                   "fpb_incidence_nodes")
+        self.incn = None
+        if not gauss:
+            # inline node ids per entry (int4), rotated so the row's node is
+            # local node 0: one dependent load level less in the hot loop
+            # (profiles/r01_rows_variants.txt) and no per-element node search
+            self.incn = torch.empty(max(self.ncols, 1) * 32 * 4, dtype=torch.int32, device=conn_d.device)
+            _lib.check(lib.fpb_incidence_nodes(n, self.ncols, nn, self.slice_ptr.data_ptr(),
+                                               self.inc.data_ptr(), conn_d.data_ptr(), self.incn.data_ptr(),
+                                               _lib.stream()), "fpb_incidence_nodes")
         self.slots = None
         self.rowcap = 0
 
     def ensure_slots(self, conn_d: torch.Tensor, pattern: "CsrMatrix") -> None:
         if self.slots is not None:
             return
-        slots = torch.empty(max(self.ncols, 1) * 32, dtype=torch.int32, device=conn_d.device)
+        words = 2 if self.gauss else 1  # uint2 per entry for up to 8 nodes
+        slots = torch.empty(max(self.ncols, 1) * 32 * words, dtype=torch.int32, device=conn_d.device)
         cap = np.zeros(1, dtype=np.int32)
-        _lib.check(_lib.load().fpb_incidence_slots(
+        fn = "fpb_incidence_slots8" if self.gauss else "fpb_incidence_slots"
+        _lib.check(getattr(_lib.load(), fn)(
             self.n, self.nn, self.ncols, self.slice_ptr.data_ptr(), self.inc.data_ptr(),
             conn_d.data_ptr(), pattern.rowptr_d.data_ptr(), pattern.colind_d.data_ptr(),
-            slots.data_ptr(), cap.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _lib.stream()),
-            "fpb_incidence_slots")
+            slots.data_ptr(), cap.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _lib.stream()), fn)
         self.slots, self.rowcap = slots, int(cap[0])
 
 
@@ -263,8 +267,8 @@ class AssemblyContext:
             gd = GroupData(reference_element(g.etype), g.conn_d, offset, ps, lane32, pattern)
             if scatter == "auto":
                 gd.blocks = BlockPlan(g.conn_d, mesh.nnode)
-            if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED:
-                gd.rows = RowPlan(g.conn_d, mesh.nnode)
+            if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
+                gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time
             else:
                 _ = gd.pos32  # ScatterPatternError at build time, as in the reference
@@ -336,7 +340,8 @@ class AssemblyContext:
         matrix = kind_id in (0, 1, 2, GRADIENT_XYZ)
         # owner-writes paths (row-owned matrices, element-block RHS) overwrite
         # their output; anything else accumulates into a zeroed buffer
-        owner = [(g.rows is not None) if matrix else (g.blocks is not None or g.rows is not None)
+        owner = [(g.rows is not None) if matrix
+                 else (g.blocks is not None or (g.rows is not None and not g.rows.gauss))
                  for g in self.groups]
         single_rows = len(self.groups) == 1 and owner[0]
         if not single_rows:
@@ -360,6 +365,12 @@ class AssemblyContext:
                           bp.blk_lidx.data_ptr(), bp.maxnu,
                           bp.partial(nv, out.device).data_ptr(), self.mesh.nnode, bp.node_pptr.data_ptr(),
                           bp.node_plist.data_ptr(), 0 if single_rows else 1, out.data_ptr(), _lib.stream())
+            elif own and g.rows.gauss:
+                r = g.rows
+                _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
+                          r.inc.data_ptr(), g.conn_d.data_ptr(), r.slots.data_ptr(), xyz4, uvw4,
+                          self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
+                          0 if single_rows else 1, out.data_ptr(), _lib.stream())
             elif own:
                 r = g.rows
                 _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
