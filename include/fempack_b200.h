@@ -301,6 +301,58 @@ int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, c
                       int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream);
 int fpb_bicgstab_finish(int step, double* state, double* hist, int64_t hist_cap, double tol, void* stream);
 
+/* ---- time-loop support (flow.cu) --------------
+ * Pressure-operator setup on the device, each mirroring a reference routine:
+ *   fpb_csr_transpose      transpose_csr (sparse.py:133-138); trowptr[n+1]
+ *   fpb_spgemm_count/fill  spgemm (sparse.py:141-188): counts[n] per row,
+ *                          then colind/vals at the caller's rowptr (exclusive
+ *                          scan of counts); values summed in the reference's
+ *                          product order (bitwise equal)
+ *   fpb_scale_rows         A.vals * d[rows] (normal_product, sparse.py:191-194)
+ *   fpb_csr_add_count/fill csr_add (sparse.py:197-214), union of patterns
+ *   fpb_apply_dirichlet    apply_dirichlet (sparse.py:219-254): flag[n] (1 =
+ *                          constrained), lift[n] = values on constrained
+ *                          nodes; b (nullable) updated in place
+ *   fpb_robin              assemble_boundary (assembly.py:383-411) for one
+ *                          face group: face rule N[nnf][ng], dN[dim-1][nnf][ng],
+ *                          wts[ng]; vals (via the face->CSR map pos) and rhs
+ *                          accumulated
+ * FlowSolver.step stages (timeloop.py:367-440), numpy rounding order:
+ *   fpb_stage_momentum  un = a u0 + b (uc + dt_rho ((r [+ load - Ru_k] - grad_p) / lumped))
+ *                       (u0, uc, r, grad_p, un: [n][dim]; Ru: [dim][n])
+ *   fpb_stage_scalar    sn = a phi0 + b (phi + dt (rs / lumped))
+ *   fpb_set_rows        u[nodes[q]][:] = values[q][:] (values NULL -> 0)
+ *   fpb_sub_into        div -= s; g = scale * div when g != NULL
+ *   fpb_correct         un[:, k] = uc[:, k] - dt_rho * (dflag ? 0 : s / lumped) */
+int fpb_csr_transpose(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                      int32_t* trowptr, int32_t* tcolind, double* tvals, void* stream);
+int fpb_spgemm_count(int32_t n, const int32_t* arp, const int32_t* aci, const int32_t* brp, const int32_t* bci,
+                     int32_t* counts, void* stream);
+int fpb_spgemm_fill(int32_t n, const int32_t* arp, const int32_t* aci, const double* av, const int32_t* brp,
+                    const int32_t* bci, const double* bv, const int32_t* rowptr, int32_t* colind, double* vals,
+                    void* stream);
+int fpb_scale_rows(int32_t n, const int32_t* rowptr, const double* vals, const double* d, double* out,
+                   void* stream);
+int fpb_csr_add_count(int32_t n, const int32_t* arp, const int32_t* aci, const int32_t* brp, const int32_t* bci,
+                      int32_t* counts, void* stream);
+int fpb_csr_add_fill(int32_t n, const int32_t* arp, const int32_t* aci, const double* av, const int32_t* brp,
+                     const int32_t* bci, const double* bv, const int32_t* rowptr, int32_t* colind, double* vals,
+                     void* stream);
+int fpb_apply_dirichlet(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+                        const uint8_t* flag, const double* lift, double* out, double* b, void* stream);
+int fpb_robin(int64_t nf, int nnf, int ng, int dim, const int32_t* conn, const double* coords, const double* N,
+              const double* dN, const double* wts, const int32_t* pos, double alpha, double beta, double* vals,
+              double* rhs, void* stream);
+int fpb_stage_momentum(int64_t n, int dim, double a, double b, double dt_rho, const double* u0, const double* uc,
+                       const double* r, const double* grad_p, const double* lumped, const double* load,
+                       const double* Ru, double* un, void* stream);
+int fpb_stage_scalar(int64_t n, double a, double b, double dt, const double* phi0, const double* phi,
+                     const double* rs, const double* lumped, double* sn, void* stream);
+int fpb_set_rows(int64_t m, int dim, const int64_t* nodes, const double* values, double* u, void* stream);
+int fpb_sub_into(int64_t n, const double* s, double* div, double scale, double* g, void* stream);
+int fpb_correct(int64_t n, int dim, int k, double dt_rho, const double* s, const double* lumped,
+                const uint8_t* dflag, const double* uc, double* un, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

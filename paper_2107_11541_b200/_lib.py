@@ -46,6 +46,19 @@ SIGNATURES = {
     "fpb_incidence_slots8": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
     "fpb_assemble_rows_gl": (_int, [_int, _int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int,
                                     _vp, _vp]),
+    "fpb_csr_transpose": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_spgemm_count": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_spgemm_fill": (_int, [_i32] + [_vp] * 10),
+    "fpb_scale_rows": (_int, [_i32, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_csr_add_count": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_csr_add_fill": (_int, [_i32] + [_vp] * 10),
+    "fpb_apply_dirichlet": (_int, [_i32] + [_vp] * 8),
+    "fpb_robin": (_int, [_i64, _int, _int, _int] + [_vp] * 6 + [_dbl, _dbl, _vp, _vp, _vp]),
+    "fpb_stage_momentum": (_int, [_i64, _int, _dbl, _dbl, _dbl] + [_vp] * 9),
+    "fpb_stage_scalar": (_int, [_i64, _dbl, _dbl, _dbl] + [_vp] * 6),
+    "fpb_set_rows": (_int, [_i64, _int, _vp, _vp, _vp, _vp]),
+    "fpb_sub_into": (_int, [_i64, _vp, _vp, _dbl, _vp, _vp]),
+    "fpb_correct": (_int, [_i64, _int, _int, _dbl] + [_vp] * 6),
     "fpb_block_elems": (_int, []),
     "fpb_blocks_build": (_int, [_i64, _int, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
     "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,

@@ -487,3 +487,50 @@ def lumped_mass(ctx: AssemblyContext, layout: str = "packed") -> np.ndarray:
     if not (lumped > 0.0).all():
         raise ConfigurationError("lumped mass has non-positive entries")
     return lumped
+
+
+# --------------------------------------------------------------------------
+# Robin boundary assembly (assembly.py:383-411)
+# --------------------------------------------------------------------------
+
+def face_rule(nnodes: int):
+    """(ng, N[nnf][ng], dN[fdim][nnf][ng], weights[ng]) of a face (elements.py:348-363)."""
+    from .elements import ElementType
+
+    if nnodes == 2:
+        s3 = 1.0 / np.sqrt(3.0)
+        pts = np.array([-s3, s3])
+        N = np.stack([0.5 * (1.0 - pts), 0.5 * (1.0 + pts)])
+        dN = np.empty((1, 2, 2))
+        dN[0, 0], dN[0, 1] = -0.5, 0.5
+        return 2, N, dN, np.ones(2)
+    if nnodes in (3, 4):
+        ref = reference_element(ElementType.TRI03 if nnodes == 3 else ElementType.QUAD04)
+        return ref.ngauss, np.asarray(ref.N), np.asarray(ref.dN), np.asarray(ref.weights)
+    raise ValueError(f"no face rule for {nnodes}-node faces")
+
+
+def assemble_boundary_d(mesh, pattern: CsrMatrix, alpha: float = 0.0, beta: float = 0.0):
+    """Device Robin structures: (vals[nnz], rhs[n]) as CUDA tensors."""
+    mesh = as_device_mesh(mesh)
+    dev = mesh.coords_d.device
+    vals = torch.zeros(pattern.nnz, dtype=torch.float64, device=dev)
+    rhs = torch.zeros(pattern.n, dtype=torch.float64, device=dev)
+    if alpha == 0.0 and beta == 0.0:
+        return vals, rhs
+    for fg in mesh.boundary:
+        ng, N, dN, w = face_rule(fg.nnodes)
+        Nd, dNd, wd = (torch.as_tensor(np.array(a, dtype=np.float64), device=dev) for a in (N, dN, w))
+        conn = fg.conn_d.to(torch.int32).contiguous()
+        pos = positions_d(conn, pattern, 0, 1) if alpha != 0.0 else None
+        _lib.call("fpb_robin", fg.nfaces, fg.nnodes, ng, mesh.dim, conn.data_ptr(), mesh.coords_d.data_ptr(),
+                  Nd.data_ptr(), dNd.data_ptr(), wd.data_ptr(), pos.data_ptr() if pos is not None else None,
+                  float(alpha), float(beta), vals.data_ptr(), rhs.data_ptr(), _lib.stream())
+    return vals, rhs
+
+
+def assemble_boundary(mesh, pattern: CsrMatrix, alpha: float = 0.0, beta: float = 0.0):
+    """alpha * face mass and beta * face load (assembly.py:383-411): returns
+    (CsrMatrix sharing the pattern, numpy rhs)."""
+    vals, rhs = assemble_boundary_d(mesh, pattern, alpha, beta)
+    return pattern.with_vals(vals), to_host(rhs)

@@ -8,8 +8,10 @@ the reference's (tests/test_gpu_setup.py).  Connectivity is int32 on the
 device; the numpy views (`.coords`, `.conn`) are materialised on demand with
 the reference dtypes (float64 / int64).
 
-Boundary-face extraction (mesh.py:115-155) feeds only the Robin boundary
-assembly, which is outside this path (scope); `boundary` is empty.
+Boundary faces (mesh.py:115-155) are extracted on the device on first use
+(`Mesh.boundary`): faces shared by exactly one element, outward-oriented, in
+the reference's template order; they feed the Robin boundary assembly and
+`boundary_nodes()`.
 """
 
 from __future__ import annotations
@@ -49,8 +51,22 @@ class Mesh:
     dim: int
     coords_d: torch.Tensor
     groups: list[ElementGroup] = field(default_factory=list)
-    boundary: list = field(default_factory=list)
+    _boundary: list | None = field(default=None, repr=False)
     _coords_h: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def boundary(self) -> list:
+        """Boundary FaceGroups (mesh.py:140-155), extracted on first use."""
+        if self._boundary is None:
+            self._boundary = extract_boundary(self.groups)
+        return self._boundary
+
+    def boundary_nodes(self) -> np.ndarray:
+        """Sorted unique node ids on any boundary face (mesh.py:82-86)."""
+        if not self.boundary:
+            return np.empty(0, dtype=np.int64)
+        allnodes = torch.cat([fg.conn_d.reshape(-1) for fg in self.boundary])
+        return torch.unique(allnodes).cpu().numpy().astype(np.int64)
 
     @property
     def coords(self) -> np.ndarray:
@@ -75,6 +91,65 @@ class Mesh:
     def is_grouped_by_type(self) -> bool:
         types = [g.etype for g in self.groups]
         return len(types) == len(set(types))
+
+
+# outward-oriented face templates (elements.py:73-86)
+ELEMENT_FACES = {
+    ElementType.TRI03: ((0, 1), (1, 2), (2, 0)),
+    ElementType.QUAD04: ((0, 1), (1, 2), (2, 3), (3, 0)),
+    ElementType.TET04: ((0, 2, 1), (0, 1, 3), (1, 2, 3), (0, 3, 2)),
+    ElementType.PYR05: ((0, 3, 2, 1), (0, 1, 4), (1, 2, 4), (2, 3, 4), (3, 0, 4)),
+    ElementType.HEX08: ((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (2, 3, 7, 6), (0, 4, 7, 3), (1, 2, 6, 5)),
+}
+
+
+@dataclass
+class FaceGroup:
+    """Boundary faces of one node count (mesh.py:33-47): owner element ids and
+    outward-oriented face nodes, in HBM."""
+
+    nnodes: int
+    owner_d: torch.Tensor
+    conn_d: torch.Tensor
+
+    @property
+    def nfaces(self) -> int:
+        return int(self.conn_d.shape[0])
+
+    @property
+    def owner(self) -> np.ndarray:
+        return self.owner_d.cpu().numpy()
+
+    @property
+    def conn(self) -> np.ndarray:
+        return self.conn_d.cpu().numpy().astype(np.int64)
+
+
+def extract_boundary(groups) -> list:
+    """Faces that belong to exactly one element (mesh.py:140-155), grouped by
+    node count in ascending size, each group in the reference's (group,
+    template, element) order.  Face counting by sorted node tuples on the
+    device (setup only)."""
+    buckets: dict = {}
+    offset = 0
+    for g in groups:
+        for tmpl in ELEMENT_FACES[g.etype]:
+            idx = torch.as_tensor(tmpl, dtype=torch.int64, device=g.conn_d.device)
+            owner = torch.arange(offset, offset + g.nelem, dtype=torch.int64, device=g.conn_d.device)
+            buckets.setdefault(len(tmpl), []).append((owner, g.conn_d.index_select(1, idx)))
+        offset += g.nelem
+    out = []
+    for size in sorted(buckets):
+        owners = torch.cat([o for o, _ in buckets[size]])
+        faces = torch.cat([f for _, f in buckets[size]], dim=0)
+        if faces.shape[0] == 0:
+            continue
+        key = torch.sort(faces.to(torch.int64), dim=1).values
+        _, inverse, counts = torch.unique(key, dim=0, return_inverse=True, return_counts=True)
+        keep = counts[inverse] == 1
+        if bool(keep.any()):
+            out.append(FaceGroup(size, owners[keep].contiguous(), faces[keep].contiguous()))
+    return out
 
 
 def as_device_mesh(mesh) -> Mesh:

@@ -209,3 +209,99 @@ def dot(x, y) -> float:
 def norm2(x) -> float:
     xd, _ = to_device(x)
     return float(np.sqrt(dot_d(xd, xd).item()))
+
+
+# --------------------------------------------------------------------------
+# Pressure-operator setup on the device (sparse.py:133-254; SURVEY.md 8(f)
+# rank 4).  CsrMatrix in, CsrMatrix out; every array stays in HBM.
+# --------------------------------------------------------------------------
+
+def _scan_rowptr(counts: torch.Tensor) -> torch.Tensor:
+    rowptr = torch.zeros(counts.numel() + 1, dtype=torch.int64, device=counts.device)
+    torch.cumsum(counts.to(torch.int64), 0, out=rowptr[1:])
+    if int(rowptr[-1]) >= 2**31:
+        raise ValueError("result has 2^31 or more entries")
+    return rowptr.to(torch.int32)
+
+
+def transpose_csr(A: CsrMatrix) -> CsrMatrix:
+    """A^T; each row lists its entries in ascending original row (sparse.py:133-138)."""
+    dev = A.vals_d.device
+    trp = torch.empty(A.n + 1, dtype=torch.int32, device=dev)
+    tci = torch.empty(A.nnz, dtype=torch.int32, device=dev)
+    tv = torch.empty(A.nnz, dtype=torch.float64, device=dev)
+    _lib.call("fpb_csr_transpose", A.n, A.nnz, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+              trp.data_ptr(), tci.data_ptr(), tv.data_ptr(), _lib.stream())
+    return CsrMatrix(A.n, trp, tci, tv)
+
+
+def spgemm(A: CsrMatrix, B: CsrMatrix) -> CsrMatrix:
+    """A @ B with sorted columns; values summed in the reference's product
+    order, so they are bitwise _spgemm_fill's (sparse.py:141-188)."""
+    if A.n != B.n:
+        raise ValueError("dimension mismatch")
+    dev = A.vals_d.device
+    counts = torch.empty(A.n, dtype=torch.int32, device=dev)
+    _lib.call("fpb_spgemm_count", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), B.rowptr_d.data_ptr(),
+              B.colind_d.data_ptr(), counts.data_ptr(), _lib.stream())
+    rowptr = _scan_rowptr(counts)
+    nnz = int(rowptr[-1])
+    colind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.call("fpb_spgemm_fill", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+              B.rowptr_d.data_ptr(), B.colind_d.data_ptr(), B.vals_d.data_ptr(), rowptr.data_ptr(),
+              colind.data_ptr(), vals.data_ptr(), _lib.stream())
+    return CsrMatrix(A.n, rowptr, colind, vals)
+
+
+def normal_product(A: CsrMatrix, d) -> CsrMatrix:
+    """A^T diag(d) A (sparse.py:191-194)."""
+    dd = to_device(d)[0]
+    scaled = torch.empty_like(A.vals_d)
+    _lib.call("fpb_scale_rows", A.n, A.rowptr_d.data_ptr(), A.vals_d.data_ptr(), dd.data_ptr(),
+              scaled.data_ptr(), _lib.stream())
+    return spgemm(transpose_csr(A), A.with_vals(scaled))
+
+
+def csr_add(A: CsrMatrix, B: CsrMatrix) -> CsrMatrix:
+    """A + B over the union pattern (sparse.py:197-214)."""
+    if A.n != B.n:
+        raise ValueError("dimension mismatch")
+    dev = A.vals_d.device
+    counts = torch.empty(A.n, dtype=torch.int32, device=dev)
+    _lib.call("fpb_csr_add_count", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), B.rowptr_d.data_ptr(),
+              B.colind_d.data_ptr(), counts.data_ptr(), _lib.stream())
+    rowptr = _scan_rowptr(counts)
+    nnz = int(rowptr[-1])
+    colind = torch.empty(nnz, dtype=torch.int32, device=dev)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.call("fpb_csr_add_fill", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+              B.rowptr_d.data_ptr(), B.colind_d.data_ptr(), B.vals_d.data_ptr(), rowptr.data_ptr(),
+              colind.data_ptr(), vals.data_ptr(), _lib.stream())
+    return CsrMatrix(A.n, rowptr, colind, vals)
+
+
+def apply_dirichlet(A: CsrMatrix, nodes, values=None, b=None):
+    """Symmetric elimination of Dirichlet nodes (sparse.py:219-254): returns
+    (modified copy, modified b or None); numpy b -> numpy b."""
+    dev = A.vals_d.device
+    nodes_d = torch.as_tensor(np.asarray(nodes, dtype=np.int64) if not isinstance(nodes, torch.Tensor) else nodes,
+                              device=dev).to(torch.int64)
+    flag = torch.zeros(A.n, dtype=torch.uint8, device=dev)
+    flag[nodes_d] = 1
+    out = torch.empty_like(A.vals_d)
+    bd, host = (None, False)
+    lift = None
+    if b is not None:
+        bd, host = to_device(b)
+        bd = bd.clone()
+        lift = torch.zeros(A.n, dtype=torch.float64, device=dev)
+        if values is not None:
+            lift[nodes_d] = to_device(values)[0]
+    _lib.call("fpb_apply_dirichlet", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+              flag.data_ptr(), lift.data_ptr() if lift is not None else None, out.data_ptr(),
+              bd.data_ptr() if bd is not None else None, _lib.stream())
+    res = CsrMatrix(A.n, A.rowptr_d, A.colind_d, out, A._host)
+    if bd is None:
+        return res, None
+    return res, (to_host(bd) if host else bd)
