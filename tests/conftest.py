@@ -21,7 +21,10 @@ def load_golden(name):
 
 
 def golden_names():
-    return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f != "elements.npz")
+    """Assembly / solver cases (tools/make_golden.py); the time-loop fixtures
+    flow_*.npz (tools/make_golden_flow.py) are listed by tests/test_flow.py."""
+    return sorted(f[:-4] for f in os.listdir(GOLDEN)
+                  if f.endswith(".npz") and f != "elements.npz" and not f.startswith("flow_"))
 
 
 @pytest.fixture(scope="session")
