@@ -138,6 +138,64 @@ __global__ void __launch_bounds__(256) k_spmv(int32_t n, const int32_t* __restri
   }
 }
 
+// Multi-group SpMV: each warp pass covers R groups of 32/G rows and issues
+// every (column, value) load of all R groups before the first dependent x
+// gather, so a warp keeps R times more bytes in flight across the
+// load -> gather -> reduce chain (the one-group kernel above is latency-bound
+// at ~56 % of HBM on config 2, profiles/r01f_spmv).  Same per-row order:
+// lane sums in ascending entry order, then the fixed xor tree.
+#ifndef FPB_SPMV_ITEMS
+#define FPB_SPMV_ITEMS 2
+#endif
+template <int G, int R, int ITEMS = FPB_SPMV_ITEMS>
+__global__ void __launch_bounds__(256) k_spmv_r(int32_t n, const int32_t* __restrict__ rowptr,
+                                                const int32_t* __restrict__ colind,
+                                                const double* __restrict__ vals,
+                                                const double* __restrict__ x, double* __restrict__ y) {
+  constexpr int RPW = 32 / G;  // rows per group
+  const int sub = threadIdx.x & (G - 1);
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = wid * RPW * R; base < n; base += nw * RPW * R) {
+    int lo[R], hi[R], col[R][ITEMS];
+    double v[R][ITEMS], acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int64_t row = base + r * RPW + (threadIdx.x & 31) / G;
+      lo[r] = row < n ? __ldg(rowptr + row) : 0;
+      hi[r] = row < n ? __ldg(rowptr + row + 1) : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int it = 0; it < ITEMS; ++it) {
+        const int k = lo[r] + sub + it * G;
+        col[r][it] = k < hi[r] ? __ldcs(colind + k) : -1;
+        v[r][it] = k < hi[r] ? __ldcs(vals + k) : 0.0;
+      }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double a = 0.0;
+#pragma unroll
+      for (int it = 0; it < ITEMS; ++it)
+        if (col[r][it] >= 0) a += v[r][it] * __ldg(x + col[r][it]);
+      for (int k = lo[r] + sub + ITEMS * G; k < hi[r]; k += G) a += __ldcs(vals + k) * __ldg(x + __ldcs(colind + k));
+      acc[r] = a;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o, G);
+      const int64_t row = base + r * RPW + (threadIdx.x & 31) / G;
+      if (row < n && sub == 0) y[row] = acc[r];
+    }
+  }
+}
+
+#ifndef FPB_SPMV_GROUPS
+#define FPB_SPMV_GROUPS 4
+#endif
+
 __global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x,
                        const double* __restrict__ y, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -603,11 +661,16 @@ int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colin
   cudaStream_t s = as_stream(stream);
   // lanes per row from the mean row length (tet ~15 -> 8, hex ~27 -> 16)
   const double mean = (double)nnz / n;
+#ifdef FPB_SPMV_G
+  const int G = FPB_SPMV_G;
+#else
   const int G = mean <= 6.0 ? 4 : (mean <= 20.0 ? 8 : 16);
-  int grid = grid_for((int64_t)n * G, 256, 16);
-  if (G == 4) k_spmv<4><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
-  else if (G == 8) k_spmv<8><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
-  else k_spmv<16><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+#endif
+  constexpr int R = FPB_SPMV_GROUPS;
+  int grid = grid_for(((int64_t)n * G + R - 1) / R, 256, 16);
+  if (G == 4) k_spmv_r<4, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  else if (G == 8) k_spmv_r<8, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  else k_spmv_r<16, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }

@@ -22,6 +22,46 @@ from .sparse import CsrMatrix, axpy_d, dot_d, dot_work, spmv_d, to_device, to_ho
 
 S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 
+# Solver workspaces (vectors, device state, history ring, captured CUDA graph
+# of one full batch), keyed by the operator's device arrays and the batch
+# size: repeated solves with the same matrix reuse the buffers, so the
+# batch graph is captured once and replayed by every later solve.
+_WS: dict = {}
+_WS_MAX = 8
+
+
+def _workspace(kind: str, A: CsrMatrix, nvec: int, nstate: int, cap: int, jacobi: bool) -> dict:
+    key = (kind, torch.cuda.current_device(), _lib.stream(), A.rowptr_d.data_ptr(), A.colind_d.data_ptr(),
+           A.vals_d.data_ptr(), A.n, cap, jacobi)
+    ws = _WS.pop(key, None)
+    if ws is None:
+        dev = A.vals_d.device
+        ws = {"v": [torch.empty(A.n, dtype=torch.float64, device=dev) for _ in range(nvec)],
+              "d": torch.empty(A.n, dtype=torch.float64, device=dev),
+              "state": torch.zeros(nstate, dtype=torch.float64, device=dev),
+              "hist": torch.zeros(cap, dtype=torch.float64, device=dev), "graph": None}
+        while len(_WS) >= _WS_MAX:
+            _WS.pop(next(iter(_WS)))
+    _WS[key] = ws  # most recently used last
+    return ws
+
+
+def _batch(ws: dict, graph: bool, full: bool, launch) -> None:
+    """Run one batch of iterations: replay the captured graph for full
+    batches after the first, launch directly otherwise."""
+    if graph and full:
+        if ws["graph"] is None:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=side):
+                launch(_lib.stream())
+            torch.cuda.current_stream().wait_stream(side)
+            ws["graph"] = g
+        ws["graph"].replay()
+    else:
+        launch(_lib.stream())
+
 
 @dataclass
 class SolverStats:
@@ -39,17 +79,20 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     dev = bd.device
     if max_iter is None:
         max_iter = 10 * n
+    cap = max(1, min(batch, max_iter))
+    ws = _workspace("pcg", A, 5, 8, cap, jacobi)
+    d = ws["d"]
     if jacobi:
-        d = A.diagonal_d()
+        _lib.call("fpb_diagonal", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+                  d.data_ptr(), _lib.stream())
         if bool((d <= 0.0).any()):
             raise SolverBreakdownError("Jacobi preconditioner needs a positive diagonal")
     else:
-        d = torch.ones(n, dtype=torch.float64, device=dev)
+        d.fill_(1.0)
     x0d = to_device(x0)[0] if x0 is not None else None
-    x, r, p, q, z = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(5))
-    state = torch.zeros(8, dtype=torch.float64, device=dev)
-    cap = max(1, min(batch, max_iter))
-    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)  # hist[it % cap]
+    x, r, p, q, z = ws["v"]
+    state = ws["state"]
+    hist_d = ws["hist"]  # hist[it % cap]
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
@@ -62,25 +105,15 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
         return out(torch.zeros(n, dtype=torch.float64, device=dev)), SolverStats(0, True, [0.0], 0.0)
     history = [float(hist_d[0].item())]
     if st[S_STATUS] == 1.0:
-        return out(x), SolverStats(0, True, history, history[0])
+        return out(x.clone()), SolverStats(0, True, history, history[0])
     args = (n, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
             d.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
-    cuda_graph = None
     done = 0
     while done < max_iter:
         k = min(cap, max_iter - done)
-        if graph and k == cap and done > 0:
-            # every full batch launches identical arguments: capture it once
-            # and replay (3 kernels x cap iterations, no per-launch overhead)
-            if cuda_graph is None:
-                cuda_graph = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream()
-                side.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.graph(cuda_graph, stream=side):
-                    _lib.call("fpb_pcg_iterate", *args, k, work.data_ptr(), _lib.stream())
-            cuda_graph.replay()
-        else:
-            _lib.call("fpb_pcg_iterate", *args, k, work.data_ptr(), s)
+        # every full batch launches identical arguments: captured once per
+        # workspace and replayed (3 kernels x cap iterations per replay)
+        _batch(ws, graph, k == cap, lambda st, k=k: _lib.call("fpb_pcg_iterate", *args, k, work.data_ptr(), st))
         st = state.cpu().numpy()
         it = int(st[S_IT])
         if it > done:
@@ -95,7 +128,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     res = axpy_d(-1.0, spmv_d(A, x), bd)
     bnorm = float(st[S_BNORM])
     true_residual = float(np.sqrt(dot_d(res, res).item())) / bnorm
-    return out(x), SolverStats(done, converged, history, true_residual)
+    return out(x.clone()), SolverStats(done, converged, history, true_residual)
 
 
 # --------------------------------------------------------------------------
@@ -122,18 +155,21 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
     dev = bd.device
     if max_iter is None:
         max_iter = 10 * n
+    cap = max(1, min(batch, max_iter))
+    lib = _lib.load()
+    ws = _workspace("bicgstab", A, 9, int(lib.fpb_bicgstab_state_size()), cap, jacobi)
+    d = None
     if jacobi:
-        d = A.diagonal_d()
+        d = ws["d"]
+        _lib.call("fpb_diagonal", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+                  d.data_ptr(), _lib.stream())
         if bool((d == 0.0).any()):
             raise SolverBreakdownError("Jacobi preconditioner needs a nonzero diagonal")
-    else:
-        d = None
     x0d = to_device(x0)[0] if x0 is not None else None
-    x, r, rt, p, ph, v, sv, sh, t = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(9))
-    lib = _lib.load()
-    state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
-    cap = max(1, min(batch, max_iter))
-    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
+    x, r, rt, p, ph, v, sv, sh, t = ws["v"]
+    state = ws["state"]
+    state.zero_()
+    hist_d = ws["hist"]
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
@@ -148,26 +184,17 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
         return out(torch.zeros(n, dtype=torch.float64, device=dev)), SolverStats(0, True, [0.0], 0.0)
     history = [float(hist_d[0].item())]
     if st[B_STATUS] == 1.0:
-        return out(x), SolverStats(0, True, history, history[0])
+        return out(x.clone()), SolverStats(0, True, history, history[0])
     if st[B_STATUS] in _BICG_BREAKDOWN:
         raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
     args = (n, nnz, rp, ci, va, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
             rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
             t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
-    cuda_graph = None
     done = 0
     while done < max_iter:
         k = min(cap, max_iter - done)
-        if graph and k == cap and done > 0:
-            if cuda_graph is None:
-                cuda_graph = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream()
-                side.wait_stream(torch.cuda.current_stream())
-                with torch.cuda.graph(cuda_graph, stream=side):
-                    _lib.call("fpb_bicgstab_iterate", *args, k, work.data_ptr(), _lib.stream())
-            cuda_graph.replay()
-        else:
-            _lib.call("fpb_bicgstab_iterate", *args, k, work.data_ptr(), s)
+        _batch(ws, graph, k == cap,
+               lambda st, k=k: _lib.call("fpb_bicgstab_iterate", *args, k, work.data_ptr(), st))
         st = state.cpu().numpy()
         it = int(st[B_IT])
         if it > done:
@@ -181,4 +208,4 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
     converged = bool(st[B_STATUS] == 1.0)
     res = axpy_d(-1.0, spmv_d(A, x), bd)
     true_residual = float(np.sqrt(dot_d(res, res).item())) / float(st[B_BNORM])
-    return out(x), SolverStats(done, converged, history, true_residual)
+    return out(x.clone()), SolverStats(done, converged, history, true_residual)
