@@ -203,6 +203,48 @@ def config4_block(flush, hbm, n=272, reps=5):
             "value": ne / (total / 1e3) / 1e6, "unit": "Melem/s", "kernels": roof}
 
 
+def flow_block(nx, ny, nz, steps=2):
+    """FlowSolver.step on the device on the config-2
+    mesh: a Table-1-style profile — CUDA-event time per (category, equation)
+    of a full fractional step (3 RK3 stages of momentum + 3 scalar RHS,
+    pressure Poisson PCG on the pinned B^T M_L^-1 B operator, correction)."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200.timeloop import DeviceState
+
+    mesh = P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz)
+    t0 = time.perf_counter()
+    solver = P.FlowSolver(mesh, P.TimeConfig(dt=5e-4, tol=1e-8), robin_alpha=1.0, robin_beta=0.1)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    x, y, z = (solver.mesh.coords_d[:, k] for k in range(3))
+    pi = np.pi
+    vel = torch.stack([torch.sin(pi * x) * torch.cos(pi * y), -torch.cos(pi * x) * torch.sin(pi * y),
+                       0.1 * torch.sin(pi * z)], dim=1).contiguous()
+    n = mesh.nnode
+    zeros = torch.zeros(n, dtype=torch.float64, device=vel.device)
+    st = DeviceState(vel, zeros.clone(), (torch.cos(pi * x) * torch.cos(pi * z)).contiguous(),
+                     torch.stack([x * y, z * (1.0 - z)]).contiguous(), 1.0, 1e-2, 1e-2, 1e-2)
+    st, _ = solver.step_d(st)  # warm (graph capture, workspaces)
+    cells: dict = {}
+    its, ms = [], []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st, diag = solver.step_d(st)
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+        its.append(diag.solver.iterations)
+        for k, v in diag.timings.items():
+            cells[" / ".join(k)] = cells.get(" / ".join(k), 0.0) + v * 1e3 / steps
+    return {"workload": f"FlowSolver.step, TET04 box {nx}x{ny}x{nz} ({mesh.nelem} elements, {n} nodes), "
+                        "Robin alpha 1 beta 0.1, dt 5e-4, PCG tol 1e-8", "setup_s": setup_s,
+            "ms_per_step": statistics.mean(ms), "pcg_iterations": its, "ms_by_cell": cells,
+            "pressure_operator_nnz": solver.laplacian.nnz}
+
+
 def cpu_baseline(nx, ny, nz_sample, steps=3, warmup=1):
     from oracle import cport
     from oracle.baseline import CpuWorkload
@@ -419,6 +461,8 @@ def main():
         del mats
         torch.cuda.empty_cache()
         configs["c4"] = config4_block(flush, hbm)
+        torch.cuda.empty_cache()
+        configs["flow"] = flow_block(args.nx, args.ny, args.nz)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -197,3 +197,28 @@ def test_transpose_spgemm_add_dirichlet_vs_scipy(cuda_ok):
     want[nodes, nodes] = 1.0
     np.testing.assert_array_equal(Dd.to_dense(), want)
     np.testing.assert_allclose(bd, bw, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.gpu
+def test_mesh_size_and_cfl_warning(cuda_ok):
+    """hmin = min element volume^(1/dim) (timeloop.py:293-301) and the CFL
+    warning (timeloop.py:317-330)."""
+    import warnings
+
+    import paper_2107_11541_b200 as P
+
+    mesh = P.generate_box_mesh(P.ElementType.TET04, 5, 4, 3)
+    solver = P.FlowSolver(mesh, P.TimeConfig(dt=1e-3))
+    h = (1.0 / 5) * (1.0 / 4) * (1.0 / 3) / 6.0
+    assert solver._hmin == pytest.approx(h ** (1.0 / 3.0), rel=1e-12)
+    st = P.FlowState.zeros(mesh)
+    st.velocity[:, 0] = 1.0
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        solver.step(st)  # CFL = 1e-3 / hmin < 1: silent
+    fast = P.FlowSolver(mesh, P.TimeConfig(dt=1.0))
+    with pytest.warns(RuntimeWarning, match="CFL"):
+        try:
+            fast.step(st)
+        except P.StepFailureError:
+            pass
