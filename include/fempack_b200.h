@@ -197,7 +197,9 @@ int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_pt
                          double* out, void* stream);
 
 /* ---- element-block RHS assembly (deterministic, atomic-free) ------------
- * Blocks of fpb_block_elems() consecutive elements; phase 1 integrates each
+ * Blocks of fpb_block_elems(etype) consecutive elements (256 for the affine
+ * simplices, integrated two per thread; 128 for Gauss-loop types); phase 1
+ * integrates each
  * element once and reduces inside the block (sorted gather lists), phase 2
  * sums the per-(block, node) partials per node in ascending block order.
  * fpb_blocks_build: with blk_nodes == NULL fills blk_ptr[nblocks+1] and
@@ -210,8 +212,8 @@ int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_pt
  * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; node records as for
  * fpb_assemble_rows; partial[P * nv] is scratch; out overwritten
  * (accumulate = 0) or added to. */
-int fpb_block_elems(void);
-int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int32_t* blk_ptr,
+int fpb_block_elems(int etype);
+int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, int32_t* blk_ptr,
                      int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
                      int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
                      void* stream);

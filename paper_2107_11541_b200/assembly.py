@@ -132,10 +132,10 @@ class BlockPlan:
     assembly (blocks.cu): per-block distinct nodes + sorted gather slots,
     and per-node lists of block partials."""
 
-    def __init__(self, conn_d: torch.Tensor, n: int):
+    def __init__(self, conn_d: torch.Tensor, n: int, etype_id: int):
         lib = _lib.load()
         ne, nn = int(conn_d.shape[0]), int(conn_d.shape[1])
-        be = int(lib.fpb_block_elems())
+        be = int(lib.fpb_block_elems(etype_id))
         nblocks = -(-ne // be)
         dev = conn_d.device
         self.n, self.nelem = n, ne
@@ -145,7 +145,7 @@ class BlockPlan:
         pp = P.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         pm = mx.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
         s = _lib.stream()
-        _lib.check(lib.fpb_blocks_build(ne, nn, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(), None, None,
+        _lib.check(lib.fpb_blocks_build(etype_id, ne, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(), None, None,
                                         None, None, None, None, pp, pm, s), "fpb_blocks_build")
         self.npartial, self.maxnu = int(P[0]), int(mx[0])
         self.blk_nodes = torch.empty(max(self.npartial, 1), dtype=torch.int32, device=dev)
@@ -154,7 +154,7 @@ class BlockPlan:
         self.blk_lidx = torch.empty(max(nblocks * be * nn, 4), dtype=torch.int16, device=dev)
         self.node_pptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
         self.node_plist = torch.empty(max(self.npartial, 1), dtype=torch.int32, device=dev)
-        _lib.check(lib.fpb_blocks_build(ne, nn, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(),
+        _lib.check(lib.fpb_blocks_build(etype_id, ne, conn_d.data_ptr(), n, self.blk_ptr.data_ptr(),
                                         self.blk_nodes.data_ptr(), self.blk_gptr.data_ptr(),
                                         self.blk_gslot.data_ptr(), self.blk_lidx.data_ptr(),
                                         self.node_pptr.data_ptr(), self.node_plist.data_ptr(), pp, pm, s),
@@ -266,7 +266,7 @@ class AssemblyContext:
             lane32 = ps.lane_conn_d if cfg.vector_size == KERNEL_LANES else pack_lanes(g.conn_d, KERNEL_LANES)
             gd = GroupData(reference_element(g.etype), g.conn_d, offset, ps, lane32, pattern)
             if scatter == "auto":
-                gd.blocks = BlockPlan(g.conn_d, mesh.nnode)
+                gd.blocks = BlockPlan(g.conn_d, mesh.nnode, ETYPE_ID[g.etype])
             if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
                 gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time

@@ -41,18 +41,32 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 
 #ifndef FPB_BLK_ELEMS
-#define FPB_BLK_ELEMS 128
+#define FPB_BLK_ELEMS 256  // affine simplices: 2 elements per thread
+#endif
+#ifndef FPB_BLK_ELEMS_GAUSS
+#define FPB_BLK_ELEMS_GAUSS 128  // Gauss-loop types: 1 element per thread
+#endif
+#ifndef FPB_BLK_THREADS
+#define FPB_BLK_THREADS 128
 #endif
 #ifndef FPB_BLK_MINB
-#define FPB_BLK_MINB 6
+#define FPB_BLK_MINB 5
 #endif
 #ifndef FPB_BLK_MINB_NONAFFINE
 #define FPB_BLK_MINB_NONAFFINE 2  // Gauss-loop elements (QUAD04, PYR05, HEX08): registers, not spills
 #endif
-constexpr int kBlockElems = FPB_BLK_ELEMS;
+constexpr int kBlockThreads = FPB_BLK_THREADS;  // threads of the RHS kernel
+// elements per block (= setup threads): the affine kernels integrate EPT = 2
+// elements per thread so the CTA's fixed latencies (node-id and record
+// gathers, two barriers) are paid once per 256 elements; the Gauss-loop
+// kernels (~230 registers, two CTAs per SM) keep one element per thread
+template <int ET> constexpr int blk_elems() { return Elem<ET>::AFFINE ? FPB_BLK_ELEMS : FPB_BLK_ELEMS_GAUSS; }
+inline int blk_elems_rt(int et) { return (et == FPB_TRI03 || et == FPB_TET04) ? FPB_BLK_ELEMS : FPB_BLK_ELEMS_GAUSS; }
+static_assert(FPB_BLK_ELEMS % FPB_BLK_THREADS == 0 && FPB_BLK_ELEMS / FPB_BLK_THREADS <= 2, "EPT must be 1 or 2");
+static_assert(FPB_BLK_ELEMS_GAUSS % FPB_BLK_THREADS == 0 && FPB_BLK_ELEMS_GAUSS / FPB_BLK_THREADS <= 2, "EPT");
 
 // ---- setup -------------------------------------------------------------------
-template <int NN>
+template <int NN, int kBlockElems>
 __global__ void __launch_bounds__(kBlockElems)
 k_blk_setup(int64_t nelem, const int32_t* __restrict__ conn, int pass, int32_t* __restrict__ blk_count,
             const int32_t* __restrict__ blk_ptr, int32_t* __restrict__ blk_nodes,
@@ -152,10 +166,15 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 }
 
 // ---- phase 1: stage nodes, integrate, in-block gather ---------------------------
-// Shared memory: [node data of the block's distinct nodes: maxnu x NDAT]
-// followed by [contributions: NN * NV x kBlockElems].
+// kBlockThreads threads per CTA integrate kBlockElems = EPT x kBlockThreads
+// elements (EPT per thread, one after the other): the CTA's fixed
+// latencies — node-id and node-record gathers, two barriers — are paid once
+// per EPT elements of compute.
+// Shared memory: [contributions: NN * NV x kBlockElems], [gather slots:
+// NN x kBlockElems uint16], [node data of the block's distinct nodes:
+// maxnu x NDAT].
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kBlockElems, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
+__global__ void __launch_bounds__(kBlockThreads, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
 k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
@@ -163,6 +182,10 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
   constexpr int NV = Out<ET, KIND>::NV;
   constexpr int NDAT = 2 * DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);  // x, u (, phi)
+  constexpr int TPB = kBlockThreads;
+  constexpr int kBlockElems = blk_elems<ET>();
+  constexpr int EPT = kBlockElems / TPB;
+  constexpr int NGR = EPT == 2 ? 3 : 2;  // gather ranges prefetched per thread (nu <= NGR * TPB)
   extern __shared__ __align__(16) double smem[];
   double* sm = smem;                                                    // [NN * NV][kBlockElems]
   uint16_t* sgslot = reinterpret_cast<uint16_t*>(sm + NN * NV * kBlockElems);  // [NN * kBlockElems]
@@ -173,23 +196,36 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   // staging and integration: slots via cp.async, range bounds in registers
   {
     const uint16_t* g = blk_gslot + b * kBlockElems * NN;
-    for (int c = tid; c < NN * kBlockElems / 8; c += kBlockElems) cp_async16(sgslot + 8 * c, g + 8 * c);
+    for (int c = tid; c < NN * kBlockElems / 8; c += TPB) cp_async16(sgslot + 8 * c, g + 8 * c);
     cp_async_commit();
   }
   const int64_t base = blk_ptr[b];
   const int nu = blk_ptr[b + 1] - (int)base;
   const uint16_t* gptr = blk_gptr + base + b;
-  int glo[2] = {0, 0}, ghi[2] = {0, 0};
+  int glo[NGR], ghi[NGR];
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int u = tid + j * kBlockElems;
-    if (u < nu) {
-      glo[j] = __ldg(gptr + u);
-      ghi[j] = __ldg(gptr + u + 1);
+  for (int j = 0; j < NGR; ++j) {
+    const int u = tid + j * TPB;
+    glo[j] = u < nu ? __ldg(gptr + u) : 0;
+    ghi[j] = u < nu ? __ldg(gptr + u + 1) : 0;
+  }
+  int li[EPT][NN];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int64_t e = b * kBlockElems + tid + j * TPB;
+    if (e < nelem) {
+      const uint16_t* lp = blk_lidx + e * NN;
+      if constexpr (NN == 4) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(lp));
+        li[j][0] = v.x & 0xffff; li[j][1] = v.x >> 16; li[j][2] = v.y & 0xffff; li[j][3] = v.y >> 16;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NN; ++a) li[j][a] = __ldg(lp + a);
+      }
     }
   }
   // stage the block's distinct nodes: two 256-bit loads per node record
-  for (int u = tid; u < nu; u += kBlockElems) {
+  for (int u = tid; u < nu; u += TPB) {
     const int64_t node = __ldg(blk_nodes + base + u);
     double rx[4], ru[4];
     ld256(xyz4 + 4 * node, rx);
@@ -201,29 +237,21 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
     }
     if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = ru[3];
   }
-  const int64_t e = b * kBlockElems + tid;
-  int li[NN];
-  if (e < nelem) {
-    const uint16_t* lp = blk_lidx + e * NN;
-    if constexpr (NN == 4) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(lp));
-      li[0] = v.x & 0xffff; li[1] = v.x >> 16; li[2] = v.y & 0xffff; li[3] = v.y >> 16;
-    } else {
-#pragma unroll
-      for (int a = 0; a < NN; ++a) li[a] = __ldg(lp + a);
-    }
-  }
   __syncthreads();
-  if (e < nelem) {
+#pragma unroll 1
+  for (int j = 0; j < EPT; ++j) {
+    const int el = tid + j * TPB;
+    if (b * kBlockElems + el >= nelem) break;
     double xe[NN][DIM], ue[Out<ET, KIND>::NU][DIM], fe[Out<ET, KIND>::NF];
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
+      const int l = j == 0 ? li[0][a] : li[EPT - 1][a];
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        xe[a][d] = snode[li[a] * NDAT + d];
-        ue[a][d] = snode[li[a] * NDAT + DIM + d];
+        xe[a][d] = snode[l * NDAT + d];
+        ue[a][d] = snode[l * NDAT + DIM + d];
       }
-      if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = snode[li[a] * NDAT + 2 * DIM];
+      if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = snode[l * NDAT + 2 * DIM];
     }
     double acc[Out<ET, KIND>::NOUT];
     if constexpr (Elem<ET>::AFFINE) {
@@ -234,15 +262,28 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
 #pragma unroll
     for (int a = 0; a < NN; ++a)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) sm[(a * NV + k) * kBlockElems + tid] = acc[a * NV + k];
+      for (int k = 0; k < NV; ++k) sm[(a * NV + k) * kBlockElems + el] = acc[a * NV + k];
   }
   cp_async_wait_all();
   __syncthreads();
-  for (int u = tid, j = 0; u < nu; u += kBlockElems, ++j) {
+  for (int u = tid, j = 0; u < nu; u += TPB, ++j) {
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
-    const int lo = j < 2 ? glo[j] : __ldg(gptr + u), hi = j < 2 ? ghi[j] : __ldg(gptr + u + 1);
+    int lo, hi;
+    if (j < NGR) {
+      lo = glo[0];
+      hi = ghi[0];
+#pragma unroll
+      for (int q = 1; q < NGR; ++q)
+        if (j == q) {
+          lo = glo[q];
+          hi = ghi[q];
+        }
+    } else {
+      lo = __ldg(gptr + u);
+      hi = __ldg(gptr + u + 1);
+    }
     for (int q = lo; q < hi; ++q) {
       const int slot = sgslot[q];
       const int el = slot / NN, a = slot - el * NN;
@@ -280,6 +321,7 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
                       int maxnu, double* partial, cudaStream_t s) {
   constexpr int NV = Out<ET, KIND>::NV;
   constexpr int NDAT = 2 * Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);
+  constexpr int kBlockElems = blk_elems<ET>();
   const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
   const size_t contrib = (size_t)Elem<ET>::NN * NV * kBlockElems * sizeof(double) +
                          (size_t)Elem<ET>::NN * kBlockElems * sizeof(uint16_t);
@@ -287,7 +329,7 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
   FPB_REQUIRE(smem <= 227 * 1024, "element block needs %zu bytes of shared memory", smem);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockElems, smem, s>>>(nelem, lidx, xyz4, uvw4, rho, mu, kappa,
+  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockThreads, smem, s>>>(nelem, lidx, xyz4, uvw4, rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
   FPB_LAUNCH_CHECK();
@@ -312,16 +354,35 @@ using namespace fpb;
 
 extern "C" {
 
-int fpb_block_elems(void) { return kBlockElems; }
+int fpb_block_elems(int etype) { return blk_elems_rt(etype); }
 
-int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int32_t* blk_ptr,
+// setup kernel launch for (node count, block size)
+static void launch_setup(int nn, int be, int64_t nblocks, cudaStream_t s, int64_t nelem, const int32_t* conn,
+                         int pass, int32_t* cnt, const int32_t* blk_ptr, int32_t* blk_nodes, uint16_t* blk_gptr,
+                         uint16_t* blk_gslot, uint16_t* blk_lidx) {
+#define FPB_SETUP(NN_, BE_)                                                                                      \
+  k_blk_setup<NN_, BE_><<<(unsigned)nblocks, BE_, 0, s>>>(nelem, conn, pass, cnt, blk_ptr, blk_nodes, blk_gptr, \
+                                                          blk_gslot, blk_lidx)
+  if (be == FPB_BLK_ELEMS) {
+    if (nn == 3) FPB_SETUP(3, FPB_BLK_ELEMS);
+    else FPB_SETUP(4, FPB_BLK_ELEMS);
+  } else {
+    if (nn == 4) FPB_SETUP(4, FPB_BLK_ELEMS_GAUSS);
+    else if (nn == 5) FPB_SETUP(5, FPB_BLK_ELEMS_GAUSS);
+    else FPB_SETUP(8, FPB_BLK_ELEMS_GAUSS);
+  }
+#undef FPB_SETUP
+}
+
+int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, int32_t* blk_ptr,
                      int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
                      int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
                      void* stream) {
-  FPB_REQUIRE(nn == 3 || nn == 4 || nn == 5 || nn == 8, "unsupported node count %d", nn);
+  FPB_REQUIRE(etype >= 0 && etype < 5, "unsupported element type %d", etype);
   FPB_REQUIRE(nelem >= 0 && n >= 0, "bad sizes");
   cudaStream_t s = as_stream(stream);
-  const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
+  const int nn = etype_nn(etype), be = blk_elems_rt(etype);
+  const int64_t nblocks = (nelem + be - 1) / be;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   if (blk_nodes == nullptr) {  // pass 0: sizes
@@ -329,12 +390,7 @@ int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int3
     FPB_CUDA(cudaMallocAsync(&cnt, sizeof(int32_t) * (nblocks + 1), s));
     FPB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nblocks + 1), s));
     if (nblocks > 0) {
-      switch (nn) {
-        case 3: k_blk_setup<3><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 4: k_blk_setup<4><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 5: k_blk_setup<5><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-        case 8: k_blk_setup<8><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr); break;
-      }
+      launch_setup(nn, be, nblocks, s, nelem, conn, 0, cnt, nullptr, nullptr, nullptr, nullptr, nullptr);
       FPB_LAUNCH_CHECK();
     }
     cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, blk_ptr, nblocks + 1, s);
@@ -358,12 +414,7 @@ int fpb_blocks_build(int64_t nelem, int nn, const int32_t* conn, int32_t n, int3
   }
   const int64_t P = *npartial_h;
   if (nblocks > 0) {
-    switch (nn) {
-      case 3: k_blk_setup<3><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
-      case 4: k_blk_setup<4><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
-      case 5: k_blk_setup<5><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
-      case 8: k_blk_setup<8><<<(unsigned)nblocks, kBlockElems, 0, s>>>(nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx); break;
-    }
+    launch_setup(nn, be, nblocks, s, nelem, conn, 1, nullptr, blk_ptr, blk_nodes, blk_gptr, blk_gslot, blk_lidx);
     FPB_LAUNCH_CHECK();
   }
   int32_t* cnt = nullptr;
