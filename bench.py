@@ -203,6 +203,46 @@ def config4_block(flush, hbm, n=272, reps=5):
             "value": ne / (total / 1e3) / 1e6, "unit": "Melem/s", "kernels": roof}
 
 
+def dist_bicgstab_block(sub, vel, dev, dist, iters=60):
+    """Config 5's solver leg at N > 1: Jacobi-BiCGSTAB on the slab-decomposed
+    advection-diffusion operator M + dt (C(u) + kappa L) — per iteration the
+    fused device kernels with owned-row reductions, four 2-double NCCL
+    allreduces and two ghost-plane exchanges.  A fixed iteration count
+    (tol 0) is timed with CUDA events between barriers, max over ranks."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200.distributed import bicgstab_slab
+
+    ctx = sub.ctx
+    nnz = ctx.pattern.nnz
+    mats = []
+    for kind, v in ((P.KernelKind.MASS, None), (P.KernelKind.CONVECTION, vel), (P.KernelKind.LAPLACIAN, None)):
+        m = torch.empty(nnz, dtype=torch.float64, device=dev)
+        ctx.assemble_matrix_d(kind, v, m)
+        sub.halo_sum_matrix(m)
+        mats.append(m)
+    A = ctx.pattern.with_vals(mats[0] + 0.05 * (mats[1] + 1e-2 * mats[2]))
+    L = sub.layout
+    nglob = (L.nx + 1) * (L.ny + 1) * (L.nz + 1)
+    b = torch.as_tensor(np.random.default_rng(1).standard_normal(nglob)[L.node_offset:L.node_offset + L.nnode],
+                        device=dev)
+    bicgstab_slab(L, A, b, tol=0.0, max_iter=8, check_every=8)  # warm
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, st = bicgstab_slab(L, A, b, tol=0.0, max_iter=iters, check_every=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": "slab BiCGSTAB on M + 0.05 (C(u) + 1e-2 L), local 94x94x95 cells per GPU",
+            "iterations": st.iterations, "ms": ms, "ms_per_iter": ms / max(st.iterations, 1),
+            "rows_per_rank": L.owned_rows[1] - L.owned_rows[0], "relres": st.residual_history[-1]}
+
+
 def flow_block(nx, ny, nz, steps=2):
     """FlowSolver.step on the device on the config-2
     mesh: a Table-1-style profile — CUDA-event time per (category, equation)
@@ -316,12 +356,19 @@ def main():
 
     import torch
 
+    # one GPU per rank; FPB_DIST_BACKEND=gloo lets several ranks share a GPU
+    # (functional check of the N > 1 path on a one-GPU box, not a timing)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("FPB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2107_11541_b200 as P
 
@@ -446,8 +493,12 @@ def main():
                "d2h_bytes_per_step": int(r.nbytes + sum(v.nbytes for v in vals)),
                "api": "AssemblyContext.assemble_rhs(MOMENTUM_RHS, numpy) + gradient_matrices(ctx) + .vals"}
 
+    dist_solver = None
+    if world > 1 and not args.no_solver:
+        dist_solver = dist_bicgstab_block(sub, vel, dev, dist)
+
     solver = None
-    if rank == 0 and not args.no_solver:
+    if rank == 0 and world == 1 and not args.no_solver:
         # config 3 companions: SpMV on the MASS matrix, axpy / dot on vectors
         # larger than L2 (C5's node count), Jacobi-PCG on the pinned LAPLACIAN
         sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -490,6 +541,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "solver": solver,
+            "dist_solver": dist_solver,
             "configs": configs,
             "cpu_baseline": cpu,
         }
