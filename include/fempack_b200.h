@@ -52,10 +52,9 @@ typedef enum {
 
 const char* fpb_last_error(void);
 int fpb_version(void);
-/* Performance knobs with no effect on results (for measured design
- * choices): "gradient_split" = 1 assembles the continuity
- * matrices B_x, B_y, B_z with one row-owned pass each instead of one fused
- * pass. */
+/* Performance knobs with no effect beyond rounding (for measured design
+ * choices, profiles/): "rows_nb" = 0 assembles simplex matrices with the
+ * incidence-walking row kernel instead of the neighbour-staged one. */
 int fpb_set_tuning(const char* name, int value);
 
 /* Upload one reference element's tables (host pointers) to device constant

@@ -41,31 +41,28 @@ constexpr int kRowsBlock = 128;
 #define FPB_ROWS_MINB 4  // matrix kinds: CTAs per SM the register budget is sized for
 #endif
 constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
-int g_tuning_gradient_split = 0;  // fpb_set_tuning("gradient_split", 0|1)
 int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
 #ifndef FPB_ROWS_LD256
 #define FPB_ROWS_LD256 1
 #endif
 
-constexpr int KIND_GRAD1 = 101;  // one gradient direction (kdir) per launch
 
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kRowsBlock, (KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS) ? 1 : (KIND == FPB_CONVECTION ? 4 : FPB_ROWS_MINB))
 k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict__ incn,
        const uint32_t* __restrict__ slots, const double* __restrict__ xyz4,
        const double* __restrict__ uvw4, double rho, double mu, double kappa,
-       const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate, int kdir,
+       const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate,
        double* __restrict__ out) {
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
   constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
-                       KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
+                       KIND == FPB_GRADIENT_XYZ;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? DIM : 1;
   constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS;
   constexpr int NACC = KIND == FPB_MOMENTUM_RHS ? DIM : (MAT ? NMAT : 1);
   // MASS / CONVECTION / GRADIENT are linear in det*gN: adjugate form, no
   // reciprocal (gN then holds det*gN and det_s is 1)
-  constexpr bool ADJ = KIND == FPB_MASS || KIND == FPB_CONVECTION || KIND == FPB_GRADIENT_XYZ ||
-                       KIND == KIND_GRAD1;
+  constexpr bool ADJ = KIND == FPB_MASS || KIND == FPB_CONVECTION || KIND == FPB_GRADIENT_XYZ;
   // off-diagonal accumulators [NMAT][rowcap-1][kRowsBlock]; the diagonal
   // entry (local node 0 of every record) lives in registers
   extern __shared__ double sacc[];
@@ -213,17 +210,12 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict_
           for (int d = 0; d < DIM; ++d) s += ubar[d] * gN[d][b];
           val[0][b] = det_s * s;
         }
-      } else {  // GRADIENT_XYZ / GRAD1
+      } else {  // GRADIENT_XYZ
         const double f = det_s * mN0;
-        if constexpr (KIND == KIND_GRAD1) {
 #pragma unroll
-          for (int b = 0; b < NN; ++b) val[0][b] = f * (kdir == 0 ? gN[0][b] : (kdir == 1 ? gN[1][b] : gN[DIM - 1][b]));
-        } else {
+        for (int k = 0; k < NMAT; ++k)
 #pragma unroll
-          for (int k = 0; k < NMAT; ++k)
-#pragma unroll
-            for (int b = 0; b < NN; ++b) val[k][b] = f * gN[k][b];
-        }
+          for (int b = 0; b < NN; ++b) val[k][b] = f * gN[k][b];
       }
 #pragma unroll
       for (int k = 0; k < NMAT; ++k) acc[k] += val[k][0];
@@ -753,9 +745,9 @@ template <int ET, int KIND>
 static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
                        const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
                        double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
-                       double* out, cudaStream_t s, int kdir = 0) {
+                       double* out, cudaStream_t s) {
   constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
-                       KIND == FPB_GRADIENT_XYZ || KIND == KIND_GRAD1;
+                       KIND == FPB_GRADIENT_XYZ;
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? Elem<ET>::DIM : 1;
   size_t smem = MAT ? (size_t)NMAT * (rowcap > 1 ? rowcap - 1 : 1) * kRowsBlock * sizeof(double) : 0;
   if (smem > 48 * 1024)
@@ -763,7 +755,7 @@ static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
   int blocks = (n + kRowsBlock - 1) / kRowsBlock;
   k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, reinterpret_cast<const int4*>(incn), slots,
                                                     xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,
-                                                    accumulate, kdir, out);
+                                                    accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -810,14 +802,6 @@ static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_
       if (nb)
         return launch_rows_nb<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap,
                                                     accumulate, out, s);
-      if (g_tuning_gradient_split) {
-        for (int k = 0; k < Elem<ET>::DIM; ++k) {
-          int rc = launch_rows<ET, KIND_GRAD1>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
-                                               nnz, rowcap, accumulate, out + k * nnz, s, k);
-          if (rc) return rc;
-        }
-        return FPB_OK;
-      }
       return launch_rows<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
                                                nnz, rowcap, accumulate, out, s);
   }
@@ -834,10 +818,6 @@ using namespace fpb;
 extern "C" {
 
 int fpb_set_tuning(const char* name, int value) {
-  if (name && strcmp(name, "gradient_split") == 0) {
-    g_tuning_gradient_split = value;
-    return FPB_OK;
-  }
   if (name && strcmp(name, "rows_nb") == 0) {
     g_tuning_rows_nb = value;
     return FPB_OK;

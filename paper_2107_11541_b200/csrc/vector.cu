@@ -126,24 +126,12 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
   for (int64_t base_ = wid_ * (32 / (G)); base_ < (n); base_ += nwarps_ * (32 / (G)))  \
     for (int64_t row = base_ + (threadIdx.x & 31) / (G), once_ = 0; once_ < 1; ++once_)
 
-template <int G>
-__global__ void __launch_bounds__(256) k_spmv(int32_t n, const int32_t* __restrict__ rowptr,
-                                              const int32_t* __restrict__ colind,
-                                              const double* __restrict__ vals,
-                                              const double* __restrict__ x, double* __restrict__ y) {
-  FPB_ROW_LOOP(G, n) {
-    const bool valid = row < n;
-    double acc = row_dot<G>(rowptr, colind, vals, x, row, valid, sub);
-    if (valid && sub == 0) y[row] = acc;
-  }
-}
-
 // Multi-group SpMV: each warp pass covers R groups of 32/G rows and issues
 // every (column, value) load of all R groups before the first dependent x
 // gather, so a warp keeps R times more bytes in flight across the
-// load -> gather -> reduce chain (the one-group kernel above is latency-bound
-// at ~56 % of HBM on config 2, profiles/r01f_spmv).  Same per-row order:
-// lane sums in ascending entry order, then the fixed xor tree.
+// load -> gather -> reduce chain (one group per pass was latency-bound at
+// ~53 % of HBM on config 2; R = 4 reaches ~58 %).  Same per-row order: lane
+// sums in ascending entry order, then the fixed xor tree.
 #ifndef FPB_SPMV_ITEMS
 #define FPB_SPMV_ITEMS 2
 #endif
