@@ -36,6 +36,8 @@ __device__ __forceinline__ void element_integrate(
   for (int q = 0; q < NOUT; ++q) acc[q] = 0.0;
 
   double J[DIM][DIM], gN[DIM][NN], det = 0.0;
+  HexCoef hc;
+  if constexpr (ET == FPB_HEX08) hex_coeffs(xe, hc);
   if constexpr (Elem<ET>::AFFINE) {
     det = jacobian<ET>(xe, 0, J);
     if constexpr (NEED_GRAD) grad_shape<ET>(J, det, 0, gN);
@@ -44,7 +46,8 @@ __device__ __forceinline__ void element_integrate(
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     if constexpr (!Elem<ET>::AFFINE) {
-      det = jacobian<ET>(xe, g, J);
+      if constexpr (ET == FPB_HEX08) det = hex_jacobian(hc, g, J);
+      else det = jacobian<ET>(xe, g, J);
       if constexpr (NEED_GRAD) grad_shape<ET>(J, det, g, gN);
     }
     const double w = det * refW<ET>(g);  // detJw

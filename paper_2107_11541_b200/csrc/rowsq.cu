@@ -170,18 +170,24 @@ k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __res
 #pragma unroll
       for (int b = 0; b < NN; ++b) acc[k][b] = 0.0;
 
+    HexCoef hc;
+    if constexpr (ET == FPB_HEX08) hex_coeffs(cur.x, hc);
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
       double J[DIM][DIM];
+      if constexpr (ET == FPB_HEX08) {
+        hex_jacobian(hc, g, J);  // sum-factorised (common.cuh)
+      } else {
 #pragma unroll
-      for (int d = 0; d < DIM; ++d)
+        for (int d = 0; d < DIM; ++d)
 #pragma unroll
-        for (int l = 0; l < DIM; ++l) {
-          double s = 0.0;
+          for (int l = 0; l < DIM; ++l) {
+            double s = 0.0;
 #pragma unroll
-          for (int b = 0; b < NN; ++b) s += cur.x[b][d] * refdN<ET>(l, b, g);
-          J[d][l] = s;
-        }
+            for (int b = 0; b < NN; ++b) s += cur.x[b][d] * refdN<ET>(l, b, g);
+            J[d][l] = s;
+          }
+      }
       double A[DIM][DIM], det;  // A[l][d] = det * Ji[l][d]
       if constexpr (DIM == 2) {
         det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
