@@ -252,12 +252,13 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
  * batch can be captured once in a CUDA graph and replayed.  Once status != 0 the
  * remaining iterations are no-ops, so batches can be launched without a host
  * round trip per iteration.  vectors: x, r, p, q, z and the Jacobi diagonal d
- * (z = r / d, krylov.py:65,84), all of length n. */
-int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+ * (z = r / d, krylov.py:65,84), all of length n; nnz picks the lanes per
+ * row of the fused SpMV. */
+int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
                  const double* b, const double* x0, double* x, double* r, double* p,
                  double* z, const double* d, double* state, double* hist, double tol,
                  double* work, void* stream);
-int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind,
+int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
                     const double* vals, double* x, double* r, double* p, double* q, double* z,
                     const double* d, double* state, double* hist, int64_t hist_cap, int iters,
                     double* work, void* stream);

@@ -69,8 +69,8 @@ SIGNATURES = {
     "fpb_dot": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "fpb_diagonal": (_int, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "fpb_row_sums": (_int, [_i32, _vp, _vp, _vp, _vp]),
-    "fpb_pcg_init": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
-    "fpb_pcg_iterate": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
+    "fpb_pcg_init": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _vp, _vp]),
+    "fpb_pcg_iterate": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
     "fpb_bicgstab_state_size": (_int, []),
     "fpb_bicgstab_init": (_int, [_i32, _i64] + [_vp] * 12 + [_dbl, _i64, _i64, _int, _vp, _vp]),
     "fpb_bicgstab_iterate": (_int, [_i32, _i64] + [_vp] * 15 + [_i64, _int, _vp, _vp]),

@@ -89,7 +89,7 @@ __device__ __forceinline__ bool grid_finish(double (&v)[NV], double* work, int s
 // dependent x gathers) — rows up to G*ITEMS entries (tet ~15, hex ~27) take
 // one round trip; longer rows continue in a remainder loop.  Each lane sums
 // its entries in ascending order, then a fixed xor-tree: deterministic.
-template <int G, int ITEMS = 2>
+template <int G, int ITEMS = (G == 16 ? 4 : 2)>
 __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
                                           const int32_t* __restrict__ colind,
                                           const double* __restrict__ vals,
@@ -132,10 +132,7 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
 // load -> gather -> reduce chain (one group per pass was latency-bound at
 // ~53 % of HBM on config 2; R = 4 reaches ~58 %).  Same per-row order: lane
 // sums in ascending entry order, then the fixed xor tree.
-#ifndef FPB_SPMV_ITEMS
-#define FPB_SPMV_ITEMS 2
-#endif
-template <int G, int R, int ITEMS = FPB_SPMV_ITEMS>
+template <int G, int R, int ITEMS = (G == 16 ? 4 : 2)>
 __global__ void __launch_bounds__(256) k_spmv_r(int32_t n, const int32_t* __restrict__ rowptr,
                                                 const int32_t* __restrict__ colind,
                                                 const double* __restrict__ vals,
@@ -701,26 +698,32 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
   return FPB_OK;
 }
 
-int fpb_pcg_init(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
                  const double* b, const double* x0, double* x, double* r, double* p, double* z,
                  const double* d, double* state, double* hist, double tol, double* work,
                  void* stream) {
   cudaStream_t s = as_stream(stream);
-  k_pcg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state,
-                                                   hist, tol, work);
+  switch (lanes_per_row(n, nnz)) {
+    case 4: k_pcg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
+    case 8: k_pcg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
+    default: k_pcg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
+  }
   FPB_LAUNCH_CHECK();
   k_pcg_init2<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, d, z, p, state, work);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
 
-int fpb_pcg_iterate(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals,
+int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
                     double* x, double* r, double* p, double* q, double* z, const double* d,
                     double* state, double* hist, int64_t hist_cap, int iters, double* work,
                     void* stream) {
   cudaStream_t s = as_stream(stream);
+  const int G = lanes_per_row(n, nnz);
   for (int it = 0; it < iters; ++it) {
-    k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
+    if (G == 4) k_pcg_spmv<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
+    else if (G == 8) k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
+    else k_pcg_spmv<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_cap, work);
     k_pcg_direction<<<grid_for(n, 256, 8), 256, 0, s>>>(n, p, z, state);
   }

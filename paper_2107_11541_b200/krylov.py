@@ -96,7 +96,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
-    _lib.call("fpb_pcg_init", n, rp, ci, va, bd.data_ptr(), x0d.data_ptr() if x0d is not None else None,
+    _lib.call("fpb_pcg_init", n, A.nnz, rp, ci, va, bd.data_ptr(), x0d.data_ptr() if x0d is not None else None,
               x.data_ptr(), r.data_ptr(), p.data_ptr(), z.data_ptr(), d.data_ptr(), state.data_ptr(),
               hist_d.data_ptr(), float(tol), work.data_ptr(), s)
     st = state.cpu().numpy()
@@ -106,7 +106,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     history = [float(hist_d[0].item())]
     if st[S_STATUS] == 1.0:
         return out(x.clone()), SolverStats(0, True, history, history[0])
-    args = (n, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
+    args = (n, A.nnz, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
             d.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
     done = 0
     while done < max_iter:
