@@ -534,10 +534,10 @@ def main():
                        "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
             "kernels_ms": kern,
-            # per step: pack the velocity records, element-block momentum RHS
-            # (integrate + partial gather), row-owned B_x,B_y,B_z — 4 launches
-            # (profiles/r01e_step/launches.csv); + halo has no kernels of ours
-            "gpu_launches": args.steps * 4,
+            # per step: element-block momentum RHS (integrate + partial
+            # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
+            # launches (ncu launch list under profiles/); the halo (N > 1) is NCCL
+            "gpu_launches": args.steps * 3,
             "clocks": clk,
             "e2e": e2e,
             "solver": solver,

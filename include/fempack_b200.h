@@ -208,8 +208,10 @@ int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_pt
  * blk_gslot and blk_lidx [nblocks * block_elems * nn], node_pptr[n+1],
  * node_plist[P].  Phase 1 stages each block's distinct nodes through shared
  * memory (blk_lidx = local node of every element slot).
- * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; node records as for
- * fpb_assemble_rows; partial[P * nv] is scratch; out overwritten
+ * fpb_assemble_blocks: kind MOMENTUM_RHS or SCALAR_RHS; coordinates as
+ * 32-byte records (fpb_pack4); velocity (+ scalar) either as records uvw4
+ * or, with uvw4 = NULL, straight from the caller's vel[n][dim] (+ phi[n]) —
+ * no packing pass; partial[P * nv] is scratch; out overwritten
  * (accumulate = 0) or added to. */
 int fpb_block_elems(int etype);
 int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, int32_t* blk_ptr,
@@ -217,7 +219,7 @@ int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, i
                      int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
                      void* stream);
 int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
-                        double rho, double mu, double kappa, const int32_t* blk_ptr,
+                        const double* vel, const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
                         const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                         const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
                         const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,

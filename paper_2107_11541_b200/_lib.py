@@ -61,7 +61,7 @@ SIGNATURES = {
     "fpb_correct": (_int, [_i64, _int, _int, _dbl] + [_vp] * 6),
     "fpb_block_elems": (_int, [_int]),
     "fpb_blocks_build": (_int, [_int, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
-    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
+    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
                                    _vp, _int, _vp, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),

@@ -351,7 +351,11 @@ class AssemblyContext:
         vp = vel.data_ptr() if vel is not None else None
         pp = phi.data_ptr() if phi is not None else None
         uvw4 = None
-        if vel is not None and any(owner):
+        # 32-byte (u, v, w, phi) records for the row-owned kernels; the
+        # element-block kernels read the caller's arrays directly
+        needs_records = any(own and g.rows is not None and (matrix or g.blocks is None)
+                            for g, own in zip(self.groups, owner))
+        if vel is not None and needs_records:
             _lib.call("fpb_pack4", self.mesh.nnode, self.mesh.dim, vp, pp, self._uvw4.data_ptr(), _lib.stream())
             uvw4 = self._uvw4.data_ptr()
         xyz4 = self.xyz4.data_ptr()
@@ -359,7 +363,7 @@ class AssemblyContext:
             if own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
-                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, xyz4, uvw4,
+                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, xyz4, uvw4, vp, pp,
                           float(rho), float(mu), float(kappa), bp.blk_ptr.data_ptr(),
                           bp.blk_nodes.data_ptr(), bp.blk_gptr.data_ptr(), bp.blk_gslot.data_ptr(),
                           bp.blk_lidx.data_ptr(), bp.maxnu,
@@ -401,7 +405,9 @@ class AssemblyContext:
     def assemble_rhs_d(self, kind: KernelKind, velocity_d: torch.Tensor, scalar_d, rho: float,
                        mu: float, kappa: float, out: torch.Tensor) -> torch.Tensor:
         """Device fast path: overwrite out with the global RHS."""
-        return self._run(KIND_ID[kind], velocity_d, scalar_d, rho, mu, kappa, out)
+        vel = velocity_d.contiguous() if velocity_d is not None else None
+        phi = scalar_d.contiguous() if scalar_d is not None else None
+        return self._run(KIND_ID[kind], vel, phi, rho, mu, kappa, out)
 
     def assemble_matrix(self, kind: KernelKind, layout: str = "packed", velocity=None,
                         reuse: bool = False) -> CsrMatrix:

@@ -176,7 +176,8 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kBlockThreads, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
 k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
-          const double* __restrict__ uvw4, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
+          const double* __restrict__ uvw4, const double* __restrict__ vel, const double* __restrict__ phi,
+          double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
           double* __restrict__ partial) {
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
@@ -227,9 +228,15 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   // stage the block's distinct nodes: two 256-bit loads per node record
   for (int u = tid; u < nu; u += TPB) {
     const int64_t node = __ldg(blk_nodes + base + u);
-    double rx[4], ru[4];
+    double rx[4], ru[4] = {0.0, 0.0, 0.0, 0.0};
     ld256(xyz4 + 4 * node, rx);
-    ld256(uvw4 + 4 * node, ru);
+    if (uvw4) {
+      ld256(uvw4 + 4 * node, ru);
+    } else {  // the caller's velocity rows [n][dim] (+ scalar) directly: no packing pass
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) ru[d] = __ldg(vel + node * DIM + d);
+      if constexpr (KIND == FPB_SCALAR_RHS) ru[3] = __ldg(phi + node);
+    }
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
       snode[u * NDAT + d] = rx[d];
@@ -316,6 +323,7 @@ __global__ void k_blk_gather(int32_t n, const int32_t* __restrict__ ptr, const i
 
 template <int ET, int KIND>
 static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+                      const double* vel, const double* phi,
                       double rho, double mu, double kappa, const int32_t* blk_ptr,
                       const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                       int maxnu, double* partial, cudaStream_t s) {
@@ -329,7 +337,7 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
   FPB_REQUIRE(smem <= 227 * 1024, "element block needs %zu bytes of shared memory", smem);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockThreads, smem, s>>>(nelem, lidx, xyz4, uvw4, rho, mu, kappa,
+  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockThreads, smem, s>>>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
   FPB_LAUNCH_CHECK();
@@ -338,13 +346,14 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
 
 template <int ET>
 static int blk_kind(int kind, int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+                    const double* vel, const double* phi,
                     double rho, double mu, double kappa, const int32_t* blk_ptr,
                     const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot, int maxnu,
                     double* partial, cudaStream_t s) {
   if (kind == FPB_MOMENTUM_RHS)
-    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes,
+    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
                                             blk_gptr, blk_gslot, maxnu, partial, s);
-  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes,
+  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
                                         blk_gptr, blk_gslot, maxnu, partial, s);
 }
 
@@ -435,6 +444,7 @@ int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, i
 }
 
 int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
+                        const double* vel, const double* phi,
                         double rho, double mu, double kappa, const int32_t* blk_ptr,
                         const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                         const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
@@ -444,16 +454,17 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, 
               "reference tables for element type %d not uploaded", etype);
   FPB_REQUIRE(kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS,
               "element-block assembly covers the RHS kinds (got %d)", kind);
-  FPB_REQUIRE(xyz4 != nullptr && uvw4 != nullptr, "kind %d needs node records", kind);
+  FPB_REQUIRE(xyz4 != nullptr && (uvw4 != nullptr || (vel != nullptr && (kind != FPB_SCALAR_RHS || phi))),
+              "kind %d needs node records or the velocity (+ scalar) arrays", kind);
   cudaStream_t s = as_stream(stream);
   if (nelem > 0) {
     int rc = FPB_OK;
     switch (etype) {
-      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, xyz4, uvw4, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
     }
     if (rc) return rc;
   }
