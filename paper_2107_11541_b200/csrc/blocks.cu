@@ -50,7 +50,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define FPB_BLK_THREADS 128
 #endif
 #ifndef FPB_BLK_MINB
-#define FPB_BLK_MINB 5
+#define FPB_BLK_MINB 4
+#endif
+#ifndef FPB_BLK_INTERLEAVE
+#define FPB_BLK_INTERLEAVE 1  // the compiler interleaves a thread's two elements (ILP)
 #endif
 #ifndef FPB_BLK_MINB_NONAFFINE
 #define FPB_BLK_MINB_NONAFFINE 2  // Gauss-loop elements (QUAD04, PYR05, HEX08): registers, not spills
@@ -245,7 +248,11 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
     if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = ru[3];
   }
   __syncthreads();
+#if FPB_BLK_INTERLEAVE
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
   for (int j = 0; j < EPT; ++j) {
     const int el = tid + j * TPB;
     if (b * kBlockElems + el >= nelem) break;
