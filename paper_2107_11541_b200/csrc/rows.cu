@@ -360,7 +360,16 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict_
 // accumulator of column s.  Shared memory per thread, per off-diagonal
 // slot: DIM coordinates (+ DIM velocities for CONVECTION) + NMAT sums, laid
 // out [s][field][thread] so every access is conflict-free.
-constexpr int kNbBlock = 64;
+#ifndef FPB_NB_BLOCK
+#define FPB_NB_BLOCK 32  // one warp per CTA: finest occupancy granularity (measured best)
+#endif
+#ifndef FPB_NB_W
+#define FPB_NB_W 8
+#endif
+#ifndef FPB_NB_MINB
+#define FPB_NB_MINB 1
+#endif
+constexpr int kNbBlock = FPB_NB_BLOCK;
 
 template <int ET, int KIND>
 struct NbLayout {
@@ -372,7 +381,7 @@ struct NbLayout {
 };
 
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kNbBlock)
+__global__ void __launch_bounds__(kNbBlock, FPB_NB_MINB)
 k_rows_nb(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
           const double* __restrict__ xyz4, const double* __restrict__ uvw4,
           const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz, int rowcap,
@@ -533,7 +542,7 @@ k_rows_nb(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __re
 
   // slot words in groups of kW, double-buffered: group g+1 is in flight
   // while group g is integrated (one register copy per step)
-  constexpr int kW = 8;
+  constexpr int kW = FPB_NB_W;
   uint32_t wc[kW], wn[kW];
   auto ld_w = [&](int mm, uint32_t (&w)[kW]) {
 #pragma unroll
