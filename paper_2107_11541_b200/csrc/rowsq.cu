@@ -28,7 +28,13 @@
 
 namespace fpb {
 
-constexpr int kGlBlock = 64;
+#ifndef FPB_GL_BLOCK
+#define FPB_GL_BLOCK 64
+#endif
+#ifndef FPB_GL_MINB
+#define FPB_GL_MINB 4
+#endif
+constexpr int kGlBlock = FPB_GL_BLOCK;
 
 // slot bytes of every SELL entry (nn <= 8), see header comment; also
 // reports the longest row (rowcap) and missing node pairs
@@ -88,7 +94,7 @@ __global__ void k_rowlen_max(int32_t n, const int32_t* rowptr, int* out) {
 }
 
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kGlBlock, 4)
+__global__ void __launch_bounds__(kGlBlock, FPB_GL_MINB)
 k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ inc,
           const int32_t* __restrict__ conn, const uint2* __restrict__ slots, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
@@ -146,13 +152,14 @@ k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __res
     }
   };
 
-  // FPB_GL_PREFETCH: keep the next element's node records in flight while
-  // integrating the current one (two register stages); off by default for
-  // 8-node elements, whose two stages would spill
+  // keep the next element's node records in flight while integrating the
+  // current one (two register stages): measured faster for every kind but
+  // the 3-matrix GRADIENT_XYZ of 8-node elements, whose extra registers cost
+  // more than the hidden latency (profiles/r01i/gl_variants.txt)
 #ifndef FPB_GL_PREFETCH
 #define FPB_GL_PREFETCH 0
 #endif
-  constexpr bool PREFETCH = FPB_GL_PREFETCH || NN <= 4;
+  constexpr bool PREFETCH = FPB_GL_PREFETCH || NN <= 4 || KIND != FPB_GRADIENT_XYZ;
   Stage cur, nxt;
   load(m0, cur);
   for (int m = m0; m < m1 && cur.e >= 0; ++m) {
