@@ -12,7 +12,7 @@ import pytest
 from conftest import load_golden
 from oracle import fempack_np as O
 
-CASES = ["mixed", "tet_rest", "tet_smooth", "quad_tg", "hex_uniform", "tri_smooth"]
+CASES = ["mixed", "tet_rest", "tet_smooth", "quad_tg", "hex_uniform", "tri_smooth", "tet_jitter", "hex_jitter"]
 
 
 def _close(got, want, rtol=1e-9):
@@ -54,11 +54,24 @@ def test_config_and_state_validation():
 
 # ------------------------------------------------------------------ device
 def _mesh(P, spec):
+    import torch
+
     spec = [str(s) for s in spec]
     if spec[0] == "mixed":
         m, _ = P.renumber_by_type(P.generate_mixed_mesh(*map(int, spec[1:]), fraction=0.5))
         return m
-    return P.generate_box_mesh(P.ElementType[spec[1]], *map(int, spec[2:]))
+    dims = list(map(int, spec[2:]))
+    m = P.generate_box_mesh(P.ElementType[spec[1]], *dims)
+    if spec[0] == "jitter":  # same jitter as tools/make_golden_flow.py
+        rng = np.random.default_rng(3)
+        x = m.coords.copy()
+        h = np.array([1.0 / d for d in dims])
+        lo, hi = x.min(axis=0), x.max(axis=0)
+        interior = np.all((x > lo + 1e-12) & (x < hi - 1e-12), axis=1)
+        x[interior] += 0.2 * h * rng.uniform(-1.0, 1.0, size=(int(interior.sum()), x.shape[1]))
+        m.coords_d.copy_(torch.as_tensor(x, device="cuda"))
+        m._coords_h = None
+    return m
 
 
 def _initial(P, name, mesh, g):

@@ -62,14 +62,31 @@ CASES = {
     "quad_tg": (("box", "QUAD04", 8, 8), "taylor-green-2d", {}, dict(dt=1e-2, tol=1e-12)),
     "hex_uniform": (("box", "HEX08", 3, 3, 2), "uniform", {}, dict(dt=1e-2, tol=1e-12)),
     "tri_smooth": (("box", "TRI03", 6, 5), "smooth", dict(robin_alpha=2.0), dict(dt=1e-2, tol=1e-12)),
+    # interior nodes moved by up to 0.2 h (tests/test_flow.py applies the same jitter)
+    "tet_jitter": (("jitter", "TET04", 5, 4, 4), "smooth", dict(robin_alpha=3.0, robin_beta=0.2), dict(dt=5e-3, tol=1e-12)),
+    "hex_jitter": (("jitter", "HEX08", 4, 4, 3), "smooth", dict(robin_alpha=1.0), dict(dt=5e-3, tol=1e-12)),
 }
+
+
+def jitter(coords, dims, seed=3):
+    """Move interior nodes by up to 0.2 h per axis (boundary nodes stay)."""
+    rng = np.random.default_rng(seed)
+    x = coords.copy()
+    h = np.array([1.0 / d for d in dims])
+    lo, hi = x.min(axis=0), x.max(axis=0)
+    interior = np.all((x > lo + 1e-12) & (x < hi - 1e-12), axis=1)
+    x[interior] += 0.2 * h * rng.uniform(-1.0, 1.0, size=(int(interior.sum()), x.shape[1]))
+    return x
 
 
 def build_mesh(spec):
     if spec[0] == "mixed":
         mesh, _ = renumber_by_type(generate_mixed_mesh(*spec[1:], fraction=0.5))
         return mesh
-    return generate_box_mesh(ElementType[spec[1]], *spec[2:])
+    mesh = generate_box_mesh(ElementType[spec[1]], *spec[2:])
+    if spec[0] == "jitter":
+        mesh.coords = jitter(mesh.coords, spec[2:])
+    return mesh
 
 
 def main():
