@@ -243,6 +243,57 @@ def dist_bicgstab_block(sub, vel, dev, dist, iters=60):
             "rows_per_rank": L.owned_rows[1] - L.owned_rows[0], "relres": st.residual_history[-1]}
 
 
+def config5_block(flush, hbm, n=256, reps=5, iters=40):
+    """Config 5's mesh (100,663,296 tets, 256^3 cells) on ONE B200: the
+    headline step (momentum RHS + B_x,B_y,B_z) and Jacobi-BiCGSTAB iterations
+    on M + 0.05 (C(u) + 1e-2 L) — the single-GPU reference point of the
+    2/4/8-GPU decomposition."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+
+    t0 = time.perf_counter()
+    mesh = P.generate_box_mesh(P.ElementType.TET04, n, n, n)
+    ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    ctx.refresh_geometry("packed", need_grad=False)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    nn_, ne, nnz = mesh.nnode, mesh.nelem, ctx.pattern.nnz
+    dev = flush.device
+    vel = torch.as_tensor(np.random.default_rng(0).standard_normal((nn_, 3)), device=dev)
+    rhs = torch.empty((nn_, 3), dtype=torch.float64, device=dev)
+    mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
+    K = P.KernelKind
+    ms_mom = _time_ms(lambda: ctx.assemble_rhs_d(K.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs), reps, flush)
+    ms_grad = _time_ms(lambda: ctx.assemble_gradients_d(mats), reps, flush)
+    del mats
+    M = ctx.assemble_matrix(K.MASS)
+    C = ctx.assemble_matrix(K.CONVECTION, velocity=vel)
+    L = ctx.assemble_matrix(K.LAPLACIAN)
+    A = M.with_vals(M.vals_d + 0.05 * (C.vals_d + 1e-2 * L.vals_d))
+    del C, L
+    b = torch.as_tensor(np.random.default_rng(1).standard_normal(nn_), device=dev)
+    P.bicgstab_solve(A, b, tol=0.0, max_iter=iters)  # warm: same workspace + batch graph as the timed solve
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, st = P.bicgstab_solve(A, b, tol=0.0, max_iter=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_bicg = e0.elapsed_time(e1)
+    F, B = WORK["gradient_xyz"]
+    out = {"workload": f"config 5 mesh on one GPU: TET04 box {n}^3 ({ne} elements, {nn_} nodes, nnz {nnz})",
+           "setup_s": setup_s, "ms_per_step": ms_mom + ms_grad, "value": ne / ((ms_mom + ms_grad) / 1e3) / 1e6,
+           "unit": UNIT, "kernels_ms": {"momentum_rhs": ms_mom, "gradient_xyz": ms_grad},
+           "gradient_roofline": _roof(F, B, ms_grad, ne, hbm),
+           "bicgstab": {"iterations": st.iterations, "ms_per_iter": ms_bicg / max(st.iterations, 1),
+                        "GB_s_equiv": (2 * (12 * nnz + 4 * (nn_ + 1) + 8 * nn_) + 23 * 8 * nn_) * st.iterations
+                        / ms_bicg / 1e6}}
+    del ctx, A, M
+    torch.cuda.empty_cache()
+    return out
+
+
 def flow_block(nx, ny, nz, steps=2):
     """FlowSolver.step on the device on the config-2
     mesh: a Table-1-style profile — CUDA-event time per (category, equation)
@@ -513,6 +564,7 @@ def main():
         torch.cuda.empty_cache()
         configs["c4"] = config4_block(flush, hbm)
         torch.cuda.empty_cache()
+        configs["c5_one_gpu"] = config5_block(flush, hbm)
         configs["flow"] = flow_block(args.nx, args.ny, args.nz)
 
     cpu = None

@@ -8,8 +8,14 @@
 
 namespace fpb {
 
-constexpr int kDotBlocks = 2 * kNumSMs;  // 296
-constexpr int kDotThreads = 512;
+#ifndef FPB_DOT_BLOCKS_PER_SM
+#define FPB_DOT_BLOCKS_PER_SM 4
+#endif
+#ifndef FPB_DOT_THREADS
+#define FPB_DOT_THREADS 512
+#endif
+constexpr int kDotBlocks = FPB_DOT_BLOCKS_PER_SM * kNumSMs;
+constexpr int kDotThreads = FPB_DOT_THREADS;
 // work layout (doubles): [0, 4*kDotBlocks) partials for up to 4 fused dots,
 // then 4 ticket counters (as unsigned int in the low word).
 constexpr int kWorkDoubles = 4 * kDotBlocks + 8;
@@ -115,6 +121,56 @@ __device__ __forceinline__ double row_dot(const int32_t* __restrict__ rowptr,
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
   return acc;
 }
+
+// R groups of 32/G rows per warp pass (rows base + r * 32/G + lane/G): every
+// index/value load of the R groups is issued before the first dependent x
+// gather (the single-group loop is latency-bound on large matrices); per
+// row the same order as row_dot.  Returns the dots in out[r] (all lanes of
+// a row group), row ids in row[r] (>= n: no row).
+template <int G, int R, int ITEMS = (G == 16 ? 4 : 2)>
+__device__ __forceinline__ void row_dot_grp(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                                            const double* __restrict__ vals, const double* __restrict__ x,
+                                            int64_t base, int64_t n, int sub, int64_t (&row)[R],
+                                            double (&out)[R]) {
+  constexpr int RPW = 32 / G;
+  int lo[R], hi[R], col[R][ITEMS];
+  double v[R][ITEMS];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    row[r] = base + r * RPW + (threadIdx.x & 31) / G;
+    lo[r] = row[r] < n ? __ldg(rowptr + row[r]) : 0;
+    hi[r] = row[r] < n ? __ldg(rowptr + row[r] + 1) : 0;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+      const int k = lo[r] + sub + it * G;
+      col[r][it] = k < hi[r] ? __ldcs(colind + k) : -1;
+      v[r][it] = k < hi[r] ? __ldcs(vals + k) : 0.0;
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double a = 0.0;
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it)
+      if (col[r][it] >= 0) a += v[r][it] * __ldg(x + col[r][it]);
+    for (int k = lo[r] + sub + ITEMS * G; k < hi[r]; k += G) a += __ldcs(vals + k) * __ldg(x + __ldcs(colind + k));
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o, G);
+    out[r] = a;
+  }
+}
+
+#ifndef FPB_FUSED_GROUPS
+#define FPB_FUSED_GROUPS 4
+#endif
+// grid-stride loop over warp passes of R row groups
+#define FPB_ROW_LOOP_R(G, R, n)                                                          \
+  const int sub = threadIdx.x & ((G) - 1);                                              \
+  const int64_t wid_ = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;           \
+  const int64_t nwarps_ = ((int64_t)gridDim.x * blockDim.x) >> 5;                       \
+  for (int64_t base_ = wid_ * (32 / (G)) * (R); base_ < (n); base_ += nwarps_ * (32 / (G)) * (R))
 
 // Warp-uniform row loop: each warp covers 32/G consecutive rows per trip, so
 // every lane of a warp runs the same number of trips (the shuffles above need
@@ -304,13 +360,17 @@ k_pcg_spmv(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restr
            double* state, double* work) {
   if (state[S_STATUS] != 0.0) return;
   double v[1] = {0.0};
-  FPB_ROW_LOOP(G, n) {
-    const bool valid = row < n;
-    double qi = row_dot<G>(rowptr, colind, vals, p, row, valid, sub);
-    if (valid && sub == 0) {
-      q[row] = qi;
-      v[0] += p[row] * qi;
-    }
+  constexpr int R = FPB_FUSED_GROUPS;
+  FPB_ROW_LOOP_R(G, R, n) {
+    int64_t row[R];
+    double qi[R];
+    row_dot_grp<G, R>(rowptr, colind, vals, p, base_, n, sub, row, qi);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (row[r] < n && sub == 0) {
+        q[row[r]] = qi[r];
+        v[0] += p[row[r]] * qi[r];
+      }
   }
   block_sum<1>(v);
   double tot[1];
@@ -544,13 +604,17 @@ k_bicg_av(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restri
           double* __restrict__ v, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[1] = {0.0};
-  FPB_ROW_LOOP(G, n) {
-    const bool valid = row < n;
-    const double vi = row_dot<G>(rowptr, colind, vals, ph, row, valid, sub);
-    if (valid && sub == 0) {
-      v[row] = vi;
-      if (row >= R.own_lo && row < R.own_hi) acc[0] += rt[row] * vi;
-    }
+  constexpr int NG = FPB_FUSED_GROUPS;
+  FPB_ROW_LOOP_R(G, NG, n) {
+    int64_t row[NG];
+    double vi[NG];
+    row_dot_grp<G, NG>(rowptr, colind, vals, ph, base_, n, sub, row, vi);
+#pragma unroll
+    for (int r = 0; r < NG; ++r)
+      if (row[r] < n && sub == 0) {
+        v[row[r]] = vi[r];
+        if (row[r] >= R.own_lo && row[r] < R.own_hi) acc[0] += rt[row[r]] * vi[r];
+      }
   }
   bicg_reduce<1>(acc, BSTEP_AV, state, work, 1, R);
 }
@@ -580,16 +644,20 @@ k_bicg_at(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restri
           double* __restrict__ t, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[2] = {0.0, 0.0};
-  FPB_ROW_LOOP(G, n) {
-    const bool valid = row < n;
-    const double ti = row_dot<G>(rowptr, colind, vals, sh, row, valid, sub);
-    if (valid && sub == 0) {
-      t[row] = ti;
-      if (row >= R.own_lo && row < R.own_hi) {
-        acc[0] += ti * sv[row];
-        acc[1] += ti * ti;
+  constexpr int NG = FPB_FUSED_GROUPS;
+  FPB_ROW_LOOP_R(G, NG, n) {
+    int64_t row[NG];
+    double ti[NG];
+    row_dot_grp<G, NG>(rowptr, colind, vals, sh, base_, n, sub, row, ti);
+#pragma unroll
+    for (int r = 0; r < NG; ++r)
+      if (row[r] < n && sub == 0) {
+        t[row[r]] = ti[r];
+        if (row[r] >= R.own_lo && row[r] < R.own_hi) {
+          acc[0] += ti[r] * sv[row[r]];
+          acc[1] += ti[r] * ti[r];
+        }
       }
-    }
   }
   bicg_reduce<2>(acc, BSTEP_AT, state, work, 3, R);
 }
