@@ -436,7 +436,10 @@ def main():
     ctx.refresh_geometry("packed", need_grad=False)
     nelem, nnode, nnz = mesh.nelem, mesh.nnode, ctx.pattern.nnz
     rng = np.random.default_rng(0)
-    vel_h = rng.standard_normal((nnode, 3))
+    # host inputs live in pinned memory (the e2e contract: H2D from pinned
+    # host buffers); the numpy view is what a reference user passes
+    vel_h = torch.empty((nnode, 3), dtype=torch.float64, pin_memory=True).numpy()
+    vel_h[:] = rng.standard_normal((nnode, 3))
     vel = torch.as_tensor(vel_h, device=dev)
     rhs = torch.zeros((nnode, 3), dtype=torch.float64, device=dev)
     mats = torch.zeros(3 * nnz, dtype=torch.float64, device=dev)
