@@ -14,8 +14,9 @@ with CUDA events per step, L2 flushed (512 MiB write) between steps.
 outputs: velocity H2D in, RHS + three matrices' values D2H out.
 
 Multi-GPU (torchrun, N > 1): weak scaling — rank r assembles z-slab r of an
-(94, 94, 95 N) mesh, and interface-plane RHS/matrix contributions are summed
-by an NCCL halo exchange (paper_2107_11541_b200/distributed.py).
+(94, 94, 95 N) mesh; interface-plane RHS/matrix contributions are summed by
+an NCCL halo exchange that runs on a side stream while the interior rows are
+assembled (interface windows first, paper_2107_11541_b200/distributed.py).
 
 `--impl reference`: the reference's CPU algorithm (C restatement of the
 packed kernels, oracle/fempack_ref.c, all host threads) on a bounded sample of
@@ -446,7 +447,18 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(ev=None):
+    side = torch.cuda.Stream() if sub is not None else None
+    launches_per_step = 3
+    if sub is not None:  # windowed schedule: one launch per non-empty window
+        from paper_2107_11541_b200.distributed import _step_windows
+
+        w = _step_windows(sub)
+        nonempty = lambda r: r[1] > r[0]  # noqa: E731
+        launches_per_step = (sum(map(nonempty, w["blocks_A"])) + sum(map(nonempty, w["nodes_A"]))
+                             + sum(map(nonempty, w["rows_A"])) + nonempty(w["blocks_B"])
+                             + sum(map(nonempty, w["nodes_B"])) + nonempty(w["rows_B"]))
+
+    def kernels(ev=None):
         if ev:
             ev[0].record(stream)
         ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs)
@@ -455,17 +467,32 @@ def main():
         ctx.assemble_gradients_d(mats)
         if ev:
             ev[2].record(stream)
-        if sub is not None:
-            sub.halo_sum_rhs(rhs)
-            sub.halo_sum_matrix(mats, 3)
+
+    def step(ev=None):
+        if sub is None:
+            kernels(ev)
+        else:
+            # interface rows first, NCCL halo on a side stream overlapping the
+            # interior (distributed.assemble_step)
+            sub.assemble_step(vel, rhs, mats, 1.0, 1e-2, overlap=True, side=side)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
-    # soak (untimed) so the clock sampler sees the loaded state
+    # soak (untimed) so the clock sampler sees the loaded state; every rank
+    # must run the same number of steps (each step has halo exchanges), so
+    # rank 0's clock decides and the decision is shared
     t_end = time.perf_counter() + args.soak
-    while time.perf_counter() < t_end:
+    flag = torch.zeros(1, dtype=torch.float64, device=dev)
+    while True:
+        go = time.perf_counter() < t_end
+        if dist:
+            flag.fill_(1.0 if (go and rank == 0) else 0.0)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            go = bool(flag.item() > 0.0)
+        if not go:
+            break
         step()
         torch.cuda.synchronize()
     if dist:
@@ -481,12 +508,21 @@ def main():
         e_end.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e_start.elapsed_time(e_end))
-        k_mom.append(ev[0].elapsed_time(ev[1]))
-        k_grad.append(ev[1].elapsed_time(ev[2]))
+        if sub is None:
+            k_mom.append(ev[0].elapsed_time(ev[1]))
+            k_grad.append(ev[1].elapsed_time(ev[2]))
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    if sub is not None:  # per-kernel times of this rank's slab, outside the timed region
+        for _ in range(5):
+            flush.fill_(1.0)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            kernels(ev)
+            torch.cuda.synchronize()
+            k_mom.append(ev[0].elapsed_time(ev[1]))
+            k_grad.append(ev[1].elapsed_time(ev[2]))
     total_ms = sum(step_ms)
     if dist:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -592,7 +628,7 @@ def main():
             # per step: element-block momentum RHS (integrate + partial
             # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
             # launches (ncu launch list under profiles/); the halo (N > 1) is NCCL
-            "gpu_launches": args.steps * 3,
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk,
             "e2e": e2e,
             "solver": solver,

@@ -159,6 +159,9 @@ int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* 
  * column list, bytes 1.. = offsets with the diagonal skipped (the kernel
  * keeps the diagonal in registers); returns the longest row through
  * rowcap_h (synchronous).
+ * Row windows: only rows [row0, row1) are assembled (row0 a multiple of 32,
+ * row1 <= n; 0, n = all) — e.g. interface rows first so a halo exchange
+ * can overlap the interior (distributed.py).
  * fpb_assemble_rows: element nodes come from incn (required; inc and conn
  * are accepted for ABI stability and unused); node data come as 32-byte
  * records (fpb_pack4): xyz4[n] = (x, y, z|0, 0), uvw4[n] = (u, v, w|0,
@@ -172,7 +175,8 @@ int fpb_incidence_slots(int32_t n, int nn, int64_t ncols, const int32_t* slice_p
                         const int32_t* colind, uint32_t* slots, int* rowcap_h, void* stream);
 int fpb_incidence_nodes(int32_t n, int64_t ncols, int nn, const int32_t* slice_ptr, const int32_t* inc,
                         const int32_t* conn, int32_t* incn, void* stream);
-int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+int fpb_assemble_rows(int kind, int etype, int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                      const int32_t* inc,
                       const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4,
                       const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
                       const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream);
@@ -190,7 +194,8 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, 
 int fpb_incidence_slots8(int32_t n, int nn, int64_t ncols, const int32_t* slice_ptr, const int32_t* inc,
                          const int32_t* conn, const int32_t* rowptr, const int32_t* colind, uint32_t* slots,
                          int* rowcap_h, void* stream);
-int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+int fpb_assemble_rows_gl(int kind, int etype, int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                         const int32_t* inc,
                          const int32_t* conn, const uint32_t* slots, const double* xyz4, const double* uvw4,
                          const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap, int accumulate,
                          double* out, void* stream);
@@ -212,18 +217,22 @@ int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_pt
  * 32-byte records (fpb_pack4); velocity (+ scalar) either as records uvw4
  * or, with uvw4 = NULL, straight from the caller's vel[n][dim] (+ phi[n]) —
  * no packing pass; partial[P * nv] is scratch; out overwritten
- * (accumulate = 0) or added to. */
+ * (accumulate = 0) or added to.  Windows: phase 1 integrates blocks
+ * [blk0, blk1), phase 2 sums the partials of nodes [node0, node1) — the
+ * full call is (0, nblocks) and (0, n); a node's partials must all have
+ * been integrated before its phase 2 (interface-first schedules,
+ * distributed.py). */
 int fpb_block_elems(int etype);
 int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, int32_t* blk_ptr,
                      int32_t* blk_nodes, uint16_t* blk_gptr, uint16_t* blk_gslot, uint16_t* blk_lidx,
                      int32_t* node_pptr, int32_t* node_plist, int64_t* npartial_h, int* maxnu_h,
                      void* stream);
-int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
-                        const double* vel, const double* phi, double rho, double mu, double kappa, const int32_t* blk_ptr,
-                        const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
-                        const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
-                        const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,
-                        void* stream);
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, int64_t blk0, int64_t blk1, const double* xyz4,
+                        const double* uvw4, const double* vel, const double* phi, double rho, double mu, double kappa,
+                        const int32_t* blk_ptr, const int32_t* blk_nodes, const uint16_t* blk_gptr,
+                        const uint16_t* blk_gslot, const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
+                        int32_t node0, int32_t node1, const int32_t* node_pptr, const int32_t* node_plist,
+                        int accumulate, double* out, void* stream);
 
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 

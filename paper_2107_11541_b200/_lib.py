@@ -41,10 +41,10 @@ SIGNATURES = {
     "fpb_incidence_slots": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
     "fpb_pack4": (_int, [_i64, _int, _vp, _vp, _vp, _vp]),
     "fpb_incidence_nodes": (_int, [_i32, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
-    "fpb_assemble_rows": (_int, [_int, _int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl,
+    "fpb_assemble_rows": (_int, [_int, _int, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl,
                                  _vp, _vp, _i64, _int, _int, _vp, _vp]),
     "fpb_incidence_slots8": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
-    "fpb_assemble_rows_gl": (_int, [_int, _int, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int,
+    "fpb_assemble_rows_gl": (_int, [_int, _int, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int,
                                     _vp, _vp]),
     "fpb_csr_transpose": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_spgemm_count": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -61,8 +61,8 @@ SIGNATURES = {
     "fpb_correct": (_int, [_i64, _int, _int, _dbl] + [_vp] * 6),
     "fpb_block_elems": (_int, [_int]),
     "fpb_blocks_build": (_int, [_int, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
-    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp, _vp,
-                                   _vp, _int, _vp, _i32, _vp, _vp, _int, _vp, _vp]),
+    "fpb_assemble_blocks": (_int, [_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp,
+                                   _vp, _vp, _vp, _int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),
     "fpb_dot_work_size": (_i64, []),

@@ -139,6 +139,7 @@ class BlockPlan:
         nblocks = -(-ne // be)
         dev = conn_d.device
         self.n, self.nelem = n, ne
+        self.block_elems, self.nblocks = be, nblocks
         self.blk_ptr = torch.empty(nblocks + 1, dtype=torch.int32, device=dev)
         P = np.zeros(1, dtype=np.int64)
         mx = np.zeros(1, dtype=np.int32)
@@ -334,8 +335,11 @@ class AssemblyContext:
         return buf  # overwritten by the next assembly
 
     def _run(self, kind_id: int, vel, phi, rho: float, mu: float, kappa: float,
-             out: torch.Tensor) -> torch.Tensor:
-        """Overwrite `out` with one assembly over every group."""
+             out: torch.Tensor, window: dict | None = None) -> torch.Tensor:
+        """Overwrite `out` with one assembly over every group.  window
+        (single owner-writes group only) restricts the work: "rows" =
+        (row0, row1) for row-owned matrices, "blocks" = (b0, b1) and
+        "nodes" = (n0, n1) for the element-block RHS phases."""
         self._ensure_checked()
         matrix = kind_id in (0, 1, 2, GRADIENT_XYZ)
         # owner-writes paths (row-owned matrices, element-block RHS) overwrite
@@ -344,8 +348,13 @@ class AssemblyContext:
                  else (g.blocks is not None or (g.rows is not None and not g.rows.gauss))
                  for g in self.groups]
         single_rows = len(self.groups) == 1 and owner[0]
+        if window is not None and not single_rows:
+            raise ConfigurationError("assembly windows need a single owner-writes element group")
         if not single_rows:
             out.zero_()
+        n = self.mesh.nnode
+        r0, r1 = window.get("rows", (0, n)) if window else (0, n)
+        n0, n1 = window.get("nodes", (0, n)) if window else (0, n)
         nnz = self.pattern.nnz
         coords = self.mesh.coords_d.data_ptr()
         vp = vel.data_ptr() if vel is not None else None
@@ -363,21 +372,22 @@ class AssemblyContext:
             if own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
-                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, xyz4, uvw4, vp, pp,
+                b0, b1 = window.get("blocks", (0, bp.nblocks)) if window else (0, bp.nblocks)
+                _lib.call("fpb_assemble_blocks", kind_id, g.etype_id, g.nelem, b0, b1, xyz4, uvw4, vp, pp,
                           float(rho), float(mu), float(kappa), bp.blk_ptr.data_ptr(),
                           bp.blk_nodes.data_ptr(), bp.blk_gptr.data_ptr(), bp.blk_gslot.data_ptr(),
                           bp.blk_lidx.data_ptr(), bp.maxnu,
-                          bp.partial(nv, out.device).data_ptr(), self.mesh.nnode, bp.node_pptr.data_ptr(),
+                          bp.partial(nv, out.device).data_ptr(), n, n0, n1, bp.node_pptr.data_ptr(),
                           bp.node_plist.data_ptr(), 0 if single_rows else 1, out.data_ptr(), _lib.stream())
             elif own and g.rows.gauss:
                 r = g.rows
-                _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
+                _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),
                           r.inc.data_ptr(), g.conn_d.data_ptr(), r.slots.data_ptr(), xyz4, uvw4,
                           self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
                           0 if single_rows else 1, out.data_ptr(), _lib.stream())
             elif own:
                 r = g.rows
-                _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r.slice_ptr.data_ptr(),
+                _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),
                           r.inc.data_ptr(), g.conn_d.data_ptr(),
                           r.incn.data_ptr(),
                           r.slots.data_ptr() if matrix else None, xyz4, uvw4,
@@ -397,17 +407,17 @@ class AssemblyContext:
         vel = velocity_d if kind is KernelKind.CONVECTION else None
         return self._run(KIND_ID[kind], vel, None, 1.0, 0.0, 0.0, out)
 
-    def assemble_gradients_d(self, out: torch.Tensor) -> torch.Tensor:
+    def assemble_gradients_d(self, out: torch.Tensor, window: dict | None = None) -> torch.Tensor:
         """Fused continuity assembly: out[k*nnz:(k+1)*nnz] = B_k, k < dim,
         where B_k = CONVECTION with unit velocity e_k (timeloop.py:159-171)."""
-        return self._run(GRADIENT_XYZ, None, None, 1.0, 0.0, 0.0, out)
+        return self._run(GRADIENT_XYZ, None, None, 1.0, 0.0, 0.0, out, window)
 
     def assemble_rhs_d(self, kind: KernelKind, velocity_d: torch.Tensor, scalar_d, rho: float,
-                       mu: float, kappa: float, out: torch.Tensor) -> torch.Tensor:
+                       mu: float, kappa: float, out: torch.Tensor, window: dict | None = None) -> torch.Tensor:
         """Device fast path: overwrite out with the global RHS."""
         vel = velocity_d.contiguous() if velocity_d is not None else None
         phi = scalar_d.contiguous() if scalar_d is not None else None
-        return self._run(KIND_ID[kind], vel, phi, rho, mu, kappa, out)
+        return self._run(KIND_ID[kind], vel, phi, rho, mu, kappa, out, window)
 
     def assemble_matrix(self, kind: KernelKind, layout: str = "packed", velocity=None,
                         reuse: bool = False) -> CsrMatrix:

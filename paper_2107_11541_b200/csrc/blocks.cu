@@ -178,7 +178,7 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 // maxnu x NDAT].
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kBlockThreads, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
-k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
+k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const double* __restrict__ vel, const double* __restrict__ phi,
           double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
@@ -195,7 +195,7 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
   uint16_t* sgslot = reinterpret_cast<uint16_t*>(sm + NN * NV * kBlockElems);  // [NN * kBlockElems]
   double* snode = sm + NN * NV * kBlockElems + NN * kBlockElems / 4;  // [maxnu][NDAT]
   const int tid = threadIdx.x;
-  const int64_t b = blockIdx.x;
+  const int64_t b = blk0 + blockIdx.x;  // blocks [blk0, blk0 + gridDim.x)
   // gather metadata of phase 3 is fetched now so its latency hides behind
   // staging and integration: slots via cp.async, range bounds in registers
   {
@@ -311,9 +311,11 @@ k_blk_rhs(int64_t nelem, const uint16_t* __restrict__ blk_lidx, const double* __
 
 // ---- phase 2: per-node gather of block partials ---------------------------------
 template <int NV>
-__global__ void k_blk_gather(int32_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ list,
-                             const double* __restrict__ partial, int accumulate, double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_blk_gather(int32_t node0, int32_t node1, const int32_t* __restrict__ ptr,
+                             const int32_t* __restrict__ list, const double* __restrict__ partial, int accumulate,
+                             double* __restrict__ out) {
+  for (int64_t i = node0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < node1;
+       i += (int64_t)gridDim.x * blockDim.x) {
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
@@ -329,7 +331,7 @@ __global__ void k_blk_gather(int32_t n, const int32_t* __restrict__ ptr, const i
 }
 
 template <int ET, int KIND>
-static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+static int launch_blk(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t* lidx, const double* xyz4, const double* uvw4,
                       const double* vel, const double* phi,
                       double rho, double mu, double kappa, const int32_t* blk_ptr,
                       const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
@@ -344,7 +346,10 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
   FPB_REQUIRE(smem <= 227 * 1024, "element block needs %zu bytes of shared memory", smem);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_blk_rhs<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_blk_rhs<ET, KIND><<<(unsigned)nblocks, kBlockThreads, smem, s>>>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa,
+  FPB_REQUIRE(blk0 >= 0 && blk0 <= blk1 && blk1 <= nblocks, "block window [%lld, %lld) outside [0, %lld)",
+              (long long)blk0, (long long)blk1, (long long)nblocks);
+  if (blk1 == blk0) return FPB_OK;
+  k_blk_rhs<ET, KIND><<<(unsigned)(blk1 - blk0), kBlockThreads, smem, s>>>(nelem, blk0, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
   FPB_LAUNCH_CHECK();
@@ -352,15 +357,15 @@ static int launch_blk(int64_t nelem, const uint16_t* lidx, const double* xyz4, c
 }
 
 template <int ET>
-static int blk_kind(int kind, int64_t nelem, const uint16_t* lidx, const double* xyz4, const double* uvw4,
+static int blk_kind(int kind, int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t* lidx, const double* xyz4, const double* uvw4,
                     const double* vel, const double* phi,
                     double rho, double mu, double kappa, const int32_t* blk_ptr,
                     const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot, int maxnu,
                     double* partial, cudaStream_t s) {
   if (kind == FPB_MOMENTUM_RHS)
-    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
                                             blk_gptr, blk_gslot, maxnu, partial, s);
-  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
+  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
                                         blk_gptr, blk_gslot, maxnu, partial, s);
 }
 
@@ -450,13 +455,13 @@ int fpb_blocks_build(int etype, int64_t nelem, const int32_t* conn, int32_t n, i
   return FPB_OK;
 }
 
-int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, const double* uvw4,
-                        const double* vel, const double* phi,
+int fpb_assemble_blocks(int kind, int etype, int64_t nelem, int64_t blk0, int64_t blk1, const double* xyz4,
+                        const double* uvw4, const double* vel, const double* phi,
                         double rho, double mu, double kappa, const int32_t* blk_ptr,
                         const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
-                        const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n,
-                        const int32_t* node_pptr, const int32_t* node_plist, int accumulate, double* out,
-                        void* stream) {
+                        const uint16_t* blk_lidx, int maxnu, double* partial, int32_t n, int32_t node0,
+                        int32_t node1, const int32_t* node_pptr, const int32_t* node_plist, int accumulate,
+                        double* out, void* stream) {
   FPB_REQUIRE(etype >= 0 && etype < 5 && g_ref_loaded[etype],
               "reference tables for element type %d not uploaded", etype);
   FPB_REQUIRE(kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS,
@@ -467,21 +472,23 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, const double* xyz4, 
   if (nelem > 0) {
     int rc = FPB_OK;
     switch (etype) {
-      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
     }
     if (rc) return rc;
   }
-  if (n > 0) {
+  FPB_REQUIRE(node0 >= 0 && node0 <= node1 && node1 <= n, "node window [%d, %d) outside [0, %d)", node0, node1, n);
+  if (node1 > node0) {
+    const int64_t w = node1 - node0;
     if (kind == FPB_MOMENTUM_RHS && etype_dim(etype) == 3)
-      k_blk_gather<3><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+      k_blk_gather<3><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out);
     else if (kind == FPB_MOMENTUM_RHS)
-      k_blk_gather<2><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+      k_blk_gather<2><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out);
     else
-      k_blk_gather<1><<<grid_for(n, 256), 256, 0, s>>>(n, node_pptr, node_plist, partial, accumulate, out);
+      k_blk_gather<1><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out);
     FPB_LAUNCH_CHECK();
   }
   return FPB_OK;

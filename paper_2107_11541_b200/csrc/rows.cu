@@ -49,7 +49,7 @@ int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-s
 
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kRowsBlock, (KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS) ? 1 : (KIND == FPB_CONVECTION ? 4 : FPB_ROWS_MINB))
-k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict__ incn,
+k_rows(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const int4* __restrict__ incn,
        const uint32_t* __restrict__ slots, const double* __restrict__ xyz4,
        const double* __restrict__ uvw4, double rho, double mu, double kappa,
        const int32_t* __restrict__ rowptr, int64_t nnz, int rowcap, int accumulate,
@@ -68,7 +68,7 @@ k_rows(int32_t n, const int32_t* __restrict__ slice_ptr, const int4* __restrict_
   extern __shared__ double sacc[];
 
   const int tid = threadIdx.x;
-  const int row = blockIdx.x * kRowsBlock + tid;
+  const int row = row0 + blockIdx.x * kRowsBlock + tid;  // rows [row0, n), row0 % 32 == 0
   // matrix kinds keep every lane alive for the warp-cooperative write-out;
   // rows past n get an empty incidence range
   if (!MAT && row >= n) return;
@@ -382,7 +382,7 @@ struct NbLayout {
 
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kNbBlock, FPB_NB_MINB)
-k_rows_nb(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
+k_rows_nb(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
           const double* __restrict__ xyz4, const double* __restrict__ uvw4,
           const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz, int rowcap,
           int accumulate, double* __restrict__ out) {
@@ -393,7 +393,7 @@ k_rows_nb(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __re
   extern __shared__ double sm[];
 
   const int tid = threadIdx.x;
-  const int row = blockIdx.x * kNbBlock + tid;
+  const int row = row0 + blockIdx.x * kNbBlock + tid;  // rows [row0, n), row0 % 32 == 0
   const bool live = row < n;
   const int lane = row & 31;
   const int m0 = live ? __ldg(slice_ptr + (row >> 5)) : 0;
@@ -751,7 +751,7 @@ __global__ void k_max_rowlen(int32_t n, const int32_t* rowptr, int* out) {
 }
 
 template <int ET, int KIND>
-static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
+static int launch_rows(int32_t n, int32_t row0, const int32_t* slice_ptr, const int32_t* incn,
                        const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
                        double kappa, const int32_t* rowptr, int64_t nnz, int rowcap, int accumulate,
                        double* out, cudaStream_t s) {
@@ -761,8 +761,8 @@ static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
   size_t smem = MAT ? (size_t)NMAT * (rowcap > 1 ? rowcap - 1 : 1) * kRowsBlock * sizeof(double) : 0;
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int blocks = (n + kRowsBlock - 1) / kRowsBlock;
-  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, slice_ptr, reinterpret_cast<const int4*>(incn), slots,
+  int blocks = (n - row0 + kRowsBlock - 1) / kRowsBlock;
+  k_rows<ET, KIND><<<blocks, kRowsBlock, smem, s>>>(n, row0, slice_ptr, reinterpret_cast<const int4*>(incn), slots,
                                                     xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,
                                                     accumulate, out);
   FPB_LAUNCH_CHECK();
@@ -770,36 +770,36 @@ static int launch_rows(int32_t n, const int32_t* slice_ptr, const int32_t* incn,
 }
 
 template <int ET, int KIND>
-static int launch_rows_nb(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const double* xyz4,
+static int launch_rows_nb(int32_t n, int32_t row0, const int32_t* slice_ptr, const uint32_t* slots, const double* xyz4,
                           const double* uvw4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
                           int rowcap, int accumulate, double* out, cudaStream_t s) {
   using L = NbLayout<ET, KIND>;
   const size_t smem = (size_t)L::FIELDS * (rowcap > 1 ? rowcap - 1 : 1) * kNbBlock * sizeof(double);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows_nb<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int blocks = (n + kNbBlock - 1) / kNbBlock;
-  k_rows_nb<ET, KIND><<<blocks, kNbBlock, smem, s>>>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz,
+  const int blocks = (n - row0 + kNbBlock - 1) / kNbBlock;
+  k_rows_nb<ET, KIND><<<blocks, kNbBlock, smem, s>>>(n, row0, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz,
                                                      rowcap, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
 
 template <int ET>
-static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_t* incn,
+static int rows_kind(int kind, int32_t n, int32_t row0, const int32_t* slice_ptr, const int32_t* incn,
                      const uint32_t* slots, const double* xyz4, const double* uvw4, double rho, double mu,
                      double kappa, const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap,
                      int accumulate, double* out, cudaStream_t s) {
   const bool nb = g_tuning_rows_nb && colind && rowcap >= 2 && rowcap <= 256;
 #define FPB_ROWS_CASE(K)                                                                                 \
   case K:                                                                                                \
-    return launch_rows<ET, K>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap, \
+    return launch_rows<ET, K>(n, row0, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap, \
                               accumulate, out, s);
 #define FPB_ROWS_NB_CASE(K)                                                                                  \
   case K:                                                                                                    \
     if (nb)                                                                                                  \
-      return launch_rows_nb<ET, K>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, \
+      return launch_rows_nb<ET, K>(n, row0, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, \
                                    out, s);                                                                  \
-    return launch_rows<ET, K>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,     \
+    return launch_rows<ET, K>(n, row0, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, nnz, rowcap,     \
                               accumulate, out, s);
   switch (kind) {
     FPB_ROWS_NB_CASE(FPB_MASS)
@@ -809,9 +809,9 @@ static int rows_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_
     FPB_ROWS_CASE(FPB_SCALAR_RHS)
     case FPB_GRADIENT_XYZ:
       if (nb)
-        return launch_rows_nb<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap,
+        return launch_rows_nb<ET, FPB_GRADIENT_XYZ>(n, row0, slice_ptr, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap,
                                                     accumulate, out, s);
-      return launch_rows<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
+      return launch_rows<ET, FPB_GRADIENT_XYZ>(n, row0, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr,
                                                nnz, rowcap, accumulate, out, s);
   }
 #undef FPB_ROWS_CASE
@@ -919,7 +919,8 @@ int fpb_pack4(int64_t n, int dim, const double* a, const double* extra, double* 
   return FPB_OK;
 }
 
-int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+int fpb_assemble_rows(int kind, int etype, int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                      const int32_t* inc,
                       const int32_t* conn, const int32_t* incn, const uint32_t* slots, const double* xyz4,
                       const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
                       const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream) {
@@ -934,12 +935,14 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, const int32_t* slice_ptr, 
               "kind %d needs a velocity field", kind);
   FPB_REQUIRE(rowcap <= 256, "row too long for row-owned assembly");
   FPB_REQUIRE(incn, "row-owned assembly needs the rotated inline node records (fpb_incidence_nodes)");
-  if (n <= 0) return FPB_OK;
+  FPB_REQUIRE(row0 >= 0 && row0 % 32 == 0 && row1 <= n && row0 <= row1, "row window [%d, %d) must start on a 32-row slice",
+              row0, row1);
+  if (row1 <= row0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   if (etype == FPB_TET04)
-    return rows_kind<FPB_TET04>(kind, n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
+    return rows_kind<FPB_TET04>(kind, row1, row0, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
                                 rowcap, accumulate, out, s);
-  return rows_kind<FPB_TRI03>(kind, n, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
+  return rows_kind<FPB_TRI03>(kind, row1, row0, slice_ptr, incn, slots, xyz4, uvw4, rho, mu, kappa, rowptr, colind, nnz,
                               rowcap, accumulate, out, s);
 }
 

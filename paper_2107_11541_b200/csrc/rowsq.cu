@@ -95,7 +95,7 @@ __global__ void k_rowlen_max(int32_t n, const int32_t* rowptr, int* out) {
 
 template <int ET, int KIND>
 __global__ void __launch_bounds__(kGlBlock, FPB_GL_MINB)
-k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ inc,
+k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ inc,
           const int32_t* __restrict__ conn, const uint2* __restrict__ slots, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
           int64_t nnz, int rowcap, int accumulate, double* __restrict__ out) {
@@ -112,7 +112,7 @@ k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __res
     for (int i = tid; i < DIM * NN * NG; i += kGlBlock) sdN[i] = c_ref[ET].dN[i];
   __syncthreads();
 
-  const int row = blockIdx.x * kGlBlock + tid;
+  const int row = row0 + blockIdx.x * kGlBlock + tid;  // rows [row0, n)
   if (row >= n) return;
   const int lane = row & 31;
   const int m0 = __ldg(slice_ptr + (row >> 5)), m1 = __ldg(slice_ptr + (row >> 5) + 1);
@@ -333,7 +333,7 @@ k_rows_gl(int32_t n, const int32_t* __restrict__ slice_ptr, const int32_t* __res
 }
 
 template <int ET, int KIND>
-static int launch_gl(int32_t n, const int32_t* slice_ptr, const int32_t* inc, const int32_t* conn,
+static int launch_gl(int32_t n, int32_t row0, const int32_t* slice_ptr, const int32_t* inc, const int32_t* conn,
                      const uint2* slots, const double* xyz4, const double* uvw4, const int32_t* rowptr,
                      const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, cudaStream_t s) {
   constexpr int NMAT = KIND == FPB_GRADIENT_XYZ ? Elem<ET>::DIM : 1;
@@ -341,25 +341,25 @@ static int launch_gl(int32_t n, const int32_t* slice_ptr, const int32_t* inc, co
   FPB_REQUIRE(smem <= 200 * 1024, "row too long for row-owned assembly (%d entries)", rowcap);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows_gl<ET, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_rows_gl<ET, KIND><<<(n + kGlBlock - 1) / kGlBlock, kGlBlock, smem, s>>>(
-      n, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out);
+  k_rows_gl<ET, KIND><<<(n - row0 + kGlBlock - 1) / kGlBlock, kGlBlock, smem, s>>>(
+      n, row0, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
 
 template <int ET>
-static int gl_kind(int kind, int32_t n, const int32_t* slice_ptr, const int32_t* inc, const int32_t* conn,
+static int gl_kind(int kind, int32_t n, int32_t row0, const int32_t* slice_ptr, const int32_t* inc, const int32_t* conn,
                    const uint2* slots, const double* xyz4, const double* uvw4, const int32_t* rowptr,
                    const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, cudaStream_t s) {
   switch (kind) {
     case FPB_MASS:
-      return launch_gl<ET, FPB_MASS>(n, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+      return launch_gl<ET, FPB_MASS>(n, row0, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
     case FPB_LAPLACIAN:
-      return launch_gl<ET, FPB_LAPLACIAN>(n, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+      return launch_gl<ET, FPB_LAPLACIAN>(n, row0, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
     case FPB_CONVECTION:
-      return launch_gl<ET, FPB_CONVECTION>(n, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+      return launch_gl<ET, FPB_CONVECTION>(n, row0, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
     case FPB_GRADIENT_XYZ:
-      return launch_gl<ET, FPB_GRADIENT_XYZ>(n, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+      return launch_gl<ET, FPB_GRADIENT_XYZ>(n, row0, slice_ptr, inc, conn, slots, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
   }
   set_error("row-owned Gauss-loop assembly covers the matrix kinds (got %d)", kind);
   return FPB_ECONFIG;
@@ -397,7 +397,8 @@ int fpb_incidence_slots8(int32_t n, int nn, int64_t ncols, const int32_t* slice_
   return FPB_OK;
 }
 
-int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_ptr, const int32_t* inc,
+int fpb_assemble_rows_gl(int kind, int etype, int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                         const int32_t* inc,
                          const int32_t* conn, const uint32_t* slots, const double* xyz4, const double* uvw4,
                          const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap, int accumulate,
                          double* out, void* stream) {
@@ -407,13 +408,15 @@ int fpb_assemble_rows_gl(int kind, int etype, int32_t n, const int32_t* slice_pt
   FPB_REQUIRE(slots && rowptr && colind && inc && conn && rowcap > 0, "missing incidence / pattern arrays");
   FPB_REQUIRE(kind != FPB_CONVECTION || uvw4, "CONVECTION needs a velocity field");
   FPB_REQUIRE(rowcap <= 256, "row too long for row-owned assembly");
-  if (n <= 0) return FPB_OK;
+  FPB_REQUIRE(row0 >= 0 && row0 % 32 == 0 && row1 <= n && row0 <= row1, "row window [%d, %d) must start on a 32-row slice",
+              row0, row1);
+  if (row1 <= row0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   const uint2* sl = reinterpret_cast<const uint2*>(slots);
   switch (etype) {
-    case FPB_QUAD04: return gl_kind<FPB_QUAD04>(kind, n, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
-    case FPB_PYR05: return gl_kind<FPB_PYR05>(kind, n, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
-    default: return gl_kind<FPB_HEX08>(kind, n, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+    case FPB_QUAD04: return gl_kind<FPB_QUAD04>(kind, row1, row0, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+    case FPB_PYR05: return gl_kind<FPB_PYR05>(kind, row1, row0, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
+    default: return gl_kind<FPB_HEX08>(kind, row1, row0, slice_ptr, inc, conn, sl, xyz4, uvw4, rowptr, colind, nnz, rowcap, accumulate, out, s);
   }
 }
 

@@ -223,6 +223,9 @@ class SlabDomain:
         return halo_sum_rows(self.layout, self.ctx.pattern.rowptr_d, vals, nmat, self.ctx.pattern.nnz,
                              self.group, self.segs)
 
+    def assemble_step(self, vel, rhs, mats, rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side=None):
+        return assemble_step(self, vel, rhs, mats, rho, mu, overlap, side)
+
 
 # --------------------------------------------------------------------------
 # Distributed solver plumbing ("Solver: x-halo of one plane
@@ -369,3 +372,88 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     allreduce_sum_(rr, group)
     true_residual = float(np.sqrt(rr.item())) / float(st[B_BNORM])
     return x, SolverStats(done, converged, history, true_residual)
+
+
+# --------------------------------------------------------------------------
+# Interface-first step with the halo on a side stream (SURVEY.md 8(e):
+# "assemble interface-layer elements first, launch the NCCL halo on a side
+# stream, then assemble interior elements").
+# --------------------------------------------------------------------------
+
+def _step_windows(dom: "SlabDomain") -> dict:
+    """Work windows of one rank's step: element blocks and nodes touching an
+    interface plane (phase A) and the rest (phase B); row windows start on
+    32-row slices and partition [0, n)."""
+    L, g = dom.layout, dom.ctx.groups[0]
+    bp = g.blocks
+    n = dom.ctx.mesh.nnode
+    epl, nlay = L.elems_per_layer, L.k1 - L.k0
+    be, nb = bp.block_elems, bp.nblocks
+    lo_b = -(-epl // be) if L.rank > 0 else 0
+    hi_b = ((nlay - 1) * epl) // be if L.rank < L.world - 1 else nb
+    if lo_b > hi_b:  # thin slab: everything touches an interface
+        lo_b = hi_b = nb
+    planes = [L.plane_rows(k) for _, k in L.interfaces()]
+    A = ((L.plane_rows(L.k0)[1] + 31) // 32) * 32 if L.rank > 0 else 0
+    B = (L.plane_rows(L.k1)[0] // 32) * 32 if L.rank < L.world - 1 else n
+    A, B = min(A, n), max(min(B, n), 0)
+    if A > B:
+        A = B = n if L.rank > 0 else 0
+    # nodes outside the interface planes, as contiguous windows
+    cuts = sorted(planes)
+    rest, at = [], 0
+    for lo, hi in cuts:
+        if lo > at:
+            rest.append((at, lo))
+        at = max(at, hi)
+    if at < n:
+        rest.append((at, n))
+    return {"blocks_A": [(0, lo_b), (hi_b, nb)], "blocks_B": (lo_b, hi_b),
+            "nodes_A": planes, "nodes_B": rest,
+            "rows_A": [(0, A), (B, n)], "rows_B": (A, B)}
+
+
+def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats: torch.Tensor,
+                  rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side: torch.cuda.Stream | None = None):
+    """One decomposed NS step: momentum RHS into rhs[n][dim] and B_x, B_y, B_z
+    into mats[3 nnz], interface rows summed across ranks.  overlap = True runs
+    the interface windows first and the halo exchange on `side` while the
+    interior is assembled; False is the plain sequence (reference for
+    tests).  Results are bitwise identical either way (owner-writes kernels,
+    fixed per-row / per-node summation order)."""
+    from .assembly import KernelKind
+
+    ctx = dom.ctx
+    K = KernelKind.MOMENTUM_RHS
+    if not overlap or dom.layout.world == 1:
+        ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs)
+        ctx.assemble_gradients_d(mats)
+        dom.halo_sum_rhs(rhs)
+        dom.halo_sum_matrix(mats, dom.ctx.mesh.dim)
+        return rhs, mats
+    w = _step_windows(dom)
+    none = (0, 0)
+    # phase A: everything an interface row depends on
+    for b in w["blocks_A"]:
+        if b[1] > b[0]:
+            ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": b, "nodes": none})
+    for nd in w["nodes_A"]:
+        ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": none, "nodes": nd})
+    for r in w["rows_A"]:
+        if r[1] > r[0]:
+            ctx.assemble_gradients_d(mats, {"rows": r})
+    # halo on the side stream, overlapping phase B
+    main = torch.cuda.current_stream()
+    side = side or torch.cuda.Stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        dom.halo_sum_rhs(rhs)
+        dom.halo_sum_matrix(mats, dom.ctx.mesh.dim)
+    # phase B: interior
+    ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": w["blocks_B"], "nodes": none})
+    for nd in w["nodes_B"]:
+        ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": none, "nodes": nd})
+    if w["rows_B"][1] > w["rows_B"][0]:
+        ctx.assemble_gradients_d(mats, {"rows": w["rows_B"]})
+    main.wait_stream(side)
+    return rhs, mats
