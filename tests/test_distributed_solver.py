@@ -231,3 +231,52 @@ def test_interface_first_step_matches_plain_step(cuda_ok, world):
     vel_g, _ = O.bench_fields(full.mesh.nnode, 3)
     want = full.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel_g, None, 1.0, 1e-2, 0.0)
     assert O.rel_diff(np.concatenate([p["rhs"] for p in parts]), want) < 1e-13
+
+
+def _fake_domain(nx, ny, nz, rank, world, be=256):
+    from types import SimpleNamespace
+
+    L = SlabLayout.make(nx, ny, nz, rank, world)
+    ne = (L.k1 - L.k0) * L.elems_per_layer
+    blocks = SimpleNamespace(block_elems=be, nblocks=-(-ne // be))
+    ctx = SimpleNamespace(groups=[SimpleNamespace(blocks=blocks)], mesh=SimpleNamespace(nnode=L.nnode))
+    return SimpleNamespace(layout=L, ctx=ctx), ne
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("dims", [(9, 8, 11), (94, 94, 95), (4, 3, 7)])
+def test_step_windows_partition_the_work(world, dims):
+    """Interface-first windows (distributed._step_windows): row windows start
+    on 32-row slices and tile [0, n); the interface planes lie in the
+    phase-A rows and nodes; node and block windows tile their ranges; the
+    phase-A blocks contain every element of the first / last own layer."""
+    from paper_2107_11541_b200.distributed import _step_windows
+
+    nx, ny, nz = dims
+    if nz < world:
+        pytest.skip("fewer layers than ranks")
+    for r in range(world):
+        dom, ne = _fake_domain(nx, ny, nz * world if nz < 20 else nz, r, world)
+        L, n = dom.layout, dom.ctx.mesh.nnode
+        w = _step_windows(dom)
+        rows = sorted([x for x in w["rows_A"] if x[1] > x[0]] + ([w["rows_B"]] if w["rows_B"][1] > w["rows_B"][0] else []))
+        assert rows[0][0] == 0 and rows[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        assert all(x[0] % 32 == 0 for x in rows)
+        for _, k in L.interfaces():
+            lo, hi = L.plane_rows(k)
+            assert any(a <= lo and hi <= b for a, b in w["rows_A"])
+            assert (lo, hi) in w["nodes_A"]
+        nodes = sorted(w["nodes_A"] + w["nodes_B"])
+        assert nodes[0][0] == 0 and nodes[-1][1] == n and all(a[1] == b[0] for a, b in zip(nodes, nodes[1:]))
+        nb, be = dom.ctx.groups[0].blocks.nblocks, dom.ctx.groups[0].blocks.block_elems
+        blk = sorted([x for x in w["blocks_A"] if x[1] > x[0]] + ([w["blocks_B"]] if w["blocks_B"][1] > w["blocks_B"][0] else []))
+        assert blk[0][0] == 0 and blk[-1][1] == nb and all(a[1] == b[0] for a, b in zip(blk, blk[1:]))
+        covered = set()
+        for a, b in w["blocks_A"]:
+            covered.update(range(a * be, min(b * be, ne)))
+        epl, nlay = L.elems_per_layer, L.k1 - L.k0
+        if r > 0:
+            assert covered.issuperset(range(0, epl))
+        if r < world - 1:
+            assert covered.issuperset(range((nlay - 1) * epl, nlay * epl))
