@@ -305,9 +305,10 @@ int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const in
 /* One reduction step of an iteration, for domain decomposition: step 1 =
  * direction + v = A phat with (rtilde, v); 2 = s, shat with ||s||^2; 3 =
  * t = A shat with (t, s), (t, t); 4 = x, r update with ||r||^2, (rtilde, r).
- * With defer = 1 the partial sums land in state[16..17]; the caller
- * allreduces them (and refreshes ghost entries of v / t after steps 1 / 3)
- * before fpb_bicgstab_finish(step). */
+ * With defer = 1 the partial sums land in state[16..17] (step 2's ||s||^2
+ * in state[18], so it can ride on step 3's reduction); the caller allreduces
+ * them (and refreshes ghost entries of v / t after steps 1 / 3) before
+ * fpb_bicgstab_finish(step) — finish(2) then finish(3) after step 3. */
 int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
                       const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
                       double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,

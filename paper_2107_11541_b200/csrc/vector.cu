@@ -448,7 +448,7 @@ __global__ void k_pcg_direction(int64_t n, double* __restrict__ p, const double*
 // ---------------------------------------------------------------------------
 enum {
   B_RHO = 0, B_RHO_PREV, B_ALPHA, B_OMEGA, B_BNORM, B_ATOL, B_STATUS, B_IT, B_RELRES, B_BETA, B_RV,
-  B_TS, B_TT, B_FIRST, B_RED = 16, B_NSTATE = 20
+  B_TS, B_TT, B_FIRST, B_RED = 16, B_NSTATE = 20  // B_RED..B_RED+2: deferred partial sums
 };
 enum { BSTEP_INIT = 0, BSTEP_AV, BSTEP_S, BSTEP_AT, BSTEP_UPDATE };
 constexpr double kBreakTol = 4.930380657631324e-32;  // eps^2 (scipy's rhotol / omegatol)
@@ -533,13 +533,13 @@ struct BicgRed {  // where a kernel's totals go
 
 template <int NV>
 __device__ __forceinline__ void bicg_reduce(double (&acc)[NV], int step, double* state, double* work,
-                                            int slot, const BicgRed& R) {
+                                            int slot, const BicgRed& R, int red_off = 0) {
   block_sum<NV>(acc);
   double tot[NV];
   if (grid_finish<NV>(acc, work, slot, tot)) {
     if (R.defer) {
 #pragma unroll
-      for (int q = 0; q < NV; ++q) state[B_RED + q] = tot[q];
+      for (int q = 0; q < NV; ++q) state[B_RED + red_off + q] = tot[q];
     } else {
       bicg_finish(step, tot, state, R.hist, R.hist_cap, R.tol);
     }
@@ -633,7 +633,9 @@ k_bicg_s(int64_t n, const double* __restrict__ r, const double* __restrict__ v, 
     sh[i] = d ? __ddiv_rn(si, d[i]) : si;
     if (i >= R.own_lo && i < R.own_hi) acc[0] += si * si;
   }
-  bicg_reduce<1>(acc, BSTEP_S, state, work, 2, R);
+  // deferred: ||s||^2 goes to state[B_RED + 2] and rides on the allreduce
+  // after K4 (three reductions per iteration cross ranks, not four)
+  bicg_reduce<1>(acc, BSTEP_S, state, work, 2, R, 2);
 }
 
 // K4: t = A shat; (t, s), (t, t); omega = ts / tt
@@ -694,6 +696,7 @@ k_bicg_update(int64_t n, double* __restrict__ x, double* __restrict__ r, const d
 
 __global__ void k_bicg_finish(int step, double* state, double* hist, int64_t hist_cap, double tol) {
   double tot[2] = {state[B_RED], state[B_RED + 1]};
+  if (step == BSTEP_S) tot[0] = state[B_RED + 2];
   bicg_finish(step, tot, state, hist, hist_cap, tol);
 }
 

@@ -287,8 +287,9 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     A is this rank's extended-slab CSR with halo-summed values (rows of
     planes k0..k1 are global rows), b a node vector consistent on every local
     plane.  Every iteration runs the one-GPU fused kernels with reductions
-    restricted to the owned rows, allreduces the 2-double partials (four
-    times) and refreshes the ghost planes of v = A phat and t = A shat.
+    restricted to the owned rows, allreduces the partial sums three times
+    (||s|| rides on the (t, s), (t, t) reduction) and refreshes the ghost
+    planes of v = A phat and t = A shat.
     Returns (x, SolverStats) with x consistent on every local plane; the
     iterates are those of krylov.bicgstab_solve on the global system up to
     the order of the cross-rank sums.
@@ -318,6 +319,7 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     lib = _lib.load()
     state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
     red = state[16:18]
+    red3 = state[16:19]  # after K4: (t, s), (t, t) and the deferred ||s||^2
     cap = max(1, min(64, max_iter))
     hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
     work = dot_work()
@@ -347,12 +349,21 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     while done < max_iter:
         k = min(check_every, max_iter - done)
         for _ in range(k):
-            for step, ghost in ((1, v), (2, None), (3, t), (4, None)):
-                _lib.call("fpb_bicgstab_step", step, *args)
-                if ghost is not None:
-                    refresh_ghosts(layout, ghost, group)
-                allreduce_sum_(red, group)
-                _lib.call("fpb_bicgstab_finish", step, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+            # three cross-rank reductions per iteration: K2's (r~, v); K3's
+            # ||s||^2 together with K4's (t, s), (t, t); K5's ||r||^2, (r~, r)
+            _lib.call("fpb_bicgstab_step", 1, *args)
+            refresh_ghosts(layout, v, group)
+            allreduce_sum_(red, group)
+            _lib.call("fpb_bicgstab_finish", 1, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+            _lib.call("fpb_bicgstab_step", 2, *args)
+            _lib.call("fpb_bicgstab_step", 3, *args)
+            refresh_ghosts(layout, t, group)
+            allreduce_sum_(red3, group)
+            _lib.call("fpb_bicgstab_finish", 2, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+            _lib.call("fpb_bicgstab_finish", 3, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+            _lib.call("fpb_bicgstab_step", 4, *args)
+            allreduce_sum_(red, group)
+            _lib.call("fpb_bicgstab_finish", 4, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
         st = state.cpu().numpy()
         it = int(st[B_IT])
         if it > done:
