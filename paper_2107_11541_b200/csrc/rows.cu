@@ -42,9 +42,6 @@ constexpr int kRowsBlock = 128;
 #endif
 constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
 int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
-#ifndef FPB_ROWS_LD256
-#define FPB_ROWS_LD256 1
-#endif
 
 
 template <int ET, int KIND>
