@@ -149,6 +149,94 @@ __device__ __forceinline__ double hex_jacobian(const HexCoef& h, int g, double (
          J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
 }
 
+// Q1 hexahedron, Walsh (sign-product) forms on the 2x2x2 Gauss rule
+// (elements.py:148-166 corners, :226-229 points).  U is a bitmask of
+// directions (1 = xi, 2 = eta, 4 = zeta); corner b has signs s_d(b),
+// Gauss point g has x_d(g) = (bit d of g) ? q : -q.  With
+// mono(U, g) = prod_{d in U} x_d(g) and s_U(b) = prod_{d in U} s_d(b):
+//   nodal field  v(xi) = 1/8 sum_U h8[U] mono(U, xi),  h8 = hex_walsh(v)
+//   N_b(g)          = 1/8 sum_U s_U(b) mono(U, g)
+//   dN_b/dxi_m (g)  = 1/8 sum_{U ∋ m} s_U(b) mono(U \ m, g)
+// so point values, reference-space derivatives and the test-function sums
+// sum_g (W_g N_b + sum_m V_g[m] dN_b/dxi_m) all go through 8 coefficients:
+// 8 FMA per value or point instead of 8 per (node, point) and direction.
+// corner b -> p with bit d of p = (s_d(b) > 0): 0 1 3 2 4 5 7 6
+__host__ __device__ constexpr int hex_corner_p(int b) { return b ^ ((b >> 1) & 1); }
+
+__host__ __device__ constexpr double hex_mono(int U, int g) {
+  constexpr double q = 0.5773502691896258;
+  double r = 1.0;
+  for (int d = 0; d < 3; ++d)
+    if ((U >> d) & 1) r *= ((g >> d) & 1) ? q : -q;
+  return r;
+}
+
+// h8[U] = sum_b s_U(b) v_b (8x the Walsh coefficient): 24 adds
+__device__ __forceinline__ void hex_walsh(const double (&v)[8], double (&h8)[8]) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) h8[hex_corner_p(b)] = v[b];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      if (!((p >> d) & 1)) {
+        const double lo = h8[p], hi = h8[p | (1 << d)];
+        h8[p] = lo + hi;
+        h8[p | (1 << d)] = hi - lo;
+      }
+}
+
+// v(g) and dv/dxi_m(g) from h8 (g compile-time after unrolling)
+__device__ __forceinline__ double hex_value(const double (&h8)[8], int g) {
+  double r = 0.0;
+#pragma unroll
+  for (int U = 0; U < 8; ++U) r = fma(0.125 * hex_mono(U, g), h8[U], r);
+  return r;
+}
+__device__ __forceinline__ double hex_dxi(const double (&h8)[8], int m, int g) {
+  double r = 0.0;
+#pragma unroll
+  for (int U = 0; U < 8; ++U)
+    if ((U >> m) & 1) r = fma(0.125 * hex_mono(U & ~(1 << m), g), h8[U], r);
+  return r;
+}
+
+// test-function sums R_b = sum_g (W_g N_b(g) + sum_m V_g[m] dN_b/dxi_m(g))
+struct HexTest {
+  double R[8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int U = 0; U < 8; ++U) R[U] = 0.0;
+  }
+  __device__ __forceinline__ void add(int g, double W, const double (&V)[3]) {
+#pragma unroll
+    for (int U = 0; U < 8; ++U) {
+      double r = fma(0.125 * hex_mono(U, g), W, R[U]);
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+        if ((U >> m) & 1) r = fma(0.125 * hex_mono(U & ~(1 << m), g), V[m], r);
+      R[U] = r;
+    }
+  }
+  // out[b] = sum_U s_U(b) R[U]: 24 adds
+  __device__ __forceinline__ void finish(double (&out)[8]) {
+    double t[8];
+#pragma unroll
+    for (int U = 0; U < 8; ++U) t[U] = R[U];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (!((p >> d) & 1)) {
+          const double lo = t[p], hi = t[p | (1 << d)];
+          t[p] = lo - hi;
+          t[p | (1 << d)] = lo + hi;
+        }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) out[b] = t[hex_corner_p(b)];
+  }
+};
+
 template <int ET>
 __device__ __forceinline__ void grad_shape(const double (&J)[Elem<ET>::DIM][Elem<ET>::DIM], double det,
                                            int g, double (&gN)[Elem<ET>::DIM][Elem<ET>::NN]) {

@@ -23,6 +23,112 @@ struct Out {
   static constexpr int NOUT = MAT ? NN * NN : GRADXYZ ? DIM * NN * NN : KIND == FPB_MOMENTUM_RHS ? NN * DIM : NN;
 };
 
+// HEX08 momentum / scalar RHS through the Walsh forms (common.cuh): the
+// same terms as element_integrate below, regrouped so that no per-node
+// shape-gradient table is formed —
+//   grad u_k = Ji^T du_k/dxi,  du_k/dxi from the field's Walsh coefficients;
+//   sum_l S[k][l] gN_l(i) = sum_m (Ji S_k)[m] dN_i/dxi_m, and w Ji = w_g A
+//   (A the adjugate, w = det w_g), so the viscous / diffusive test sums need
+//   no reciprocal.  Equal to the reference's Gauss sums to rounding.
+template <int KIND>
+__device__ __forceinline__ void hex_rhs_integrate(const double (&xe)[8][3],
+                                                  const double (&ue)[Out<FPB_HEX08, KIND>::NU][3],
+                                                  const double (&fe)[Out<FPB_HEX08, KIND>::NF], double rho,
+                                                  double mu, double kappa,
+                                                  double (&acc)[Out<FPB_HEX08, KIND>::NOUT]) {
+  constexpr int ET = FPB_HEX08;
+  constexpr int NV = KIND == FPB_MOMENTUM_RHS ? 3 : 1;
+  HexCoef hc;
+  hex_coeffs(xe, hc);
+  double uh[3][8];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double v[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) v[b] = ue[b][k];
+    hex_walsh(v, uh[k]);
+  }
+  double fh[8];
+  if constexpr (KIND == FPB_SCALAR_RHS) hex_walsh(fe, fh);
+  HexTest T[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) T[k].zero();
+
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    double J[3][3];
+    const double det = hex_jacobian(hc, g, J);
+    double A[3][3];  // A[m][l] = det * Ji[m][l]
+    A[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    A[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+    A[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+    A[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    A[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+    A[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+    A[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    A[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+    A[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    const double inv = 1.0 / det;
+    const double w = det * refW<ET>(g);
+    double ug[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ug[k] = hex_value(uh[k], g);
+    if constexpr (KIND == FPB_MOMENTUM_RHS) {  // _kernels.py:320-382
+      double Gx[3][3], G[3][3], S[3][3], c[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) Gx[m][k] = hex_dxi(uh[k], m, g);
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) G[l][k] = inv * (A[0][l] * Gx[0][k] + A[1][l] * Gx[1][k] + A[2][l] * Gx[2][k]);
+      const double divu = G[0][0] + G[1][1] + G[2][2];
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) S[l][k] = 0.5 * (G[l][k] + G[k][l]);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double us = 0.0, gk = 0.0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          us += ug[l] * S[l][k];
+          gk += ug[l] * G[k][l];
+        }
+        c[k] = 2.0 * us + divu * ug[k] - gk;
+      }
+      const double sv = -2.0 * mu * refW<ET>(g);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double V[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) V[m] = sv * (A[m][0] * S[k][0] + A[m][1] * S[k][1] + A[m][2] * S[k][2]);
+        T[k].add(g, -w * (rho * c[k]), V);
+      }
+    } else {  // SCALAR_RHS, _kernels.py:420-461
+      double px[3], gphi[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) px[m] = hex_dxi(fh, m, g);
+#pragma unroll
+      for (int l = 0; l < 3; ++l) gphi[l] = inv * (A[0][l] * px[0] + A[1][l] * px[1] + A[2][l] * px[2]);
+      const double adv = ug[0] * gphi[0] + ug[1] * gphi[1] + ug[2] * gphi[2];
+      const double sk = -kappa * refW<ET>(g);
+      double V[3];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) V[m] = sk * (A[m][0] * gphi[0] + A[m][1] * gphi[1] + A[m][2] * gphi[2]);
+      T[0].add(g, -w * adv, V);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double o[8];
+    T[k].finish(o);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[b * NV + k] = o[b];
+  }
+}
+
 // acc: matrices [i][j] (GRADIENT_XYZ: [k][i][j]); MOMENTUM [a][k]; SCALAR [a]
 template <int ET, int KIND>
 __device__ __forceinline__ void element_integrate(
@@ -32,6 +138,10 @@ __device__ __forceinline__ void element_integrate(
   constexpr int NN = Elem<ET>::NN, NG = Elem<ET>::NG, DIM = Elem<ET>::DIM;
   constexpr int NOUT = Out<ET, KIND>::NOUT;
   constexpr bool NEED_GRAD = KIND != FPB_MASS;
+  if constexpr (ET == FPB_HEX08 && (KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS)) {
+    hex_rhs_integrate<KIND>(xe, ue, fe, rho, mu, kappa, acc);
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < NOUT; ++q) acc[q] = 0.0;
 

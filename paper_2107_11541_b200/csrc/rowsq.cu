@@ -34,7 +34,73 @@ namespace fpb {
 #ifndef FPB_GL_MINB
 #define FPB_GL_MINB 4
 #endif
+#ifndef FPB_GL_MINB_MASS
+#define FPB_GL_MINB_MASS 5  // hex MASS: 5 CTAs / SM measured faster (profiles/r01m_hexmom)
+#endif
 constexpr int kGlBlock = FPB_GL_BLOCK;
+
+// Gauss-point sign moments for the 8-node hex (elements.py:148-166 corners
+// (+-1, +-1, +-1), :226-229 the 2x2x2 rule, x fastest, unit weights):
+//   dN_l(b, g) = s_l(b)/8 * prod_{m != l} (1 + s_m(b) x_m(g)),  x_m(g) = +-q,
+// so for any Gauss-point vector V_g
+//   sum_g V_g[l] dN_l(b, g) = s_l(b)/8 * (M0 + s_m1(b) q M1 + s_m2(b) q M2 + s_m1 s_m2 q^2 M3)[l]
+// with M_t the moments of V[l] against 1, sgn x_m1, sgn x_m2, their product
+// (m1 < m2 the two directions other than l).  12 FMA per point and matrix
+// replace 24 (8 columns x 3 directions), plus 8 + 16 adds per matrix at the
+// end; the 1/8 and q powers ride in the point coefficients c, c1, c2.
+template <int NM>
+struct HexMoments {
+  double M[NM][3][4];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < NM; ++k)
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) M[k][l][t] = 0.0;
+  }
+  // c = 1/8 * point weight, c1 = c q, c2 = c q^2; g compile-time after unrolling
+  __device__ __forceinline__ void add(int g, int k, const double (&V)[3], double c, double c1, double c2) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const int m1 = l == 0 ? 1 : 0, m2 = l == 2 ? 1 : 2;
+      const double s1 = ((g >> m1) & 1) ? 1.0 : -1.0, s2 = ((g >> m2) & 1) ? 1.0 : -1.0;
+      M[k][l][0] = fma(c, V[l], M[k][l][0]);
+      M[k][l][1] = fma(s1 * c1, V[l], M[k][l][1]);
+      M[k][l][2] = fma(s2 * c1, V[l], M[k][l][2]);
+      M[k][l][3] = fma((s1 * s2) * c2, V[l], M[k][l][3]);
+    }
+  }
+  // acc[k][b] = sum_l sum_g V_g[l] dN_l(b, g) (overwrites)
+  __device__ __forceinline__ void finish(double (&acc)[NM][8]) {
+#pragma unroll
+    for (int k = 0; k < NM; ++k) {
+      double T[3][4];  // T[l][2 * (s_m2 > 0) + (s_m1 > 0)]
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const double p = M[k][l][0] + M[k][l][3], m = M[k][l][0] - M[k][l][3];
+        const double u = M[k][l][1] + M[k][l][2], v = M[k][l][1] - M[k][l][2];
+        T[l][3] = p + u;
+        T[l][0] = p - u;
+        T[l][1] = m + v;
+        T[l][2] = m - v;
+      }
+      constexpr int sg[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
+                                {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};  // corner b: s_d > 0
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        double r = 0.0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+          const int m1 = l == 0 ? 1 : 0, m2 = l == 2 ? 1 : 2;
+          const double t = T[l][2 * sg[b][m2] + sg[b][m1]];
+          r = l == 0 ? (sg[b][0] ? t : -t) : (sg[b][l] ? r + t : r - t);
+        }
+        acc[k][b] = r;
+      }
+    }
+  }
+};
 
 // slot bytes of every SELL entry (nn <= 8), see header comment; also
 // reports the longest row (rowcap) and missing node pairs
@@ -94,7 +160,7 @@ __global__ void k_rowlen_max(int32_t n, const int32_t* rowptr, int* out) {
 }
 
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kGlBlock, FPB_GL_MINB)
+__global__ void __launch_bounds__(kGlBlock, (KIND == FPB_MASS && ET == FPB_HEX08) ? FPB_GL_MINB_MASS : FPB_GL_MINB)
 k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const int32_t* __restrict__ inc,
           const int32_t* __restrict__ conn, const uint2* __restrict__ slots, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
@@ -106,8 +172,21 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
   extern __shared__ double sm[];
   __shared__ double sN[NN * NG];           // N[a][g], runtime a
   __shared__ double sdN[DIM * NN * NG];    // dN[l][a][g], runtime a (LAPLACIAN)
+  // hexes except MASS: Gauss-point sign moments (HexMoments); for GRADIENT
+  // sN holds the point coefficient 1/8 w_g N_a(g) sum_c N_c(g) instead of N
+  constexpr bool HMOM = ET == FPB_HEX08 && KIND != FPB_MASS;
+  constexpr double kQ = 0.5773502691896258, kQ2 = kQ * kQ;
   const int tid = threadIdx.x;
-  for (int i = tid; i < NN * NG; i += kGlBlock) sN[i] = c_ref[ET].N[i];
+  for (int i = tid; i < NN * NG; i += kGlBlock) {
+    if constexpr (HMOM && KIND == FPB_GRADIENT_XYZ) {
+      const int g = i % NG;
+      double sNg = 0.0;
+      for (int c = 0; c < NN; ++c) sNg += c_ref[ET].N[c * NG + g];
+      sN[i] = 0.125 * (c_ref[ET].w[g] * c_ref[ET].N[i] * sNg);
+    } else {
+      sN[i] = c_ref[ET].N[i];
+    }
+  }
   if constexpr (KIND == FPB_LAPLACIAN)
     for (int i = tid; i < DIM * NN * NG; i += kGlBlock) sdN[i] = c_ref[ET].dN[i];
   __syncthreads();
@@ -153,17 +232,13 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
   };
 
   // keep the next element's node records in flight while integrating the
-  // current one (two register stages): measured faster for every kind but
-  // the 3-matrix GRADIENT_XYZ of 8-node elements, whose extra registers cost
-  // more than the hidden latency (profiles/r01i/gl_variants.txt)
-#ifndef FPB_GL_PREFETCH
-#define FPB_GL_PREFETCH 0
-#endif
-  constexpr bool PREFETCH = FPB_GL_PREFETCH || NN <= 4 || KIND != FPB_GRADIENT_XYZ;
+  // current one (two register stages; profiles/r01i/gl_variants.txt,
+  // profiles/r01m_hexmom: with the Gauss-point moments the 3-matrix hex
+  // gradient gains too)
   Stage cur, nxt;
   load(m0, cur);
   for (int m = m0; m < m1 && cur.e >= 0; ++m) {
-    if constexpr (PREFETCH) load(m + 1, nxt);
+    load(m + 1, nxt);
     // the row's local node a (slot byte 0xff)
     int a = 0;
 #pragma unroll
@@ -176,6 +251,8 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
     for (int k = 0; k < NMAT; ++k)
 #pragma unroll
       for (int b = 0; b < NN; ++b) acc[k][b] = 0.0;
+    HexMoments<HMOM ? NMAT : 1> hm;
+    if constexpr (HMOM) hm.zero();
 
     HexCoef hc;
     if constexpr (ET == FPB_HEX08) hex_coeffs(cur.x, hc);
@@ -238,12 +315,17 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
           for (int d = 0; d < DIM; ++d) t += A[l][d] * Ga[d];
           q[l] = wd * t;
         }
+        if constexpr (HMOM) {
+          const double V[3] = {q[0], q[1], q[2]};
+          hm.add(g, 0, V, 0.125, 0.125 * kQ, 0.125 * kQ2);
+        } else {
 #pragma unroll
-        for (int b = 0; b < NN; ++b) {
-          double t = 0.0;
+          for (int b = 0; b < NN; ++b) {
+            double t = 0.0;
 #pragma unroll
-          for (int l = 0; l < DIM; ++l) t += q[l] * refdN<ET>(l, b, g);
-          acc[0][b] += t;
+            for (int l = 0; l < DIM; ++l) t += q[l] * refdN<ET>(l, b, g);
+            acc[0][b] += t;
+          }
         }
       } else if constexpr (KIND == FPB_CONVECTION) {
         double ug[DIM];
@@ -263,12 +345,25 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
           Au[l] = s;
         }
         const double wa = refW<ET>(g) * Na;
+        if constexpr (HMOM) {
+          const double c = 0.125 * wa;
+          const double V[3] = {Au[0], Au[1], Au[2]};
+          hm.add(g, 0, V, c, c * kQ, c * kQ2);
+        } else {
 #pragma unroll
-        for (int b = 0; b < NN; ++b) {
-          double adv = 0.0;
+          for (int b = 0; b < NN; ++b) {
+            double adv = 0.0;
 #pragma unroll
-          for (int l = 0; l < DIM; ++l) adv += Au[l] * refdN<ET>(l, b, g);
-          acc[0][b] += wa * adv;
+            for (int l = 0; l < DIM; ++l) adv += Au[l] * refdN<ET>(l, b, g);
+            acc[0][b] += wa * adv;
+          }
+        }
+      } else if constexpr (HMOM) {  // GRADIENT_XYZ, hex: Na is the point coefficient
+        const double c1 = Na * kQ, c2 = Na * kQ2;
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+          const double V[3] = {A[0][k], A[1][k], A[2][k]};
+          hm.add(g, k, V, Na, c1, c2);
         }
       } else {  // GRADIENT_XYZ
         double sNg = 0.0;
@@ -290,6 +385,7 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
         }
       }
     }
+    if constexpr (HMOM) hm.finish(acc);
     // scatter the row's NN x NMAT values: own node to registers, others to
     // the off-diagonal sums (distinct slots: loads before stores)
     double old[NN][NMAT];
@@ -308,8 +404,7 @@ k_rows_gl(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const 
         if (so[b] >= 0) my[so[b] * SS + k * kGlBlock] = old[b][k] + acc[k][b];
         else dacc[k] += acc[k][b];
       }
-    if constexpr (PREFETCH) cur = nxt;
-    else load(m + 1, cur);
+    cur = nxt;
   }
 
   // write the row (diagonal from registers)
