@@ -50,7 +50,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define FPB_BLK_THREADS 128
 #endif
 #ifndef FPB_BLK_MINB
-#define FPB_BLK_MINB 4
+#define FPB_BLK_MINB 4  // affine, other kinds
+#endif
+// affine momentum / scalar RHS: CTAs per SM measured on config 2
+// (profiles/r01n_blk: momentum 0.222 -> 0.208 ms at 5, scalar 0.155 -> 0.151 at 6)
+#ifndef FPB_BLK_MINB_MOMENTUM
+#define FPB_BLK_MINB_MOMENTUM 5
+#endif
+#ifndef FPB_BLK_MINB_SCALAR
+#define FPB_BLK_MINB_SCALAR 6
 #endif
 #ifndef FPB_BLK_INTERLEAVE
 #define FPB_BLK_INTERLEAVE 1  // the compiler interleaves a thread's two elements (ILP)
@@ -177,7 +185,11 @@ __global__ void k_p2_sort(int32_t n, const int32_t* ptr, int32_t* list) {
 // NN x kBlockElems uint16], [node data of the block's distinct nodes:
 // maxnu x NDAT].
 template <int ET, int KIND>
-__global__ void __launch_bounds__(kBlockThreads, Elem<ET>::AFFINE ? FPB_BLK_MINB : FPB_BLK_MINB_NONAFFINE)
+__global__ void __launch_bounds__(kBlockThreads,
+                                  !Elem<ET>::AFFINE              ? FPB_BLK_MINB_NONAFFINE
+                                  : KIND == FPB_MOMENTUM_RHS     ? FPB_BLK_MINB_MOMENTUM
+                                  : KIND == FPB_SCALAR_RHS       ? FPB_BLK_MINB_SCALAR
+                                                                 : FPB_BLK_MINB)
 k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const double* __restrict__ vel, const double* __restrict__ phi,
           double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
