@@ -4,6 +4,7 @@
 // the last block to finish (atomic ticket) folds the per-block partials in
 // index order.  Repeated calls are therefore bitwise reproducible, like the
 // reference's sequential loops (test_sparse.py:93-107).
+#include <cub/device/device_scan.cuh>
 #include "common.cuh"
 
 namespace fpb {
@@ -236,6 +237,89 @@ __global__ void __launch_bounds__(256) k_spmv_r(int32_t n, const int32_t* __rest
 #ifndef FPB_SPMV_GROUPS
 #define FPB_SPMV_GROUPS 4
 #endif
+
+// ---- SELL-32 copy of a CSR matrix (solver-side format) -------------------------
+// Slice s = rows [32 s, 32 s + 32), width w_s = its longest row; entry k of
+// row 32 s + l at sell_ptr[s] + 32 k + l (padding never read: each row stops
+// at its own length).  One thread per row: every index / value load of a
+// warp is one contiguous 128 / 256-byte line (no rowptr -> entry dependency,
+// no idle lanes on short rows), and the row is summed in ascending column
+// order with separately rounded products and sums — the reference's order
+// and rounding (sparse.py:80-84), bit for bit.
+__global__ void k_sell_width(int32_t n, const int32_t* __restrict__ rowptr, int64_t* __restrict__ width) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int len = row < n ? rowptr[row + 1] - rowptr[row] : 0;
+  len = __reduce_max_sync(0xffffffffu, len);
+  if ((threadIdx.x & 31) == 0 && (row >> 5) < ((int64_t)n + 31) / 32) width[row >> 5] = 32 * (int64_t)len;
+}
+
+__global__ void k_sell_fill(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                            const double* __restrict__ vals, const int64_t* __restrict__ sell_ptr,
+                            int32_t* __restrict__ scol, double* __restrict__ sval) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // rows past n: padding only
+  if (row >= ((int64_t)n + 31) / 32 * 32) return;
+  const int64_t base = sell_ptr[row >> 5] + (row & 31);
+  const int w = (int)((sell_ptr[(row >> 5) + 1] - sell_ptr[row >> 5]) >> 5);
+  const int lo = row < n ? rowptr[row] : 0, len = row < n ? rowptr[row + 1] - lo : 0;
+  for (int k = 0; k < w; ++k) {
+    if (scol) scol[base + 32 * (int64_t)k] = k < len ? colind[lo + k] : -1;
+    if (sval) sval[base + 32 * (int64_t)k] = k < len ? vals[lo + k] : 0.0;
+  }
+}
+
+// entries per load batch: 16 keeps more bytes in flight on large matrices,
+// 8 more warps resident on small ones (tools/spmv_probe.py: config-2 MASS
+// 71 % vs 61 % of HBM with 8; config-5 / config-4 ~100 % with 16)
+constexpr int kSellSmallRows = 4 << 20;
+inline int sell_batch(int32_t n) { return n >= kSellSmallRows ? 16 : 8; }
+#ifndef FPB_SELL_LDG
+#define FPB_SELL_LDG 0
+#endif
+__device__ __forceinline__ int sell_ld(const int32_t* p) { return FPB_SELL_LDG ? __ldg(p) : __ldcs(p); }
+__device__ __forceinline__ double sell_ld(const double* p) { return FPB_SELL_LDG ? __ldg(p) : __ldcs(p); }
+
+// row . x for one SELL row; rows of a warp are one slice (row >> 5
+// uniform).  Padding entries carry column -1 (and value 0), so a row needs
+// no length lookup: index and value loads of a batch go out together, then
+// the x gathers of the valid entries.
+template <int B>
+__device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sell_ptr,
+                                               const int32_t* __restrict__ scol,
+                                               const double* __restrict__ sval,
+                                               const double* __restrict__ x, int64_t row) {
+  const int64_t s0 = __ldg(sell_ptr + (row >> 5));
+  const int w = (int)((__ldg(sell_ptr + (row >> 5) + 1) - s0) >> 5);
+  const int64_t base = s0 + (row & 31);
+  double acc = 0.0;
+  for (int k0 = 0; k0 < w; k0 += B) {
+    int c[B];
+    double v[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const bool ok = k0 + j < w;
+      c[j] = ok ? sell_ld(scol + base + 32 * (int64_t)(k0 + j)) : -1;
+      v[j] = ok ? sell_ld(sval + base + 32 * (int64_t)(k0 + j)) : 0.0;
+    }
+    double xv[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], xv[j]));
+  }
+  return acc;
+}
+
+template <int B>
+__global__ void __launch_bounds__(256) k_spmv_sell(int32_t n, const int64_t* __restrict__ sell_ptr,
+                                                   const int32_t* __restrict__ scol,
+                                                   const double* __restrict__ sval,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if ((row & ~31LL) >= n) return;  // whole warps past the end
+  const double a = sell_row_dot<B>(sell_ptr, scol, sval, x, row);
+  if (row < n) y[row] = a;
+}
 
 __global__ void k_axpy(int64_t n, double alpha, const double* __restrict__ x,
                        const double* __restrict__ y, double* __restrict__ out) {
@@ -700,6 +784,132 @@ __global__ void k_bicg_finish(int step, double* state, double* hist, int64_t his
   bicg_finish(step, tot, state, hist, hist_cap, tol);
 }
 
+// ---- SELL-32 twins of the fused solver kernels (sparse.SellCopy) -----------
+// Same epilogues as the CSR kernels above; the matrix rows come from
+// sell_row_dot (one thread per row, the reference's per-row order).  Rows
+// are walked grid-stride in whole slices (n32 = n rounded up to 32).
+#define FPB_SELL_LOOP(n)                                                          \
+  const int64_t n32_ = ((int64_t)(n) + 31) & ~31LL;                              \
+  const int64_t stride_ = (int64_t)gridDim.x * blockDim.x;                       \
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < n32_; row += stride_)
+
+struct SellMat {
+  const int64_t* ptr;
+  const int32_t* col;
+  const double* val;
+};
+
+template <int B>
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const double* __restrict__ x0,
+                double* __restrict__ x, double* __restrict__ r, double* state, double* hist, double tol,
+                double* work) {
+  double v[2] = {0.0, 0.0};
+  FPB_SELL_LOOP(n) {
+    const double ax = x0 ? sell_row_dot<B>(A.ptr, A.col, A.val, x0, row) : 0.0;
+    if (row < n) {
+      const double ri = x0 ? axpy1(-1.0, ax, b[row]) : b[row];  // krylov.py:59
+      x[row] = x0 ? x0[row] : 0.0;
+      r[row] = ri;
+      v[0] += b[row] * b[row];
+      v[1] += ri * ri;
+    }
+  }
+  block_sum<2>(v);
+  double tot[2];
+  if (grid_finish<2>(v, work, 0, tot)) {
+    double bnorm = sqrt(tot[0]);
+    double relres = bnorm == 0.0 ? 0.0 : sqrt(tot[1]) / bnorm;
+    state[S_BNORM] = bnorm;
+    state[S_TOL] = tol;
+    state[S_IT] = 0.0;
+    state[S_RELRES] = relres;
+    state[S_PQ] = 0.0;
+    state[S_STATUS] = (bnorm == 0.0 || relres <= tol) ? 1.0 : 0.0;
+    hist[0] = relres;
+  }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDotThreads)
+k_pcg_spmv_sell(int32_t n, SellMat A, const double* __restrict__ p, double* __restrict__ q, double* state,
+                double* work) {
+  if (state[S_STATUS] != 0.0) return;
+  double v[1] = {0.0};
+  FPB_SELL_LOOP(n) {
+    const double qi = sell_row_dot<B>(A.ptr, A.col, A.val, p, row);
+    if (row < n) {
+      q[row] = qi;
+      v[0] += p[row] * qi;
+    }
+  }
+  block_sum<1>(v);
+  double tot[1];
+  if (grid_finish<1>(v, work, 2, tot)) {
+    state[S_PQ] = tot[0];
+    if (tot[0] <= 0.0) state[S_STATUS] = 2.0;
+  }
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const double* __restrict__ x0,
+                 double* __restrict__ x, double* __restrict__ r, double* __restrict__ rt, double* __restrict__ p,
+                 double* __restrict__ v, double* state, double* work, BicgRed R) {
+  double acc[2] = {0.0, 0.0};
+  FPB_SELL_LOOP(n) {
+    const double ax = x0 ? sell_row_dot<B>(A.ptr, A.col, A.val, x0, row) : 0.0;
+    if (row < n) {
+      const double ri = x0 ? __dsub_rn(b[row], ax) : b[row];  // r = b - A x0
+      x[row] = x0 ? x0[row] : 0.0;
+      r[row] = ri;
+      rt[row] = ri;
+      p[row] = 0.0;
+      v[row] = 0.0;
+      if (row >= R.own_lo && row < R.own_hi) {
+        acc[0] += b[row] * b[row];
+        acc[1] += ri * ri;
+      }
+    }
+  }
+  bicg_reduce<2>(acc, BSTEP_INIT, state, work, 0, R);
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_av_sell(int32_t n, SellMat A, const double* __restrict__ ph, const double* __restrict__ rt,
+               double* __restrict__ v, double* state, double* work, BicgRed R) {
+  if (state[B_STATUS] != 0.0) return;
+  double acc[1] = {0.0};
+  FPB_SELL_LOOP(n) {
+    const double vi = sell_row_dot<B>(A.ptr, A.col, A.val, ph, row);
+    if (row < n) {
+      v[row] = vi;
+      if (row >= R.own_lo && row < R.own_hi) acc[0] += rt[row] * vi;
+    }
+  }
+  bicg_reduce<1>(acc, BSTEP_AV, state, work, 1, R);
+}
+
+template <int B>
+__global__ void __launch_bounds__(kDotThreads)
+k_bicg_at_sell(int32_t n, SellMat A, const double* __restrict__ sh, const double* __restrict__ sv,
+               double* __restrict__ t, double* state, double* work, BicgRed R) {
+  if (state[B_STATUS] != 0.0) return;
+  double acc[2] = {0.0, 0.0};
+  FPB_SELL_LOOP(n) {
+    const double ti = sell_row_dot<B>(A.ptr, A.col, A.val, sh, row);
+    if (row < n) {
+      t[row] = ti;
+      if (row >= R.own_lo && row < R.own_hi) {
+        acc[0] += ti * sv[row];
+        acc[1] += ti * ti;
+      }
+    }
+  }
+  bicg_reduce<2>(acc, BSTEP_AT, state, work, 3, R);
+}
+
 inline int lanes_per_row(int32_t n, int64_t nnz) {
   const double mean = n > 0 ? (double)nnz / n : 0.0;
   return mean <= 6.0 ? 4 : (mean <= 20.0 ? 8 : 16);
@@ -727,6 +937,45 @@ int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colin
   if (G == 4) k_spmv_r<4, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
   else if (G == 8) k_spmv_r<8, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
   else k_spmv_r<16, R><<<grid, 256, 0, s>>>(n, rowptr, colind, vals, x, y);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_sell_build(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals, int64_t* sell_ptr,
+                   int32_t* scol, double* sval, int64_t* total_h, void* stream) {
+  FPB_REQUIRE(n >= 0 && rowptr && sell_ptr, "bad SELL arguments");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nsl = ((int64_t)n + 31) / 32;
+  if (!scol && !sval) {  // widths and slice offsets
+    FPB_CUDA(cudaMemsetAsync(sell_ptr, 0, sizeof(int64_t), s));
+    if (nsl > 0) {
+      k_sell_width<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(n, rowptr, sell_ptr + 1);
+      FPB_LAUNCH_CHECK();
+      size_t tmp_bytes = 0;
+      void* tmp = nullptr;
+      cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, sell_ptr + 1, sell_ptr + 1, nsl, s);
+      FPB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+      FPB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, sell_ptr + 1, sell_ptr + 1, nsl, s));
+      FPB_CUDA(cudaFreeAsync(tmp, s));
+    }
+    FPB_CUDA(cudaMemcpyAsync(total_h, sell_ptr + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    FPB_CUDA(cudaStreamSynchronize(s));
+    return FPB_OK;
+  }
+  if (n > 0) {
+    k_sell_fill<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(n, rowptr, colind, vals, sell_ptr, scol, sval);
+    FPB_LAUNCH_CHECK();
+  }
+  return FPB_OK;
+}
+
+int fpb_spmv_sell(int32_t n, const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* x,
+                  double* y, void* stream) {
+  if (n <= 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  const unsigned grid = (unsigned)(((int64_t)n + 255) / 256);
+  if (sell_batch(n) == 16) k_spmv_sell<16><<<grid, 256, 0, s>>>(n, sell_ptr, scol, sval, x, y);
+  else k_spmv_sell<8><<<grid, 256, 0, s>>>(n, sell_ptr, scol, sval, x, y);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -770,11 +1019,16 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
 }
 
 int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                 const double* b, const double* x0, double* x, double* r, double* p, double* z,
+                 const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* p, double* z,
                  const double* d, double* state, double* hist, double tol, double* work,
                  void* stream) {
   cudaStream_t s = as_stream(stream);
-  switch (lanes_per_row(n, nnz)) {
+  const SellMat A{sell_ptr, scol, sval};
+  if (sell_ptr && sell_batch(n) == 16)
+    k_pcg_init_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, state, hist, tol, work);
+  else if (sell_ptr)
+    k_pcg_init_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, state, hist, tol, work);
+  else switch (lanes_per_row(n, nnz)) {
     case 4: k_pcg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
     case 8: k_pcg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
     default: k_pcg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
@@ -786,13 +1040,17 @@ int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* c
 }
 
 int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                    double* x, double* r, double* p, double* q, double* z, const double* d,
+                    const int64_t* sell_ptr, const int32_t* scol, const double* sval, double* x, double* r, double* p, double* q, double* z, const double* d,
                     double* state, double* hist, int64_t hist_cap, int iters, double* work,
                     void* stream) {
   cudaStream_t s = as_stream(stream);
   const int G = lanes_per_row(n, nnz);
+  const SellMat A{sell_ptr, scol, sval};
+  const int SB = sell_ptr ? sell_batch(n) : 0;
   for (int it = 0; it < iters; ++it) {
-    if (G == 4) k_pcg_spmv<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
+    if (SB == 16) k_pcg_spmv_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, p, q, state, work);
+    else if (SB == 8) k_pcg_spmv_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, p, q, state, work);
+    else if (G == 4) k_pcg_spmv<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     else if (G == 8) k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     else k_pcg_spmv<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     k_pcg_update<<<kDotBlocks, kDotThreads, 0, s>>>(n, x, r, p, q, d, z, state, hist, hist_cap, work);
@@ -806,12 +1064,17 @@ int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t
 int fpb_bicgstab_state_size(void) { return B_NSTATE; }
 
 int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                      const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
+                      const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
                       double* state, double* hist, double tol, int64_t own_lo, int64_t own_hi, int defer,
                       double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   const BicgRed R{own_lo, own_hi, defer, hist, 1, tol};
-  switch (lanes_per_row(n, nnz)) {
+  const SellMat A{sell_ptr, scol, sval};
+  if (sell_ptr && sell_batch(n) == 16)
+    k_bicg_init_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, rt, p, v, state, work, R);
+  else if (sell_ptr)
+    k_bicg_init_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, rt, p, v, state, work, R);
+  else switch (lanes_per_row(n, nnz)) {
     case 4: k_bicg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
     case 8: k_bicg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
     default: k_bicg_init<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
@@ -821,13 +1084,14 @@ int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32
 }
 
 int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                         const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                         const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                         const double* d, double* x, double* r, const double* rt, double* p,
                          double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                          int64_t hist_cap, int iters, double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   for (int it = 0; it < iters; ++it)
     for (int step = BSTEP_AV; step <= BSTEP_UPDATE; ++step) {
-      int rc = fpb_bicgstab_step(step, n, nnz, rowptr, colind, vals, d, x, r, rt, p, ph, v, sv, sh, t, state,
+      int rc = fpb_bicgstab_step(step, n, nnz, rowptr, colind, vals, sell_ptr, scol, sval, d, x, r, rt, p, ph, v, sv, sh, t, state,
                                  hist, hist_cap, 0, n, 0, work, stream);
       if (rc) return rc;
     }
@@ -836,16 +1100,21 @@ int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const in
 }
 
 int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                      const double* vals, const double* d, double* x, double* r, const double* rt, double* p,
+                      const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                      const double* d, double* x, double* r, const double* rt, double* p,
                       double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                       int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   const int G = lanes_per_row(n, nnz);
   const BicgRed R{own_lo, own_hi, defer, hist, hist_cap, 0.0};
+  const SellMat A{sell_ptr, scol, sval};
+  const int SB = sell_ptr ? sell_batch(n) : 0;
   switch (step) {
     case BSTEP_AV:  // K1 + K2
       k_bicg_dir<<<grid_for(n, 256, 8), 256, 0, s>>>(n, r, v, d, p, ph, state);
-      if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
+      if (SB == 16) k_bicg_av_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, ph, rt, v, state, work, R);
+      else if (SB == 8) k_bicg_av_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, ph, rt, v, state, work, R);
+      else if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
       else if (G == 8) k_bicg_av<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
       else k_bicg_av<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
       break;
@@ -853,7 +1122,9 @@ int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, c
       k_bicg_s<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, v, d, sv, sh, state, work, R);
       break;
     case BSTEP_AT:
-      if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
+      if (SB == 16) k_bicg_at_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, sh, sv, t, state, work, R);
+      else if (SB == 8) k_bicg_at_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, sh, sv, t, state, work, R);
+      else if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
       else if (G == 8) k_bicg_at<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
       else k_bicg_at<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
       break;

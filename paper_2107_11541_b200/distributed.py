@@ -326,7 +326,7 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
     x0p = x0.data_ptr() if x0 is not None else None
-    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
+    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, None, None, None, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
               rt.data_ptr(), p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol),
               own_lo, own_hi, 1, work.data_ptr(), s)
     if x0 is not None:  # r = b - A x0 is exact on computed rows only
@@ -342,8 +342,8 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
         return x, SolverStats(0, True, history, history[0])
     if st[B_STATUS] in _BICG_BREAKDOWN:
         raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
-    args = (n, nnz, rp, ci, va, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
-            rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
+    args = (n, nnz, rp, ci, va, None, None, None, d.data_ptr() if d is not None else None, x.data_ptr(),
+            r.data_ptr(), rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
             t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap, own_lo, own_hi, 1, work.data_ptr(), s)
     done = 0
     while done < max_iter:

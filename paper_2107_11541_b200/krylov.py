@@ -18,14 +18,24 @@ import torch
 
 from . import _lib
 from .errors import SolverBreakdownError
-from .sparse import CsrMatrix, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
+from .sparse import CsrMatrix, SellCopy, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
 
 S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 
-# Solver workspaces (vectors, device state, history ring, captured CUDA graph
-# of one full batch), keyed by the operator's device arrays and the batch
-# size: repeated solves with the same matrix reuse the buffers, so the
-# batch graph is captured once and replayed by every later solve.
+# Solver workspaces (vectors, device state, history ring, the operator's
+# SELL-32 copy, captured CUDA graph of one full batch), keyed by the
+# operator's device arrays and the batch size: repeated solves with the same
+# matrix reuse the buffers, so the batch graph is captured once and replayed
+# by every later solve.
+#
+# The fused SpMVs run on a SELL-32 copy of the operator (sparse.SellCopy:
+# one thread per row, coalesced loads, the reference's per-row summation
+# order) when rows are short — the assembled FE matrices, ~15 (TET04) to
+# ~27 (HEX08) entries; its values are re-copied at every solve start
+# (inside the solve, ~one SpMV of traffic).  Longer rows (the pressure
+# operator B M^-1 B^T, ~63) keep the lanes-per-row CSR kernels, which
+# already stream them at the HBM rate (profiles/r01o_sell).
+SELL_MAX_MEAN_ROW = 32.0
 _WS: dict = {}
 _WS_MAX = 8
 
@@ -39,11 +49,22 @@ def _workspace(kind: str, A: CsrMatrix, nvec: int, nstate: int, cap: int, jacobi
         ws = {"v": [torch.empty(A.n, dtype=torch.float64, device=dev) for _ in range(nvec)],
               "d": torch.empty(A.n, dtype=torch.float64, device=dev),
               "state": torch.zeros(nstate, dtype=torch.float64, device=dev),
-              "hist": torch.zeros(cap, dtype=torch.float64, device=dev), "graph": None}
+              "hist": torch.zeros(cap, dtype=torch.float64, device=dev), "graph": None,
+              "sell": SellCopy(A) if A.nnz <= SELL_MAX_MEAN_ROW * max(A.n, 1) else None}
         while len(_WS) >= _WS_MAX:
             _WS.pop(next(iter(_WS)))
     _WS[key] = ws  # most recently used last
     return ws
+
+
+def _sell_args(ws: dict, A: CsrMatrix) -> tuple:
+    """(sell_ptr, scol, sval) for the solver kernels, values refreshed from
+    A; (None, None, None) = CSR kernels."""
+    sc = ws["sell"]
+    if sc is None:
+        return None, None, None
+    sc.refresh(A, force=True)
+    return sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr()
 
 
 def _batch(ws: dict, graph: bool, full: bool, launch) -> None:
@@ -96,7 +117,8 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
-    _lib.call("fpb_pcg_init", n, A.nnz, rp, ci, va, bd.data_ptr(), x0d.data_ptr() if x0d is not None else None,
+    sell = _sell_args(ws, A)
+    _lib.call("fpb_pcg_init", n, A.nnz, rp, ci, va, *sell, bd.data_ptr(), x0d.data_ptr() if x0d is not None else None,
               x.data_ptr(), r.data_ptr(), p.data_ptr(), z.data_ptr(), d.data_ptr(), state.data_ptr(),
               hist_d.data_ptr(), float(tol), work.data_ptr(), s)
     st = state.cpu().numpy()
@@ -106,7 +128,7 @@ def pcg_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | None 
     history = [float(hist_d[0].item())]
     if st[S_STATUS] == 1.0:
         return out(x.clone()), SolverStats(0, True, history, history[0])
-    args = (n, A.nnz, rp, ci, va, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
+    args = (n, A.nnz, rp, ci, va, *sell, x.data_ptr(), r.data_ptr(), p.data_ptr(), q.data_ptr(), z.data_ptr(),
             d.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
     done = 0
     while done < max_iter:
@@ -174,7 +196,8 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
     nnz = A.nnz
-    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, bd.data_ptr(),
+    sell = _sell_args(ws, A)
+    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, *sell, bd.data_ptr(),
               x0d.data_ptr() if x0d is not None else None, x.data_ptr(), r.data_ptr(), rt.data_ptr(),
               p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol), 0, n, 0,
               work.data_ptr(), s)
@@ -187,7 +210,7 @@ def bicgstab_solve(A: CsrMatrix, b, x0=None, tol: float = 1e-8, max_iter: int | 
         return out(x.clone()), SolverStats(0, True, history, history[0])
     if st[B_STATUS] in _BICG_BREAKDOWN:
         raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
-    args = (n, nnz, rp, ci, va, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
+    args = (n, nnz, rp, ci, va, *sell, d.data_ptr() if d is not None else None, x.data_ptr(), r.data_ptr(),
             rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
             t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap)
     done = 0

@@ -161,6 +161,51 @@ def dot_work() -> torch.Tensor:
     return w
 
 
+class SellCopy:
+    """SELL-32 copy of a device CsrMatrix for the solver kernels
+    (fpb_sell_build, vector.cu): slices of 32 rows, entries column-major
+    inside a slice, one thread per row, the reference's per-row summation
+    order (sparse.py:80-84) bit for bit.  The slice pattern is shared by
+    every matrix on the same CSR pattern (cached in the pattern's host-side
+    dict); values are refreshed when the matrix's value tensor changes."""
+
+    def __init__(self, A: CsrMatrix):
+        pat = A._host.get("sell_pattern")
+        if pat is None or pat[0] is not A.rowptr_d:
+            n, dev = A.n, A.vals_d.device
+            ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
+            total = ctypes.c_int64(0)
+            _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), None, None, ptr.data_ptr(), None, None,
+                      ctypes.byref(total), _lib.stream())
+            col = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
+            _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(),
+                      col.data_ptr(), None, ctypes.byref(total), _lib.stream())
+            pat = (A.rowptr_d, ptr, col, total.value)
+            A._host["sell_pattern"] = pat
+        self.rowptr_d, self.ptr, self.col, self.total = pat
+        self.n = A.n
+        self.val = torch.empty(max(self.total, 1), dtype=torch.float64, device=A.vals_d.device)
+        self.key = None
+        self.refresh(A)
+
+    def refresh(self, A: CsrMatrix, force: bool = False) -> "SellCopy":
+        """Copy A's values in (skipped when A's value tensor is unchanged
+        as far as torch can tell; force=True after kernel writes)."""
+        key = (A.vals_d.data_ptr(), A.vals_d._version)
+        if force or key != self.key:
+            _lib.call("fpb_sell_build", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
+                      self.ptr.data_ptr(), None, self.val.data_ptr(), ctypes.byref(ctypes.c_int64(0)),
+                      _lib.stream())
+            self.key = key
+        return self
+
+    def spmv_d(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        y = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=x.device)
+        _lib.call("fpb_spmv_sell", self.n, self.ptr.data_ptr(), self.col.data_ptr(), self.val.data_ptr(),
+                  x.data_ptr(), y.data_ptr(), _lib.stream())
+        return y
+
+
 def spmv_d(A: CsrMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     y = out if out is not None else torch.empty(A.n, dtype=torch.float64, device=x.device)
     _lib.call("fpb_spmv", A.n, A.nnz, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(),

@@ -41,7 +41,16 @@ def solver_metrics(ctx, vec_n, reps=20, hbm=6541.1):
     out = {}
     ms = timed(lambda: S.spmv_d(M, x, y), reps, flush)
     by = 12 * nnz + 4 * (n + 1) + 16 * n
-    out["spmv"] = {"n": n, "nnz": nnz, "ms": ms, "GB_s": by / ms / 1e6, "frac_hbm": by / ms / 1e6 / hbm}
+    out["spmv"] = {"n": n, "nnz": nnz, "ms": ms, "GB_s": by / ms / 1e6, "frac_hbm": by / ms / 1e6 / hbm,
+                   "kernel": "CSR, lanes per row (sparse.spmv)"}
+    # the solvers' format: SELL-32 copy (built once per solve from the CSR
+    # values; its build is timed separately), bit-identical to the reference
+    sc = S.SellCopy(M)
+    ms_b = timed(lambda: sc.refresh(M, force=True), reps, flush)
+    ms = timed(lambda: sc.spmv_d(x, y), reps, flush)
+    out["spmv_sell"] = {"n": n, "nnz": nnz, "padded": sc.total, "ms": ms, "GB_s": by / ms / 1e6,
+                        "frac_hbm": by / ms / 1e6 / hbm, "value_copy_ms": ms_b,
+                        "kernel": "SELL-32, thread per row (solver kernels), reference summation order"}
     a = torch.randn(vec_n, dtype=torch.float64, device=dev)
     b = torch.randn(vec_n, dtype=torch.float64, device=dev)
     c = torch.empty_like(a)
