@@ -31,7 +31,7 @@ from .elements import ETYPE_ID, ReferenceElement, reference_element, upload_tabl
 from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
 from .mesh import Mesh, as_device_mesh
 from .packing import KERNEL_LANES, PackConfig, PackSet, pack_lanes
-from .sparse import CsrMatrix, build_node_pattern, to_device, to_host
+from .sparse import CsrMatrix, build_node_pattern, mark_written, to_device, to_host
 
 LAYOUTS = ("scalar", "packed")
 
@@ -399,6 +399,7 @@ class AssemblyContext:
                 _lib.call("fpb_assemble", kind_id, g.etype_id, g.nelem, g.lane_conn32.data_ptr(),
                           coords, vp, pp, float(rho), float(mu), float(kappa),
                           g.pos32.data_ptr() if matrix else None, nnz, out.data_ptr(), _lib.stream())
+        mark_written(out)
         return out
 
     def assemble_matrix_d(self, kind: KernelKind, velocity_d: torch.Tensor | None,
@@ -542,6 +543,8 @@ def assemble_boundary_d(mesh, pattern: CsrMatrix, alpha: float = 0.0, beta: floa
         _lib.call("fpb_robin", fg.nfaces, fg.nnodes, ng, mesh.dim, conn.data_ptr(), mesh.coords_d.data_ptr(),
                   Nd.data_ptr(), dNd.data_ptr(), wd.data_ptr(), pos.data_ptr() if pos is not None else None,
                   float(alpha), float(beta), vals.data_ptr(), rhs.data_ptr(), _lib.stream())
+        mark_written(vals)
+        mark_written(rhs)
     return vals, rhs
 
 

@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .errors import SolverBreakdownError
-from .sparse import CsrMatrix, SellCopy, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
+from .sparse import SELL_MAX_MEAN_ROW, CsrMatrix, SellCopy, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
 
 S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 
@@ -35,7 +35,6 @@ S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 # (inside the solve, ~one SpMV of traffic).  Longer rows (the pressure
 # operator B M^-1 B^T, ~63) keep the lanes-per-row CSR kernels, which
 # already stream them at the HBM rate (profiles/r01o_sell).
-SELL_MAX_MEAN_ROW = 32.0
 _WS: dict = {}
 _WS_MAX = 8
 
@@ -63,7 +62,11 @@ def _sell_args(ws: dict, A: CsrMatrix) -> tuple:
     sc = ws["sell"]
     if sc is None:
         return None, None, None
+    if not sc.same_pattern(A):  # another pattern at recycled addresses
+        sc = ws["sell"] = SellCopy(A)
+        ws["graph"] = None
     sc.refresh(A, force=True)
+    A._sell = sc  # the exit residual's spmv_d reuses this copy
     return sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr()
 
 

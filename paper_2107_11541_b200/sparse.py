@@ -16,6 +16,7 @@ import ctypes
 
 import numpy as np
 import torch
+from torch.autograd.graph import increment_version
 
 from . import _lib
 
@@ -161,17 +162,31 @@ def dot_work() -> torch.Tensor:
     return w
 
 
+# Operators with at most this many entries per row on average (assembled FE
+# matrices: ~15 TET04, ~27 HEX08) get a SELL-32 copy for repeated SpMVs;
+# longer rows (the pressure operator B M^-1 B^T, ~63) stay on the CSR
+# lanes-per-row kernel, which already streams them at the HBM rate.
+SELL_MAX_MEAN_ROW = 32.0
+
+
+def mark_written(t: torch.Tensor) -> None:
+    """Tell torch (and the SELL copies keyed on its version counter) that a
+    kernel wrote `t` in place through its raw pointer."""
+    increment_version(t)
+
+
 class SellCopy:
     """SELL-32 copy of a device CsrMatrix for the solver kernels
     (fpb_sell_build, vector.cu): slices of 32 rows, entries column-major
     inside a slice, one thread per row, the reference's per-row summation
     order (sparse.py:80-84) bit for bit.  The slice pattern is shared by
     every matrix on the same CSR pattern (cached in the pattern's host-side
-    dict); values are refreshed when the matrix's value tensor changes."""
+    dict); values are re-copied when the matrix's value tensor is replaced
+    or written (torch version counter; kernel writes call mark_written)."""
 
     def __init__(self, A: CsrMatrix):
         pat = A._host.get("sell_pattern")
-        if pat is None or pat[0] is not A.rowptr_d:
+        if pat is None or pat[0] is not A.rowptr_d or pat[1] is not A.colind_d:
             n, dev = A.n, A.vals_d.device
             ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
             total = ctypes.c_int64(0)
@@ -180,23 +195,29 @@ class SellCopy:
             col = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
             _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(),
                       col.data_ptr(), None, ctypes.byref(total), _lib.stream())
-            pat = (A.rowptr_d, ptr, col, total.value)
+            pat = (A.rowptr_d, A.colind_d, ptr, col, total.value)
             A._host["sell_pattern"] = pat
-        self.rowptr_d, self.ptr, self.col, self.total = pat
+        # strong references to the CSR pattern: its addresses cannot be
+        # recycled for another pattern while this copy lives
+        self.rowptr_d, self.colind_d, self.ptr, self.col, self.total = pat
         self.n = A.n
         self.val = torch.empty(max(self.total, 1), dtype=torch.float64, device=A.vals_d.device)
-        self.key = None
+        self._src, self._ver = None, -1
         self.refresh(A)
 
+    def same_pattern(self, A: CsrMatrix) -> bool:
+        return self.rowptr_d is A.rowptr_d and self.colind_d is A.colind_d
+
+    def current(self, A: CsrMatrix) -> bool:
+        return self.same_pattern(A) and self._src is A.vals_d and self._ver == A.vals_d._version
+
     def refresh(self, A: CsrMatrix, force: bool = False) -> "SellCopy":
-        """Copy A's values in (skipped when A's value tensor is unchanged
-        as far as torch can tell; force=True after kernel writes)."""
-        key = (A.vals_d.data_ptr(), A.vals_d._version)
-        if force or key != self.key:
+        """Copy A's values in (skipped when they are current, unless force)."""
+        if force or not self.current(A):
             _lib.call("fpb_sell_build", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
                       self.ptr.data_ptr(), None, self.val.data_ptr(), ctypes.byref(ctypes.c_int64(0)),
                       _lib.stream())
-            self.key = key
+            self._src, self._ver = A.vals_d, A.vals_d._version  # strong ref: the address cannot be recycled
         return self
 
     def spmv_d(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -206,7 +227,26 @@ class SellCopy:
         return y
 
 
+def _sell_for_spmv(A: CsrMatrix) -> SellCopy | None:
+    """A's SELL copy for short-row operators (built on first use, values
+    re-copied when they change), None for long rows.  Every SpMV on a
+    short-row operator goes through it, so repeated products are
+    bit-identical to each other and to the reference's row sums."""
+    if A.nnz > SELL_MAX_MEAN_ROW * max(A.n, 1):
+        return None
+    sc = getattr(A, "_sell", None)
+    if sc is None or not sc.same_pattern(A):
+        sc = A._sell = SellCopy(A)
+    return sc.refresh(A)
+
+
 def spmv_d(A: CsrMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """y = A x on the device: through the SELL-32 copy for short rows
+    (bit-identical to the reference's sparse.py:80-84), else the CSR
+    lanes-per-row kernel."""
+    sc = _sell_for_spmv(A)
+    if sc is not None:
+        return sc.spmv_d(x, out)
     y = out if out is not None else torch.empty(A.n, dtype=torch.float64, device=x.device)
     _lib.call("fpb_spmv", A.n, A.nnz, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(),
               A.vals_d.data_ptr(), x.data_ptr(), y.data_ptr(), _lib.stream())

@@ -25,7 +25,7 @@ def test_spmv_axpy_dot(case):
     name, ctx, g = case
     M = ctx.assemble_matrix(P.KernelKind.MASS)
     y = P.spmv(M, g["spmv_x"])
-    assert O.rel_diff(y, g["spmv_y"]) < 1e-12
+    assert O.rel_diff(y, g["spmv_y"]) < 1e-12  # own MASS values: parity 1e-12
     assert P.spmv(M, g["spmv_x"]).tobytes() == y.tobytes()  # deterministic
     out = P.axpy(2.5, g["bench_scalar0"], g["bench_scalar1"])
     assert out.tobytes() == g["axpy_out"].tobytes()  # one rounding per entry, as the reference
@@ -144,3 +144,43 @@ def test_pcg_known_answers(cuda_ok):
     B = rng.standard_normal((30, 30))
     x, st = P.pcg_solve(_csr(B @ B.T + 1e-2 * np.eye(30)), rng.standard_normal(30), tol=1e-14, max_iter=3)
     assert not st.converged and st.iterations == 3 and len(st.residual_history) == 4
+
+
+def test_spmv_sell_cache_follows_writes(cuda_ok):
+    """Public spmv runs on the SELL copy (bit-identical to the reference
+    order); assembling new values into the same buffer (kernel write) and
+    torch in-place edits are seen by the cached copy."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200 import sparse
+    from gpu_cases import CASES
+
+    ctx = P.AssemblyContext.build(CASES["tet_6"](), 8)
+    n = ctx.mesh.nnode
+    vel = torch.as_tensor(np.random.default_rng(3).standard_normal((n, 3)), device="cuda")
+    out = torch.empty(ctx.pattern.nnz, dtype=torch.float64, device="cuda")
+    A = ctx.pattern.with_vals(out)
+    x = torch.as_tensor(np.random.default_rng(4).standard_normal(n), device="cuda")
+
+    def seq(vals):
+        rp, ci, v, xx = A.rowptr, A.colind, vals.cpu().numpy(), x.cpu().numpy()
+        y = np.zeros(n)
+        for i in range(n):
+            acc = 0.0
+            for k in range(rp[i], rp[i + 1]):
+                acc += v[k] * xx[ci[k]]
+            y[i] = acc
+        return y
+
+    ctx.assemble_matrix_d(P.KernelKind.MASS, None, out)
+    y1 = sparse.spmv_d(A, x).cpu().numpy()  # SELL copy built
+    y2 = sparse.spmv_d(A, x).cpu().numpy()  # reused
+    assert getattr(A, "_sell", None) is not None
+    assert y1.tobytes() == y2.tobytes() == seq(out).tobytes()
+    ctx.assemble_matrix_d(P.KernelKind.CONVECTION, vel, out)  # kernel write, same buffer
+    y3 = sparse.spmv_d(A, x).cpu().numpy()
+    assert y3.tobytes() == seq(out).tobytes()
+    out.mul_(2.0)  # torch in-place edit
+    y4 = sparse.spmv_d(A, x).cpu().numpy()
+    assert np.abs(y4 - 2.0 * y3).max() <= 1e-14 * np.abs(y3).max()

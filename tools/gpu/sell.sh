@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -q -x -m gpu -p no:cacheprovider 2>&1 | tail -2
-timeout 600 python tools/solver_bench.py 2>&1 | tail -60
-timeout 600 python tools/c5_solver.py 2>&1 | tail -20
-timeout 900 python tools/spmv_probe.py 2>&1 | tail -3
+timeout 900 python -m pytest tests -q -x -m gpu -p no:cacheprovider 2>&1 | tail -3
+timeout 600 python tools/solver_bench.py 2>&1 | python -c "import json,sys; d=json.load(sys.stdin); print({k: (round(v['ms'],4), round(v.get('frac_hbm', 0),3), v.get('ms_per_iter')) for k,v in d.items()})"
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; python -c "
+import json; d=json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e']['value']); print(json.dumps(d['configs']['flow'])[:700]); print(json.dumps(d['configs']['c5_one_gpu'])[-300:])"

@@ -13,6 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_11541_b200 as P  # noqa: E402
+from paper_2107_11541_b200 import _lib  # noqa: E402
 from paper_2107_11541_b200 import sparse as S  # noqa: E402
 
 
@@ -39,18 +40,19 @@ def solver_metrics(ctx, vec_n, reps=20, hbm=6541.1):
     x = torch.randn(n, dtype=torch.float64, device=dev)
     y = torch.empty_like(x)
     out = {}
-    ms = timed(lambda: S.spmv_d(M, x, y), reps, flush)
+    # public sparse.spmv path: short rows run on the matrix's SELL-32 copy
+    # (built once per matrix; its value copy is timed separately)
     by = 12 * nnz + 4 * (n + 1) + 16 * n
-    out["spmv"] = {"n": n, "nnz": nnz, "ms": ms, "GB_s": by / ms / 1e6, "frac_hbm": by / ms / 1e6 / hbm,
-                   "kernel": "CSR, lanes per row (sparse.spmv)"}
-    # the solvers' format: SELL-32 copy (built once per solve from the CSR
-    # values; its build is timed separately), bit-identical to the reference
-    sc = S.SellCopy(M)
+    ms = timed(lambda: S.spmv_d(M, x, y), reps, flush)
+    sc = M._sell
     ms_b = timed(lambda: sc.refresh(M, force=True), reps, flush)
-    ms = timed(lambda: sc.spmv_d(x, y), reps, flush)
-    out["spmv_sell"] = {"n": n, "nnz": nnz, "padded": sc.total, "ms": ms, "GB_s": by / ms / 1e6,
-                        "frac_hbm": by / ms / 1e6 / hbm, "value_copy_ms": ms_b,
-                        "kernel": "SELL-32, thread per row (solver kernels), reference summation order"}
+    out["spmv"] = {"n": n, "nnz": nnz, "padded": sc.total, "ms": ms, "GB_s": by / ms / 1e6,
+                   "frac_hbm": by / ms / 1e6 / hbm, "value_copy_ms": ms_b,
+                   "kernel": "SELL-32, thread per row, the reference's row-sum order (sparse.spmv)"}
+    ms = timed(lambda: _lib.call("fpb_spmv", n, nnz, M.rowptr_d.data_ptr(), M.colind_d.data_ptr(),
+                                 M.vals_d.data_ptr(), x.data_ptr(), y.data_ptr(), _lib.stream()), reps, flush)
+    out["spmv_csr"] = {"n": n, "nnz": nnz, "ms": ms, "GB_s": by / ms / 1e6, "frac_hbm": by / ms / 1e6 / hbm,
+                       "kernel": "CSR, lanes per row (fpb_spmv; long-row operators)"}
     a = torch.randn(vec_n, dtype=torch.float64, device=dev)
     b = torch.randn(vec_n, dtype=torch.float64, device=dev)
     c = torch.empty_like(a)
