@@ -9,8 +9,12 @@
 
 namespace fpb {
 
+// One resident wave of 512-thread blocks (2 per SM = 1024 threads): the
+// fused SELL solver kernels hold 2 such blocks per SM, so a larger grid runs
+// a second partial wave (profiles/r01o_sell: config-2 PCG 51.7 -> 47.2 us
+// per iteration, BiCGSTAB 118 -> 108 us; 3 per SM is the worst of all)
 #ifndef FPB_DOT_BLOCKS_PER_SM
-#define FPB_DOT_BLOCKS_PER_SM 4
+#define FPB_DOT_BLOCKS_PER_SM 2
 #endif
 #ifndef FPB_DOT_THREADS
 #define FPB_DOT_THREADS 512
@@ -20,6 +24,9 @@ constexpr int kDotThreads = FPB_DOT_THREADS;
 // work layout (doubles): [0, 4*kDotBlocks) partials for up to 4 fused dots,
 // then 4 ticket counters (as unsigned int in the low word).
 constexpr int kWorkDoubles = 4 * kDotBlocks + 8;
+#ifndef FPB_DOT_UNROLL
+#define FPB_DOT_UNROLL 1
+#endif
 
 // alpha*x + y with the reference's two roundings (no DFMA contraction), so
 // axpy is bitwise identical to sparse.py:96-99
@@ -342,8 +349,22 @@ __global__ void __launch_bounds__(kDotThreads) k_dot(int64_t n, const double* __
                                                      double* __restrict__ result, double* work) {
   double v[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    v[0] += __ldcs(x + i) * __ldcs(y + i);
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+#if FPB_DOT_UNROLL > 1
+  // FPB_DOT_UNROLL independent loads per operand in flight per trip
+  constexpr int U = FPB_DOT_UNROLL;
+  for (; i + (U - 1) * stride < n; i += U * stride) {
+    double a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = __ldcs(x + i + u * stride);
+      b[u] = __ldcs(y + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[0] += a[u] * b[u];
+  }
+#endif
+  for (; i < n; i += stride) v[0] += __ldcs(x + i) * __ldcs(y + i);
   block_sum<1>(v);
   double tot[1];
   if (grid_finish<1>(v, work, 0, tot)) *result = tot[0];
