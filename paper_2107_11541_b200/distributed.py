@@ -299,7 +299,7 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     from . import _lib
     from .errors import SolverBreakdownError
     from .krylov import _BICG_BREAKDOWN, B_BNORM, B_IT, B_STATUS, SolverStats
-    from .sparse import axpy_d, dot_d, dot_work, spmv_d
+    from .sparse import SELL_MAX_MEAN_ROW, SellCopy, axpy_d, dot_d, dot_work, spmv_d
 
     n, nnz = A.n, A.nnz
     dev = b.device
@@ -325,8 +325,13 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
+    # the fused SpMVs on the local operator's SELL-32 copy (krylov.py)
+    sell = (None, None, None)
+    if nnz <= SELL_MAX_MEAN_ROW * max(n, 1):
+        sc = A._sell = SellCopy(A)
+        sell = (sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr())
     x0p = x0.data_ptr() if x0 is not None else None
-    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, None, None, None, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
+    _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, *sell, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
               rt.data_ptr(), p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol),
               own_lo, own_hi, 1, work.data_ptr(), s)
     if x0 is not None:  # r = b - A x0 is exact on computed rows only
@@ -342,7 +347,7 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
         return x, SolverStats(0, True, history, history[0])
     if st[B_STATUS] in _BICG_BREAKDOWN:
         raise SolverBreakdownError(f"BiCGSTAB breakdown: {_BICG_BREAKDOWN[st[B_STATUS]]}")
-    args = (n, nnz, rp, ci, va, None, None, None, d.data_ptr() if d is not None else None, x.data_ptr(),
+    args = (n, nnz, rp, ci, va, *sell, d.data_ptr() if d is not None else None, x.data_ptr(),
             r.data_ptr(), rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
             t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap, own_lo, own_hi, 1, work.data_ptr(), s)
     done = 0
