@@ -263,7 +263,7 @@ __global__ void k_pattern_rows(Groups G, int32_t n, const int64_t* ptr, const in
 }
 
 // element->CSR position: binary search of conn[e][j] in row conn[e][i]
-__global__ void k_positions(int64_t nelem, int nn, const int32_t* conn, const int32_t* rowptr,
+__global__ void k_positions(int64_t nelem, int nn, const int32_t* conn, int32_t n, const int32_t* rowptr,
                             const int32_t* colind, int layout, int vs, int32_t* pos, int* missing) {
   int64_t npacks = (nelem + vs - 1) / vs;
   int64_t total = layout == 0 ? nelem * nn * nn : npacks * nn * nn * vs;
@@ -286,6 +286,11 @@ __global__ void k_positions(int64_t nelem, int nn, const int32_t* conn, const in
       if (e >= nelem) e = nelem - 1;
     }
     int row = conn[e * nn + i], col = conn[e * nn + j];
+    if (row < 0 || row >= n || col < 0 || col >= n) {  // node outside the pattern: a missing pair
+      pos[t] = -1;
+      atomicExch(missing, 1);
+      continue;
+    }
     int lo = rowptr[row], hi = rowptr[row + 1];
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
@@ -522,7 +527,7 @@ int fpb_matrix_positions(int64_t nelem, int nn, const int32_t* conn, int32_t n,
   FPB_CUDA(cudaMemsetAsync(missing, 0, sizeof(int), s));
   int64_t npacks = (nelem + vs - 1) / vs;
   int64_t total = layout == 0 ? nelem * nn * nn : npacks * nn * nn * vs;
-  k_positions<<<grid_for(total, 256), 256, 0, s>>>(nelem, nn, conn, rowptr, colind, layout, vs,
+  k_positions<<<grid_for(total, 256), 256, 0, s>>>(nelem, nn, conn, n, rowptr, colind, layout, vs,
                                                    pos, missing);
   FPB_LAUNCH_CHECK();
   int h = 0;

@@ -299,7 +299,7 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     from . import _lib
     from .errors import SolverBreakdownError
     from .krylov import _BICG_BREAKDOWN, B_BNORM, B_IT, B_STATUS, SolverStats
-    from .sparse import SELL_MAX_MEAN_ROW, SellCopy, axpy_d, dot_d, dot_work, spmv_d
+    from .sparse import axpy_d, dot_d, dot_work, sell_copy, spmv_d
 
     n, nnz = A.n, A.nnz
     dev = b.device
@@ -327,8 +327,9 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
     # the fused SpMVs on the local operator's SELL-32 copy (krylov.py)
     sell = (None, None, None)
-    if nnz <= SELL_MAX_MEAN_ROW * max(n, 1):
-        sc = A._sell = SellCopy(A)
+    sc = sell_copy(A)
+    if sc is not None:
+        A._sell = sc
         sell = (sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr())
     x0p = x0.data_ptr() if x0 is not None else None
     _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, *sell, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),

@@ -18,7 +18,7 @@ import torch
 
 from . import _lib
 from .errors import SolverBreakdownError
-from .sparse import SELL_MAX_MEAN_ROW, CsrMatrix, SellCopy, axpy_d, dot_d, dot_work, spmv_d, to_device, to_host
+from .sparse import CsrMatrix, axpy_d, dot_d, dot_work, sell_copy, spmv_d, to_device, to_host
 
 S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 
@@ -30,11 +30,9 @@ S_RZ, S_BNORM, S_TOL, S_STATUS, S_IT, S_RELRES, S_PQ, S_BETA = range(8)
 #
 # The fused SpMVs run on a SELL-32 copy of the operator (sparse.SellCopy:
 # one thread per row, coalesced loads, the reference's per-row summation
-# order) when rows are short — the assembled FE matrices, ~15 (TET04) to
-# ~27 (HEX08) entries; its values are re-copied at every solve start
-# (inside the solve, ~one SpMV of traffic).  Longer rows (the pressure
-# operator B M^-1 B^T, ~63) keep the lanes-per-row CSR kernels, which
-# already stream them at the HBM rate (profiles/r01o_sell).
+# order) unless its slice padding is excessive (sparse.SELL_MAX_PADDING);
+# its values are re-copied at every solve start (inside the solve, ~one
+# SpMV of traffic; profiles/r01o_sell).
 _WS: dict = {}
 _WS_MAX = 8
 
@@ -49,7 +47,7 @@ def _workspace(kind: str, A: CsrMatrix, nvec: int, nstate: int, cap: int, jacobi
               "d": torch.empty(A.n, dtype=torch.float64, device=dev),
               "state": torch.zeros(nstate, dtype=torch.float64, device=dev),
               "hist": torch.zeros(cap, dtype=torch.float64, device=dev), "graph": None,
-              "sell": SellCopy(A) if A.nnz <= SELL_MAX_MEAN_ROW * max(A.n, 1) else None}
+              "sell": sell_copy(A)}
         while len(_WS) >= _WS_MAX:
             _WS.pop(next(iter(_WS)))
     _WS[key] = ws  # most recently used last
@@ -63,8 +61,10 @@ def _sell_args(ws: dict, A: CsrMatrix) -> tuple:
     if sc is None:
         return None, None, None
     if not sc.same_pattern(A):  # another pattern at recycled addresses
-        sc = ws["sell"] = SellCopy(A)
+        sc = ws["sell"] = sell_copy(A)
         ws["graph"] = None
+        if sc is None:
+            return None, None, None
     sc.refresh(A, force=True)
     A._sell = sc  # the exit residual's spmv_d reuses this copy
     return sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr()

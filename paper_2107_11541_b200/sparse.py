@@ -162,17 +162,50 @@ def dot_work() -> torch.Tensor:
     return w
 
 
-# Operators with at most this many entries per row on average (assembled FE
-# matrices: ~15 TET04, ~27 HEX08) get a SELL-32 copy for repeated SpMVs;
-# longer rows (the pressure operator B M^-1 B^T, ~63) stay on the CSR
-# lanes-per-row kernel, which already streams them at the HBM rate.
-SELL_MAX_MEAN_ROW = 32.0
+# Every operator whose SELL-32 padding stays below this factor of its nnz
+# (FE matrices and the pressure operator: < 1.02) gets a SELL-32 copy for
+# its SpMVs; only matrices whose row lengths vary wildly inside 32-row
+# slices stay on the CSR lanes-per-row kernel (profiles/r01o_sell: SELL
+# 71-103 % of HBM vs CSR 34-72 %; pressure operator 88 % vs 49 %).
+SELL_MAX_PADDING = 1.5
 
 
 def mark_written(t: torch.Tensor) -> None:
     """Tell torch (and the SELL copies keyed on its version counter) that a
     kernel wrote `t` in place through its raw pointer."""
     increment_version(t)
+
+
+def sell_pattern(A: CsrMatrix, max_padding: float | None = None):
+    """(rowptr, colind, slice offsets, SELL column array, padded total) of
+    A's pattern, cached in the pattern's host-side dict; None when the
+    padding would exceed max_padding (default SELL_MAX_PADDING) x nnz."""
+    limit = SELL_MAX_PADDING if max_padding is None else max_padding
+    pat = A._host.get("sell_pattern")
+    if pat is not None and pat[0] is A.rowptr_d and pat[1] is A.colind_d:
+        if pat[3] is not None:
+            return pat
+        if pat[4] > limit * A.nnz + 32:
+            return None
+    n, dev = A.n, A.vals_d.device
+    ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
+    total = ctypes.c_int64(0)
+    _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), None, None, ptr.data_ptr(), None, None,
+              ctypes.byref(total), _lib.stream())
+    if total.value > limit * A.nnz + 32:
+        A._host["sell_pattern"] = (A.rowptr_d, A.colind_d, None, None, total.value)
+        return None
+    col = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
+    _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(),
+              col.data_ptr(), None, ctypes.byref(total), _lib.stream())
+    pat = (A.rowptr_d, A.colind_d, ptr, col, total.value)
+    A._host["sell_pattern"] = pat
+    return pat
+
+
+def sell_copy(A: CsrMatrix):
+    """A new SELL copy of A, or None when its padding is too large."""
+    return SellCopy(A) if sell_pattern(A) is not None else None
 
 
 class SellCopy:
@@ -184,19 +217,10 @@ class SellCopy:
     dict); values are re-copied when the matrix's value tensor is replaced
     or written (torch version counter; kernel writes call mark_written)."""
 
-    def __init__(self, A: CsrMatrix):
-        pat = A._host.get("sell_pattern")
-        if pat is None or pat[0] is not A.rowptr_d or pat[1] is not A.colind_d:
-            n, dev = A.n, A.vals_d.device
-            ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
-            total = ctypes.c_int64(0)
-            _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), None, None, ptr.data_ptr(), None, None,
-                      ctypes.byref(total), _lib.stream())
-            col = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
-            _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(),
-                      col.data_ptr(), None, ctypes.byref(total), _lib.stream())
-            pat = (A.rowptr_d, A.colind_d, ptr, col, total.value)
-            A._host["sell_pattern"] = pat
+    def __init__(self, A: CsrMatrix, max_padding: float | None = None):
+        pat = sell_pattern(A, max_padding)
+        if pat is None:
+            raise ValueError("SELL-32 padding too large for this matrix (sparse.sell_pattern)")
         # strong references to the CSR pattern: its addresses cannot be
         # recycled for another pattern while this copy lives
         self.rowptr_d, self.colind_d, self.ptr, self.col, self.total = pat
@@ -228,22 +252,23 @@ class SellCopy:
 
 
 def _sell_for_spmv(A: CsrMatrix) -> SellCopy | None:
-    """A's SELL copy for short-row operators (built on first use, values
-    re-copied when they change), None for long rows.  Every SpMV on a
-    short-row operator goes through it, so repeated products are
-    bit-identical to each other and to the reference's row sums."""
-    if A.nnz > SELL_MAX_MEAN_ROW * max(A.n, 1):
-        return None
+    """A's SELL copy (built on first use, values re-copied when they
+    change), None when the padding is too large.  Every SpMV on an eligible
+    operator goes through it, so repeated products are bit-identical to
+    each other and to the reference's row sums."""
     sc = getattr(A, "_sell", None)
     if sc is None or not sc.same_pattern(A):
-        sc = A._sell = SellCopy(A)
+        sc = sell_copy(A)
+        if sc is None:
+            return None
+        A._sell = sc
     return sc.refresh(A)
 
 
 def spmv_d(A: CsrMatrix, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """y = A x on the device: through the SELL-32 copy for short rows
-    (bit-identical to the reference's sparse.py:80-84), else the CSR
-    lanes-per-row kernel."""
+    """y = A x on the device: through the SELL-32 copy (bit-identical to
+    the reference's sparse.py:80-84), or the CSR lanes-per-row kernel for
+    matrices whose SELL padding would be too large."""
     sc = _sell_for_spmv(A)
     if sc is not None:
         return sc.spmv_d(x, out)
