@@ -242,13 +242,16 @@ int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colin
 /* SELL-32 copy of a CSR matrix for the solver kernels (one thread per row,
  * coalesced loads, the reference's summation order and rounding).  Call 1
  * (scol = sval = NULL): sell_ptr[nslices + 1] slice offsets, *total_h =
- * sell_ptr[nslices] (entries incl. padding).  Call 2: fills scol and / or
- * sval [total] (either may be NULL: pattern and values are separable). */
+ * sell_ptr[nslices] (entries incl. padding) and, if maxoff_h, the largest
+ * |col - row| (needs colind).  Call 2: fills scol and / or sval [total]
+ * (either may be NULL: pattern and values are separable); scol holds int32
+ * columns, or with idx16 int16 offsets col - row (requires maxoff < 32768;
+ * 10 instead of 12 bytes per entry). */
 int fpb_sell_build(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals, int64_t* sell_ptr,
-                   int32_t* scol, double* sval, int64_t* total_h, void* stream);
+                   void* scol, int idx16, double* sval, int64_t* total_h, int32_t* maxoff_h, void* stream);
 /* y = A x on the SELL-32 copy; bit-identical to sparse.py:80-84 */
-int fpb_spmv_sell(int32_t n, const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* x,
-                  double* y, void* stream);
+int fpb_spmv_sell(int32_t n, const int64_t* sell_ptr, const void* scol, int idx16, const double* sval,
+                  const double* x, double* y, void* stream);
 /* out = alpha*x + y (sparse.py:96-99) */
 int fpb_axpy(int64_t n, double alpha, const double* x, const double* y, double* out,
              void* stream);
@@ -274,15 +277,16 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
  * remaining iterations are no-ops, so batches can be launched without a host
  * round trip per iteration.  vectors: x, r, p, q, z and the Jacobi diagonal d
  * (z = r / d, krylov.py:65,84), all of length n; nnz picks the lanes per
- * row of the fused CSR SpMV.  sell_ptr / scol / sval (fpb_sell_build; NULL
- * = CSR): the fused SpMVs run on the SELL-32 copy instead (one thread per
- * row, the reference's per-row summation order). */
+ * row of the fused CSR SpMV.  sell_ptr / scol / sval / sell_idx16
+ * (fpb_sell_build; sell_ptr NULL = CSR): the fused SpMVs run on the SELL-32
+ * copy instead (one thread per row, the reference's per-row summation
+ * order). */
 int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                 const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* p,
+                 const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, const double* b, const double* x0, double* x, double* r, double* p,
                  double* z, const double* d, double* state, double* hist, double tol,
                  double* work, void* stream);
 int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                    const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval, double* x, double* r, double* p, double* q, double* z,
+                    const double* vals, const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, double* x, double* r, double* p, double* q, double* z,
                     const double* d, double* state, double* hist, int64_t hist_cap, int iters,
                     double* work, void* stream);
 
@@ -299,19 +303,20 @@ int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t
  * 2 rho breakdown, 3 (rtilde, v) = 0, 4 omega breakdown), [7] iterations,
  * [8] ||r|| / ||b||.  Five fused kernels per iteration; iterations after
  * status != 0 are no-ops, so batches need no host round trip and replay
- * from a CUDA graph like the PCG's.  sell_ptr / scol / sval as for the PCG. */
+ * from a CUDA graph like the PCG's.  sell_ptr / scol / sval / sell_idx16 as
+ * for the PCG. */
 int fpb_bicgstab_state_size(void);
 /* x = x0 | 0, r = rtilde = b - A x0 | b, p = v = 0; reductions over the
  * owned rows [own_lo, own_hi) (0, n on one GPU).  defer = 0 finishes the
  * scalars on the device; defer = 1 leaves {||b||^2, ||r||^2} (partial, this
  * rank) in state[16..17] for an allreduce followed by fpb_bicgstab_finish(0). */
 int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                      const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
+                      const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
                       double* state, double* hist, double tol, int64_t own_lo, int64_t own_hi, int defer,
                       double* work, void* stream);
 /* `iters` whole iterations on one GPU (all rows owned, scalars on device). */
 int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                         const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                         const double* vals, const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16,
                          const double* d, double* x, double* r, const double* rt, double* p,
                          double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                          int64_t hist_cap, int iters, double* work, void* stream);
@@ -323,7 +328,7 @@ int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const in
  * them (and refreshes ghost entries of v / t after steps 1 / 3) before
  * fpb_bicgstab_finish(step) — finish(2) then finish(3) after step 3. */
 int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                      const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                      const double* vals, const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16,
                       const double* d, double* x, double* r, const double* rt, double* p,
                       double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                       int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream);

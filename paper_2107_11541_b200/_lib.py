@@ -64,19 +64,19 @@ SIGNATURES = {
     "fpb_assemble_blocks": (_int, [_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp,
                                    _vp, _vp, _vp, _int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "fpb_sell_build": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _vp]),
-    "fpb_spmv_sell": (_int, [_i32] + [_vp] * 6),
+    "fpb_sell_build": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _int, _vp, _pi64, _vp, _vp]),
+    "fpb_spmv_sell": (_int, [_i32, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
     "fpb_axpy": (_int, [_i64, _dbl, _vp, _vp, _vp, _vp]),
     "fpb_dot_work_size": (_i64, []),
     "fpb_dot": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "fpb_diagonal": (_int, [_i32, _vp, _vp, _vp, _vp, _vp]),
     "fpb_row_sums": (_int, [_i32, _vp, _vp, _vp, _vp]),
-    "fpb_pcg_init": (_int, [_i32, _i64] + [_vp] * 15 + [_dbl, _vp, _vp]),
-    "fpb_pcg_iterate": (_int, [_i32, _i64] + [_vp] * 14 + [_i64, _int, _vp, _vp]),
+    "fpb_pcg_init": (_int, [_i32, _i64] + [_vp] * 6 + [_int] + [_vp] * 9 + [_dbl, _vp, _vp]),
+    "fpb_pcg_iterate": (_int, [_i32, _i64] + [_vp] * 6 + [_int] + [_vp] * 8 + [_i64, _int, _vp, _vp]),
     "fpb_bicgstab_state_size": (_int, []),
-    "fpb_bicgstab_init": (_int, [_i32, _i64] + [_vp] * 15 + [_dbl, _i64, _i64, _int, _vp, _vp]),
-    "fpb_bicgstab_iterate": (_int, [_i32, _i64] + [_vp] * 18 + [_i64, _int, _vp, _vp]),
-    "fpb_bicgstab_step": (_int, [_int, _i32, _i64] + [_vp] * 18 + [_i64, _i64, _i64, _int, _vp, _vp]),
+    "fpb_bicgstab_init": (_int, [_i32, _i64] + [_vp] * 6 + [_int] + [_vp] * 9 + [_dbl, _i64, _i64, _int, _vp, _vp]),
+    "fpb_bicgstab_iterate": (_int, [_i32, _i64] + [_vp] * 6 + [_int] + [_vp] * 12 + [_i64, _int, _vp, _vp]),
+    "fpb_bicgstab_step": (_int, [_int, _i32, _i64] + [_vp] * 6 + [_int] + [_vp] * 12 + [_i64, _i64, _i64, _int, _vp, _vp]),
     "fpb_bicgstab_finish": (_int, [_int, _vp, _vp, _i64, _dbl, _vp]),
 }
 

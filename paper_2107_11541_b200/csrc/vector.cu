@@ -260,38 +260,69 @@ __global__ void k_sell_width(int32_t n, const int32_t* __restrict__ rowptr, int6
   if ((threadIdx.x & 31) == 0 && (row >> 5) < ((int64_t)n + 31) / 32) width[row >> 5] = 32 * (int64_t)len;
 }
 
+// column storage: int32 columns (padding -1), or int16 offsets col - row
+// (padding -32768) when every |col - row| < 32768 — 2 bytes less per entry
+// of a bandwidth-bound SpMV (10 instead of 12 bytes per entry)
+constexpr int kSellPad16 = -32768;
+
 __global__ void k_sell_fill(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
                             const double* __restrict__ vals, const int64_t* __restrict__ sell_ptr,
-                            int32_t* __restrict__ scol, double* __restrict__ sval) {
+                            void* __restrict__ scol, int idx16, double* __restrict__ sval, int* bad) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // rows past n: padding only
   if (row >= ((int64_t)n + 31) / 32 * 32) return;
   const int64_t base = sell_ptr[row >> 5] + (row & 31);
   const int w = (int)((sell_ptr[(row >> 5) + 1] - sell_ptr[row >> 5]) >> 5);
   const int lo = row < n ? rowptr[row] : 0, len = row < n ? rowptr[row + 1] - lo : 0;
   for (int k = 0; k < w; ++k) {
-    if (scol) scol[base + 32 * (int64_t)k] = k < len ? colind[lo + k] : -1;
-    if (sval) sval[base + 32 * (int64_t)k] = k < len ? vals[lo + k] : 0.0;
+    const int64_t at = base + 32 * (int64_t)k;
+    if (scol && idx16) {
+      int o = kSellPad16;
+      if (k < len) {
+        o = colind[lo + k] - (int)row;
+        if (o <= kSellPad16 || o > 32767) atomicExch(bad, 1);
+      }
+      static_cast<int16_t*>(scol)[at] = (int16_t)o;
+    } else if (scol) {
+      static_cast<int32_t*>(scol)[at] = k < len ? colind[lo + k] : -1;
+    }
+    if (sval) sval[at] = k < len ? vals[lo + k] : 0.0;
   }
 }
 
-// entries per load batch: 16 keeps more bytes in flight on large matrices,
-// 8 more warps resident on small ones (tools/spmv_probe.py: config-2 MASS
-// 71 % vs 61 % of HBM with 8; config-5 / config-4 ~100 % with 16)
-constexpr int kSellSmallRows = 4 << 20;
-inline int sell_batch(int32_t n) { return n >= kSellSmallRows ? 16 : 8; }
-#ifndef FPB_SELL_LDG
-#define FPB_SELL_LDG 0
-#endif
-__device__ __forceinline__ int sell_ld(const int32_t* p) { return FPB_SELL_LDG ? __ldg(p) : __ldcs(p); }
-__device__ __forceinline__ double sell_ld(const double* p) { return FPB_SELL_LDG ? __ldg(p) : __ldcs(p); }
+__global__ void k_max_offset(int32_t n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                             int* out) {
+  int m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) m = max(m, abs(colind[k] - (int)i));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
 
+// entries per load batch (index + value loads of a batch in flight
+// together, then its x gathers): 16 (tools/spmv_probe.py, tools/flow_probe.py:
+// config-2 MASS 75 % of HBM vs 71 % with 8, pressure operator 0.111 vs
+// 0.117 ms; configs 4 / 5 ~100 %)
+#ifndef FPB_SELL_BATCH
+#define FPB_SELL_BATCH 16
+#endif
+constexpr int kSellBatch = FPB_SELL_BATCH;
 // row . x for one SELL row; rows of a warp are one slice (row >> 5
-// uniform).  Padding entries carry column -1 (and value 0), so a row needs
+// uniform).  Padding entries are marked in the column array, so a row needs
 // no length lookup: index and value loads of a batch go out together, then
 // the x gathers of the valid entries.
-template <int B>
+template <typename IDX>
+__device__ __forceinline__ int sell_col(const IDX* scol, int64_t at, int64_t row) {
+  if constexpr (sizeof(IDX) == 2) {
+    const int o = __ldcs(reinterpret_cast<const short*>(scol) + at);
+    return o == kSellPad16 ? -1 : (int)row + o;
+  } else {
+    return __ldcs(scol + at);
+  }
+}
+
+template <int B, typename IDX>
 __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sell_ptr,
-                                               const int32_t* __restrict__ scol,
+                                               const IDX* __restrict__ scol,
                                                const double* __restrict__ sval,
                                                const double* __restrict__ x, int64_t row) {
   const int64_t s0 = __ldg(sell_ptr + (row >> 5));
@@ -304,8 +335,8 @@ __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sell_
 #pragma unroll
     for (int j = 0; j < B; ++j) {
       const bool ok = k0 + j < w;
-      c[j] = ok ? sell_ld(scol + base + 32 * (int64_t)(k0 + j)) : -1;
-      v[j] = ok ? sell_ld(sval + base + 32 * (int64_t)(k0 + j)) : 0.0;
+      c[j] = ok ? sell_col(scol, base + 32 * (int64_t)(k0 + j), row) : -1;
+      v[j] = ok ? __ldcs(sval + base + 32 * (int64_t)(k0 + j)) : 0.0;
     }
     double xv[B];
 #pragma unroll
@@ -317,14 +348,14 @@ __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sell_
   return acc;
 }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(256) k_spmv_sell(int32_t n, const int64_t* __restrict__ sell_ptr,
-                                                   const int32_t* __restrict__ scol,
+                                                   const IDX* __restrict__ scol,
                                                    const double* __restrict__ sval,
                                                    const double* __restrict__ x, double* __restrict__ y) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if ((row & ~31LL) >= n) return;  // whole warps past the end
-  const double a = sell_row_dot<B>(sell_ptr, scol, sval, x, row);
+  const double a = sell_row_dot<B, IDX>(sell_ptr, scol, sval, x, row);
   if (row < n) y[row] = a;
 }
 
@@ -816,18 +847,21 @@ __global__ void k_bicg_finish(int step, double* state, double* hist, int64_t his
 
 struct SellMat {
   const int64_t* ptr;
-  const int32_t* col;
+  const void* col;  // int32 columns or int16 offsets (idx16)
   const double* val;
+  int idx16;
 };
+template <typename IDX>
+__device__ __forceinline__ const IDX* sell_cols(const SellMat& A) { return static_cast<const IDX*>(A.col); }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(kDotThreads)
 k_pcg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const double* __restrict__ x0,
                 double* __restrict__ x, double* __restrict__ r, double* state, double* hist, double tol,
                 double* work) {
   double v[2] = {0.0, 0.0};
   FPB_SELL_LOOP(n) {
-    const double ax = x0 ? sell_row_dot<B>(A.ptr, A.col, A.val, x0, row) : 0.0;
+    const double ax = x0 ? sell_row_dot<B, IDX>(A.ptr, sell_cols<IDX>(A), A.val, x0, row) : 0.0;
     if (row < n) {
       const double ri = x0 ? axpy1(-1.0, ax, b[row]) : b[row];  // krylov.py:59
       x[row] = x0 ? x0[row] : 0.0;
@@ -851,14 +885,14 @@ k_pcg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const double
   }
 }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(kDotThreads)
 k_pcg_spmv_sell(int32_t n, SellMat A, const double* __restrict__ p, double* __restrict__ q, double* state,
                 double* work) {
   if (state[S_STATUS] != 0.0) return;
   double v[1] = {0.0};
   FPB_SELL_LOOP(n) {
-    const double qi = sell_row_dot<B>(A.ptr, A.col, A.val, p, row);
+    const double qi = sell_row_dot<B, IDX>(A.ptr, sell_cols<IDX>(A), A.val, p, row);
     if (row < n) {
       q[row] = qi;
       v[0] += p[row] * qi;
@@ -872,14 +906,14 @@ k_pcg_spmv_sell(int32_t n, SellMat A, const double* __restrict__ p, double* __re
   }
 }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const double* __restrict__ x0,
                  double* __restrict__ x, double* __restrict__ r, double* __restrict__ rt, double* __restrict__ p,
                  double* __restrict__ v, double* state, double* work, BicgRed R) {
   double acc[2] = {0.0, 0.0};
   FPB_SELL_LOOP(n) {
-    const double ax = x0 ? sell_row_dot<B>(A.ptr, A.col, A.val, x0, row) : 0.0;
+    const double ax = x0 ? sell_row_dot<B, IDX>(A.ptr, sell_cols<IDX>(A), A.val, x0, row) : 0.0;
     if (row < n) {
       const double ri = x0 ? __dsub_rn(b[row], ax) : b[row];  // r = b - A x0
       x[row] = x0 ? x0[row] : 0.0;
@@ -896,14 +930,14 @@ k_bicg_init_sell(int32_t n, SellMat A, const double* __restrict__ b, const doubl
   bicg_reduce<2>(acc, BSTEP_INIT, state, work, 0, R);
 }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_av_sell(int32_t n, SellMat A, const double* __restrict__ ph, const double* __restrict__ rt,
                double* __restrict__ v, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[1] = {0.0};
   FPB_SELL_LOOP(n) {
-    const double vi = sell_row_dot<B>(A.ptr, A.col, A.val, ph, row);
+    const double vi = sell_row_dot<B, IDX>(A.ptr, sell_cols<IDX>(A), A.val, ph, row);
     if (row < n) {
       v[row] = vi;
       if (row >= R.own_lo && row < R.own_hi) acc[0] += rt[row] * vi;
@@ -912,14 +946,14 @@ k_bicg_av_sell(int32_t n, SellMat A, const double* __restrict__ ph, const double
   bicg_reduce<1>(acc, BSTEP_AV, state, work, 1, R);
 }
 
-template <int B>
+template <int B, typename IDX>
 __global__ void __launch_bounds__(kDotThreads)
 k_bicg_at_sell(int32_t n, SellMat A, const double* __restrict__ sh, const double* __restrict__ sv,
                double* __restrict__ t, double* state, double* work, BicgRed R) {
   if (state[B_STATUS] != 0.0) return;
   double acc[2] = {0.0, 0.0};
   FPB_SELL_LOOP(n) {
-    const double ti = sell_row_dot<B>(A.ptr, A.col, A.val, sh, row);
+    const double ti = sell_row_dot<B, IDX>(A.ptr, sell_cols<IDX>(A), A.val, sh, row);
     if (row < n) {
       t[row] = ti;
       if (row >= R.own_lo && row < R.own_hi) {
@@ -930,6 +964,13 @@ k_bicg_at_sell(int32_t n, SellMat A, const double* __restrict__ sh, const double
   }
   bicg_reduce<2>(acc, BSTEP_AT, state, work, 3, R);
 }
+
+// launch a SELL kernel for the matrix's column storage
+#define FPB_SELL_LAUNCH(KER, GRID, BLOCK, N, A, ...)                                \
+  do {                                                                              \
+    if ((A).idx16) KER<kSellBatch, int16_t><<<GRID, BLOCK, 0, s>>>(N, A, __VA_ARGS__); \
+    else KER<kSellBatch, int32_t><<<GRID, BLOCK, 0, s>>>(N, A, __VA_ARGS__);           \
+  } while (0)
 
 inline int lanes_per_row(int32_t n, int64_t nnz) {
   const double mean = n > 0 ? (double)nnz / n : 0.0;
@@ -963,12 +1004,19 @@ int fpb_spmv(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colin
 }
 
 int fpb_sell_build(int32_t n, const int32_t* rowptr, const int32_t* colind, const double* vals, int64_t* sell_ptr,
-                   int32_t* scol, double* sval, int64_t* total_h, void* stream) {
+                   void* scol, int idx16, double* sval, int64_t* total_h, int32_t* maxoff_h, void* stream) {
   FPB_REQUIRE(n >= 0 && rowptr && sell_ptr, "bad SELL arguments");
   cudaStream_t s = as_stream(stream);
   const int64_t nsl = ((int64_t)n + 31) / 32;
-  if (!scol && !sval) {  // widths and slice offsets
+  if (!scol && !sval) {  // widths and slice offsets (+ the largest |col - row|)
     FPB_CUDA(cudaMemsetAsync(sell_ptr, 0, sizeof(int64_t), s));
+    int* dmax = nullptr;
+    if (maxoff_h) {
+      FPB_REQUIRE(colind, "the offset range needs colind");
+      FPB_CUDA(cudaMallocAsync(&dmax, sizeof(int), s));
+      FPB_CUDA(cudaMemsetAsync(dmax, 0, sizeof(int), s));
+      if (n > 0) k_max_offset<<<grid_for(n, 256), 256, 0, s>>>(n, rowptr, colind, dmax);
+    }
     if (nsl > 0) {
       k_sell_width<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(n, rowptr, sell_ptr + 1);
       FPB_LAUNCH_CHECK();
@@ -980,23 +1028,42 @@ int fpb_sell_build(int32_t n, const int32_t* rowptr, const int32_t* colind, cons
       FPB_CUDA(cudaFreeAsync(tmp, s));
     }
     FPB_CUDA(cudaMemcpyAsync(total_h, sell_ptr + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (dmax) {
+      FPB_CUDA(cudaMemcpyAsync(maxoff_h, dmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+      FPB_CUDA(cudaFreeAsync(dmax, s));
+    }
     FPB_CUDA(cudaStreamSynchronize(s));
     return FPB_OK;
   }
   if (n > 0) {
-    k_sell_fill<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(n, rowptr, colind, vals, sell_ptr, scol, sval);
+    int* bad = nullptr;
+    if (scol && idx16) {
+      FPB_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+      FPB_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    }
+    k_sell_fill<<<(unsigned)((nsl * 32 + 255) / 256), 256, 0, s>>>(n, rowptr, colind, vals, sell_ptr, scol, idx16,
+                                                                  sval, bad);
     FPB_LAUNCH_CHECK();
+    if (bad) {
+      int h = 0;
+      FPB_CUDA(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      FPB_CUDA(cudaFreeAsync(bad, s));
+      FPB_CUDA(cudaStreamSynchronize(s));
+      FPB_REQUIRE(!h, "column offsets do not fit 16 bits (check maxoff first)");
+    }
   }
   return FPB_OK;
 }
 
-int fpb_spmv_sell(int32_t n, const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* x,
-                  double* y, void* stream) {
+int fpb_spmv_sell(int32_t n, const int64_t* sell_ptr, const void* scol, int idx16, const double* sval,
+                  const double* x, double* y, void* stream) {
   if (n <= 0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   const unsigned grid = (unsigned)(((int64_t)n + 255) / 256);
-  if (sell_batch(n) == 16) k_spmv_sell<16><<<grid, 256, 0, s>>>(n, sell_ptr, scol, sval, x, y);
-  else k_spmv_sell<8><<<grid, 256, 0, s>>>(n, sell_ptr, scol, sval, x, y);
+  if (idx16)
+    k_spmv_sell<kSellBatch, int16_t><<<grid, 256, 0, s>>>(n, sell_ptr, static_cast<const int16_t*>(scol), sval, x, y);
+  else
+    k_spmv_sell<kSellBatch, int32_t><<<grid, 256, 0, s>>>(n, sell_ptr, static_cast<const int32_t*>(scol), sval, x, y);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -1040,15 +1107,13 @@ int fpb_row_sums(int32_t n, const int32_t* rowptr, const double* vals, double* o
 }
 
 int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                 const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* p, double* z,
+                 const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, const double* b, const double* x0, double* x, double* r, double* p, double* z,
                  const double* d, double* state, double* hist, double tol, double* work,
                  void* stream) {
   cudaStream_t s = as_stream(stream);
-  const SellMat A{sell_ptr, scol, sval};
-  if (sell_ptr && sell_batch(n) == 16)
-    k_pcg_init_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, state, hist, tol, work);
-  else if (sell_ptr)
-    k_pcg_init_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, state, hist, tol, work);
+  const SellMat A{sell_ptr, scol, sval, sell_idx16};
+  if (sell_ptr)
+    FPB_SELL_LAUNCH(k_pcg_init_sell, kDotBlocks, kDotThreads, n, A, b, x0, x, r, state, hist, tol, work);
   else switch (lanes_per_row(n, nnz)) {
     case 4: k_pcg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
     case 8: k_pcg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, state, hist, tol, work); break;
@@ -1061,16 +1126,15 @@ int fpb_pcg_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* c
 }
 
 int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                    const int64_t* sell_ptr, const int32_t* scol, const double* sval, double* x, double* r, double* p, double* q, double* z, const double* d,
+                    const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, double* x, double* r, double* p, double* q, double* z, const double* d,
                     double* state, double* hist, int64_t hist_cap, int iters, double* work,
                     void* stream) {
   cudaStream_t s = as_stream(stream);
   const int G = lanes_per_row(n, nnz);
-  const SellMat A{sell_ptr, scol, sval};
-  const int SB = sell_ptr ? sell_batch(n) : 0;
+  const SellMat A{sell_ptr, scol, sval, sell_idx16};
+  const bool SB = sell_ptr != nullptr;
   for (int it = 0; it < iters; ++it) {
-    if (SB == 16) k_pcg_spmv_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, p, q, state, work);
-    else if (SB == 8) k_pcg_spmv_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, p, q, state, work);
+    if (SB) FPB_SELL_LAUNCH(k_pcg_spmv_sell, kDotBlocks, kDotThreads, n, A, p, q, state, work);
     else if (G == 4) k_pcg_spmv<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     else if (G == 8) k_pcg_spmv<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
     else k_pcg_spmv<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, p, q, state, work);
@@ -1085,16 +1149,14 @@ int fpb_pcg_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t
 int fpb_bicgstab_state_size(void) { return B_NSTATE; }
 
 int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind, const double* vals,
-                      const int64_t* sell_ptr, const int32_t* scol, const double* sval, const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
+                      const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16, const double* b, const double* x0, double* x, double* r, double* rt, double* p, double* v,
                       double* state, double* hist, double tol, int64_t own_lo, int64_t own_hi, int defer,
                       double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   const BicgRed R{own_lo, own_hi, defer, hist, 1, tol};
-  const SellMat A{sell_ptr, scol, sval};
-  if (sell_ptr && sell_batch(n) == 16)
-    k_bicg_init_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, rt, p, v, state, work, R);
-  else if (sell_ptr)
-    k_bicg_init_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, b, x0, x, r, rt, p, v, state, work, R);
+  const SellMat A{sell_ptr, scol, sval, sell_idx16};
+  if (sell_ptr)
+    FPB_SELL_LAUNCH(k_bicg_init_sell, kDotBlocks, kDotThreads, n, A, b, x0, x, r, rt, p, v, state, work, R);
   else switch (lanes_per_row(n, nnz)) {
     case 4: k_bicg_init<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
     case 8: k_bicg_init<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, b, x0, x, r, rt, p, v, state, work, R); break;
@@ -1105,14 +1167,14 @@ int fpb_bicgstab_init(int32_t n, int64_t nnz, const int32_t* rowptr, const int32
 }
 
 int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                         const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                         const double* vals, const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16,
                          const double* d, double* x, double* r, const double* rt, double* p,
                          double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                          int64_t hist_cap, int iters, double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   for (int it = 0; it < iters; ++it)
     for (int step = BSTEP_AV; step <= BSTEP_UPDATE; ++step) {
-      int rc = fpb_bicgstab_step(step, n, nnz, rowptr, colind, vals, sell_ptr, scol, sval, d, x, r, rt, p, ph, v, sv, sh, t, state,
+      int rc = fpb_bicgstab_step(step, n, nnz, rowptr, colind, vals, sell_ptr, scol, sval, sell_idx16, d, x, r, rt, p, ph, v, sv, sh, t, state,
                                  hist, hist_cap, 0, n, 0, work, stream);
       if (rc) return rc;
     }
@@ -1121,20 +1183,19 @@ int fpb_bicgstab_iterate(int32_t n, int64_t nnz, const int32_t* rowptr, const in
 }
 
 int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, const int32_t* colind,
-                      const double* vals, const int64_t* sell_ptr, const int32_t* scol, const double* sval,
+                      const double* vals, const int64_t* sell_ptr, const void* scol, const double* sval, int sell_idx16,
                       const double* d, double* x, double* r, const double* rt, double* p,
                       double* ph, double* v, double* sv, double* sh, double* t, double* state, double* hist,
                       int64_t hist_cap, int64_t own_lo, int64_t own_hi, int defer, double* work, void* stream) {
   cudaStream_t s = as_stream(stream);
   const int G = lanes_per_row(n, nnz);
   const BicgRed R{own_lo, own_hi, defer, hist, hist_cap, 0.0};
-  const SellMat A{sell_ptr, scol, sval};
-  const int SB = sell_ptr ? sell_batch(n) : 0;
+  const SellMat A{sell_ptr, scol, sval, sell_idx16};
+  const bool SB = sell_ptr != nullptr;
   switch (step) {
     case BSTEP_AV:  // K1 + K2
       k_bicg_dir<<<grid_for(n, 256, 8), 256, 0, s>>>(n, r, v, d, p, ph, state);
-      if (SB == 16) k_bicg_av_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, ph, rt, v, state, work, R);
-      else if (SB == 8) k_bicg_av_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, ph, rt, v, state, work, R);
+      if (SB) FPB_SELL_LAUNCH(k_bicg_av_sell, kDotBlocks, kDotThreads, n, A, ph, rt, v, state, work, R);
       else if (G == 4) k_bicg_av<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
       else if (G == 8) k_bicg_av<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
       else k_bicg_av<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, ph, rt, v, state, work, R);
@@ -1143,8 +1204,7 @@ int fpb_bicgstab_step(int step, int32_t n, int64_t nnz, const int32_t* rowptr, c
       k_bicg_s<<<kDotBlocks, kDotThreads, 0, s>>>(n, r, v, d, sv, sh, state, work, R);
       break;
     case BSTEP_AT:
-      if (SB == 16) k_bicg_at_sell<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, sh, sv, t, state, work, R);
-      else if (SB == 8) k_bicg_at_sell<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, A, sh, sv, t, state, work, R);
+      if (SB) FPB_SELL_LAUNCH(k_bicg_at_sell, kDotBlocks, kDotThreads, n, A, sh, sv, t, state, work, R);
       else if (G == 4) k_bicg_at<4><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
       else if (G == 8) k_bicg_at<8><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);
       else k_bicg_at<16><<<kDotBlocks, kDotThreads, 0, s>>>(n, rowptr, colind, vals, sh, sv, t, state, work, R);

@@ -326,11 +326,11 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
     # the fused SpMVs on the local operator's SELL-32 copy (krylov.py)
-    sell = (None, None, None)
+    sell = (None, None, None, 0)
     sc = sell_copy(A)
     if sc is not None:
         A._sell = sc
-        sell = (sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr())
+        sell = sc.args()
     x0p = x0.data_ptr() if x0 is not None else None
     _lib.call("fpb_bicgstab_init", n, nnz, rp, ci, va, *sell, b.data_ptr(), x0p, x.data_ptr(), r.data_ptr(),
               rt.data_ptr(), p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol),

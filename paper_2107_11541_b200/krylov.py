@@ -55,19 +55,19 @@ def _workspace(kind: str, A: CsrMatrix, nvec: int, nstate: int, cap: int, jacobi
 
 
 def _sell_args(ws: dict, A: CsrMatrix) -> tuple:
-    """(sell_ptr, scol, sval) for the solver kernels, values refreshed from
-    A; (None, None, None) = CSR kernels."""
+    """(sell_ptr, scol, sval, idx16) for the solver kernels, values
+    refreshed from A; (None, None, None, 0) = CSR kernels."""
     sc = ws["sell"]
     if sc is None:
-        return None, None, None
+        return None, None, None, 0
     if not sc.same_pattern(A):  # another pattern at recycled addresses
         sc = ws["sell"] = sell_copy(A)
         ws["graph"] = None
         if sc is None:
-            return None, None, None
+            return None, None, None, 0
     sc.refresh(A, force=True)
     A._sell = sc  # the exit residual's spmv_d reuses this copy
-    return sc.ptr.data_ptr(), sc.col.data_ptr(), sc.val.data_ptr()
+    return sc.args()
 
 
 def _batch(ws: dict, graph: bool, full: bool, launch) -> None:

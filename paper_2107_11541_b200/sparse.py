@@ -176,29 +176,35 @@ def mark_written(t: torch.Tensor) -> None:
     increment_version(t)
 
 
+# 16-bit column offsets (col - row) when every offset fits: 10 instead of
+# 12 bytes per entry streamed by the SpMV
+SELL_IDX16 = True
+
+
 def sell_pattern(A: CsrMatrix, max_padding: float | None = None):
-    """(rowptr, colind, slice offsets, SELL column array, padded total) of
-    A's pattern, cached in the pattern's host-side dict; None when the
-    padding would exceed max_padding (default SELL_MAX_PADDING) x nnz."""
+    """(rowptr, colind, slice offsets, SELL column array, padded total,
+    idx16) of A's pattern, cached in the pattern's host-side dict; None when
+    the padding would exceed max_padding (default SELL_MAX_PADDING) x nnz."""
     limit = SELL_MAX_PADDING if max_padding is None else max_padding
     pat = A._host.get("sell_pattern")
     if pat is not None and pat[0] is A.rowptr_d and pat[1] is A.colind_d:
-        if pat[3] is not None:
+        if pat[3] is not None and pat[5] == (SELL_IDX16 and pat[6] < 32768):
             return pat
-        if pat[4] > limit * A.nnz + 32:
+        if pat[3] is None and pat[4] > limit * A.nnz + 32:
             return None
     n, dev = A.n, A.vals_d.device
     ptr = torch.empty((n + 31) // 32 + 1, dtype=torch.int64, device=dev)
-    total = ctypes.c_int64(0)
-    _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), None, None, ptr.data_ptr(), None, None,
-              ctypes.byref(total), _lib.stream())
+    total, maxoff = ctypes.c_int64(0), ctypes.c_int32(0)
+    _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(), None, 0,
+              None, ctypes.byref(total), ctypes.byref(maxoff), _lib.stream())
     if total.value > limit * A.nnz + 32:
-        A._host["sell_pattern"] = (A.rowptr_d, A.colind_d, None, None, total.value)
+        A._host["sell_pattern"] = (A.rowptr_d, A.colind_d, None, None, total.value, False, maxoff.value)
         return None
-    col = torch.empty(max(total.value, 1), dtype=torch.int32, device=dev)
+    idx16 = SELL_IDX16 and maxoff.value < 32768
+    col = torch.empty(max(total.value, 1), dtype=torch.int16 if idx16 else torch.int32, device=dev)
     _lib.call("fpb_sell_build", n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), None, ptr.data_ptr(),
-              col.data_ptr(), None, ctypes.byref(total), _lib.stream())
-    pat = (A.rowptr_d, A.colind_d, ptr, col, total.value)
+              col.data_ptr(), int(idx16), None, ctypes.byref(total), None, _lib.stream())
+    pat = (A.rowptr_d, A.colind_d, ptr, col, total.value, idx16, maxoff.value)
     A._host["sell_pattern"] = pat
     return pat
 
@@ -223,7 +229,7 @@ class SellCopy:
             raise ValueError("SELL-32 padding too large for this matrix (sparse.sell_pattern)")
         # strong references to the CSR pattern: its addresses cannot be
         # recycled for another pattern while this copy lives
-        self.rowptr_d, self.colind_d, self.ptr, self.col, self.total = pat
+        self.rowptr_d, self.colind_d, self.ptr, self.col, self.total, self.idx16, _ = pat
         self.n = A.n
         self.val = torch.empty(max(self.total, 1), dtype=torch.float64, device=A.vals_d.device)
         self._src, self._ver = None, -1
@@ -239,15 +245,19 @@ class SellCopy:
         """Copy A's values in (skipped when they are current, unless force)."""
         if force or not self.current(A):
             _lib.call("fpb_sell_build", A.n, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr(),
-                      self.ptr.data_ptr(), None, self.val.data_ptr(), ctypes.byref(ctypes.c_int64(0)),
+                      self.ptr.data_ptr(), None, 0, self.val.data_ptr(), ctypes.byref(ctypes.c_int64(0)), None,
                       _lib.stream())
             self._src, self._ver = A.vals_d, A.vals_d._version  # strong ref: the address cannot be recycled
         return self
 
+    def args(self) -> tuple:
+        """(sell_ptr, scol, sval, idx16) for the fused solver entry points."""
+        return self.ptr.data_ptr(), self.col.data_ptr(), self.val.data_ptr(), int(self.idx16)
+
     def spmv_d(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         y = out if out is not None else torch.empty(self.n, dtype=torch.float64, device=x.device)
-        _lib.call("fpb_spmv_sell", self.n, self.ptr.data_ptr(), self.col.data_ptr(), self.val.data_ptr(),
-                  x.data_ptr(), y.data_ptr(), _lib.stream())
+        _lib.call("fpb_spmv_sell", self.n, self.ptr.data_ptr(), self.col.data_ptr(), int(self.idx16),
+                  self.val.data_ptr(), x.data_ptr(), y.data_ptr(), _lib.stream())
         return y
 
 

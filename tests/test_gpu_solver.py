@@ -51,12 +51,16 @@ def test_sell_spmv_bitwise_reference(case):
     assert y.tobytes() == g["spmv_y"].tobytes()
 
 
-def test_sell_spmv_ragged(cuda_ok):
+@pytest.mark.parametrize("idx16", [True, False])
+def test_sell_spmv_ragged(cuda_ok, monkeypatch, idx16):
     """Empty rows, a partial last slice, rows of 1..70 entries: SELL equals
-    a sequential per-row sum exactly; refresh follows value changes."""
+    a sequential per-row sum exactly (16-bit column offsets and int32
+    columns); refresh follows value changes."""
     import torch
 
     from paper_2107_11541_b200 import sparse
+
+    monkeypatch.setattr(sparse, "SELL_IDX16", idx16)
 
     rng = np.random.default_rng(5)
     n = 1000
@@ -80,6 +84,7 @@ def test_sell_spmv_ragged(cuda_ok):
     assert sparse.sell_copy(A) is None  # ~2x padding: public paths keep CSR
     sc = sparse.SellCopy(A, max_padding=float("inf"))
     assert sc.total % 32 == 0 and sc.total >= rowptr[-1]
+    assert sc.idx16 == idx16 and sc.col.element_size() == (2 if idx16 else 4)
     xd = torch.as_tensor(x, device="cuda")
     assert sc.spmv_d(xd).cpu().numpy().tobytes() == ref(vals).tobytes()
     A.vals_d.mul_(-0.5)  # torch-visible change -> refresh picks it up

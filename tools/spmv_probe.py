@@ -17,7 +17,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_11541_b200 as P  # noqa: E402
-from paper_2107_11541_b200 import sparse  # noqa: E402
+from paper_2107_11541_b200 import _lib, sparse  # noqa: E402
 
 
 def main():
@@ -57,7 +57,8 @@ def main():
         torch.cuda.synchronize()
         sc = sparse.SellCopy(A)
         byt = 12 * nnz + 20 * n
-        t_csr = timeit(lambda: sparse.spmv_d(A, x, y1))
+        t_csr = timeit(lambda: _lib.call("fpb_spmv", n, nnz, A.rowptr_d.data_ptr(), A.colind_d.data_ptr(),
+                                         A.vals_d.data_ptr(), x.data_ptr(), y1.data_ptr(), _lib.stream()))
         t_sell = timeit(lambda: sc.spmv_d(x, y2))
         t_build = timeit(lambda: sparse.SellCopy(A))
         torch.cuda.synchronize()
