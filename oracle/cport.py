@@ -71,4 +71,10 @@ def spmv(rowptr, colind, vals, x, nthreads=1):
 
 
 def max_threads() -> int:
-    return int(lib().orc_max_threads())
+    """Host threads this process may run on (its CPU affinity), not
+    omp_get_max_threads(): torchrun exports OMP_NUM_THREADS=1 to every rank,
+    and the baseline should use every core it is allowed."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or int(lib().orc_max_threads())
