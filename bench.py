@@ -149,20 +149,29 @@ def config3_block(ctx, vel, flush, hbm, reps=10):
     n, ne = ctx.mesh.nnode, ctx.mesh.nelem
     rng = np.random.default_rng(0)
     rng.standard_normal((n, 3))
-    phis = [torch.as_tensor(rng.standard_normal(n), device=vel.device) for _ in range(3)]
-    outs = [torch.empty(n, dtype=torch.float64, device=vel.device) for _ in range(3)]
+    phi3 = torch.as_tensor(np.stack([rng.standard_normal(n) for _ in range(3)]), device=vel.device)
+    out3 = torch.empty((3, n), dtype=torch.float64, device=vel.device)
     kap = (1e-2, 1e-2, 1e-2)  # kappa, D, D (timeloop.py:76-79)
 
-    def three():
-        for phi, o, k in zip(phis, outs, kap):
-            ctx.assemble_rhs_d(P.KernelKind.SCALAR_RHS, vel, phi, 1.0, 0.0, k, o)
+    def fused():  # one element-block pass for the three fields (fpb_assemble_blocks_scalar3)
+        ctx.assemble_scalar_rhs3_d(vel, phi3, kap, out3)
 
-    ms = _time_ms(three, reps, flush)
+    def three():
+        for f in range(3):
+            ctx.assemble_rhs_d(P.KernelKind.SCALAR_RHS, vel, phi3[f], 1.0, 0.0, kap[f], out3[f])
+
+    ms = _time_ms(fused, reps, flush)
+    ms_three = _time_ms(three, reps, flush)
     F, B = WORK_C[("TET04", "scalar_rhs")]
     return {"workload": "config 3: TET04 94x94x95, SCALAR_RHS x3 (heat kappa, 2 species D), velocity + scalars "
-                        "default_rng(0) draws", "elements": ne, "ms_per_step": ms,
+                        "default_rng(0) draws; one fused element-block pass", "elements": ne, "ms_per_step": ms,
+            "ms_three_separate_passes": ms_three,
             "value": 3 * ne / (ms / 1e3) / 1e6, "unit": "Melem/s (element-scalar assemblies)",
-            "roofline": dict(_roof(F, B, ms / 3, ne, hbm), kernel="scalar_rhs", work_per_element={"flops": F, "bytes": B})}
+            "roofline": dict(_roof(F, B, ms / 3, ne, hbm), kernel="scalar_rhs3 (fused)",
+                             work_per_element={"flops": F, "bytes": B},
+                             note="F is the reference's per-element work for ONE scalar (geometry included); "
+                                  "the fused pass shares geometry, velocity moments and node staging across the "
+                                  "three fields, so this reference-flop rate can exceed the FP64 peak")}
 
 
 def config4_block(flush, hbm, n=272, reps=5):
@@ -180,15 +189,16 @@ def config4_block(flush, hbm, n=272, reps=5):
     dev = flush.device
     rng = np.random.default_rng(0)
     vel = torch.as_tensor(rng.standard_normal((nn_, 3)), device=dev)
-    phis = [torch.as_tensor(rng.standard_normal(nn_), device=dev) for _ in range(3)]
+    phi3 = torch.as_tensor(np.stack([rng.standard_normal(nn_) for _ in range(3)]), device=dev)
     rhs = torch.empty((nn_, 3), dtype=torch.float64, device=dev)
-    srhs = torch.empty(nn_, dtype=torch.float64, device=dev)
+    srhs3 = torch.empty((3, nn_), dtype=torch.float64, device=dev)
     mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
     K = P.KernelKind
     parts = {
         "momentum_rhs": lambda: ctx.assemble_rhs_d(K.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs),
         "gradient_xyz": lambda: ctx.assemble_gradients_d(mats),
-        "scalar_rhs": lambda: [ctx.assemble_rhs_d(K.SCALAR_RHS, vel, ph, 1.0, 0.0, 1e-2, srhs) for ph in phis],
+        # the three scalars in one fused element-block pass
+        "scalar_rhs": lambda: ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 1e-2, 1e-2), srhs3),
     }
     ms = {k: _time_ms(f, reps, flush) for k, f in parts.items()}
     roof = {}
@@ -196,6 +206,8 @@ def config4_block(flush, hbm, n=272, reps=5):
         F, B = WORK_C[("HEX08", k)]
         per = t / (3 if k == "scalar_rhs" else 1)
         roof[k] = dict(_roof(F, B, per, ne, hbm), ms=per)
+    roof["scalar_rhs"]["note"] = ("per scalar of the fused three-field pass (shared staging); F is the "
+                                  "reference's one-scalar work")
     total = sum(ms.values())
     del ctx, mats
     torch.cuda.empty_cache()

@@ -234,6 +234,19 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, int64_t blk0, int64_
                         int32_t node0, int32_t node1, const int32_t* node_pptr, const int32_t* node_plist,
                         int accumulate, double* out, void* stream);
 
+/* Three scalar-transport RHS sharing one velocity in one element-block pass
+ * (enthalpy + two species, timeloop.py:76-79, :361-363; BASELINE config 3):
+ * phi3 / out3 are [3][n] (field-major), kappa_f the diffusivity of field f;
+ * each field's RHS equals fpb_assemble_blocks(FPB_SCALAR_RHS, ..., kappa_f)
+ * to rounding.  Staging, geometry and the velocity moments are shared;
+ * partial holds 3 doubles per (block, node). */
+int fpb_assemble_blocks_scalar3(int etype, int64_t nelem, int64_t blk0, int64_t blk1, const double* xyz4,
+                                const double* vel, const double* phi3, double kappa0, double kappa1, double kappa2,
+                                const int32_t* blk_ptr, const int32_t* blk_nodes, const uint16_t* blk_gptr,
+                                const uint16_t* blk_gslot, const uint16_t* blk_lidx, int maxnu, double* partial,
+                                int32_t n, int32_t node0, int32_t node1, const int32_t* node_pptr,
+                                const int32_t* node_plist, int accumulate, double* out3, void* stream);
+
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 
 /* y = A x (sparse.py:78-84).  nnz = rowptr[n] sizes the lanes per row. */

@@ -63,6 +63,8 @@ SIGNATURES = {
     "fpb_blocks_build": (_int, [_int, _i64, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
     "fpb_assemble_blocks": (_int, [_int, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp,
                                    _vp, _vp, _vp, _int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp, _vp]),
+    "fpb_assemble_blocks_scalar3": (_int, [_int, _i64, _i64, _i64, _vp, _vp, _vp, _dbl, _dbl, _dbl] + [_vp] * 5
+                                    + [_int, _vp, _i32, _i32, _i32, _vp, _vp, _int, _vp, _vp]),
     "fpb_spmv": (_int, [_i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fpb_sell_build": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _int, _vp, _pi64, _vp, _vp]),
     "fpb_spmv_sell": (_int, [_i32, _vp, _vp, _int, _vp, _vp, _vp, _vp]),

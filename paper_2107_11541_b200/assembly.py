@@ -420,6 +420,38 @@ class AssemblyContext:
         phi = scalar_d.contiguous() if scalar_d is not None else None
         return self._run(KIND_ID[kind], vel, phi, rho, mu, kappa, out, window)
 
+    def assemble_scalar_rhs3_d(self, velocity_d: torch.Tensor, phi3_d: torch.Tensor, kappas, out3: torch.Tensor,
+                               window: dict | None = None) -> torch.Tensor:
+        """Three SCALAR_RHS sharing one velocity (enthalpy + two species,
+        timeloop.py:76-79, :361-363) in one element-block pass:
+        out3[f] = assemble_rhs(SCALAR_RHS, velocity, phi3[f], kappa=kappas[f])
+        to rounding.  phi3 / out3 are (3, n) CUDA tensors; a mesh that is
+        not a single element-block group falls back to three passes."""
+        self._ensure_checked()
+        vel = velocity_d.contiguous()
+        phi3 = phi3_d.contiguous()
+        k0, k1, k2 = (float(k) for k in kappas)
+        n = self.mesh.nnode
+        if phi3.shape != (3, n) or out3.shape != (3, n) or not out3.is_contiguous():
+            raise ConfigurationError("phi3 and out3 must be (3, nnode); out3 contiguous")
+        g = self.groups[0] if len(self.groups) == 1 else None
+        if g is None or g.blocks is None:
+            if window is not None:
+                raise ConfigurationError("assembly windows need a single owner-writes element group")
+            for f, kap in enumerate((k0, k1, k2)):
+                self._run(KIND_ID[KernelKind.SCALAR_RHS], vel, phi3[f], 1.0, 0.0, kap, out3[f])
+            return out3
+        bp = g.blocks
+        b0, b1 = window.get("blocks", (0, bp.nblocks)) if window else (0, bp.nblocks)
+        n0, n1 = window.get("nodes", (0, n)) if window else (0, n)
+        _lib.call("fpb_assemble_blocks_scalar3", g.etype_id, g.nelem, b0, b1, self.xyz4.data_ptr(), vel.data_ptr(),
+                  phi3.data_ptr(), k0, k1, k2, bp.blk_ptr.data_ptr(), bp.blk_nodes.data_ptr(),
+                  bp.blk_gptr.data_ptr(), bp.blk_gslot.data_ptr(), bp.blk_lidx.data_ptr(), bp.maxnu,
+                  bp.partial(3, out3.device).data_ptr(), n, n0, n1, bp.node_pptr.data_ptr(),
+                  bp.node_plist.data_ptr(), 0, out3.data_ptr(), _lib.stream())
+        mark_written(out3)
+        return out3
+
     def assemble_matrix(self, kind: KernelKind, layout: str = "packed", velocity=None,
                         reuse: bool = False) -> CsrMatrix:
         """Global matrix sharing the context pattern (assembly.py:209-233).

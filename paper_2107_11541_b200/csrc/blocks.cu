@@ -60,6 +60,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef FPB_BLK_MINB_SCALAR
 #define FPB_BLK_MINB_SCALAR 6
 #endif
+#ifndef FPB_BLK_MINB_SCALAR3
+#define FPB_BLK_MINB_SCALAR3 5
+#endif
 #ifndef FPB_BLK_INTERLEAVE
 #define FPB_BLK_INTERLEAVE 1  // the compiler interleaves a thread's two elements (ILP)
 #endif
@@ -189,15 +192,17 @@ __global__ void __launch_bounds__(kBlockThreads,
                                   !Elem<ET>::AFFINE              ? FPB_BLK_MINB_NONAFFINE
                                   : KIND == FPB_MOMENTUM_RHS     ? FPB_BLK_MINB_MOMENTUM
                                   : KIND == FPB_SCALAR_RHS       ? FPB_BLK_MINB_SCALAR
+                                  : KIND == KIND_SCALAR3         ? FPB_BLK_MINB_SCALAR3
                                                                  : FPB_BLK_MINB)
 k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, const double* __restrict__ xyz4,
           const double* __restrict__ uvw4, const double* __restrict__ vel, const double* __restrict__ phi,
-          double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
+          int64_t fstride, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr, const int32_t* __restrict__ blk_nodes,
           const uint16_t* __restrict__ blk_gptr, const uint16_t* __restrict__ blk_gslot, int maxnu,
           double* __restrict__ partial) {
   constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
   constexpr int NV = Out<ET, KIND>::NV;
-  constexpr int NDAT = 2 * DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);  // x, u (, phi)
+  constexpr int NF = KIND == FPB_SCALAR_RHS ? 1 : KIND == KIND_SCALAR3 ? 3 : 0;  // scalar fields
+  constexpr int NDAT = 2 * DIM + NF;  // x, u (, phi...)
   constexpr int TPB = kBlockThreads;
   constexpr int kBlockElems = blk_elems<ET>();
   constexpr int EPT = kBlockElems / TPB;
@@ -258,6 +263,10 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
       snode[u * NDAT + DIM + d] = ru[d];
     }
     if constexpr (KIND == FPB_SCALAR_RHS) snode[u * NDAT + 2 * DIM] = ru[3];
+    if constexpr (KIND == KIND_SCALAR3) {  // fields [3][fstride], read in place
+#pragma unroll
+      for (int f = 0; f < 3; ++f) snode[u * NDAT + 2 * DIM + f] = __ldg(phi + f * fstride + node);
+    }
   }
   __syncthreads();
 #if FPB_BLK_INTERLEAVE
@@ -278,10 +287,25 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
         ue[a][d] = snode[l * NDAT + DIM + d];
       }
       if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = snode[l * NDAT + 2 * DIM];
+      if constexpr (KIND == KIND_SCALAR3) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) fe[f * NN + a] = snode[l * NDAT + 2 * DIM + f];
+      }
     }
     double acc[Out<ET, KIND>::NOUT];
     if constexpr (Elem<ET>::AFFINE) {
       simplex_rhs_all<ET, KIND>(xe, ue, fe, rho, mu, kappa, acc);
+    } else if constexpr (KIND == KIND_SCALAR3) {  // Gauss loop per field (staging shared)
+      const double kap[3] = {rho, mu, kappa};
+#pragma unroll 1
+      for (int f = 0; f < 3; ++f) {
+        double ff[NN], af[NN];
+#pragma unroll
+        for (int a = 0; a < NN; ++a) ff[a] = fe[f * NN + a];
+        element_integrate<ET, FPB_SCALAR_RHS>(xe, ue, ff, 0.0, 0.0, kap[f], 0, af);
+#pragma unroll
+        for (int a = 0; a < NN; ++a) acc[a * 3 + f] = af[a];
+      }
     } else {
       element_integrate<ET, KIND>(xe, ue, fe, rho, mu, kappa, 0, acc);
     }
@@ -322,10 +346,11 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
 }
 
 // ---- phase 2: per-node gather of block partials ---------------------------------
+// out[i][k] (node-major), or out[k][fstride] (field-major) when fstride > 0
 template <int NV>
 __global__ void k_blk_gather(int32_t node0, int32_t node1, const int32_t* __restrict__ ptr,
                              const int32_t* __restrict__ list, const double* __restrict__ partial, int accumulate,
-                             double* __restrict__ out) {
+                             double* __restrict__ out, int64_t fstride = 0) {
   for (int64_t i = node0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < node1;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s[NV];
@@ -338,18 +363,21 @@ __global__ void k_blk_gather(int32_t node0, int32_t node1, const int32_t* __rest
       for (int k = 0; k < NV; ++k) s[k] += __ldg(partial + p * NV + k);
     }
 #pragma unroll
-    for (int k = 0; k < NV; ++k) out[i * NV + k] = accumulate ? out[i * NV + k] + s[k] : s[k];
+    for (int k = 0; k < NV; ++k) {
+      double* o = fstride > 0 ? out + k * fstride + i : out + i * NV + k;
+      *o = accumulate ? *o + s[k] : s[k];
+    }
   }
 }
 
 template <int ET, int KIND>
 static int launch_blk(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t* lidx, const double* xyz4, const double* uvw4,
-                      const double* vel, const double* phi,
+                      const double* vel, const double* phi, int64_t fstride,
                       double rho, double mu, double kappa, const int32_t* blk_ptr,
                       const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot,
                       int maxnu, double* partial, cudaStream_t s) {
   constexpr int NV = Out<ET, KIND>::NV;
-  constexpr int NDAT = 2 * Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : 0);
+  constexpr int NDAT = 2 * Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : KIND == KIND_SCALAR3 ? 3 : 0);
   constexpr int kBlockElems = blk_elems<ET>();
   const int64_t nblocks = (nelem + kBlockElems - 1) / kBlockElems;
   const size_t contrib = (size_t)Elem<ET>::NN * NV * kBlockElems * sizeof(double) +
@@ -361,7 +389,8 @@ static int launch_blk(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t*
   FPB_REQUIRE(blk0 >= 0 && blk0 <= blk1 && blk1 <= nblocks, "block window [%lld, %lld) outside [0, %lld)",
               (long long)blk0, (long long)blk1, (long long)nblocks);
   if (blk1 == blk0) return FPB_OK;
-  k_blk_rhs<ET, KIND><<<(unsigned)(blk1 - blk0), kBlockThreads, smem, s>>>(nelem, blk0, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa,
+  k_blk_rhs<ET, KIND><<<(unsigned)(blk1 - blk0), kBlockThreads, smem, s>>>(nelem, blk0, lidx, xyz4, uvw4, vel, phi, fstride,
+                                                                   rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
                                                                    partial);
   FPB_LAUNCH_CHECK();
@@ -370,15 +399,18 @@ static int launch_blk(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t*
 
 template <int ET>
 static int blk_kind(int kind, int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t* lidx, const double* xyz4, const double* uvw4,
-                    const double* vel, const double* phi,
+                    const double* vel, const double* phi, int64_t fstride,
                     double rho, double mu, double kappa, const int32_t* blk_ptr,
                     const int32_t* blk_nodes, const uint16_t* blk_gptr, const uint16_t* blk_gslot, int maxnu,
                     double* partial, cudaStream_t s) {
   if (kind == FPB_MOMENTUM_RHS)
-    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
-                                            blk_gptr, blk_gslot, maxnu, partial, s);
-  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes,
-                                        blk_gptr, blk_gslot, maxnu, partial, s);
+    return launch_blk<ET, FPB_MOMENTUM_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr,
+                                            blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s);
+  if (kind == KIND_SCALAR3)
+    return launch_blk<ET, KIND_SCALAR3>(nelem, blk0, blk1, lidx, xyz4, nullptr, vel, phi, fstride, rho, mu, kappa,
+                                        blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s);
+  return launch_blk<ET, FPB_SCALAR_RHS>(nelem, blk0, blk1, lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr,
+                                        blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s);
 }
 
 }  // namespace fpb
@@ -484,11 +516,11 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, int64_t blk0, int64_
   if (nelem > 0) {
     int rc = FPB_OK;
     switch (etype) {
-      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
-      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TRI03: rc = blk_kind<FPB_TRI03>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_QUAD04: rc = blk_kind<FPB_QUAD04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_TET04: rc = blk_kind<FPB_TET04>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_PYR05: rc = blk_kind<FPB_PYR05>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
+      case FPB_HEX08: rc = blk_kind<FPB_HEX08>(kind, nelem, blk0, blk1, blk_lidx, xyz4, uvw4, vel, phi, 0, rho, mu, kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s); break;
     }
     if (rc) return rc;
   }
@@ -501,6 +533,40 @@ int fpb_assemble_blocks(int kind, int etype, int64_t nelem, int64_t blk0, int64_
       k_blk_gather<2><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out);
     else
       k_blk_gather<1><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out);
+    FPB_LAUNCH_CHECK();
+  }
+  return FPB_OK;
+}
+
+int fpb_assemble_blocks_scalar3(int etype, int64_t nelem, int64_t blk0, int64_t blk1, const double* xyz4,
+                                const double* vel, const double* phi3, double kappa0, double kappa1, double kappa2,
+                                const int32_t* blk_ptr, const int32_t* blk_nodes, const uint16_t* blk_gptr,
+                                const uint16_t* blk_gslot, const uint16_t* blk_lidx, int maxnu, double* partial,
+                                int32_t n, int32_t node0, int32_t node1, const int32_t* node_pptr,
+                                const int32_t* node_plist, int accumulate, double* out3, void* stream) {
+  FPB_REQUIRE(etype >= 0 && etype < 5 && g_ref_loaded[etype],
+              "reference tables for element type %d not uploaded", etype);
+  FPB_REQUIRE(xyz4 && vel && phi3 && out3, "three-scalar RHS needs node records, velocity, phi[3][n], out[3][n]");
+  cudaStream_t s = as_stream(stream);
+  if (nelem > 0) {
+    int rc = FPB_OK;
+#define FPB_S3(ET_)                                                                                               \
+  rc = blk_kind<ET_>(KIND_SCALAR3, nelem, blk0, blk1, blk_lidx, xyz4, nullptr, vel, phi3, n, kappa0, kappa1, kappa2, \
+                     blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu, partial, s)
+    switch (etype) {
+      case FPB_TRI03: FPB_S3(FPB_TRI03); break;
+      case FPB_QUAD04: FPB_S3(FPB_QUAD04); break;
+      case FPB_TET04: FPB_S3(FPB_TET04); break;
+      case FPB_PYR05: FPB_S3(FPB_PYR05); break;
+      case FPB_HEX08: FPB_S3(FPB_HEX08); break;
+    }
+#undef FPB_S3
+    if (rc) return rc;
+  }
+  FPB_REQUIRE(node0 >= 0 && node0 <= node1 && node1 <= n, "node window [%d, %d) outside [0, %d)", node0, node1, n);
+  if (node1 > node0) {
+    const int64_t w = node1 - node0;
+    k_blk_gather<3><<<grid_for(w, 256), 256, 0, s>>>(node0, node1, node_pptr, node_plist, partial, accumulate, out3, n);
     FPB_LAUNCH_CHECK();
   }
   return FPB_OK;

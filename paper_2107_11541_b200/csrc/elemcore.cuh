@@ -8,6 +8,10 @@
 namespace fpb {
 
 constexpr int KIND_GRADIENT_K = 100;  // CONVECTION with unit e_k, one direction k
+// three SCALAR_RHS sharing one velocity (enthalpy + 2 species, timeloop.py:
+// 76-79, 361-363): fields fe[s * NN + a], diffusivities (rho, mu, kappa)
+// carry kappa_0..2 internally, outputs acc[a * 3 + s]
+constexpr int KIND_SCALAR3 = 101;
 
 template <int ET, int KIND>
 struct Out {
@@ -15,12 +19,14 @@ struct Out {
   static constexpr bool MAT = KIND == FPB_MASS || KIND == FPB_LAPLACIAN || KIND == FPB_CONVECTION ||
                               KIND == KIND_GRADIENT_K;
   static constexpr bool GRADXYZ = KIND == FPB_GRADIENT_XYZ;
-  static constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS;
+  static constexpr bool NEED_VEL = KIND == FPB_CONVECTION || KIND == FPB_MOMENTUM_RHS || KIND == FPB_SCALAR_RHS ||
+                                   KIND == KIND_SCALAR3;
   static constexpr int NU = NEED_VEL ? NN : 1;
-  static constexpr int NF = KIND == FPB_SCALAR_RHS ? NN : 1;
+  static constexpr int NF = KIND == FPB_SCALAR_RHS ? NN : KIND == KIND_SCALAR3 ? 3 * NN : 1;
   // values per node for RHS kinds
-  static constexpr int NV = KIND == FPB_MOMENTUM_RHS ? DIM : 1;
-  static constexpr int NOUT = MAT ? NN * NN : GRADXYZ ? DIM * NN * NN : KIND == FPB_MOMENTUM_RHS ? NN * DIM : NN;
+  static constexpr int NV = KIND == FPB_MOMENTUM_RHS ? DIM : KIND == KIND_SCALAR3 ? 3 : 1;
+  static constexpr int NOUT = MAT ? NN * NN : GRADXYZ ? DIM * NN * NN : KIND == FPB_MOMENTUM_RHS ? NN * DIM
+                              : KIND == KIND_SCALAR3 ? 3 * NN : NN;
 };
 
 // HEX08 momentum / scalar RHS through the Walsh forms (common.cuh): the

@@ -168,6 +168,39 @@ __device__ __forceinline__ void simplex_rhs_all(
         acc[a * DIM + k] = -(drho * conv + dvisc * visc);
       }
     }
+  } else if constexpr (KIND == KIND_SCALAR3) {  // three scalars, one velocity: ubar shared
+    const double kap[3] = {rho, mu, kappa};
+    double gphi[3][DIM];
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NN; ++c) s += fe[f * NN + c] * gN[d][c];
+        gphi[f][d] = s;
+      }
+#pragma unroll
+    for (int a = 0; a < NN; ++a) {
+      double ub[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < NN; ++c) s += refM<ET>(a, c) * ue[c][d];
+        ub[d] = s;
+      }
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        double adv = 0.0, diff = 0.0;
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          adv += ub[d] * gphi[f][d];
+          diff += gphi[f][d] * gN[d][a];
+        }
+        acc[a * 3 + f] = -(det * adv + kap[f] * det * W * diff);
+      }
+    }
   } else {  // SCALAR_RHS
     double gphi[DIM];
 #pragma unroll
