@@ -572,6 +572,18 @@ def main():
                  "algorithmic_bytes": B * nelem,
                  "work_per_element": {"flops": F, "bytes": B, "source": "SURVEY.md 8(d)"}})
 
+    # the whole step against its own roofline: per element, SURVEY 8(d)'s
+    # work of each kernel at the binding one of its two roofs, summed
+    def _kernel_ns(k):
+        Fk, Bk = WORK[k]
+        return max(Fk / (FP64_PEAK_TFLOPS * 1e3), Bk / hbm)  # ns per element
+    bound_ns = sum(_kernel_ns(k) for k in kern)
+    step_roof = {"bound_Gelem_s": 1.0 / bound_ns, "achieved_Gelem_s": nelem / (ms_per_step * 1e6),
+                 "frac": (nelem / (ms_per_step * 1e6)) * bound_ns,
+                 "per_kernel_bound": {k: ("fp64" if WORK[k][0] / (FP64_PEAK_TFLOPS * 1e3) > WORK[k][1] / hbm
+                                          else "hbm") for k in kern},
+                 "note": "time-sum of each kernel's roofline bound (momentum FP64, B_xyz HBM) per element"}
+
     # e2e through the public API with host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -639,6 +651,7 @@ def main():
                        "elements_per_step": total_elems, "l2": "flushed (512 MiB write) between steps", "scatter": args.scatter,
                        "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
             "roofline": roof,
+            "step_roofline": step_roof,
             "kernels_ms": kern,
             # per step: element-block momentum RHS (integrate + partial
             # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
