@@ -181,6 +181,22 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, int32_t row0, int32_t row1
                       const double* uvw4, double rho, double mu, double kappa, const int32_t* rowptr,
                       const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out, void* stream);
 
+/* ---- TET04 continuity matrices by column pairs (pairs.cu) --------------
+ * B_x, B_y, B_z (FPB_GRADIENT_XYZ) with one register sum per CSR column:
+ * every row walks a stream of (q, r) edge-vector slot pairs sorted by
+ * target column (det grad N_j = e_q x e_r for the tets on edge ij) instead
+ * of accumulating each incidence into three columns in shared memory.
+ * fpb_pair_stream_build fills words[4 * ncols * 32] (uint16) from the
+ * incidence slices and slot words (fpb_incidence_slots); it returns
+ * FPB_ECONFIG when a pattern column is touched by no incident element or a
+ * row is too long — callers then use fpb_assemble_rows. */
+int fpb_pair_stream_build(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const int32_t* rowptr,
+                          uint16_t* words, void* stream);
+int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                                const uint16_t* words, const double* xyz4, const int32_t* rowptr,
+                                const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
+                                void* stream);
+
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices
  * (fpb_incidence_build, element ids); fpb_incidence_slots8 fills

@@ -27,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .elements import ETYPE_ID, ReferenceElement, reference_element, upload_tables
+from .elements import ETYPE_ID, ElementType, ReferenceElement, reference_element, upload_tables
 from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
 from .mesh import Mesh, as_device_mesh
 from .packing import KERNEL_LANES, PackConfig, PackSet, pack_lanes
@@ -83,6 +83,11 @@ ROW_OWNED = ("TRI03", "TET04")  # affine simplices: row-owned kernels (rows.cu)
 ROW_OWNED_GAUSS = ("QUAD04", "PYR05", "HEX08")  # Gauss-loop elements: row-owned matrices (rowsq.cu)
 
 
+# TET04 continuity matrices by column pairs (pairs.cu) instead of the
+# incidence-accumulating row kernel; module switch for A/B measurements
+GRADIENT_PAIRS = True
+
+
 class RowPlan:
     """SELL-32 node->element incidence of one affine group, plus (for
     matrices) the row-local column offsets of every incidence (rows.cu)."""
@@ -112,6 +117,19 @@ class RowPlan:
                                                _lib.stream()), "fpb_incidence_nodes")
         self.slots = None
         self.rowcap = 0
+        self.pairs = None  # TET04 continuity pair stream (pairs.cu); False = not eligible
+
+    def ensure_pairs(self, pattern: "CsrMatrix"):
+        """The column-pair stream of the TET04 continuity kernel, built on
+        first use; None when the pattern is not eligible (a column no
+        incident element touches, rows over 128 entries)."""
+        if self.pairs is None:
+            # 4 x 32 words per incidence slot covers both stream layouts (pairs.cu)
+            words = torch.zeros(max(self.ncols, 1) * 4 * 32, dtype=torch.int16, device=self.slice_ptr.device)
+            rc = _lib.load().fpb_pair_stream_build(self.n, self.slice_ptr.data_ptr(), self.slots.data_ptr(),
+                                                   pattern.rowptr_d.data_ptr(), words.data_ptr(), _lib.stream())
+            self.pairs = words if rc == _lib.FPB_OK and self.rowcap <= 129 else False
+        return self.pairs if self.pairs is not False else None
 
     def ensure_slots(self, conn_d: torch.Tensor, pattern: "CsrMatrix") -> None:
         if self.slots is not None:
@@ -384,6 +402,12 @@ class AssemblyContext:
                 _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),
                           r.inc.data_ptr(), g.conn_d.data_ptr(), r.slots.data_ptr(), xyz4, uvw4,
                           self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
+                          0 if single_rows else 1, out.data_ptr(), _lib.stream())
+            elif own and kind_id == GRADIENT_XYZ and GRADIENT_PAIRS and g.etype_id == ETYPE_ID[ElementType.TET04] \
+                    and g.rows.ensure_pairs(self.pattern) is not None:
+                r = g.rows
+                _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.slice_ptr.data_ptr(), r.pairs.data_ptr(),
+                          xyz4, self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
                           0 if single_rows else 1, out.data_ptr(), _lib.stream())
             elif own:
                 r = g.rows

@@ -1,0 +1,293 @@
+// Row-owned continuity matrices B_x, B_y, B_z for TET04 by column pairs
+// (timeloop.py:159-171: CONVECTION with unit e_k; _kernels.py:238-266).
+//
+// For an affine tet rotated so the row node i is local node 0 (even
+// permutation, rows.cu), det grad N_p for the other three nodes is the cross
+// product of the two remaining edge vectors in cyclic order,
+//   det grad N_1 = e_2 x e_3,  det grad N_2 = e_3 x e_1,  det grad N_3 = e_1 x e_2,
+// e_l = x_l - x_0, and B_k[i][j] = mN_0 sum_{tets on edge ij} (det grad N_j)[k].
+// So row i's entry in column j is a sum of edge-vector cross products over
+// the tets containing edge ij, and the diagonal is minus the sum of all of
+// them (sum_p grad N_p = 0).  k_rows_nb accumulates each incidence into its
+// three columns (nine shared-memory read-modify-writes per incidence);
+// here every row walks a precomputed stream of (q, r) slot pairs sorted by
+// target column, keeps the column's sum in registers and writes it once:
+// six staged-coordinate loads per pair, no read-modify-write.
+//
+// Stream: SELL-32 over the incidence slices (rows.cu), three 16-bit words
+// per incidence: q | r << 7 | last << 14 (q, r = off-diagonal slots of the
+// two edge vectors, last = final pair of the current target column; the
+// targets run 0, 1, 2, ... because every off-diagonal column has at least
+// one pair).  Row 32 s + l, entry k at uint32 (2 slice_ptr[s] + k / 2) 32 + l,
+// half k & 1 (two words per load); padding 0 (the pair (0, 0): adds an
+// exact zero, stores nothing).  Rows longer than 128 entries use k_rows_nb.
+//
+// Config 2 (B200): 0.242 ms vs 0.264 ms for k_rows_nb; L1 wavefronts drop
+// from 79 % to ~60 % of peak and the walk becomes latency-bound on the
+// stream loads, hence the 24-word (one third of an interior row) batches.
+#include "elemcore.cuh"
+
+namespace fpb {
+
+constexpr int kPairMaxInc = 64;      // incidences per row the setup sort handles
+#ifndef FPB_PAIR_PACK2
+#define FPB_PAIR_PACK2 1  // two stream words per 32-bit load ([2 m0 + k / 2][lane][2]; 0.242 vs 0.250 ms on config 2)
+#endif
+// padding word = pair (0, 0), not last: e_0 x e_0 = 0 joins no column, so
+// the hot loop needs no end-of-row test
+constexpr uint16_t kPairPad = 0;
+
+__global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
+                              const int32_t* __restrict__ rowptr, uint16_t* __restrict__ words, int* err) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nsl = ((int64_t)n + 31) / 32;
+  if (row >= nsl * 32) return;
+  const int64_t sl = row >> 5;
+  const int lane = (int)(row & 31);
+  const int m0 = slice_ptr[sl], m1 = slice_ptr[sl + 1];
+  uint32_t key[3 * kPairMaxInc];  // target << 16 | r << 8 | q
+  int np = 0;
+  if (row < n) {
+    for (int m = m0; m < m1; ++m) {
+      const uint32_t w = slots[(int64_t)m * 32 + lane];
+      if (w == 0xffffffffu) break;
+      if (m - m0 >= kPairMaxInc) {
+        atomicExch(err, 1);
+        break;
+      }
+      const uint32_t s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff, s3 = (w >> 24) & 0xff;
+      if (s1 > 127 || s2 > 127 || s3 > 127) atomicExch(err, 1);
+      key[np++] = s1 << 16 | s3 << 8 | s2;  // column of node 1: e_2 x e_3
+      key[np++] = s2 << 16 | s1 << 8 | s3;  // node 2: e_3 x e_1
+      key[np++] = s3 << 16 | s2 << 8 | s1;  // node 3: e_1 x e_2
+    }
+  }
+  // stable insertion sort by target column (incidence order within a column)
+  for (int i = 1; i < np; ++i) {
+    const uint32_t k = key[i];
+    int j = i - 1;
+    while (j >= 0 && (key[j] >> 16) > (k >> 16)) {
+      key[j + 1] = key[j];
+      --j;
+    }
+    key[j + 1] = k;
+  }
+  // every off-diagonal column must own at least one pair (the targets are
+  // implicit); a pattern with columns no incident element touches (a
+  // slab's ghost-shaped rows) is not eligible (err 2: use k_rows_nb)
+  if (row < n) {
+    int ntarget = 0;
+    for (int i = 0; i < np; ++i) ntarget += (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16)) ? 1 : 0;
+    const int nlast = np ? (int)(key[np - 1] >> 16) + 1 : 0;
+    if (ntarget != rowptr[row + 1] - rowptr[row] - 1 || nlast != ntarget) atomicMax(err, 2);
+  }
+  const int width = 3 * (m1 - m0);
+  for (int k = 0; k < width; ++k) {
+    uint16_t v = kPairPad;
+    if (k < np) {
+      const bool last = k + 1 == np || (key[k + 1] >> 16) != (key[k] >> 16);
+      v = (uint16_t)((key[k] & 0x7f) | ((key[k] >> 8) & 0x7f) << 7 | (last ? 1u << 14 : 0u));
+    }
+#if FPB_PAIR_PACK2
+    words[(((2LL * m0 + (k >> 1)) * 32 + lane) << 1) | (k & 1)] = v;
+#else
+    words[(3LL * m0 + k) * 32 + lane] = v;
+#endif
+  }
+}
+
+#ifndef FPB_PAIR_W
+#define FPB_PAIR_W 24  // stream words per prefetch batch (one TET04 interior row = 72 pairs)
+#endif
+
+// Shared memory per thread and off-diagonal slot: the relative coordinates
+// e_s (3 doubles, region X) and the finished column sums (3 doubles, region
+// A), each laid out [s][field][thread]; separate restrict-qualified regions
+// let the compiler hoist the next pair's loads above a column store.
+__global__ void __launch_bounds__(32, 1)
+k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const uint16_t* __restrict__ words,
+             const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+             int64_t nnz, int rowcap, int accumulate, double* __restrict__ out) {
+  constexpr int DIM = 3, T = 32;
+  constexpr int SS = DIM * T;  // doubles per slot in each region
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x;
+  const int row = row0 + blockIdx.x * T + tid;
+  const bool live = row < n;
+  const int lane = row & 31;
+  const int m0 = live ? __ldg(slice_ptr + (row >> 5)) : 0;
+  const int m1 = live ? __ldg(slice_ptr + (row >> 5) + 1) : 0;
+  int rlo = 0, rlen = 0;
+  double x0[DIM] = {0.0, 0.0, 0.0};
+  if (live) {
+    rlo = __ldg(rowptr + row);
+    rlen = __ldg(rowptr + row + 1) - rlo;
+    double r4[4];
+    ld256(xyz4 + 4 * (int64_t)row, r4);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x0[d] = r4[d];
+  }
+  const int nslot = rowcap > 1 ? rowcap - 1 : 1;
+  double* __restrict__ X = sm + tid;                    // [s][d][thread]
+  double* __restrict__ A = sm + nslot * SS + tid;       // [s][d][thread]
+
+  // ---- stage the neighbours' edge vectors e_s = x_s - x_0 ----
+  constexpr int kStage = 8;
+  int dslot = rlen - 1;
+  {
+    int s = 0;
+    for (int c0 = 0; c0 < rlen; c0 += kStage) {
+      int col[kStage];
+      double rx[kStage][4];
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) col[j] = c0 + j < rlen ? __ldg(colind + rlo + c0 + j) : -1;
+#pragma unroll
+      for (int j = 0; j < kStage; ++j)
+        if (col[j] >= 0 && col[j] != row) ld256(xyz4 + 4 * (int64_t)col[j], rx[j]);
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) {
+        if (col[j] < 0) continue;
+        if (col[j] == row) {
+          dslot = c0 + j;
+          continue;
+        }
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) X[s * SS + d * T] = rx[j][d] - x0[d];
+        ++s;
+      }
+    }
+  }
+
+  // ---- walk the pair stream: column sums in registers ----
+  const double mN0 = refmN<FPB_TET04>(0);
+  double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
+  int target = 0;
+  const int k1 = 3 * (m1 - m0);
+  constexpr int kW = FPB_PAIR_W;
+  uint16_t wc[kW], wn[kW];
+#if FPB_PAIR_PACK2
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + 2LL * m0 * 32 + lane;
+  auto ld_w = [&](int k, uint16_t (&w)[kW]) {
+#pragma unroll
+    for (int j = 0; j < kW; j += 2) {
+      const uint32_t v = k + j < k1 ? __ldg(wp + (int64_t)((k + j) >> 1) * 32) : 0u;
+      w[j] = (uint16_t)(v & 0xffffu);
+      w[j + 1] = (uint16_t)(v >> 16);
+    }
+  };
+#else
+  const uint16_t* wp = words + 3LL * m0 * 32 + lane;
+  auto ld_w = [&](int k, uint16_t (&w)[kW]) {
+#pragma unroll
+    for (int j = 0; j < kW; ++j) w[j] = k + j < k1 ? __ldg(wp + (int64_t)(k + j) * 32) : kPairPad;
+  };
+#endif
+  ld_w(0, wc);
+  ld_w(kW, wn);
+  for (int k = 0; k < k1; k += kW) {
+#pragma unroll
+    for (int j = 0; j < kW; ++j) {
+      const uint32_t w = wc[j];
+      const int q = w & 0x7f, r = (w >> 7) & 0x7f;
+      double a[DIM], b[DIM];
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        a[d] = X[q * SS + d * T];
+        b[d] = X[r * SS + d * T];
+      }
+      acc[0] += a[1] * b[2] - a[2] * b[1];
+      acc[1] += a[2] * b[0] - a[0] * b[2];
+      acc[2] += a[0] * b[1] - a[1] * b[0];
+      if (w & (1u << 14)) {  // column finished: store once, fold into the diagonal
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          A[target * SS + d * T] = mN0 * acc[d];
+          tot[d] += acc[d];
+          acc[d] = 0.0;
+        }
+        ++target;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kW; ++j) wc[j] = wn[j];
+    ld_w(k + 2 * kW, wn);
+  }
+  double dacc[DIM];
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) dacc[d] = -(mN0 * tot[d]);
+
+  // ---- coalesced write-out through a per-warp linear buffer laid over the
+  // dead coordinate region (as k_rows_nb) ----
+  const int wlane = tid & 31;
+  const int base = __shfl_sync(0xffffffffu, rlo, 0);
+  int wend = live ? rlo + rlen : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
+  const int span = wend - base;  // <= 32 rowcap <= 3 * 32 (rowcap - 1) doubles of region X
+  auto buf = [&](int i) -> double& { return sm[i]; };  // one-warp CTA: region X from offset 0
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    __syncwarp();
+    for (int r = 0; r < rlen; ++r) {
+      const double v = r == dslot ? dacc[k] : A[(r - (r > dslot)) * SS + k * T];
+      buf(rlo - base + r) = v;
+    }
+    __syncwarp();
+    double* o = out + k * nnz + base;
+    for (int q = wlane; q < span; q += 32) {
+      const double v = buf(q);
+      o[q] = accumulate ? o[q] + v : v;
+    }
+  }
+}
+
+}  // namespace fpb
+
+using namespace fpb;
+
+extern "C" {
+
+int fpb_pair_stream_build(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const int32_t* rowptr,
+                          uint16_t* words, void* stream) {
+  FPB_REQUIRE(n >= 0 && slice_ptr && slots && rowptr && words, "bad pair-stream arguments");
+  cudaStream_t s = as_stream(stream);
+  const int64_t nsl = ((int64_t)n + 31) / 32;
+  if (nsl == 0) return FPB_OK;
+  int* err = nullptr;
+  FPB_CUDA(cudaMallocAsync(&err, sizeof(int), s));
+  FPB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
+  k_pair_stream<<<(unsigned)((nsl * 32 + 127) / 128), 128, 0, s>>>(n, slice_ptr, slots, rowptr, words, err);
+  FPB_LAUNCH_CHECK();
+  int h = 0;
+  FPB_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FPB_CUDA(cudaFreeAsync(err, s));
+  FPB_CUDA(cudaStreamSynchronize(s));
+  if (h) {
+    set_error(h == 2 ? "pair stream: a pattern column is touched by no incident element"
+                     : "pair stream: a row has more than %d incidences or 128 entries", kPairMaxInc);
+    return FPB_ECONFIG;
+  }
+  return FPB_OK;
+}
+
+int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                                const uint16_t* words, const double* xyz4, const int32_t* rowptr,
+                                const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
+                                void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(words && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
+              "pair-stream gradient assembly needs the stream, the CSR pattern and rows <= 129 entries");
+  FPB_REQUIRE(row0 >= 0 && row0 % 32 == 0 && row1 <= n && row0 <= row1,
+              "row window [%d, %d) must start on a 32-row slice", row0, row1);
+  if (row1 <= row0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = (size_t)6 * (rowcap - 1) * 32 * sizeof(double);  // regions X and A
+  if (smem > 48 * 1024)
+    FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_rows_pairs<<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(row1, row0, slice_ptr, words, xyz4, rowptr,
+                                                                     colind, nnz, rowcap, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+}  // extern "C"
