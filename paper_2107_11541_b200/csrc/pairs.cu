@@ -30,6 +30,9 @@
 namespace fpb {
 
 constexpr int kPairMaxInc = 64;      // incidences per row the setup sort handles
+#ifndef FPB_PAIR_CHAIN
+#define FPB_PAIR_CHAIN 1  // ring-ordered columns: reuse the previous pair's r as q
+#endif
 #ifndef FPB_PAIR_PACK2
 #define FPB_PAIR_PACK2 1  // two stream words per 32-bit load ([2 m0 + k / 2][lane][2]; 0.242 vs 0.250 ms on config 2)
 #endif
@@ -72,21 +75,55 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
     }
     key[j + 1] = k;
   }
+  // chain each column's pairs around its edge: (q1, q2), (q2, q3), ... —
+  // the tets around edge ij form a ring (open at the boundary), so a pair
+  // whose q is the previous pair's r reuses that node's edge vector from
+  // registers (bit 15); the column's summation order is the ring order
+  for (int c0 = 0; c0 < np;) {
+    int c1 = c0 + 1;
+    while (c1 < np && (key[c1] >> 16) == (key[c0] >> 16)) ++c1;
+    // start at a pair whose q is no other pair's r (open chain), else c0
+    int start = c0;
+    for (int i = c0; i < c1; ++i) {
+      bool has_pred = false;
+      for (int j = c0; j < c1; ++j) has_pred |= j != i && ((key[j] >> 8) & 0xff) == (key[i] & 0xff);
+      if (!has_pred) {
+        start = i;
+        break;
+      }
+    }
+    uint32_t t = key[c0];
+    key[c0] = key[start];
+    key[start] = t;
+    for (int i = c0 + 1; i < c1; ++i) {  // greedy: next pair continues the chain if one does
+      const uint32_t want = (key[i - 1] >> 8) & 0xff;
+      for (int j = i; j < c1; ++j)
+        if ((key[j] & 0xff) == want) {
+          t = key[i];
+          key[i] = key[j];
+          key[j] = t;
+          key[i] |= 1u << 24;  // chained to its predecessor
+          break;
+        }
+    }
+    c0 = c1;
+  }
   // every off-diagonal column must own at least one pair (the targets are
   // implicit); a pattern with columns no incident element touches (a
   // slab's ghost-shaped rows) is not eligible (err 2: use k_rows_nb)
   if (row < n) {
     int ntarget = 0;
-    for (int i = 0; i < np; ++i) ntarget += (i == 0 || (key[i] >> 16) != (key[i - 1] >> 16)) ? 1 : 0;
-    const int nlast = np ? (int)(key[np - 1] >> 16) + 1 : 0;
+    for (int i = 0; i < np; ++i) ntarget += (i == 0 || ((key[i] >> 16) & 0xff) != ((key[i - 1] >> 16) & 0xff)) ? 1 : 0;
+    const int nlast = np ? (int)((key[np - 1] >> 16) & 0xff) + 1 : 0;
     if (ntarget != rowptr[row + 1] - rowptr[row] - 1 || nlast != ntarget) atomicMax(err, 2);
   }
   const int width = 3 * (m1 - m0);
   for (int k = 0; k < width; ++k) {
     uint16_t v = kPairPad;
     if (k < np) {
-      const bool last = k + 1 == np || (key[k + 1] >> 16) != (key[k] >> 16);
-      v = (uint16_t)((key[k] & 0x7f) | ((key[k] >> 8) & 0x7f) << 7 | (last ? 1u << 14 : 0u));
+      const bool last = k + 1 == np || ((key[k + 1] >> 16) & 0xff) != ((key[k] >> 16) & 0xff);
+      v = (uint16_t)((key[k] & 0x7f) | ((key[k] >> 8) & 0x7f) << 7 | (last ? 1u << 14 : 0u) |
+                     (FPB_PAIR_CHAIN && (key[k] >> 24) ? 1u << 15 : 0u));
     }
 #if FPB_PAIR_PACK2
     words[(((2LL * m0 + (k >> 1)) * 32 + lane) << 1) | (k & 1)] = v;
@@ -161,6 +198,7 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   // ---- walk the pair stream: column sums in registers ----
   const double mN0 = refmN<FPB_TET04>(0);
   double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
+  double pb[DIM] = {0.0, 0.0, 0.0};  // edge vector of the previous pair's r
   int target = 0;
   const int k1 = 3 * (m1 - m0);
   constexpr int kW = FPB_PAIR_W;
@@ -190,10 +228,17 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
       const uint32_t w = wc[j];
       const int q = w & 0x7f, r = (w >> 7) & 0x7f;
       double a[DIM], b[DIM];
+      if (FPB_PAIR_CHAIN && (w & (1u << 15))) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) a[d] = pb[d];
+      } else {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) a[d] = X[q * SS + d * T];
+      }
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
-        a[d] = X[q * SS + d * T];
         b[d] = X[r * SS + d * T];
+        pb[d] = b[d];
       }
       acc[0] += a[1] * b[2] - a[2] * b[1];
       acc[1] += a[2] * b[0] - a[0] * b[2];
