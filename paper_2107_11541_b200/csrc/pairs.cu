@@ -168,34 +168,8 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   double* __restrict__ X = sm + tid;                    // [s][d][thread]
   double* __restrict__ A = sm + nslot * SS + tid;       // [s][d][thread]
 
-  // ---- stage the neighbours' edge vectors e_s = x_s - x_0 ----
-  constexpr int kStage = 8;
-  int dslot = rlen - 1;
-  {
-    int s = 0;
-    for (int c0 = 0; c0 < rlen; c0 += kStage) {
-      int col[kStage];
-      double rx[kStage][4];
-#pragma unroll
-      for (int j = 0; j < kStage; ++j) col[j] = c0 + j < rlen ? __ldg(colind + rlo + c0 + j) : -1;
-#pragma unroll
-      for (int j = 0; j < kStage; ++j)
-        if (col[j] >= 0 && col[j] != row) ld256(xyz4 + 4 * (int64_t)col[j], rx[j]);
-#pragma unroll
-      for (int j = 0; j < kStage; ++j) {
-        if (col[j] < 0) continue;
-        if (col[j] == row) {
-          dslot = c0 + j;
-          continue;
-        }
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) X[s * SS + d * T] = rx[j][d] - x0[d];
-        ++s;
-      }
-    }
-  }
-
-  // ---- walk the pair stream: column sums in registers ----
+  // ---- pair stream: the first two batches are requested before staging so
+  // their latency hides behind it ----
   const double mN0 = refmN<FPB_TET04>(0);
   double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
   double pb[DIM] = {0.0, 0.0, 0.0};  // edge vector of the previous pair's r
@@ -222,6 +196,37 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
 #endif
   ld_w(0, wc);
   ld_w(kW, wn);
+  // ---- stage the neighbours' edge vectors e_s = x_s - x_0 ----
+#ifndef FPB_PAIR_STAGE
+#define FPB_PAIR_STAGE 8
+#endif
+  constexpr int kStage = FPB_PAIR_STAGE;  // neighbour records in flight per staging batch
+  int dslot = rlen - 1;
+  {
+    int s = 0;
+    for (int c0 = 0; c0 < rlen; c0 += kStage) {
+      int col[kStage];
+      double rx[kStage][4];
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) col[j] = c0 + j < rlen ? __ldg(colind + rlo + c0 + j) : -1;
+#pragma unroll
+      for (int j = 0; j < kStage; ++j)
+        if (col[j] >= 0 && col[j] != row) ld256(xyz4 + 4 * (int64_t)col[j], rx[j]);
+#pragma unroll
+      for (int j = 0; j < kStage; ++j) {
+        if (col[j] < 0) continue;
+        if (col[j] == row) {
+          dslot = c0 + j;
+          continue;
+        }
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) X[s * SS + d * T] = rx[j][d] - x0[d];
+        ++s;
+      }
+    }
+  }
+
+  // ---- walk the pair stream: column sums in registers ----
   for (int k = 0; k < k1; k += kW) {
 #pragma unroll
     for (int j = 0; j < kW; ++j) {
