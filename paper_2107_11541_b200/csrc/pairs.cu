@@ -137,10 +137,10 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
 #define FPB_PAIR_W 24  // stream words per prefetch batch (one TET04 interior row = 72 pairs)
 #endif
 
-// Shared memory per thread and off-diagonal slot: the relative coordinates
-// e_s (3 doubles, region X) and the finished column sums (3 doubles, region
-// A), each laid out [s][field][thread]; separate restrict-qualified regions
-// let the compiler hoist the next pair's loads above a column store.
+// Shared memory: the relative coordinates e_s of every thread's
+// off-diagonal slots ([s][field][thread], region X) and the warp's three
+// output row blocks (linear, one per matrix), where each finished column is
+// stored once at its CSR position.
 __global__ void __launch_bounds__(32, 1)
 k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const uint16_t* __restrict__ words,
              const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
@@ -166,13 +166,17 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   }
   const int nslot = rowcap > 1 ? rowcap - 1 : 1;
   double* __restrict__ X = sm + tid;                    // [s][d][thread]
-  double* __restrict__ A = sm + nslot * SS + tid;       // [s][d][thread]
+  // the warp's output rows, one linear buffer per matrix: entry (row, c) at
+  // rlo - base + c, so finished columns land where the coalesced write-out
+  // reads them (no intermediate copy)
+  double* __restrict__ Bo = sm + nslot * SS;          // [3][32 rowcap]
+  const int bstride = 32 * rowcap;
+  const int base = __shfl_sync(0xffffffffu, rlo, 0);
 
   // ---- pair stream: the first two batches are requested before staging so
   // their latency hides behind it ----
   const double mN0 = refmN<FPB_TET04>(0);
   double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
-  double pb[DIM] = {0.0, 0.0, 0.0};  // edge vector of the previous pair's r
   int target = 0;
   const int k1 = 3 * (m1 - m0);
   constexpr int kW = FPB_PAIR_W;
@@ -227,35 +231,49 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   }
 
   // ---- walk the pair stream: column sums in registers ----
+  // software-pipelined: the edge vectors of pair j + 1 are requested before
+  // pair j's column test, so the shared-memory latency overlaps the FP64
+  // work and the (rare) column store
+  double a[DIM], b[DIM];
+  auto fetch = [&](uint32_t w, const double (&pbv)[DIM], double (&na)[DIM], double (&nb)[DIM]) {
+    const int q = w & 0x7f, r = (w >> 7) & 0x7f;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) nb[d] = X[r * SS + d * T];
+    if (FPB_PAIR_CHAIN && (w & (1u << 15))) {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) na[d] = pbv[d];
+    } else {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) na[d] = X[q * SS + d * T];
+    }
+  };
+  {
+    const double z[DIM] = {0.0, 0.0, 0.0};
+    fetch(wc[0], z, a, b);
+  }
   for (int k = 0; k < k1; k += kW) {
 #pragma unroll
     for (int j = 0; j < kW; ++j) {
       const uint32_t w = wc[j];
-      const int q = w & 0x7f, r = (w >> 7) & 0x7f;
-      double a[DIM], b[DIM];
-      if (FPB_PAIR_CHAIN && (w & (1u << 15))) {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) a[d] = pb[d];
-      } else {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) a[d] = X[q * SS + d * T];
-      }
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        b[d] = X[r * SS + d * T];
-        pb[d] = b[d];
-      }
+      const uint32_t wnext = j + 1 < kW ? wc[j + 1] : wn[0];
+      double na[DIM], nb[DIM];
+      fetch(wnext, b, na, nb);
       acc[0] += a[1] * b[2] - a[2] * b[1];
       acc[1] += a[2] * b[0] - a[0] * b[2];
       acc[2] += a[0] * b[1] - a[1] * b[0];
       if (w & (1u << 14)) {  // column finished: store once, fold into the diagonal
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          A[target * SS + d * T] = mN0 * acc[d];
+          Bo[d * bstride + rlo - base + target + (target >= dslot)] = mN0 * acc[d];
           tot[d] += acc[d];
           acc[d] = 0.0;
         }
         ++target;
+      }
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        a[d] = na[d];
+        b[d] = nb[d];
       }
     }
 #pragma unroll
@@ -266,26 +284,22 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
 #pragma unroll
   for (int d = 0; d < DIM; ++d) dacc[d] = -(mN0 * tot[d]);
 
-  // ---- coalesced write-out through a per-warp linear buffer laid over the
-  // dead coordinate region (as k_rows_nb) ----
+  // ---- coalesced write-out of the warp's rows (diagonal added now) ----
   const int wlane = tid & 31;
-  const int base = __shfl_sync(0xffffffffu, rlo, 0);
   int wend = live ? rlo + rlen : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wend = max(wend, __shfl_xor_sync(0xffffffffu, wend, o));
-  const int span = wend - base;  // <= 32 rowcap <= 3 * 32 (rowcap - 1) doubles of region X
-  auto buf = [&](int i) -> double& { return sm[i]; };  // one-warp CTA: region X from offset 0
+  const int span = wend - base;  // <= 32 rowcap
+  if (live) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) Bo[k * bstride + rlo - base + dslot] = dacc[k];
+  }
+  __syncwarp();
 #pragma unroll
   for (int k = 0; k < DIM; ++k) {
-    __syncwarp();
-    for (int r = 0; r < rlen; ++r) {
-      const double v = r == dslot ? dacc[k] : A[(r - (r > dslot)) * SS + k * T];
-      buf(rlo - base + r) = v;
-    }
-    __syncwarp();
     double* o = out + k * nnz + base;
     for (int q = wlane; q < span; q += 32) {
-      const double v = buf(q);
+      const double v = Bo[k * bstride + q];
       o[q] = accumulate ? o[q] + v : v;
     }
   }
@@ -331,7 +345,8 @@ int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int
               "row window [%d, %d) must start on a 32-row slice", row0, row1);
   if (row1 <= row0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
-  const size_t smem = (size_t)6 * (rowcap - 1) * 32 * sizeof(double);  // regions X and A
+  // edge vectors [rowcap - 1][3][32] + output rows [3][32 rowcap]
+  const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_rows_pairs<<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(row1, row0, slice_ptr, words, xyz4, rowptr,
