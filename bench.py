@@ -562,15 +562,22 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": bytes_rate, "peak": hbm, "unit": "GB/s",
                 "frac": bytes_rate / hbm, "peak_source": hbm_src}
-    traffic = None
+    traffic, ncu = None, None
     try:  # measured DRAM bytes per launch of this kernel (ncu --set full, profiles/traffic.json)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh)[dom]["bytes"]
+            entry = json.load(fh)[dom]
+        traffic, ncu = entry["bytes"], entry.get("ncu")
     except Exception:
         traffic = None
     roof.update({"kernel": dom, "traffic": traffic, "traffic_unit": "bytes per launch",
                  "algorithmic_bytes": B * nelem,
                  "work_per_element": {"flops": F, "bytes": B, "source": "SURVEY.md 8(d)"}})
+    if ncu:
+        roof["ncu"] = ncu  # pipe / L1 utilisation of the same kernel (profiles/traffic.json source)
+    if roof["bound"] == "fp64":
+        roof["note"] = ("achieved = SURVEY 8(d)'s reference-algorithm flops per element / kernel time; the "
+                        "closed-form kernel executes fewer FP64 operations than that count, so the algorithmic "
+                        "rate can exceed the FP64 peak — the executed FP64 pipe utilisation is roofline.ncu")
 
     # the whole step against its own roofline: per element, SURVEY 8(d)'s
     # work of each kernel at the binding one of its two roofs, summed
