@@ -22,9 +22,12 @@
 // half k & 1 (two words per load); padding 0 (the pair (0, 0): adds an
 // exact zero, stores nothing).  Rows longer than 128 entries use k_rows_nb.
 //
-// Config 2 (B200): 0.242 ms vs 0.264 ms for k_rows_nb; L1 wavefronts drop
-// from 79 % to ~60 % of peak and the walk becomes latency-bound on the
-// stream loads, hence the 24-word (one third of an interior row) batches.
+// Column pairs are ordered around the edge's tet ring, so consecutive
+// pairs share an edge vector (bit 15: reuse the previous r as q); the next
+// pair's vectors are fetched before the current column test; finished
+// columns go straight into the warp's linear output rows.  Config 2
+// (B200): 0.196 ms vs 0.264 ms for k_rows_nb (profiles/r01v_pairs ..
+// r01y_step); 24-word batches = one third of an interior row's 72 pairs.
 #include "elemcore.cuh"
 
 namespace fpb {
