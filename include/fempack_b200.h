@@ -186,13 +186,14 @@ int fpb_assemble_rows(int kind, int etype, int32_t n, int32_t row0, int32_t row1
  * every row walks a stream of (q, r) edge-vector slot pairs sorted by
  * target column (det grad N_j = e_q x e_r for the tets on edge ij) instead
  * of accumulating each incidence into three columns in shared memory.
- * fpb_pair_stream_build fills words[4 * ncols * 32] (uint16) from the
- * incidence slices and slot words (fpb_incidence_slots); it returns
- * FPB_ECONFIG when a pattern column is touched by no incident element or a
- * row is too long — callers then use fpb_assemble_rows. */
+ * fpb_pair_stream_build from the incidence slices and slot words
+ * (fpb_incidence_slots): call 1 (words = NULL) fills pair_ptr[nslices + 1]
+ * (stream words per row of each 32-row slice, prefix-summed) and *total_h;
+ * call 2 fills words[total * 32] (uint16).  FPB_ECONFIG for rows over 128
+ * entries or 64 incidences — callers then use fpb_assemble_rows. */
 int fpb_pair_stream_build(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const int32_t* rowptr,
-                          uint16_t* words, void* stream);
-int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+                          int64_t* pair_ptr, uint16_t* words, int64_t* total_h, void* stream);
+int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int64_t* pair_ptr,
                                 const uint16_t* words, const double* xyz4, const int32_t* rowptr,
                                 const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
                                 void* stream);

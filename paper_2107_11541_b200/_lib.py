@@ -43,7 +43,7 @@ SIGNATURES = {
     "fpb_incidence_nodes": (_int, [_i32, _i64, _int, _vp, _vp, _vp, _vp, _vp]),
     "fpb_assemble_rows": (_int, [_int, _int, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl,
                                  _vp, _vp, _i64, _int, _int, _vp, _vp]),
-    "fpb_pair_stream_build": (_int, [_i32, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_pair_stream_build": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _pi64, _vp]),
     "fpb_assemble_gradient_pairs": (_int, [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int, _vp, _vp]),
     "fpb_incidence_slots8": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
     "fpb_assemble_rows_gl": (_int, [_int, _int, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int,

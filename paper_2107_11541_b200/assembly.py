@@ -120,15 +120,23 @@ class RowPlan:
         self.pairs = None  # TET04 continuity pair stream (pairs.cu); False = not eligible
 
     def ensure_pairs(self, pattern: "CsrMatrix"):
-        """The column-pair stream of the TET04 continuity kernel, built on
-        first use; None when the pattern is not eligible (a column no
-        incident element touches, rows over 128 entries)."""
+        """(pair_ptr, words) of the TET04 continuity pair stream (pairs.cu),
+        built on first use; None when the rows are too long for it."""
         if self.pairs is None:
-            # 4 x 32 words per incidence slot covers both stream layouts (pairs.cu)
-            words = torch.zeros(max(self.ncols, 1) * 4 * 32, dtype=torch.int16, device=self.slice_ptr.device)
-            rc = _lib.load().fpb_pair_stream_build(self.n, self.slice_ptr.data_ptr(), self.slots.data_ptr(),
-                                                   pattern.rowptr_d.data_ptr(), words.data_ptr(), _lib.stream())
-            self.pairs = words if rc == _lib.FPB_OK and self.rowcap <= 129 else False
+            lib = _lib.load()
+            dev = self.slice_ptr.device
+            ptr = torch.empty(self.slice_ptr.numel(), dtype=torch.int64, device=dev)
+            total = ctypes.c_int64(0)
+            rc = lib.fpb_pair_stream_build(self.n, self.slice_ptr.data_ptr(), self.slots.data_ptr(),
+                                           pattern.rowptr_d.data_ptr(), ptr.data_ptr(), None,
+                                           ctypes.byref(total), _lib.stream())
+            words = None
+            if rc == _lib.FPB_OK and self.rowcap <= 129:
+                words = torch.empty(max(total.value, 2) * 32, dtype=torch.int16, device=dev)
+                rc = lib.fpb_pair_stream_build(self.n, self.slice_ptr.data_ptr(), self.slots.data_ptr(),
+                                               pattern.rowptr_d.data_ptr(), ptr.data_ptr(), words.data_ptr(),
+                                               ctypes.byref(total), _lib.stream())
+            self.pairs = (ptr, words) if rc == _lib.FPB_OK and words is not None else False
         return self.pairs if self.pairs is not False else None
 
     def ensure_slots(self, conn_d: torch.Tensor, pattern: "CsrMatrix") -> None:
@@ -406,7 +414,7 @@ class AssemblyContext:
             elif own and kind_id == GRADIENT_XYZ and GRADIENT_PAIRS and g.etype_id == ETYPE_ID[ElementType.TET04] \
                     and g.rows.ensure_pairs(self.pattern) is not None:
                 r = g.rows
-                _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.slice_ptr.data_ptr(), r.pairs.data_ptr(),
+                _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.pairs[0].data_ptr(), r.pairs[1].data_ptr(),
                           xyz4, self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
                           0 if single_rows else 1, out.data_ptr(), _lib.stream())
             elif own:

@@ -18,9 +18,12 @@
 // per incidence: q | r << 7 | last << 14 (q, r = off-diagonal slots of the
 // two edge vectors, last = final pair of the current target column; the
 // targets run 0, 1, 2, ... because every off-diagonal column has at least
-// one pair).  Row 32 s + l, entry k at uint32 (2 slice_ptr[s] + k / 2) 32 + l,
-// half k & 1 (two words per load); padding 0 (the pair (0, 0): adds an
-// exact zero, stores nothing).  Rows longer than 128 entries use k_rows_nb.
+// one pair — a column no incident element touches, e.g. a slab's
+// ghost-shaped interface rows, gets the dummy pair (t, t) = 0).  Slice s
+// holds pair_ptr[s + 1] - pair_ptr[s] words per row (its longest row, even):
+// row 32 s + l, entry k at uint32 (pair_ptr[s] / 2 + k / 2) 32 + l, half
+// k & 1 (two words per load); padding 0 (the pair (0, 0): adds an exact
+// zero, stores nothing).  Rows longer than 128 entries use k_rows_nb.
 //
 // Column pairs are ordered around the edge's tet ring, so consecutive
 // pairs share an edge vector (bit 15: reuse the previous r as q); the next
@@ -28,6 +31,8 @@
 // columns go straight into the warp's linear output rows.  Config 2
 // (B200): 0.196 ms vs 0.264 ms for k_rows_nb (profiles/r01v_pairs ..
 // r01y_step); 24-word batches = one third of an interior row's 72 pairs.
+#include <cub/device/device_scan.cuh>
+
 #include "elemcore.cuh"
 
 namespace fpb {
@@ -43,15 +48,19 @@ constexpr int kPairMaxInc = 64;      // incidences per row the setup sort handle
 // the hot loop needs no end-of-row test
 constexpr uint16_t kPairPad = 0;
 
+// Pass FILL = false: per-slice stream width (the slice's longest row,
+// rounded up to even) into width[sl]; FILL = true: the words.
+template <bool FILL>
 __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, const uint32_t* __restrict__ slots,
-                              const int32_t* __restrict__ rowptr, uint16_t* __restrict__ words, int* err) {
+                              const int32_t* __restrict__ rowptr, const int64_t* __restrict__ pair_ptr,
+                              int64_t* __restrict__ width, uint16_t* __restrict__ words, int* err) {
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nsl = ((int64_t)n + 31) / 32;
   if (row >= nsl * 32) return;
   const int64_t sl = row >> 5;
   const int lane = (int)(row & 31);
   const int m0 = slice_ptr[sl], m1 = slice_ptr[sl + 1];
-  uint32_t key[3 * kPairMaxInc];  // target << 16 | r << 8 | q
+  uint32_t key[3 * kPairMaxInc + 128];  // target << 16 | r << 8 | q (+ bit 24: chained, bit 25: last)
   int np = 0;
   if (row < n) {
     for (int m = m0; m < m1; ++m) {
@@ -109,30 +118,54 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
           break;
         }
     }
+    key[c1 - 1] |= 1u << 25;  // last pair of the column
     c0 = c1;
   }
-  // every off-diagonal column must own at least one pair (the targets are
-  // implicit); a pattern with columns no incident element touches (a
-  // slab's ghost-shaped rows) is not eligible (err 2: use k_rows_nb)
+  // the targets are implicit (0, 1, 2, ... in order), so a pattern column no
+  // incident element touches (a slab's ghost-shaped interface rows) gets a
+  // dummy pair (t, t): e_t x e_t = 0 exactly, and the column stores 0
+  int total = np;
   if (row < n) {
-    int ntarget = 0;
-    for (int i = 0; i < np; ++i) ntarget += (i == 0 || ((key[i] >> 16) & 0xff) != ((key[i - 1] >> 16) & 0xff)) ? 1 : 0;
-    const int nlast = np ? (int)((key[np - 1] >> 16) & 0xff) + 1 : 0;
-    if (ntarget != rowptr[row + 1] - rowptr[row] - 1 || nlast != ntarget) atomicMax(err, 2);
-  }
-  const int width = 3 * (m1 - m0);
-  for (int k = 0; k < width; ++k) {
-    uint16_t v = kPairPad;
-    if (k < np) {
-      const bool last = k + 1 == np || ((key[k + 1] >> 16) & 0xff) != ((key[k] >> 16) & 0xff);
-      v = (uint16_t)((key[k] & 0x7f) | ((key[k] >> 8) & 0x7f) << 7 | (last ? 1u << 14 : 0u) |
-                     (FPB_PAIR_CHAIN && (key[k] >> 24) ? 1u << 15 : 0u));
+    const int ncol = rowptr[row + 1] - rowptr[row] - 1;
+    if (ncol > 128) atomicExch(err, 1);
+    int have = 0;
+    for (int i = 0; i < np; ++i) have += (i == 0 || ((key[i] >> 16) & 0xff) != ((key[i - 1] >> 16) & 0xff)) ? 1 : 0;
+    const int missing = ncol - have;
+    if (missing < 0 || np + missing > 3 * kPairMaxInc + 128) atomicExch(err, 1);
+    if (missing > 0 && missing <= 128 && np + missing <= 3 * kPairMaxInc + 128) {
+      // merge from the back: targets ncol-1 .. 0
+      int src = np - 1, dst = np + missing - 1;
+      for (int t = ncol - 1; t >= 0; --t) {
+        bool found = false;
+        while (src >= 0 && (int)((key[src] >> 16) & 0xff) == t) {
+          key[dst--] = key[src--];
+          found = true;
+        }
+        if (!found) key[dst--] = (uint32_t)t << 16 | (uint32_t)t << 8 | (uint32_t)t | 1u << 25;
+      }
+      total = np + missing;
     }
+  }
+  if constexpr (!FILL) {
+    int wdt = (total + 1) & ~1;  // even: two words per 32-bit load
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wdt = max(wdt, __shfl_xor_sync(0xffffffffu, wdt, o));
+    if (lane == 0) width[sl] = wdt;
+    return;
+  } else {
+    const int64_t p0 = pair_ptr[sl];
+    const int wdt = (int)(pair_ptr[sl + 1] - p0);
+    for (int k = 0; k < wdt; ++k) {
+      uint16_t v = kPairPad;
+      if (k < total)
+        v = (uint16_t)((key[k] & 0x7f) | ((key[k] >> 8) & 0x7f) << 7 | (key[k] & (1u << 25) ? 1u << 14 : 0u) |
+                       (FPB_PAIR_CHAIN && (key[k] & (1u << 24)) ? 1u << 15 : 0u));
 #if FPB_PAIR_PACK2
-    words[(((2LL * m0 + (k >> 1)) * 32 + lane) << 1) | (k & 1)] = v;
+      words[((((p0 >> 1) + (k >> 1)) * 32 + lane) << 1) | (k & 1)] = v;
 #else
-    words[(3LL * m0 + k) * 32 + lane] = v;
+      words[(p0 + k) * 32 + lane] = v;
 #endif
+    }
   }
 }
 
@@ -145,7 +178,7 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
 // output row blocks (linear, one per matrix), where each finished column is
 // stored once at its CSR position.
 __global__ void __launch_bounds__(32, 1)
-k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, const uint16_t* __restrict__ words,
+k_rows_pairs(int32_t n, int32_t row0, const int64_t* __restrict__ pair_ptr, const uint16_t* __restrict__ words,
              const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
              int64_t nnz, int rowcap, int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, T = 32;
@@ -155,8 +188,8 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   const int row = row0 + blockIdx.x * T + tid;
   const bool live = row < n;
   const int lane = row & 31;
-  const int m0 = live ? __ldg(slice_ptr + (row >> 5)) : 0;
-  const int m1 = live ? __ldg(slice_ptr + (row >> 5) + 1) : 0;
+  const int64_t p0 = __ldg(pair_ptr + (row >> 5));
+  const int k1 = live ? (int)(__ldg(pair_ptr + (row >> 5) + 1) - p0) : 0;  // stream words of the slice
   int rlo = 0, rlen = 0;
   double x0[DIM] = {0.0, 0.0, 0.0};
   if (live) {
@@ -181,11 +214,10 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
   const double mN0 = refmN<FPB_TET04>(0);
   double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
   int target = 0;
-  const int k1 = 3 * (m1 - m0);
   constexpr int kW = FPB_PAIR_W;
   uint16_t wc[kW], wn[kW];
 #if FPB_PAIR_PACK2
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + 2LL * m0 * 32 + lane;
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + (p0 >> 1) * 32 + lane;
   auto ld_w = [&](int k, uint16_t (&w)[kW]) {
 #pragma unroll
     for (int j = 0; j < kW; j += 2) {
@@ -195,7 +227,7 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slice_ptr, con
     }
   };
 #else
-  const uint16_t* wp = words + 3LL * m0 * 32 + lane;
+  const uint16_t* wp = words + p0 * 32 + lane;
   auto ld_w = [&](int k, uint16_t (&w)[kW]) {
 #pragma unroll
     for (int j = 0; j < kW; ++j) w[j] = k + j < k1 ? __ldg(wp + (int64_t)(k + j) * 32) : kPairPad;
@@ -315,34 +347,48 @@ using namespace fpb;
 extern "C" {
 
 int fpb_pair_stream_build(int32_t n, const int32_t* slice_ptr, const uint32_t* slots, const int32_t* rowptr,
-                          uint16_t* words, void* stream) {
-  FPB_REQUIRE(n >= 0 && slice_ptr && slots && rowptr && words, "bad pair-stream arguments");
+                          int64_t* pair_ptr, uint16_t* words, int64_t* total_h, void* stream) {
+  FPB_REQUIRE(n >= 0 && slice_ptr && slots && rowptr && pair_ptr, "bad pair-stream arguments");
   cudaStream_t s = as_stream(stream);
   const int64_t nsl = ((int64_t)n + 31) / 32;
-  if (nsl == 0) return FPB_OK;
   int* err = nullptr;
   FPB_CUDA(cudaMallocAsync(&err, sizeof(int), s));
   FPB_CUDA(cudaMemsetAsync(err, 0, sizeof(int), s));
-  k_pair_stream<<<(unsigned)((nsl * 32 + 127) / 128), 128, 0, s>>>(n, slice_ptr, slots, rowptr, words, err);
-  FPB_LAUNCH_CHECK();
+  const unsigned grid = (unsigned)((nsl * 32 + 127) / 128);
+  if (!words) {  // pass 1: slice widths -> pair_ptr (exclusive scan), *total_h
+    FPB_CUDA(cudaMemsetAsync(pair_ptr, 0, sizeof(int64_t), s));
+    if (nsl > 0) {
+      k_pair_stream<false><<<grid, 128, 0, s>>>(n, slice_ptr, slots, rowptr, nullptr, pair_ptr + 1, nullptr, err);
+      FPB_LAUNCH_CHECK();
+      size_t tmp_bytes = 0;
+      void* tmp = nullptr;
+      cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, pair_ptr + 1, pair_ptr + 1, nsl, s);
+      FPB_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+      FPB_CUDA(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, pair_ptr + 1, pair_ptr + 1, nsl, s));
+      FPB_CUDA(cudaFreeAsync(tmp, s));
+    }
+    FPB_CUDA(cudaMemcpyAsync(total_h, pair_ptr + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  } else if (nsl > 0) {  // pass 2: the words [pair_ptr[nsl] * 32]
+    k_pair_stream<true><<<grid, 128, 0, s>>>(n, slice_ptr, slots, rowptr, pair_ptr, nullptr, words, err);
+    FPB_LAUNCH_CHECK();
+  }
   int h = 0;
   FPB_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, s));
   FPB_CUDA(cudaFreeAsync(err, s));
   FPB_CUDA(cudaStreamSynchronize(s));
   if (h) {
-    set_error(h == 2 ? "pair stream: a pattern column is touched by no incident element"
-                     : "pair stream: a row has more than %d incidences or 128 entries", kPairMaxInc);
+    set_error("pair stream: a row has more than %d incidences or 128 entries", kPairMaxInc);
     return FPB_ECONFIG;
   }
   return FPB_OK;
 }
 
-int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int32_t* slice_ptr,
+int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int64_t* pair_ptr,
                                 const uint16_t* words, const double* xyz4, const int32_t* rowptr,
                                 const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
                                 void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
-  FPB_REQUIRE(words && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
+  FPB_REQUIRE(pair_ptr && words && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
               "pair-stream gradient assembly needs the stream, the CSR pattern and rows <= 129 entries");
   FPB_REQUIRE(row0 >= 0 && row0 % 32 == 0 && row1 <= n && row0 <= row1,
               "row window [%d, %d) must start on a 32-row slice", row0, row1);
@@ -352,7 +398,7 @@ int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int
   const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_rows_pairs<<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(row1, row0, slice_ptr, words, xyz4, rowptr,
+  k_rows_pairs<<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(row1, row0, pair_ptr, words, xyz4, rowptr,
                                                                      colind, nnz, rowcap, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
