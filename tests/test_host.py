@@ -37,6 +37,22 @@ def test_ctypes_table_covers_header():
     assert lib.fpb_dot_work_size() > 0
 
 
+def test_ctypes_argument_counts_match_header():
+    """Every prototype in include/fempack_b200.h has as many parameters as
+    its ctypes argtypes entry (a mismatch would only surface as a crash on
+    the GPU box)."""
+    from paper_2107_11541_b200 import _lib
+
+    src = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    bad = {}
+    for m in re.finditer(r"^\s*(?:const char\*|int64_t|int)\s+(fpb_\w+)\s*\(([^)]*)\)\s*;", src, re.M):
+        name, params = m.group(1), m.group(2).strip()
+        n = 0 if params in ("", "void") else len([p for p in params.split(",") if p.strip()])
+        if len(_lib.SIGNATURES[name][1]) != n:
+            bad[name] = (n, len(_lib.SIGNATURES[name][1]))
+    assert not bad, bad
+
+
 def test_library_is_sm100a_only():
     out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
     archs = set(re.findall(r"sm_(\d+a?)", out))
