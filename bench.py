@@ -1,26 +1,33 @@
-"""Headline bench: assembled elements/s for BASELINE.json config 2 —
-NS momentum RHS + continuity (B_x, B_y, B_z) assembly on the 5,036,520-tet
-box mesh (94 x 94 x 95 cells, unit cube), SIMD-packed layout, one B200.
+"""Headline bench: assembled elements/s on BASELINE.json config 5's mesh —
+NS momentum RHS + continuity (B_x, B_y, B_z) assembly on the 100,663,296-tet
+box mesh (256 x 256 x 256 cells, unit cube), SIMD-packed layout, at N B200s.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 One step = MOMENTUM_RHS (rho=1, mu=1e-2, velocity
 = default_rng(0).standard_normal((nnode, 3)), bench.py:196-207 of the
-reference) and the fused gradient/continuity matrices B_k over every element.
-`value` = elements assembled per second (each element contributes its
-momentum block and all three B_k blocks) with inputs resident in HBM, timed
-with CUDA events per step, L2 flushed (512 MiB write) between steps.
+reference) and the fused gradient/continuity matrices B_k over every element
+of the mesh.  `value` = elements assembled per second (each element
+contributes its momentum block and all three B_k blocks) with inputs
+resident in HBM, timed with CUDA events per step, L2 flushed (512 MiB
+write) between steps — the mesh data (1.6 GB connectivity, 6 GB of matrix
+values per step) is far larger than L2 anyway.
 `e2e` = the same step through the public API with host (numpy) inputs and
 outputs: velocity H2D in, RHS + three matrices' values D2H out.
 
-Multi-GPU (torchrun, N > 1): weak scaling — rank r assembles z-slab r of an
-(94, 94, 95 N) mesh; interface-plane RHS/matrix contributions are summed by
-an NCCL halo exchange that runs on a side stream while the interior rows are
-assembled (interface windows first, paper_2107_11541_b200/distributed.py).
+N > 1 (torchrun, or `--gpus N` which launches torchrun itself): STRONG
+scaling — the same 256^3 mesh split into N z-slabs, one per GPU
+(paper_2107_11541_b200/distributed.py); interface-plane RHS/matrix
+contributions are summed by an NCCL halo exchange on a side stream while
+the interior rows are assembled.  `value` = the whole mesh's elements / the
+max-over-ranks step time; per-phase times (interface, halo, interior) are
+reported beside it.
 
-`--impl reference`: the reference's CPU algorithm (C restatement of the
-packed kernels, oracle/fempack_ref.c, all host threads) on a bounded sample of
-the same workload; prints the same JSON line with "impl": "reference".
+`--impl reference`: the reference's CPU algorithm (the C restatement of the
+reference packed kernels, oracle/fempack_ref.c, all host threads) on a
+z-slab sample of the same mesh (its first --cpu-kz cell layers, with the
+full mesh's coordinates and velocity rows); elements/s of the sample is the
+extrapolated rate for the whole mesh.  Same `config` dict as this arm.
 """
 
 from __future__ import annotations
@@ -28,6 +35,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -43,6 +51,7 @@ UNIT = "Melem/s"
 # measured DFMA rate on this pool's B200 (tools/microbench/peaks.cu,
 # profiles/r01_microbench.txt); MEASURED_PEAKS.json carries no FP64 figure
 FP64_PEAK_TFLOPS = 34.1
+FP64_NOMINAL_TFLOPS = 37.2
 HBM_FALLBACK_GBS = 6650.0
 # SURVEY 8(d) algorithmic work per TET04 element (flops, compulsory bytes)
 WORK = {"momentum_rhs": (1492.0, 28.0), "gradient_xyz": (676.0, 145.0)}
@@ -60,6 +69,9 @@ WORK_C = {
     ("HEX08", "gradient_xyz"): (6169.0, 962.0),
 }
 L2_FLUSH_BYTES = 512 << 20
+C5 = (256, 256, 256)
+C4 = 272
+C2 = (94, 94, 95)
 
 
 def hbm_peak():
@@ -69,6 +81,23 @@ def hbm_peak():
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def tet_counts(nx, ny, nz):
+    return 6 * nx * ny * nz, (nx + 1) * (ny + 1) * (nz + 1)
+
+
+def workload_config(args, world: int) -> dict:
+    """The workload both arms print, key for key (the driver compares them)."""
+    nx, ny, nz = args.nx, args.ny, args.nz
+    ne, nn = tet_counts(nx, ny, nz)
+    name = "config 5" if (nx, ny, nz) == C5 else ("config 2" if (nx, ny, nz) == C2 else "custom")
+    return {"workload": f"{name}: TET04 box {nx}x{ny}x{nz} on the unit cube ({ne} elements, {nn} nodes), "
+                        "NS momentum RHS (rho 1, mu 1e-2, velocity default_rng(0)) + continuity "
+                        "B_x,B_y,B_z (3 x CONVECTION(e_k)), SIMD-packed layout, FP64",
+            "elements_per_step": ne, "cells": [nx, ny, nz],
+            "decomposition": f"{world} z-slab(s), one per GPU (strong scaling: same mesh at every N)",
+            "l2": "flushed (512 MiB write) between GPU steps; per-step data >> L2"}
 
 
 class ClockSampler:
@@ -118,8 +147,22 @@ def _roof(F, B, ms, nelem, hbm):
     fl, by = F * nelem / t / 1e12, B * nelem / t / 1e9
     if F / B > FP64_PEAK_TFLOPS * 1e3 / hbm:
         return {"bound": "fp64", "achieved": fl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": fl / FP64_PEAK_TFLOPS}
+                "frac": fl / FP64_PEAK_TFLOPS, "frac_of_nominal": fl / FP64_NOMINAL_TFLOPS}
     return {"bound": "hbm", "achieved": by, "peak": hbm, "unit": "GB/s", "frac": by / hbm}
+
+
+def _step_roofline(kern_ms: dict, work: dict, nelem: int, ms_step: float, hbm: float) -> dict:
+    """The whole step against its own roofline: per element, each kernel's
+    SURVEY 8(d) work at the binding one of its two roofs, summed."""
+    def kernel_ns(k):
+        Fk, Bk = work[k]
+        return max(Fk / (FP64_PEAK_TFLOPS * 1e3), Bk / hbm)
+    bound_ns = sum(kernel_ns(k) for k in kern_ms)
+    return {"bound_Gelem_s": 1.0 / bound_ns, "achieved_Gelem_s": nelem / (ms_step * 1e6),
+            "frac": (nelem / (ms_step * 1e6)) * bound_ns,
+            "per_kernel_bound": {k: ("fp64" if work[k][0] / (FP64_PEAK_TFLOPS * 1e3) > work[k][1] / hbm
+                                     else "hbm") for k in kern_ms},
+            "note": "time-sum of each kernel's roofline bound per element (SURVEY 8(d) work)"}
 
 
 def _time_ms(fn, reps, flush):
@@ -139,45 +182,205 @@ def _time_ms(fn, reps, flush):
     return statistics.median(ts)
 
 
-def config3_block(ctx, vel, flush, hbm, reps=10):
-    """Config 3: scalar transport (enthalpy + 2 species) on the config-2 mesh;
-    the solver vector ops are in the "solver" block."""
+# ---------------------------------------------------------------------------
+# CPU baseline (reference algorithm on the host cores; oracle/ is the checker
+# and this leg only — never the measured product)
+# ---------------------------------------------------------------------------
+
+def cpu_run(etype, nx, ny, nz, kz, kinds, steps, warmup, whole_elems):
+    from oracle import cport
+    from oracle.baseline import CpuWorkload
+
+    threads = cport.max_threads()
+    t0 = time.perf_counter()
+    wl = CpuWorkload(etype, nx, ny, nz, kz, nthreads=threads, kinds=kinds)
+    setup = time.perf_counter() - t0
+    ts = wl.time_steps(steps, warmup)
+    t = statistics.median(ts)
+    sample = (f"{etype} first {kz} of {nz} cell layers of the {nx}x{ny}x{nz} box ({wl.nelem} of {whole_elems} "
+              f"elements, the full mesh's coordinates and field rows), {' + '.join(kinds)} with the reference's "
+              f"scatters; reference packed kernels restated in C (oracle/fempack_ref.c, vs=8, geometry cached "
+              f"as in the reference bench), {threads} threads; median of {steps} steps ({sum(ts):.1f} s of timed "
+              f"CPU work, {setup:.0f} s untimed setup); elements/s extrapolated to the whole mesh "
+              f"(per-element work is identical)")
+    return {"value": wl.nelem / t / 1e6, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+            "ms_per_sample_step": t * 1e3, "extrapolated_ms_per_step": t * 1e3 * whole_elems / wl.nelem}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU algorithm on the host cores (rank 0)."""
+    if rank != 0:
+        return
+    ne, _ = tet_counts(args.nx, args.ny, args.nz)
+    cpu = cpu_run("TET04", args.nx, args.ny, args.nz, args.cpu_kz, ("momentum", "gradients"),
+                  args.steps, args.warmup, ne)
+    value = cpu["value"]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": cpu["extrapolated_ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": workload_config(args, world),
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# companion blocks (N = 1): solver at config 5 size, configs 2/3/4, FlowSolver
+# ---------------------------------------------------------------------------
+
+def solver_block(ctx, flush, hbm, reps=20, iters=40):
+    """Solver vector kernels on the config-5 mesh (n = 16.97 M rows, vectors
+    of 136 MB >> L2, L2 flushed between reps): SpMV on the MASS matrix,
+    axpy (alpha 2.5), dot, and fixed-count PCG / BiCGSTAB iterations whose
+    per-iteration HBM bytes are counted kernel by kernel."""
+    import torch
+
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200 import _lib
+    from paper_2107_11541_b200 import sparse as S
+
+    dev = ctx.mesh.coords_d.device
+    n, nnz = ctx.pattern.n, ctx.pattern.nnz
+    K = P.KernelKind
+    M = ctx.assemble_matrix(K.MASS)
+    x = torch.as_tensor(np.random.default_rng(0).standard_normal(n), device=dev)
+    y = torch.empty_like(x)
+    out = {}
+    S.spmv_d(M, x, y)
+    sc = M._sell
+    by_csr = 12 * nnz + 4 * (n + 1) + 16 * n
+    idxb = 2 if sc.idx16 else 4
+    by_sell = (8 + idxb) * sc.total + 8 * ((n + 31) // 32 + 1) + 16 * n
+    ms = _time_ms(lambda: S.spmv_d(M, x, y), reps, flush)
+    out["spmv"] = {"n": n, "nnz": nnz, "padded": sc.total, "ms": ms, "GB_s": by_sell / ms / 1e6,
+                   "frac_hbm": by_sell / ms / 1e6 / hbm, "GB_s_csr_equiv": by_csr / ms / 1e6,
+                   "kernel": f"SELL-32 ({'16' if sc.idx16 else '32'}-bit column offsets), thread per row, the "
+                             "reference's row-sum order (public sparse.spmv)",
+                   "bytes_note": "SELL bytes actually streamed (values + offsets incl. padding, slice pointers, x, y)"}
+    ms = _time_ms(lambda: _lib.call("fpb_spmv", n, nnz, M.rowptr_d.data_ptr(), M.colind_d.data_ptr(),
+                                    M.vals_d.data_ptr(), x.data_ptr(), y.data_ptr(), _lib.stream()), reps, flush)
+    out["spmv_csr"] = {"ms": ms, "GB_s": by_csr / ms / 1e6, "frac_hbm": by_csr / ms / 1e6 / hbm,
+                       "kernel": "CSR, lanes per row (fpb_spmv; long-row operators)"}
+    a = torch.randn(n, dtype=torch.float64, device=dev)
+    c = torch.empty_like(a)
+    ms = _time_ms(lambda: S.axpy_d(2.5, a, x, c), reps, flush)
+    out["axpy"] = {"n": n, "ms": ms, "GB_s": 24 * n / ms / 1e6, "frac_hbm": 24 * n / ms / 1e6 / hbm}
+    r = torch.empty((), dtype=torch.float64, device=dev)
+    ms = _time_ms(lambda: S.dot_d(a, x, r), reps, flush)
+    out["dot"] = {"n": n, "ms": ms, "GB_s": 16 * n / ms / 1e6, "frac_hbm": 16 * n / ms / 1e6 / hbm}
+    del a, c
+    # fixed-count Krylov iterations (tol 0) on the config-5 operators
+    L = ctx.assemble_matrix(K.LAPLACIAN)
+    vals = L.vals_d.clone()
+    rp, ci = L.rowptr_d.long(), L.colind_d.long()
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), rp[1:] - rp[:-1])
+    hit = (rows == 0) | (ci == 0)
+    vals[hit] = 0.0
+    vals[(rows == 0) & (ci == 0)] = 1.0
+    del rows, hit, rp, ci
+    A = L.with_vals(vals)
+    b = torch.as_tensor(np.random.default_rng(0).standard_normal(n), device=dev)
+    b[0] = 0.0
+    P.pcg_solve(A, b, tol=0.0, max_iter=iters)  # warm: workspace, SELL copy, batch graph
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, st = P.pcg_solve(A, b, tol=0.0, max_iter=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # per PCG iteration: one SELL SpMV + fused updates (x, r, z, p: read p q x r d,
+    # write x r p — 9 vector passes, DESIGN.md 5)
+    it_by = by_sell + 9 * 8 * n
+    out["pcg"] = {"n": n, "iterations": st.iterations, "ms_per_iter": ms / max(st.iterations, 1),
+                  "GB_s": it_by * st.iterations / ms / 1e6, "frac_hbm": it_by * st.iterations / ms / 1e6 / hbm,
+                  "note": "tol 0, fixed iteration count; bytes = SELL SpMV + 9 vector passes per iteration "
+                          "(vectors 136 MB each, >> L2)"}
+    vel = torch.as_tensor(np.random.default_rng(0).standard_normal((n, 3)), device=dev)
+    C = ctx.assemble_matrix(K.CONVECTION, velocity=vel)
+    del vel
+    Ab = M.with_vals(M.vals_d + 0.05 * (C.vals_d + 1e-2 * L.vals_d))
+    del C, L, A, vals
+    bb = torch.as_tensor(np.random.default_rng(1).standard_normal(n), device=dev)
+    P.bicgstab_solve(Ab, bb, tol=0.0, max_iter=iters)  # warm
+    torch.cuda.synchronize()
+    e0.record()
+    _, stb = P.bicgstab_solve(Ab, bb, tol=0.0, max_iter=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # two SpMVs + 23 vector passes per BiCGSTAB iteration (DESIGN.md 5)
+    it_by = 2 * by_sell + 23 * 8 * n
+    out["bicgstab"] = {"n": n, "iterations": stb.iterations, "ms_per_iter": ms / max(stb.iterations, 1),
+                       "GB_s": it_by * stb.iterations / ms / 1e6,
+                       "frac_hbm": it_by * stb.iterations / ms / 1e6 / hbm,
+                       "operator": "M + 0.05 (C(u) + 1e-2 L) (config 5's solver)"}
+    del M, Ab
+    torch.cuda.empty_cache()
+    return out
+
+
+def config2_block(flush, hbm, reps=10):
+    """Round-1's headline workload (config 2: 5,036,520 tets, momentum RHS +
+    B_x,B_y,B_z) and config 3 (3 scalar RHS) on the same mesh."""
     import torch
 
     import paper_2107_11541_b200 as P
 
-    n, ne = ctx.mesh.nnode, ctx.mesh.nelem
+    nx, ny, nz = C2
+    mesh = P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz)
+    ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    ctx.refresh_geometry("packed", need_grad=False)
+    n, ne, nnz = mesh.nnode, mesh.nelem, ctx.pattern.nnz
+    dev = flush.device
     rng = np.random.default_rng(0)
-    rng.standard_normal((n, 3))
-    phi3 = torch.as_tensor(np.stack([rng.standard_normal(n) for _ in range(3)]), device=vel.device)
-    out3 = torch.empty((3, n), dtype=torch.float64, device=vel.device)
+    vel = torch.as_tensor(rng.standard_normal((n, 3)), device=dev)
+    phi3 = torch.as_tensor(np.stack([rng.standard_normal(n) for _ in range(3)]), device=dev)
+    rhs = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
+    out3 = torch.empty((3, n), dtype=torch.float64, device=dev)
+    K = P.KernelKind
+    ms_mom = _time_ms(lambda: ctx.assemble_rhs_d(K.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs), reps, flush)
+    ms_grad = _time_ms(lambda: ctx.assemble_gradients_d(mats), reps, flush)
     kap = (1e-2, 1e-2, 1e-2)  # kappa, D, D (timeloop.py:76-79)
-
-    def fused():  # one element-block pass for the three fields (fpb_assemble_blocks_scalar3)
-        ctx.assemble_scalar_rhs3_d(vel, phi3, kap, out3)
+    ms_s3 = _time_ms(lambda: ctx.assemble_scalar_rhs3_d(vel, phi3, kap, out3), reps, flush)
 
     def three():
         for f in range(3):
-            ctx.assemble_rhs_d(P.KernelKind.SCALAR_RHS, vel, phi3[f], 1.0, 0.0, kap[f], out3[f])
-
-    ms = _time_ms(fused, reps, flush)
+            ctx.assemble_rhs_d(K.SCALAR_RHS, vel, phi3[f], 1.0, 0.0, kap[f], out3[f])
     ms_three = _time_ms(three, reps, flush)
     F, B = WORK_C[("TET04", "scalar_rhs")]
-    return {"workload": "config 3: TET04 94x94x95, SCALAR_RHS x3 (heat kappa, 2 species D), velocity + scalars "
-                        "default_rng(0) draws; one fused element-block pass", "elements": ne, "ms_per_step": ms,
-            "ms_three_separate_passes": ms_three,
-            "value": 3 * ne / (ms / 1e3) / 1e6, "unit": "Melem/s (element-scalar assemblies)",
-            "roofline": dict(_roof(F, B, ms / 3, ne, hbm), kernel="scalar_rhs3 (fused)",
-                             work_per_element={"flops": F, "bytes": B},
-                             note="F is the reference's per-element work for ONE scalar (geometry included); "
-                                  "the fused pass shares geometry, velocity moments and node staging across the "
-                                  "three fields, so this reference-flop rate can exceed the FP64 peak")}
+    step = ms_mom + ms_grad
+    out = {"c2": {"workload": f"config 2: TET04 box {nx}x{ny}x{nz} ({ne} elements, {n} nodes, nnz {nnz}), "
+                              "momentum RHS + B_x,B_y,B_z", "ms_per_step": step,
+                  "value": ne / (step / 1e3) / 1e6, "unit": UNIT,
+                  "kernels_ms": {"momentum_rhs": ms_mom, "gradient_xyz": ms_grad},
+                  "roofline": {k: _roof(*WORK[k], t, ne, hbm) for k, t in
+                               (("momentum_rhs", ms_mom), ("gradient_xyz", ms_grad))},
+                  "step_roofline": _step_roofline({"momentum_rhs": ms_mom, "gradient_xyz": ms_grad}, WORK, ne,
+                                                  step, hbm)},
+           "c3": {"workload": "config 3: same mesh, SCALAR_RHS x3 (heat kappa, 2 species D), velocity + scalars "
+                              "default_rng(0) draws; one fused element-block pass", "elements": ne,
+                  "ms_per_step": ms_s3, "ms_three_separate_passes": ms_three,
+                  "value": 3 * ne / (ms_s3 / 1e3) / 1e6, "unit": "Melem/s (element-scalar assemblies)",
+                  "roofline": dict(_roof(F, B, ms_s3 / 3, ne, hbm), kernel="scalar_rhs3 (fused)",
+                                   note="F is the reference's per-element work for ONE scalar (geometry "
+                                        "included); the fused pass shares geometry, velocity moments and node "
+                                        "staging across the three fields")}}
+    del ctx, mats
+    torch.cuda.empty_cache()
+    return out
 
 
-def config4_block(flush, hbm, n=272, reps=5):
+def config4_block(flush, hbm, cpu: bool, e2e: bool, n=C4, reps=5):
     """Config 4: 20,123,648-element HEX08 (Q1, 8 Gauss points) box, full NS +
     scalar assembly: momentum RHS, continuity B_x,B_y,B_z and three scalar
-    RHS per step."""
+    RHS per step; cpu_baseline on a z-slab sample; e2e through the public
+    API (numpy in, numpy out)."""
     import torch
 
     import paper_2107_11541_b200 as P
@@ -188,8 +391,10 @@ def config4_block(flush, hbm, n=272, reps=5):
     nn_, ne, nnz = mesh.nnode, mesh.nelem, ctx.pattern.nnz
     dev = flush.device
     rng = np.random.default_rng(0)
-    vel = torch.as_tensor(rng.standard_normal((nn_, 3)), device=dev)
-    phi3 = torch.as_tensor(np.stack([rng.standard_normal(nn_) for _ in range(3)]), device=dev)
+    vel_h = rng.standard_normal((nn_, 3))
+    phi_h = [rng.standard_normal(nn_) for _ in range(3)]
+    vel = torch.as_tensor(vel_h, device=dev)
+    phi3 = torch.as_tensor(np.stack(phi_h), device=dev)
     rhs = torch.empty((nn_, 3), dtype=torch.float64, device=dev)
     srhs3 = torch.empty((3, nn_), dtype=torch.float64, device=dev)
     mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
@@ -209,101 +414,40 @@ def config4_block(flush, hbm, n=272, reps=5):
     roof["scalar_rhs"]["note"] = ("per scalar of the fused three-field pass (shared staging); F is the "
                                   "reference's one-scalar work")
     total = sum(ms.values())
-    del ctx, mats
-    torch.cuda.empty_cache()
-    return {"workload": f"config 4: HEX08 box {n}^3 ({ne} elements, {nn_} nodes, nnz {nnz}), momentum RHS + "
-                        "B_x,B_y,B_z + 3 scalar RHS", "elements": ne, "ms_per_step": total,
-            "value": ne / (total / 1e3) / 1e6, "unit": "Melem/s", "kernels": roof}
-
-
-def dist_bicgstab_block(sub, vel, dev, dist, iters=60):
-    """Config 5's solver leg at N > 1: Jacobi-BiCGSTAB on the slab-decomposed
-    advection-diffusion operator M + dt (C(u) + kappa L) — per iteration the
-    fused device kernels with owned-row reductions, four 2-double NCCL
-    allreduces and two ghost-plane exchanges.  A fixed iteration count
-    (tol 0) is timed with CUDA events between barriers, max over ranks."""
-    import torch
-
-    import paper_2107_11541_b200 as P
-    from paper_2107_11541_b200.distributed import bicgstab_slab
-
-    ctx = sub.ctx
-    nnz = ctx.pattern.nnz
-    mats = []
-    for kind, v in ((P.KernelKind.MASS, None), (P.KernelKind.CONVECTION, vel), (P.KernelKind.LAPLACIAN, None)):
-        m = torch.empty(nnz, dtype=torch.float64, device=dev)
-        ctx.assemble_matrix_d(kind, v, m)
-        sub.halo_sum_matrix(m)
-        mats.append(m)
-    A = ctx.pattern.with_vals(mats[0] + 0.05 * (mats[1] + 1e-2 * mats[2]))
-    L = sub.layout
-    nglob = (L.nx + 1) * (L.ny + 1) * (L.nz + 1)
-    b = torch.as_tensor(np.random.default_rng(1).standard_normal(nglob)[L.node_offset:L.node_offset + L.nnode],
-                        device=dev)
-    bicgstab_slab(L, A, b, tol=0.0, max_iter=8, check_every=8)  # warm
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    x, st = bicgstab_slab(L, A, b, tol=0.0, max_iter=iters, check_every=iters)
-    e1.record()
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    return {"workload": "slab BiCGSTAB on M + 0.05 (C(u) + 1e-2 L), local 94x94x95 cells per GPU",
-            "iterations": st.iterations, "ms": ms, "ms_per_iter": ms / max(st.iterations, 1),
-            "rows_per_rank": L.owned_rows[1] - L.owned_rows[0], "relres": st.residual_history[-1]}
-
-
-def config5_block(flush, hbm, n=256, reps=5, iters=40):
-    """Config 5's mesh (100,663,296 tets, 256^3 cells) on ONE B200: the
-    headline step (momentum RHS + B_x,B_y,B_z) and Jacobi-BiCGSTAB iterations
-    on M + 0.05 (C(u) + 1e-2 L) — the single-GPU reference point of the
-    2/4/8-GPU decomposition."""
-    import torch
-
-    import paper_2107_11541_b200 as P
-
-    t0 = time.perf_counter()
-    mesh = P.generate_box_mesh(P.ElementType.TET04, n, n, n)
-    ctx = P.AssemblyContext.build(mesh, vector_size=8)
-    ctx.refresh_geometry("packed", need_grad=False)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
-    nn_, ne, nnz = mesh.nnode, mesh.nelem, ctx.pattern.nnz
-    dev = flush.device
-    vel = torch.as_tensor(np.random.default_rng(0).standard_normal((nn_, 3)), device=dev)
-    rhs = torch.empty((nn_, 3), dtype=torch.float64, device=dev)
-    mats = torch.empty(3 * nnz, dtype=torch.float64, device=dev)
-    K = P.KernelKind
-    ms_mom = _time_ms(lambda: ctx.assemble_rhs_d(K.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, rhs), reps, flush)
-    ms_grad = _time_ms(lambda: ctx.assemble_gradients_d(mats), reps, flush)
+    work4 = {"momentum_rhs": WORK_C[("HEX08", "momentum_rhs")], "gradient_xyz": WORK_C[("HEX08", "gradient_xyz")],
+             "scalar_rhs_x3": (3 * WORK_C[("HEX08", "scalar_rhs")][0], 3 * WORK_C[("HEX08", "scalar_rhs")][1])}
+    kern = {"momentum_rhs": ms["momentum_rhs"], "gradient_xyz": ms["gradient_xyz"], "scalar_rhs_x3": ms["scalar_rhs"]}
+    out = {"workload": f"config 4: HEX08 box {n}^3 ({ne} elements, {nn_} nodes, nnz {nnz}), momentum RHS + "
+                       "B_x,B_y,B_z + 3 scalar RHS (default_rng(0) velocity then 3 scalars)",
+           "elements": ne, "ms_per_step": total, "value": ne / (total / 1e3) / 1e6, "unit": UNIT,
+           "kernels": roof, "step_roofline": _step_roofline(kern, work4, ne, total, hbm)}
     del mats
-    M = ctx.assemble_matrix(K.MASS)
-    C = ctx.assemble_matrix(K.CONVECTION, velocity=vel)
-    L = ctx.assemble_matrix(K.LAPLACIAN)
-    A = M.with_vals(M.vals_d + 0.05 * (C.vals_d + 1e-2 * L.vals_d))
-    del C, L
-    b = torch.as_tensor(np.random.default_rng(1).standard_normal(nn_), device=dev)
-    P.bicgstab_solve(A, b, tol=0.0, max_iter=iters)  # warm: same workspace + batch graph as the timed solve
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    x, st = P.bicgstab_solve(A, b, tol=0.0, max_iter=iters)
-    e1.record()
-    torch.cuda.synchronize()
-    ms_bicg = e0.elapsed_time(e1)
-    F, B = WORK["gradient_xyz"]
-    out = {"workload": f"config 5 mesh on one GPU: TET04 box {n}^3 ({ne} elements, {nn_} nodes, nnz {nnz})",
-           "setup_s": setup_s, "ms_per_step": ms_mom + ms_grad, "value": ne / ((ms_mom + ms_grad) / 1e3) / 1e6,
-           "unit": UNIT, "kernels_ms": {"momentum_rhs": ms_mom, "gradient_xyz": ms_grad},
-           "gradient_roofline": _roof(F, B, ms_grad, ne, hbm),
-           "bicgstab": {"iterations": st.iterations, "ms_per_iter": ms_bicg / max(st.iterations, 1),
-                        "GB_s_equiv": (2 * (12 * nnz + 4 * (nn_ + 1) + 8 * nn_) + 23 * 8 * nn_) * st.iterations
-                        / ms_bicg / 1e6}}
-    del ctx, A, M
+    if e2e:
+        ts = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = ctx.assemble_rhs(K.MOMENTUM_RHS, "packed", vel_h, None, 1.0, 1e-2, 0.0)
+            vals = [B.vals for B in P.gradient_matrices(ctx)]
+            sc = [ctx.assemble_rhs(K.SCALAR_RHS, "packed", vel_h, phi_h[f], 1.0, 0.0, 1e-2) for f in range(3)]
+            torch.cuda.synchronize()
+            if i >= 1:
+                ts.append((time.perf_counter() - t0) * 1e3)
+            nbytes_out = r.nbytes + sum(v.nbytes for v in vals) + sum(s.nbytes for s in sc)
+            del r, vals, sc
+        t = statistics.mean(ts)
+        out["e2e"] = {"value": ne / (t / 1e3) / 1e6, "unit": UNIT, "ms_per_step": t,
+                      "h2d_bytes_per_step": int(4 * vel_h.nbytes + 3 * phi_h[0].nbytes),
+                      "d2h_bytes_per_step": int(nbytes_out),
+                      "api": "assemble_rhs(MOMENTUM_RHS) + gradient_matrices(ctx) .vals + 3 x "
+                             "assemble_rhs(SCALAR_RHS), numpy in / numpy out (pageable inputs)"}
+    del ctx
     torch.cuda.empty_cache()
+    if cpu:
+        try:
+            out["cpu_baseline"] = cpu_run("HEX08", n, n, n, 14, ("momentum", "gradients", "scalars"), 8, 1, ne)
+        except Exception as exc:  # reported, not fatal
+            out["cpu_baseline"] = {"error": repr(exc)}
     return out
 
 
@@ -349,48 +493,68 @@ def flow_block(nx, ny, nz, steps=2):
             "pressure_operator_nnz": solver.laplacian.nnz}
 
 
-def cpu_baseline(nx, ny, nz_sample, steps=30, warmup=2):
-    from oracle import cport
-    from oracle.baseline import CpuWorkload
+def dist_bicgstab_block(sub, vel, dev, dist, iters=40):
+    """Config 5's solver leg at N > 1: Jacobi-BiCGSTAB on the slab-decomposed
+    advection-diffusion operator M + dt (C(u) + kappa L) — per iteration the
+    fused device kernels with owned-row reductions, NCCL allreduces of 2-3
+    doubles and two ghost-plane exchanges.  A fixed iteration count (tol 0)
+    is timed with CUDA events between barriers, max over ranks."""
+    import torch
 
-    threads = cport.max_threads()
-    wl = CpuWorkload(nx, ny, nz_sample, nthreads=threads)
-    ts = wl.time_steps(steps, warmup)
-    t = statistics.median(ts)
-    whole = "the whole config-2 mesh" if nz_sample == 95 else "a slab of the config-2 mesh"
-    return {"value": wl.nelem / t / 1e6, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"TET04 {nx}x{ny}x{nz_sample} box, {whole} ({wl.nelem} elements), momentum RHS + "
-                      f"3x CONVECTION(e_k) + scatters, reference packed kernels (oracle/fempack_ref.c, vs=8, "
-                      f"geometry cached as in the reference bench), median of {steps} steps "
-                      f"({sum(ts):.1f} s of timed CPU work)"}
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200.distributed import bicgstab_slab
+
+    ctx = sub.ctx
+    nnz = ctx.pattern.nnz
+    mats = []
+    for kind, v in ((P.KernelKind.MASS, None), (P.KernelKind.CONVECTION, vel), (P.KernelKind.LAPLACIAN, None)):
+        m = torch.empty(nnz, dtype=torch.float64, device=dev)
+        ctx.assemble_matrix_d(kind, v, m)
+        sub.halo_sum_matrix(m)
+        mats.append(m)
+    A = ctx.pattern.with_vals(mats[0] + 0.05 * (mats[1] + 1e-2 * mats[2]))
+    del mats
+    L = sub.layout
+    nglob = (L.nx + 1) * (L.ny + 1) * (L.nz + 1)
+    b = torch.as_tensor(np.random.default_rng(1).standard_normal(nglob)[L.node_offset:L.node_offset + L.nnode],
+                        device=dev)
+    bicgstab_slab(L, A, b, tol=0.0, max_iter=8, check_every=8)  # warm
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, st = bicgstab_slab(L, A, b, tol=0.0, max_iter=iters, check_every=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": f"slab BiCGSTAB on M + 0.05 (C(u) + 1e-2 L), {L.nx}x{L.ny}x{L.nz} cells split {L.world} ways",
+            "iterations": st.iterations, "ms": ms, "ms_per_iter": ms / max(st.iterations, 1),
+            "rows_per_rank": L.owned_rows[1] - L.owned_rows[0]}
 
 
-def run_reference(args, rank, world):
-    """--impl reference: reference CPU algorithm on the host cores (rank 0)."""
-    if rank != 0:
-        return
-    from oracle import cport
-    from oracle.baseline import CpuWorkload
+# ---------------------------------------------------------------------------
 
-    threads = cport.max_threads()
-    wl = CpuWorkload(args.nx, args.ny, args.cpu_nz, nthreads=threads)
-    ts = wl.time_steps(args.steps, args.warmup)
-    t = statistics.mean(ts)
-    value = wl.nelem / t / 1e6
-    whole = "the whole config-2 mesh" if args.cpu_nz == 95 else "a slab of the config-2 mesh"
-    sample = (f"TET04 {args.nx}x{args.ny}x{args.cpu_nz} box, {whole} ({wl.nelem} elements) per step, "
-              f"reference packed kernels in C (oracle/fempack_ref.c), {threads} threads")
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": "config 2: TET04 94x94x95 box (5,036,520 elements), NS momentum RHS + "
-                               "continuity B_x,B_y,B_z, packed layout", "sample_elements": wl.nelem},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> None:
+    """`--gpus N` without torchrun: start N ranks with torch.distributed.run
+    and exit with its status; refuse when fewer than N GPUs are visible."""
+    import torch
+
+    ndev = torch.cuda.device_count()
+    shared = os.environ.get("FPB_DIST_BACKEND", "nccl") != "nccl"  # several ranks per GPU (functional runs)
+    if args.impl == "ours" and ndev < args.gpus and not shared:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {ndev} CUDA device(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -399,24 +563,28 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nx", type=int, default=94)
-    ap.add_argument("--ny", type=int, default=94)
-    ap.add_argument("--nz", type=int, default=95)
-    ap.add_argument("--cpu-nz", type=int, default=95,
-                    help="z-layers of the CPU baseline / reference-arm workload (95 = the whole config-2 mesh)")
+    ap.add_argument("--nx", type=int, default=C5[0])
+    ap.add_argument("--ny", type=int, default=C5[1])
+    ap.add_argument("--nz", type=int, default=C5[2])
+    ap.add_argument("--cpu-kz", type=int, default=13,
+                    help="cell layers of the CPU-baseline / reference-arm slab sample (13 of 256: 5.1 M tets)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--scatter", default="auto", choices=["auto", "rows", "atomic"],
                     help="global-assembly strategy (AssemblyContext.build)")
     ap.add_argument("--no-solver", action="store_true", help="skip the solver vector-kernel block")
-    ap.add_argument("--no-configs", action="store_true", help="skip the config-3 / config-4 blocks")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-2/3/4 and FlowSolver blocks")
     ap.add_argument("--soak", type=float, default=1.0, help="untimed seconds under load before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -440,22 +608,29 @@ def main():
     import paper_2107_11541_b200 as P
 
     dev = torch.device("cuda", local)
+    nx, ny, nz = args.nx, args.ny, args.nz
+    total_elems, nglob = tet_counts(nx, ny, nz)
+    t0 = time.perf_counter()
     if world > 1:
         from paper_2107_11541_b200 import distributed as D
 
-        sub = D.SlabDomain.build(args.nx, args.ny, args.nz * world, rank, world)
+        sub = D.SlabDomain.build(nx, ny, nz, rank, world)
         mesh, ctx = sub.mesh, sub.ctx
+        node0 = sub.layout.node_offset
     else:
         sub = None
-        mesh = P.generate_box_mesh(P.ElementType.TET04, args.nx, args.ny, args.nz)
+        mesh = P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz)
         ctx = P.AssemblyContext.build(mesh, vector_size=8, scatter=args.scatter)
+        node0 = 0
     ctx.refresh_geometry("packed", need_grad=False)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
     nelem, nnode, nnz = mesh.nelem, mesh.nnode, ctx.pattern.nnz
-    rng = np.random.default_rng(0)
-    # host inputs live in pinned memory (the e2e contract: H2D from pinned
-    # host buffers); the numpy view is what a reference user passes
+    # the global velocity field default_rng(0).standard_normal((nnode, 3));
+    # a slab takes its node rows.  Host inputs live in pinned memory (the
+    # e2e contract: H2D from pinned host buffers).
     vel_h = torch.empty((nnode, 3), dtype=torch.float64, pin_memory=True).numpy()
-    vel_h[:] = rng.standard_normal((nnode, 3))
+    vel_h[:] = np.random.default_rng(0).standard_normal((nglob, 3))[node0:node0 + nnode]
     vel = torch.as_tensor(vel_h, device=dev)
     rhs = torch.zeros((nnode, 3), dtype=torch.float64, device=dev)
     mats = torch.zeros(3 * nnz, dtype=torch.float64, device=dev)
@@ -463,7 +638,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     side = torch.cuda.Stream() if sub is not None else None
-    launches_per_step = 3
+    launches_per_step = 3  # element-block momentum RHS (integrate + node gather) + B_xyz rows
     if sub is not None:  # windowed schedule: one launch per non-empty window
         from paper_2107_11541_b200.distributed import _step_windows
 
@@ -483,13 +658,13 @@ def main():
         if ev:
             ev[2].record(stream)
 
-    def step(ev=None):
+    def step(ev=None, phases=None):
         if sub is None:
             kernels(ev)
         else:
             # interface rows first, NCCL halo on a side stream overlapping the
             # interior (distributed.assemble_step)
-            sub.assemble_step(vel, rhs, mats, 1.0, 1e-2, overlap=True, side=side)
+            sub.assemble_step(vel, rhs, mats, 1.0, 1e-2, overlap=True, side=side, events=phases)
 
     for _ in range(args.warmup):
         step()
@@ -530,7 +705,34 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
-    if sub is not None:  # per-kernel times of this rank's slab, outside the timed region
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = total_elems / (ms_per_step / 1e3) / 1e6
+
+    phases = None
+    if sub is not None:
+        # per-phase times of the overlapped step (separate, untimed steps) and
+        # this rank's kernels without windows or halo
+        acc = {"interface_ms": [], "halo_ms": [], "interior_ms": [], "step_ms": []}
+        for _ in range(5):
+            flush.fill_(1.0)
+            dist.barrier()
+            ph: dict = {}
+            step(None, ph)
+            torch.cuda.synchronize()
+            acc["interface_ms"].append(ph["start"].elapsed_time(ph["interface_done"]))
+            acc["halo_ms"].append(ph["halo_start"].elapsed_time(ph["halo_done"]))
+            acc["interior_ms"].append(ph["interface_done"].elapsed_time(ph["interior_done"]))
+            acc["step_ms"].append(ph["start"].elapsed_time(ph["interior_done"]))
+        loc = torch.tensor([statistics.median(v) for v in acc.values()], dtype=torch.float64, device=dev)
+        dist.all_reduce(loc, op=dist.ReduceOp.MAX)
+        phases = dict(zip(acc.keys(), loc.tolist()))
+        phases["note"] = ("max over ranks of each phase's median: interface windows first, halo (NCCL send/recv "
+                          "of interface RHS rows + CSR row segments) on a side stream, interior meanwhile")
         for _ in range(5):
             flush.fill_(1.0)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -538,39 +740,24 @@ def main():
             torch.cuda.synchronize()
             k_mom.append(ev[0].elapsed_time(ev[1]))
             k_grad.append(ev[1].elapsed_time(ev[2]))
-    total_ms = sum(step_ms)
-    if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    total_elems = nelem * world
-    value = total_elems / (ms_per_step / 1e3) / 1e6
 
     # roofline of the dominant kernel (mean launch duration on its stream)
     kern = {"momentum_rhs": statistics.mean(k_mom), "gradient_xyz": statistics.mean(k_grad)}
     dom = max(kern, key=kern.get)
     F, B = WORK[dom]
-    t_s = kern[dom] / 1e3
-    flops_rate = F * nelem / t_s / 1e12
-    bytes_rate = B * nelem / t_s / 1e9
     hbm, hbm_src = hbm_peak()
-    if F / B > FP64_PEAK_TFLOPS * 1e3 / hbm:  # compute-bound by the ridge point
-        roof = {"bound": "fp64", "achieved": flops_rate, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": flops_rate / FP64_PEAK_TFLOPS,
-                "peak_source": "measured DFMA microbenchmark (profiles/r01_microbench.txt)"}
-    else:
-        roof = {"bound": "hbm", "achieved": bytes_rate, "peak": hbm, "unit": "GB/s",
-                "frac": bytes_rate / hbm, "peak_source": hbm_src}
+    roof = _roof(F, B, kern[dom], nelem, hbm)
+    roof["peak_source"] = ("measured DFMA microbenchmark (profiles/r01_microbench.txt)" if roof["bound"] == "fp64"
+                           else hbm_src)
     traffic, ncu = None, None
     try:  # measured DRAM bytes per launch of this kernel (ncu --set full, profiles/traffic.json)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            entry = json.load(fh)[dom]
+            entry = json.load(fh)[f"c5_{dom}"]
         traffic, ncu = entry["bytes"], entry.get("ncu")
     except Exception:
         traffic = None
-    roof.update({"kernel": dom, "traffic": traffic, "traffic_unit": "bytes per launch",
-                 "algorithmic_bytes": B * nelem,
+    roof.update({"kernel": dom, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
+                 "algorithmic_bytes": B * nelem, "elements_per_launch": nelem,
                  "work_per_element": {"flops": F, "bytes": B, "source": "SURVEY.md 8(d)"}})
     if ncu:
         roof["ncu"] = ncu  # pipe / L1 utilisation of the same kernel (profiles/traffic.json source)
@@ -578,88 +765,94 @@ def main():
         roof["note"] = ("achieved = SURVEY 8(d)'s reference-algorithm flops per element / kernel time; the "
                         "closed-form kernel executes fewer FP64 operations than that count, so the algorithmic "
                         "rate can exceed the FP64 peak — the executed FP64 pipe utilisation is roofline.ncu")
+    step_roof = _step_roofline(kern, WORK, nelem, statistics.mean(k_mom) + statistics.mean(k_grad), hbm)
+    step_roof["achieved_Gelem_s_step"] = total_elems / (ms_per_step * 1e6) / world
 
-    # the whole step against its own roofline: per element, SURVEY 8(d)'s
-    # work of each kernel at the binding one of its two roofs, summed
-    def _kernel_ns(k):
-        Fk, Bk = WORK[k]
-        return max(Fk / (FP64_PEAK_TFLOPS * 1e3), Bk / hbm)  # ns per element
-    bound_ns = sum(_kernel_ns(k) for k in kern)
-    step_roof = {"bound_Gelem_s": 1.0 / bound_ns, "achieved_Gelem_s": nelem / (ms_per_step * 1e6),
-                 "frac": (nelem / (ms_per_step * 1e6)) * bound_ns,
-                 "per_kernel_bound": {k: ("fp64" if WORK[k][0] / (FP64_PEAK_TFLOPS * 1e3) > WORK[k][1] / hbm
-                                          else "hbm") for k in kern},
-                 "note": "time-sum of each kernel's roofline bound (momentum FP64, B_xyz HBM) per element"}
-
-    # e2e through the public API with host buffers
+    # e2e through the public API with host buffers (H2D of the velocity,
+    # D2H of the RHS and the three matrices, every step)
     e2e = None
     if args.e2e_steps > 0:
-        grads = None
         e2e_ms = []
-        e2e_warm = 3  # pinned staging blocks are allocated once, then recycled
-        for i in range(args.e2e_steps + e2e_warm):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel_h, None, 1.0, 1e-2, 0.0)
-            grads = P.gradient_matrices(ctx)
-            vals = [B.vals for B in grads]
-            torch.cuda.synchronize()
-            if i >= e2e_warm:
-                e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        assert r.shape == (nnode, 3) and all(v.shape == (nnz,) for v in vals)
+        warm = 2  # pinned staging blocks are allocated once, then recycled
+        if sub is None:
+            nbytes_out = 0
+            for i in range(args.e2e_steps + warm):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel_h, None, 1.0, 1e-2, 0.0)
+                vals = [Bk.vals for Bk in P.gradient_matrices(ctx)]
+                torch.cuda.synchronize()
+                if i >= warm:
+                    e2e_ms.append((time.perf_counter() - t0) * 1e3)
+                assert r.shape == (nnode, 3) and all(v.shape == (nnz,) for v in vals)
+                nbytes_out = r.nbytes + sum(v.nbytes for v in vals)
+                del r, vals
+            api = "AssemblyContext.assemble_rhs(MOMENTUM_RHS, numpy) + gradient_matrices(ctx) + .vals"
+        else:
+            rhs_h = torch.empty((nnode, 3), dtype=torch.float64, pin_memory=True)
+            mats_h = torch.empty(3 * nnz, dtype=torch.float64, pin_memory=True)
+            vel_pin = torch.from_numpy(vel_h)
+            for i in range(args.e2e_steps + warm):
+                dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                vel.copy_(vel_pin, non_blocking=True)
+                sub.assemble_step(vel, rhs, mats, 1.0, 1e-2, overlap=True, side=side)
+                rhs_h.copy_(rhs, non_blocking=True)
+                mats_h.copy_(mats, non_blocking=True)
+                torch.cuda.synchronize()
+                if i >= warm:
+                    e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            nbytes_out = rhs_h.numel() * 8 + mats_h.numel() * 8
+            api = "SlabDomain.assemble_step with pinned host velocity in, RHS + 3 matrices to pinned host out"
         t = statistics.mean(e2e_ms)
         if dist:
             tt = torch.tensor([t], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = float(tt.item())
         e2e = {"value": total_elems / (t / 1e3) / 1e6, "unit": UNIT, "ms_per_step": t,
-               "h2d_bytes_per_step": int(vel_h.nbytes),
-               "d2h_bytes_per_step": int(r.nbytes + sum(v.nbytes for v in vals)),
-               "api": "AssemblyContext.assemble_rhs(MOMENTUM_RHS, numpy) + gradient_matrices(ctx) + .vals"}
+               "h2d_bytes_per_step": int(vel_h.nbytes) * world, "d2h_bytes_per_step": int(nbytes_out) * world,
+               "api": api, "input": "pinned host memory (numpy view)"}
 
     dist_solver = None
     if world > 1 and not args.no_solver:
+        del mats
+        torch.cuda.empty_cache()
         dist_solver = dist_bicgstab_block(sub, vel, dev, dist)
 
     solver = None
-    if rank == 0 and world == 1 and not args.no_solver:
-        # config 3 companions: SpMV on the MASS matrix, axpy / dot on vectors
-        # larger than L2 (C5's node count), Jacobi-PCG on the pinned LAPLACIAN
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        from solver_bench import solver_metrics
-
-        solver = solver_metrics(ctx, 16_974_593, hbm=hbm)
-
     configs = None
-    if rank == 0 and world == 1 and not args.no_configs:
-        configs = {"c3": config3_block(ctx, vel, flush, hbm)}
+    cpu = None
+    if rank == 0 and world == 1:
         del mats
         torch.cuda.empty_cache()
-        configs["c4"] = config4_block(flush, hbm)
+        if not args.no_solver:
+            solver = solver_block(ctx, flush, hbm)
+        del ctx, mesh
         torch.cuda.empty_cache()
-        configs["c5_one_gpu"] = config5_block(flush, hbm)
-        configs["flow"] = flow_block(args.nx, args.ny, args.nz)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_baseline(args.nx, args.ny, args.cpu_nz)
-        except Exception as exc:  # reported, not fatal
-            cpu = {"error": repr(exc)}
+        if not args.no_configs:
+            configs = config2_block(flush, hbm)
+            torch.cuda.empty_cache()
+            configs["c4"] = config4_block(flush, hbm, cpu=not args.no_cpu_baseline, e2e=True)
+            torch.cuda.empty_cache()
+            configs["flow"] = flow_block(*C2)
+        if not args.no_cpu_baseline:
+            try:
+                cpu = cpu_run("TET04", nx, ny, nz, args.cpu_kz, ("momentum", "gradients"), 8, 1, total_elems)
+            except Exception as exc:  # reported, not fatal
+                cpu = {"error": repr(exc)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config 2: TET04 box {args.nx}x{args.ny}x{args.nz} per GPU "
-                                   f"({nelem} elements, {nnode} nodes, nnz {nnz}), NS momentum RHS + "
-                                   "continuity B_x,B_y,B_z, SIMD-packed (32-lane) layout",
-                       "elements_per_step": total_elems, "l2": "flushed (512 MiB write) between steps", "scatter": args.scatter,
-                       "parallelism": f"z-slab domain decomposition x{world}" if world > 1 else "single GPU"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, world),
+            "setup_s": setup_s,
             "roofline": roof,
             "step_roofline": step_roof,
             "kernels_ms": kern,
+            "phases": phases,
             # per step: element-block momentum RHS (integrate + partial
             # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
             # launches (ncu launch list under profiles/); the halo (N > 1) is NCCL

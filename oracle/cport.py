@@ -25,42 +25,78 @@ def lib():
     return _lib
 
 
-def _p(a):
-    return C.c_void_p(a.ctypes.data)
+def _p(a, offset_items=0):
+    return C.c_void_p(a.ctypes.data + offset_items * a.itemsize)
 
 
 class PackedGroup:
     """Reference packed state of one element group at pack width vs, with
-    cached geometry (the reference's refresh_geometry, assembly.py:121-142)."""
+    cached geometry (the reference's refresh_geometry, assembly.py:121-142).
 
-    def __init__(self, etype, conn, coords, vs=8, nthreads=1):
+    cache_geometry=False keeps only the packs and recomputes geometry chunk
+    by chunk inside every kernel call (`chunk` packs at a time) — the same
+    arithmetic as the cached path (geometry_packed per pack, bit for bit),
+    for meshes whose cached gradN would not fit in host memory (config 4's
+    20 M hexes: 31 GB at vs = 8)."""
+
+    def __init__(self, etype, conn, coords, vs=8, nthreads=1, cache_geometry=True, chunk=1 << 14):
         self.etype, self.vs, self.nthreads = etype, vs, nthreads
         self.N, self.dN, self.w = O.reference_element(etype)
         self.nn, self.ng, self.dim = self.N.shape[0], self.N.shape[1], self.dN.shape[0]
         self.nelem = conn.shape[0]
+        self.coords = np.ascontiguousarray(coords)
         self.lane_conn, self.elem_index = O.build_packs(conn.astype(np.int64), vs)
         self.npacks = self.lane_conn.shape[0]
-        self.detjw = np.zeros((self.npacks, self.ng, vs))
-        self.gradn = np.zeros((self.npacks, self.dim, self.nn, self.ng, vs))
+        self.cached = cache_geometry
+        self.chunk = self.npacks if cache_geometry else min(chunk, self.npacks)
+        self.detjw = np.zeros((self.chunk, self.ng, vs))
+        self.gradn = np.zeros((self.chunk, self.dim, self.nn, self.ng, vs))
+        if cache_geometry:
+            self._geometry(0, self.npacks)
+
+    def _geometry(self, p0, p1):
         bad_g = C.c_int(-1)
         bad = lib().orc_geometry(
-            C.c_int64(self.npacks), self.nn, self.ng, self.dim, vs, C.c_int64(self.nelem),
-            _p(self.lane_conn), _p(np.ascontiguousarray(coords)), _p(self.dN), _p(self.w),
-            _p(self.detjw), _p(self.gradn), C.byref(bad_g), nthreads)
+            C.c_int64(p1 - p0), self.nn, self.ng, self.dim, self.vs, C.c_int64(self.nelem - p0 * self.vs),
+            _p(self.lane_conn, p0 * self.nn * self.vs), _p(self.coords), _p(self.dN), _p(self.w),
+            _p(self.detjw), _p(self.gradn), C.byref(bad_g), self.nthreads)
         if bad >= 0:
-            raise ArithmeticError(f"inverted element {bad} gauss {bad_g.value}")
+            raise ArithmeticError(f"inverted element {p0 * self.vs + bad} gauss {bad_g.value}")
+
+    def _chunks(self):
+        """(first pack, pack count) per kernel call; geometry refreshed per chunk."""
+        if self.cached:
+            yield 0, self.npacks
+            return
+        for p0 in range(0, self.npacks, self.chunk):
+            p1 = min(p0 + self.chunk, self.npacks)
+            self._geometry(p0, p1)
+            yield p0, p1 - p0
 
     def momentum_rhs(self, vel, rho, mu, rhs):
-        lib().orc_momentum_rhs(C.c_int64(self.npacks), self.nn, self.ng, self.dim, self.vs,
-                               _p(self.lane_conn), _p(self.N), _p(self.detjw), _p(self.gradn),
-                               _p(np.ascontiguousarray(vel)), C.c_double(rho), C.c_double(mu),
-                               _p(rhs), self.nthreads)
+        vel = np.ascontiguousarray(vel)
+        for p0, np_ in self._chunks():
+            lib().orc_momentum_rhs(C.c_int64(np_), self.nn, self.ng, self.dim, self.vs,
+                                   _p(self.lane_conn, p0 * self.nn * self.vs), _p(self.N), _p(self.detjw),
+                                   _p(self.gradn), _p(vel), C.c_double(rho), C.c_double(mu), _p(rhs),
+                                   self.nthreads)
+        return rhs
+
+    def scalar_rhs(self, vel, phi, kappa, rhs):
+        vel, phi = np.ascontiguousarray(vel), np.ascontiguousarray(phi)
+        for p0, np_ in self._chunks():
+            lib().orc_scalar_rhs(C.c_int64(np_), self.nn, self.ng, self.dim, self.vs,
+                                 _p(self.lane_conn, p0 * self.nn * self.vs), _p(self.N), _p(self.detjw),
+                                 _p(self.gradn), _p(vel), _p(phi), C.c_double(kappa), _p(rhs), self.nthreads)
         return rhs
 
     def convection(self, vel, pos_packed, vals):
-        lib().orc_convection(C.c_int64(self.npacks), self.nn, self.ng, self.dim, self.vs,
-                             _p(self.lane_conn), _p(self.N), _p(self.detjw), _p(self.gradn),
-                             _p(np.ascontiguousarray(vel)), _p(pos_packed), _p(vals), self.nthreads)
+        vel = np.ascontiguousarray(vel)
+        for p0, np_ in self._chunks():
+            lib().orc_convection(C.c_int64(np_), self.nn, self.ng, self.dim, self.vs,
+                                 _p(self.lane_conn, p0 * self.nn * self.vs), _p(self.N), _p(self.detjw),
+                                 _p(self.gradn), _p(vel), _p(pos_packed, p0 * self.nn * self.nn * self.vs),
+                                 _p(vals), self.nthreads)
         return vals
 
 

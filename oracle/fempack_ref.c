@@ -217,6 +217,54 @@ void orc_convection(int64_t npacks, int nn, int ng, int dim, int vs, const int64
   }
 }
 
+/* scalar_rhs_packed (_kernels.py:420-461) + scatter_vector_packed
+ * (_kernels.py:492-498). */
+void orc_scalar_rhs(int64_t npacks, int nn, int ng, int dim, int vs, const int64_t* lane_conn,
+                    const double* N, const double* detjw, const double* gradn, const double* vel,
+                    const double* phi, double kappa, double* rhs, int nthreads) {
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+  for (int64_t p = 0; p < npacks; ++p) {
+    double ue[MAXNN][3][MAXVS], fe[MAXNN][MAXVS], ug[3][MAXVS], gphi[3][MAXVS];
+    double adv[MAXVS], diff[MAXVS], out[MAXNN][MAXVS];
+    const int64_t* lc = lane_conn + p * nn * vs;
+    const double* dj = detjw + p * ng * vs;
+    const double* gr = gradn + p * dim * nn * ng * vs;
+    memset(out, 0, sizeof(out));
+    for (int a = 0; a < nn; ++a)
+      for (int v = 0; v < vs; ++v) {
+        int64_t node = lc[a * vs + v];
+        fe[a][v] = phi[node];
+        for (int d = 0; d < dim; ++d) ue[a][d][v] = vel[node * dim + d];
+      }
+    for (int ig = 0; ig < ng; ++ig) {
+      for (int d = 0; d < dim; ++d) {
+        for (int v = 0; v < vs; ++v) { ug[d][v] = 0.0; gphi[d][v] = 0.0; }
+        for (int a = 0; a < nn; ++a)
+          for (int v = 0; v < vs; ++v) {
+            ug[d][v] += ue[a][d][v] * N[a * ng + ig];
+            gphi[d][v] += fe[a][v] * gr[((d * nn + a) * ng + ig) * vs + v];
+          }
+      }
+      for (int v = 0; v < vs; ++v) adv[v] = 0.0;
+      for (int d = 0; d < dim; ++d)
+        for (int v = 0; v < vs; ++v) adv[v] += ug[d][v] * gphi[d][v];
+      for (int i = 0; i < nn; ++i) {
+        for (int v = 0; v < vs; ++v) diff[v] = 0.0;
+        for (int d = 0; d < dim; ++d)
+          for (int v = 0; v < vs; ++v) diff[v] += gphi[d][v] * gr[((d * nn + i) * ng + ig) * vs + v];
+        for (int v = 0; v < vs; ++v)
+          out[i][v] -= dj[ig * vs + v] * (N[i * ng + ig] * adv[v] + kappa * diff[v]);
+      }
+    }
+    for (int i = 0; i < nn; ++i)
+      for (int v = 0; v < vs; ++v) {
+        int64_t node = lc[i * vs + v];
+        if (nthreads > 1) atomic_add(&rhs[node], out[i][v]);
+        else rhs[node] += out[i][v];
+      }
+  }
+}
+
 /* _spmv (sparse.py:78-84) */
 void orc_spmv(int64_t n, const int64_t* rowptr, const int64_t* colind, const double* vals,
               const double* x, double* y, int nthreads) {

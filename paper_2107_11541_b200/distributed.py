@@ -223,8 +223,9 @@ class SlabDomain:
         return halo_sum_rows(self.layout, self.ctx.pattern.rowptr_d, vals, nmat, self.ctx.pattern.nnz,
                              self.group, self.segs)
 
-    def assemble_step(self, vel, rhs, mats, rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side=None):
-        return assemble_step(self, vel, rhs, mats, rho, mu, overlap, side)
+    def assemble_step(self, vel, rhs, mats, rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side=None,
+                      events: dict | None = None):
+        return assemble_step(self, vel, rhs, mats, rho, mu, overlap, side, events)
 
 
 # --------------------------------------------------------------------------
@@ -431,13 +432,16 @@ def _step_windows(dom: "SlabDomain") -> dict:
 
 
 def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats: torch.Tensor,
-                  rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side: torch.cuda.Stream | None = None):
+                  rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side: torch.cuda.Stream | None = None,
+                  events: dict | None = None):
     """One decomposed NS step: momentum RHS into rhs[n][dim] and B_x, B_y, B_z
     into mats[3 nnz], interface rows summed across ranks.  overlap = True runs
     the interface windows first and the halo exchange on `side` while the
     interior is assembled; False is the plain sequence (reference for
     tests).  Results are bitwise identical either way (owner-writes kernels,
-    fixed per-row / per-node summation order)."""
+    fixed per-row / per-node summation order).  events (optional dict) gets
+    CUDA events "start", "interface_done", "halo_start", "halo_done" and
+    "interior_done" for per-phase times (overlap=True only)."""
     from .assembly import KernelKind
 
     ctx = dom.ctx
@@ -450,6 +454,12 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
         return rhs, mats
     w = _step_windows(dom)
     none = (0, 0)
+    ev = None
+    if events is not None:
+        ev = {k: torch.cuda.Event(enable_timing=True)
+              for k in ("start", "interface_done", "halo_start", "halo_done", "interior_done")}
+        events.update(ev)
+        ev["start"].record()
     # phase A: everything an interface row depends on
     for b in w["blocks_A"]:
         if b[1] > b[0]:
@@ -461,16 +471,24 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
             ctx.assemble_gradients_d(mats, {"rows": r})
     # halo on the side stream, overlapping phase B
     main = torch.cuda.current_stream()
+    if ev:
+        ev["interface_done"].record(main)
     side = side or torch.cuda.Stream()
     side.wait_stream(main)
     with torch.cuda.stream(side):
+        if ev:
+            ev["halo_start"].record(side)
         dom.halo_sum_rhs(rhs)
         dom.halo_sum_matrix(mats, dom.ctx.mesh.dim)
+        if ev:
+            ev["halo_done"].record(side)
     # phase B: interior
     ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": w["blocks_B"], "nodes": none})
     for nd in w["nodes_B"]:
         ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": none, "nodes": nd})
     if w["rows_B"][1] > w["rows_B"][0]:
         ctx.assemble_gradients_d(mats, {"rows": w["rows_B"]})
+    if ev:
+        ev["interior_done"].record(main)
     main.wait_stream(side)
     return rhs, mats

@@ -151,6 +151,17 @@ def test_c_port_bitwise_vs_reference():
         pos = O.packed_positions(O.matrix_positions(conn, rowptr, colind), pg.elem_index)
         vals = pg.convection(g["bench_vel"], np.ascontiguousarray(pos), np.zeros(colind.size))
         assert vals.tobytes() == g["mat_convection"].tobytes(), name
+        for s in range(3):
+            rs = pg.scalar_rhs(g["bench_vel"], g[f"bench_scalar{s}"], 1e-2, np.zeros(m.nnode))
+            assert rs.tobytes() == g[f"rhs_scalar{s}"].tobytes(), (name, s)
+        # geometry recomputed chunk by chunk (the config-4/5 scale path): same bits
+        pc = cport.PackedGroup(et, conn, m.coords, vs=8, nthreads=1, cache_geometry=False, chunk=7)
+        rc = pc.momentum_rhs(g["bench_vel"], 1.0, 1e-2, np.zeros((m.nnode, 3)))
+        assert rc.tobytes() == g["rhs_momentum"].tobytes(), name
+        vc = pc.convection(g["bench_vel"], np.ascontiguousarray(pos), np.zeros(colind.size))
+        assert vc.tobytes() == g["mat_convection"].tobytes(), name
+        sc = pc.scalar_rhs(g["bench_vel"], g["bench_scalar0"], 1e-2, np.zeros(m.nnode))
+        assert sc.tobytes() == g["rhs_scalar0"].tobytes(), name
         y = cport.spmv(rowptr, colind, O.assemble_matrix(m, "mass")[2], g["spmv_x"])
         assert y.tobytes() == g["spmv_y"].tobytes()
         # threaded run: same values up to summation order
