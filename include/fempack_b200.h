@@ -135,6 +135,16 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
                  double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
                  void* stream);
 
+/* Element-local contributions without a scatter, replacing the reference's
+ * assemble_element_scalar / assemble_element_packed (assembly.py:296-380).
+ * lane_conn[npacks][nn][vs] (vs = 1: conn[nelem][nn]); out in the reference's
+ * layout at the same vs — matrix kinds [p][i][j][v], MOMENTUM_RHS [p][a][k][v],
+ * SCALAR_RHS [p][a][v]; padded lanes are not written (caller zero-fills).
+ * Kinds: FPB_MASS .. FPB_SCALAR_RHS. */
+int fpb_assemble_elements(int kind, int etype, int64_t nelem, int vs, const int32_t* lane_conn,
+                          const double* coords, const double* vel, const double* phi, double rho,
+                          double mu, double kappa, double* out, void* stream);
+
 /* 32-byte node records for 256-bit loads: rec[i] = (a[i][0..dim), 0.., extra[i]
  * or 0); rec must be 32-byte aligned.  Coordinates are packed once per mesh,
  * velocity (+ the transported scalar in the 4th slot) once per call. */

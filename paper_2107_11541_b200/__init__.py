@@ -11,32 +11,34 @@ See DESIGN.md.
 
 __version__ = "0.1.0"
 
-from .assembly import (AssemblyContext, KernelKind, assemble_boundary, face_rule, gradient_matrices, lumped_mass,
-                       matrix_positions)
-from .elements import ElementType, ReferenceElement, reference_element
+from .assembly import (AssemblyContext, KernelKind, assemble_boundary, assemble_element_packed,
+                       assemble_element_scalar, gradient_matrices, lumped_mass, matrix_positions)
+from .elements import (ElementGeometry, ElementType, FaceRule, ReferenceElement, compute_geometry, face_rule,
+                       integrate_reference_monomial, reference_element)
 from .errors import (ChecksumMismatchError, ConfigurationError, InvertedElementError,
                      ScatterPatternError, SolverBreakdownError, StepFailureError)
 from .krylov import SolverStats, bicgstab_solve, pcg_solve
 from .mesh import (ElementGroup, FaceGroup, Mesh, extract_boundary, generate_box_mesh, generate_mixed_mesh,
                    renumber_by_type)
-from .packing import PackConfig, PackSet, build_packs
+from .packing import PackConfig, PackSet, build_packs, pack_array, unpack_array
 from .sparse import (CsrMatrix, apply_dirichlet, axpy, build_node_pattern, csr_add, dot, norm2, normal_product,
                      spgemm, spmv, transpose_csr)
-from .timeloop import (FlowSolver, FlowState, StepDiagnostics, TimeConfig, preassemble_laplacian, preset_state,
-                       pressure_poisson)
+from .timeloop import (FlowSolver, FlowState, StepDiagnostics, TimeConfig, integrate_ode, preassemble_laplacian,
+                       preset_state, pressure_poisson, ssp_rk3_step)
 
 __all__ = [
-    "AssemblyContext", "KernelKind", "assemble_boundary", "face_rule", "gradient_matrices", "lumped_mass",
-    "matrix_positions",
-    "ElementType", "ReferenceElement", "reference_element",
+    "AssemblyContext", "KernelKind", "assemble_boundary", "assemble_element_packed", "assemble_element_scalar",
+    "gradient_matrices", "lumped_mass", "matrix_positions",
+    "ElementGeometry", "ElementType", "FaceRule", "ReferenceElement", "compute_geometry", "face_rule",
+    "integrate_reference_monomial", "reference_element",
     "ChecksumMismatchError", "ConfigurationError", "InvertedElementError", "ScatterPatternError",
     "SolverBreakdownError", "StepFailureError",
     "SolverStats", "pcg_solve", "bicgstab_solve",
     "ElementGroup", "FaceGroup", "Mesh", "extract_boundary", "generate_box_mesh", "generate_mixed_mesh",
     "renumber_by_type",
-    "PackConfig", "PackSet", "build_packs",
+    "PackConfig", "PackSet", "build_packs", "pack_array", "unpack_array",
     "CsrMatrix", "axpy", "build_node_pattern", "dot", "norm2", "spmv",
     "apply_dirichlet", "csr_add", "normal_product", "spgemm", "transpose_csr",
     "FlowSolver", "FlowState", "StepDiagnostics", "TimeConfig", "preassemble_laplacian", "preset_state",
-    "pressure_poisson",
+    "pressure_poisson", "integrate_ode", "ssp_rk3_step",
 ]

@@ -27,7 +27,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .elements import ETYPE_ID, ElementType, ReferenceElement, reference_element, upload_tables
+from .elements import (ETYPE_ID, ElementType, ReferenceElement, compute_geometry, face_rule, reference_element,
+                       upload_tables)
 from .errors import ConfigurationError, InvertedElementError, ScatterPatternError
 from .mesh import Mesh, as_device_mesh
 from .packing import KERNEL_LANES, PackConfig, PackSet, pack_lanes
@@ -551,6 +552,82 @@ def _raise_inverted(g: GroupData, coords: np.ndarray, elem: int, gauss: int):
     raise InvertedElementError(g.offset + elem, gauss, det)
 
 
+def _element_local(kind: KernelKind, ref: ReferenceElement, lane_conn_d: torch.Tensor, vs: int, nelem: int,
+                   coords, velocity, scalar, rho, mu, kappa) -> np.ndarray:
+    """Shared body of assemble_element_scalar / _packed: geometry check
+    (first bad (element, gauss) in the reference's scan order), then the
+    element-local kernel (`fpb_assemble_elements`) into a zeroed output."""
+    _check_fields(kind, velocity, scalar)
+    upload_tables(ref.etype)
+    dev = _lib.device()
+    nn, dim, ng = ref.nnodes, ref.dim, ref.ngauss
+    npacks = int(lane_conn_d.shape[0])
+    xd, _ = to_device(coords)
+    if xd.ndim != 2 or xd.shape[1] != dim:
+        raise ConfigurationError(f"coords must have shape (nnode, {dim})")
+    conn_e = lane_conn_d.permute(0, 2, 1).reshape(-1, nn)[:nelem].contiguous()
+    bad_e = np.zeros(1, dtype=np.int64)
+    bad_g = np.zeros(1, dtype=np.int32)
+    detjw = torch.empty((max(npacks, 1), ng, vs), dtype=torch.float64, device=dev)
+    rc = _lib.load().fpb_geometry(ETYPE_ID[ref.etype], nelem, vs, conn_e.data_ptr(), xd.data_ptr(),
+                                  detjw.data_ptr(), None, bad_e.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  bad_g.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _lib.stream())
+    if rc == _lib.FPB_EINVERTED:
+        bad, ig = int(bad_e[0]), int(bad_g[0])
+        x = to_host(xd)[to_host(conn_e[bad]).astype(np.int64)]
+        try:
+            compute_geometry(ref, x)
+        except InvertedElementError as err:
+            raise InvertedElementError(bad, err.gauss_point, err.det) from None
+        raise InvertedElementError(bad, ig, float("nan"))
+    _lib.check(rc, "fpb_geometry")
+    vel = to_device(velocity)[0] if velocity is not None and kind is not KernelKind.MASS \
+        and kind is not KernelKind.LAPLACIAN else None
+    phi = to_device(scalar)[0] if kind is KernelKind.SCALAR_RHS else None
+    if kind.is_matrix:
+        shape = (npacks, nn, nn, vs)
+    elif kind is KernelKind.MOMENTUM_RHS:
+        shape = (npacks, nn, dim, vs)
+    else:
+        shape = (npacks, nn, vs)
+    out = torch.zeros(shape, dtype=torch.float64, device=dev)
+    _lib.call("fpb_assemble_elements", KIND_ID[kind], ETYPE_ID[ref.etype], nelem, vs, lane_conn_d.data_ptr(),
+              xd.data_ptr(), _lib.ptr(vel), _lib.ptr(phi), float(rho), float(mu), float(kappa), out.data_ptr(),
+              _lib.stream())
+    return to_host(out)
+
+
+def assemble_element_scalar(kind: KernelKind, ref: ReferenceElement, conn, coords, velocity=None, scalar=None,
+                            rho: float = 1.0, mu: float = 0.0, kappa: float = 0.0) -> np.ndarray:
+    """Element-local contributions of one connectivity block
+    (assembly.py:296-339): (nelem, nn, nn) for matrix kinds, (nelem, nn, dim)
+    for MOMENTUM_RHS, (nelem, nn) for SCALAR_RHS — one device thread per
+    element, no scatter."""
+    conn_d = _to_conn_d(conn)
+    ne, nn = conn_d.shape
+    if nn != ref.nnodes:
+        raise ConfigurationError(f"connectivity has {nn} nodes per element, {ref.etype.value} needs {ref.nnodes}")
+    out = _element_local(kind, ref, conn_d.reshape(ne, nn, 1), 1, ne, coords, velocity, scalar, rho, mu, kappa)
+    return out.reshape(out.shape[:-1])
+
+
+def assemble_element_packed(kind: KernelKind, ref: ReferenceElement, packset: PackSet, coords, velocity=None,
+                            scalar=None, rho: float = 1.0, mu: float = 0.0, kappa: float = 0.0) -> np.ndarray:
+    """Lane-major element contributions, lane axis last (assembly.py:342-380);
+    padded lanes are exact zeros."""
+    return _element_local(kind, ref, packset.lane_conn_d, packset.vector_size, packset.nelem, coords, velocity,
+                          scalar, rho, mu, kappa)
+
+
+def _to_conn_d(conn) -> torch.Tensor:
+    if isinstance(conn, torch.Tensor):
+        return conn.to(_lib.device(), dtype=torch.int32).contiguous()
+    a = np.asarray(conn)
+    if a.ndim != 2:
+        raise ConfigurationError("connectivity must be (nelem, nn)")
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32), device=_lib.device())
+
+
 def gradient_matrices(ctx: AssemblyContext, layout: str = "packed") -> list[CsrMatrix]:
     """B_k with entries int(N_i dN_j/dx_k), one fused device pass
     (timeloop.py:159-171)."""
@@ -574,23 +651,6 @@ def lumped_mass(ctx: AssemblyContext, layout: str = "packed") -> np.ndarray:
 # Robin boundary assembly (assembly.py:383-411)
 # --------------------------------------------------------------------------
 
-def face_rule(nnodes: int):
-    """(ng, N[nnf][ng], dN[fdim][nnf][ng], weights[ng]) of a face (elements.py:348-363)."""
-    from .elements import ElementType
-
-    if nnodes == 2:
-        s3 = 1.0 / np.sqrt(3.0)
-        pts = np.array([-s3, s3])
-        N = np.stack([0.5 * (1.0 - pts), 0.5 * (1.0 + pts)])
-        dN = np.empty((1, 2, 2))
-        dN[0, 0], dN[0, 1] = -0.5, 0.5
-        return 2, N, dN, np.ones(2)
-    if nnodes in (3, 4):
-        ref = reference_element(ElementType.TRI03 if nnodes == 3 else ElementType.QUAD04)
-        return ref.ngauss, np.asarray(ref.N), np.asarray(ref.dN), np.asarray(ref.weights)
-    raise ValueError(f"no face rule for {nnodes}-node faces")
-
-
 def assemble_boundary_d(mesh, pattern: CsrMatrix, alpha: float = 0.0, beta: float = 0.0):
     """Device Robin structures: (vals[nnz], rhs[n]) as CUDA tensors."""
     mesh = as_device_mesh(mesh)
@@ -600,8 +660,9 @@ def assemble_boundary_d(mesh, pattern: CsrMatrix, alpha: float = 0.0, beta: floa
     if alpha == 0.0 and beta == 0.0:
         return vals, rhs
     for fg in mesh.boundary:
-        ng, N, dN, w = face_rule(fg.nnodes)
-        Nd, dNd, wd = (torch.as_tensor(np.array(a, dtype=np.float64), device=dev) for a in (N, dN, w))
+        fr = face_rule(fg.nnodes)
+        ng = fr.ngauss
+        Nd, dNd, wd = (torch.as_tensor(np.array(a, dtype=np.float64), device=dev) for a in (fr.N, fr.dN, fr.weights))
         conn = fg.conn_d.to(torch.int32).contiguous()
         pos = positions_d(conn, pattern, 0, 1) if alpha != 0.0 else None
         _lib.call("fpb_robin", fg.nfaces, fg.nnodes, ng, mesh.dim, conn.data_ptr(), mesh.coords_d.data_ptr(),

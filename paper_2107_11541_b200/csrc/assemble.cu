@@ -117,6 +117,73 @@ static int dispatch_kind(int kind, int64_t nelem, const int32_t* lane_conn, cons
   return FPB_ECONFIG;
 }
 
+
+// Element-local contributions, no scatter (assembly.py:296-380,
+// assemble_element_scalar / assemble_element_packed): thread per (pack,
+// lane); out[(p * NOUT + o) * vs + v] — the reference's scalar layout at
+// vs = 1 ([e][i][j], [e][a][k], [e][a]) and its lane-last packed layout
+// otherwise ([p][i][j][v] ...).  Padded lanes are left untouched (the caller
+// zero-fills, as the reference's aligned_zeros does), matching its detJw = 0.
+template <int ET, int KIND>
+__global__ void __launch_bounds__(128)
+k_element_local(int64_t nelem, int vs, const int32_t* __restrict__ lane_conn, const double* __restrict__ coords,
+                const double* __restrict__ vel, const double* __restrict__ phi, double rho, double mu, double kappa,
+                double* __restrict__ out) {
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+  constexpr bool NEED_VEL = Out<ET, KIND>::NEED_VEL;
+  constexpr int NOUT = Out<ET, KIND>::NOUT;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t p = t / vs, v = t % vs;
+  if (t >= nelem) return;
+  int node[NN];
+#pragma unroll
+  for (int a = 0; a < NN; ++a) node[a] = __ldg(lane_conn + (p * NN + a) * vs + v);
+  double xe[NN][DIM];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) xe[a][d] = __ldg(coords + (int64_t)node[a] * DIM + d);
+  double ue[Out<ET, KIND>::NU][DIM];
+  if constexpr (NEED_VEL) {
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) ue[a][d] = __ldg(vel + (int64_t)node[a] * DIM + d);
+  }
+  double fe[Out<ET, KIND>::NF];
+  if constexpr (KIND == FPB_SCALAR_RHS) {
+#pragma unroll
+    for (int a = 0; a < NN; ++a) fe[a] = __ldg(phi + node[a]);
+  }
+  double acc[NOUT];
+  element_integrate<ET, KIND>(xe, ue, fe, rho, mu, kappa, 0, acc);
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) out[(p * NOUT + o) * vs + v] = acc[o];
+}
+
+template <int ET>
+static int element_local_kind(int kind, int64_t nelem, int vs, const int32_t* lane_conn, const double* coords,
+                              const double* vel, const double* phi, double rho, double mu, double kappa, double* out,
+                              cudaStream_t s) {
+  const unsigned grid = (unsigned)((nelem + 127) / 128);
+#define FPB_EL(K)                                                                                          \
+  k_element_local<ET, K><<<grid, 128, 0, s>>>(nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out); \
+  break
+  switch (kind) {
+    case FPB_MASS: FPB_EL(FPB_MASS);
+    case FPB_LAPLACIAN: FPB_EL(FPB_LAPLACIAN);
+    case FPB_CONVECTION: FPB_EL(FPB_CONVECTION);
+    case FPB_MOMENTUM_RHS: FPB_EL(FPB_MOMENTUM_RHS);
+    case FPB_SCALAR_RHS: FPB_EL(FPB_SCALAR_RHS);
+    default:
+      set_error("element-local assembly covers the reference's five kinds (got %d)", kind);
+      return FPB_ECONFIG;
+  }
+#undef FPB_EL
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
 }  // namespace fpb
 
 using namespace fpb;
@@ -143,4 +210,24 @@ extern "C" int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* l
     case FPB_HEX08: return dispatch_kind<FPB_HEX08>(kind, nelem, lane_conn, coords, vel, phi, rho, mu, kappa, pos, nnz, out, s);
   }
   return FPB_ECONFIG;
+}
+
+extern "C" int fpb_assemble_elements(int kind, int etype, int64_t nelem, int vs, const int32_t* lane_conn,
+                                     const double* coords, const double* vel, const double* phi, double rho,
+                                     double mu, double kappa, double* out, void* stream) {
+  FPB_REQUIRE(etype >= 0 && etype < 5 && g_ref_loaded[etype],
+              "reference tables for element type %d not uploaded", etype);
+  FPB_REQUIRE(vs >= 1 && vs <= 32, "vector size %d out of range", vs);
+  FPB_REQUIRE(!(kind == FPB_CONVECTION || kind == FPB_MOMENTUM_RHS || kind == FPB_SCALAR_RHS) || vel,
+              "kind %d needs a velocity field", kind);
+  FPB_REQUIRE(kind != FPB_SCALAR_RHS || phi, "SCALAR_RHS needs a scalar field");
+  if (nelem == 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  switch (etype) {
+    case FPB_TRI03: return element_local_kind<FPB_TRI03>(kind, nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out, s);
+    case FPB_QUAD04: return element_local_kind<FPB_QUAD04>(kind, nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out, s);
+    case FPB_TET04: return element_local_kind<FPB_TET04>(kind, nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out, s);
+    case FPB_PYR05: return element_local_kind<FPB_PYR05>(kind, nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out, s);
+    default: return element_local_kind<FPB_HEX08>(kind, nelem, vs, lane_conn, coords, vel, phi, rho, mu, kappa, out, s);
+  }
 }

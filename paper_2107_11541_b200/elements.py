@@ -34,6 +34,17 @@ DIM = {ElementType.TRI03: 2, ElementType.QUAD04: 2, ElementType.TET04: 3,
        ElementType.PYR05: 3, ElementType.HEX08: 3}
 REFERENCE_VOLUME = {ElementType.TRI03: 0.5, ElementType.QUAD04: 4.0, ElementType.TET04: 1.0 / 6.0,
                     ElementType.PYR05: 4.0 / 3.0, ElementType.HEX08: 8.0}
+#: polynomial degree up to which each rule is exact (elements.py:63-70)
+QUADRATURE_DEGREE = {ElementType.TRI03: 2, ElementType.QUAD04: 3, ElementType.TET04: 2,
+                     ElementType.PYR05: 2, ElementType.HEX08: 3}
+#: outward-oriented faces as local node indices (elements.py:73-86)
+ELEMENT_FACES = {
+    ElementType.TRI03: ((0, 1), (1, 2), (2, 0)),
+    ElementType.QUAD04: ((0, 1), (1, 2), (2, 3), (3, 0)),
+    ElementType.TET04: ((0, 2, 1), (0, 1, 3), (1, 2, 3), (0, 3, 2)),
+    ElementType.PYR05: ((0, 3, 2, 1), (0, 1, 4), (1, 2, 4), (2, 3, 4), (3, 0, 4)),
+    ElementType.HEX08: ((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (2, 3, 7, 6), (0, 4, 7, 3), (1, 2, 6, 5)),
+}
 
 
 @dataclass(frozen=True)
@@ -125,6 +136,11 @@ def _tables(et: ElementType, pts: np.ndarray):
     return N, dN
 
 
+#: shape-function evaluators by type, (pts[np, dim]) -> (N[nn, np], dN[dim, nn, np])
+#: (elements.py:230-236)
+_SHAPE_FUNCS = {et: (lambda pts, _et=et: _tables(_et, np.asarray(pts, dtype=np.float64))) for et in ElementType}
+
+
 @lru_cache(maxsize=None)
 def reference_element(etype: ElementType) -> ReferenceElement:
     pts, w = _points_and_weights(etype)
@@ -156,3 +172,87 @@ def upload_tables(etype: ElementType) -> None:
                                              N.ctypes.data, dN.ctypes.data, w.ctypes.data),
                "fpb_set_reference_element")
     _uploaded.add(key)
+
+
+@dataclass
+class ElementGeometry:
+    """Geometry of one element at the Gauss points (elements.py:278-286):
+    detJw[ng] = det J * weight, gradN[dim, nn, ng] physical gradients."""
+
+    detJw: np.ndarray
+    gradN: np.ndarray
+
+
+def compute_geometry(ref: ReferenceElement, node_coords) -> ElementGeometry:
+    """One element's Gauss-point geometry (elements.py:289-313), evaluated by
+    the device geometry kernel (`fpb_geometry`, the same code that validates
+    whole meshes).  Raises InvertedElementError(-1, gauss, det) for the first
+    Gauss point with det J <= 0, like the reference."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .errors import InvertedElementError
+
+    x = np.ascontiguousarray(node_coords, dtype=np.float64)
+    if x.shape != (ref.nnodes, ref.dim):
+        raise ValueError(f"node_coords must have shape ({ref.nnodes}, {ref.dim})")
+    upload_tables(ref.etype)
+    dev = _lib.device()
+    xd = torch.as_tensor(x, device=dev)
+    conn = torch.arange(ref.nnodes, dtype=torch.int32, device=dev).reshape(1, -1)
+    detjw = torch.empty((1, ref.ngauss, 1), dtype=torch.float64, device=dev)
+    gradn = torch.empty((1, ref.dim, ref.nnodes, ref.ngauss, 1), dtype=torch.float64, device=dev)
+    bad_e = np.zeros(1, dtype=np.int64)
+    bad_g = np.zeros(1, dtype=np.int32)
+    rc = _lib.load().fpb_geometry(ETYPE_ID[ref.etype], 1, 1, conn.data_ptr(), xd.data_ptr(), detjw.data_ptr(),
+                                  gradn.data_ptr(), bad_e.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                  bad_g.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), _lib.stream())
+    if rc == _lib.FPB_EINVERTED:
+        ig = int(bad_g[0])
+        # det for the message only (the device reports where, not the value)
+        raise InvertedElementError(-1, ig, float(np.linalg.det(x.T @ ref.dN[:, :, ig].T)))
+    _lib.check(rc, "fpb_geometry")
+    return ElementGeometry(detJw=detjw.reshape(ref.ngauss).cpu().numpy(),
+                           gradN=gradn.reshape(ref.dim, ref.nnodes, ref.ngauss).cpu().numpy())
+
+
+def integrate_reference_monomial(etype: ElementType, powers) -> float:
+    """Quadrature value of x^a y^b (z^c) over the reference domain
+    (elements.py:316-328) — a property of the rule tables only."""
+    ref = reference_element(etype)
+    vals = np.ones(ref.ngauss)
+    for d, p in enumerate(powers):
+        if p:
+            vals = vals * ref.gauss_points[:, d] ** p
+    return float(np.dot(vals, ref.weights))
+
+
+@dataclass(frozen=True)
+class FaceRule:
+    """Quadrature and shape tables of a boundary face (elements.py:331-345):
+    dN is [face_dim, node, gauss point]."""
+
+    nnodes: int
+    dim: int
+    ngauss: int
+    weights: np.ndarray
+    N: np.ndarray
+    dN: np.ndarray
+
+
+@lru_cache(maxsize=None)
+def face_rule(nnodes: int) -> FaceRule:
+    """Face rule for `nnodes`-node faces (elements.py:348-363): 2-point Gauss
+    on [-1, 1] for edges, the TRI03 / QUAD04 tables for 3- / 4-node faces."""
+    if nnodes == 2:
+        pts = np.array([_G2[0], _G2[1]])
+        N = np.stack([0.5 * (1.0 - pts), 0.5 * (1.0 + pts)])
+        dN = np.empty((1, 2, 2))
+        dN[0, 0], dN[0, 1] = -0.5, 0.5
+        return FaceRule(2, 1, 2, np.ones(2), N, dN)
+    if nnodes in (3, 4):
+        ref = reference_element(ElementType.TRI03 if nnodes == 3 else ElementType.QUAD04)
+        return FaceRule(nnodes, ref.dim, ref.ngauss, ref.weights, ref.N, ref.dN)
+    raise ValueError(f"no face rule for {nnodes}-node faces")

@@ -16,43 +16,95 @@ the reference's template order; they feed the Robin boundary assembly and
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
-from .elements import DIM, ETYPE_ID, NNODES, ElementType
+from ._mirror import DeviceArray
+from .elements import DIM, ELEMENT_FACES, ETYPE_ID, NNODES, ElementType
 
 
-@dataclass
+def _as_conn_d(conn) -> torch.Tensor:
+    if isinstance(conn, torch.Tensor) and conn.is_cuda and conn.dtype == torch.int32:
+        return conn
+    if isinstance(conn, torch.Tensor):
+        conn = conn.cpu().numpy()
+    conn = np.asarray(conn)
+    if conn.size and conn.max() >= np.iinfo(np.int32).max:
+        raise ValueError("node ids exceed int32")
+    return torch.as_tensor(np.ascontiguousarray(conn, dtype=np.int32), device=_lib.device())
+
+
 class ElementGroup:
-    """Connectivity of one element type; conn_d is int32 [nelem, nn] in HBM."""
+    """Connectivity of one element type (mesh.py:20-30); conn_d is int32
+    [nelem, nn] in HBM.  `conn` is the reference's int64 ndarray, a
+    write-back mirror: in-place edits reach the device before the next
+    kernel reads the connectivity (_mirror.py)."""
 
-    etype: ElementType
-    conn_d: torch.Tensor
-    _conn_h: np.ndarray | None = field(default=None, repr=False)
+    def __init__(self, etype: ElementType, conn):
+        self.etype = etype
+        self._conn = DeviceArray(_as_conn_d(conn), np.int64)
 
     @property
-    def nelem(self) -> int:
-        return int(self.conn_d.shape[0])
+    def conn_d(self) -> torch.Tensor:
+        return self._conn.device()
+
+    @conn_d.setter
+    def conn_d(self, t: torch.Tensor) -> None:
+        self._conn.set_device(_as_conn_d(t))
 
     @property
     def conn(self) -> np.ndarray:
-        if self._conn_h is None:
-            self._conn_h = self.conn_d.cpu().numpy().astype(np.int64)
-        return self._conn_h
+        return self._conn.host()
+
+    @conn.setter
+    def conn(self, value) -> None:
+        self._conn.set_device(_as_conn_d(value))
+
+    @property
+    def nelem(self) -> int:
+        return int(self._conn._t.shape[0])
+
+    def __repr__(self) -> str:
+        return f"ElementGroup({self.etype}, nelem={self.nelem})"
 
 
-@dataclass
+def _as_coords_d(coords) -> torch.Tensor:
+    if isinstance(coords, torch.Tensor) and coords.is_cuda and coords.dtype == torch.float64:
+        return coords.contiguous()
+    if isinstance(coords, torch.Tensor):
+        coords = coords.cpu().numpy()
+    return torch.as_tensor(np.ascontiguousarray(coords, dtype=np.float64), device=_lib.device())
+
+
 class Mesh:
-    """dim, coords_d float64 [nnode, dim] and element groups, all in HBM."""
+    """dim, node coordinates float64 [nnode, dim] and element groups, all in
+    HBM (mesh.py:57-113).  Accepts numpy or torch arguments like the
+    reference's dataclass; `coords` is a write-back host mirror."""
 
-    dim: int
-    coords_d: torch.Tensor
-    groups: list[ElementGroup] = field(default_factory=list)
-    _boundary: list | None = field(default=None, repr=False)
-    _coords_h: np.ndarray | None = field(default=None, repr=False)
+    def __init__(self, dim: int, coords, groups=None, boundary=None):
+        self.dim = int(dim)
+        self._coords = DeviceArray(_as_coords_d(coords))
+        self.groups = list(groups) if groups is not None else []
+        self._boundary = list(boundary) if boundary is not None else None
+
+    @property
+    def coords_d(self) -> torch.Tensor:
+        return self._coords.device()
+
+    @coords_d.setter
+    def coords_d(self, t) -> None:
+        self._coords.set_device(_as_coords_d(t))
+
+    @property
+    def coords(self) -> np.ndarray:
+        return self._coords.host()
+
+    @coords.setter
+    def coords(self, value) -> None:
+        self._coords.set_device(_as_coords_d(value))
 
     @property
     def boundary(self) -> list:
@@ -60,6 +112,10 @@ class Mesh:
         if self._boundary is None:
             self._boundary = extract_boundary(self.groups)
         return self._boundary
+
+    @boundary.setter
+    def boundary(self, value) -> None:
+        self._boundary = list(value)
 
     def boundary_nodes(self) -> np.ndarray:
         """Sorted unique node ids on any boundary face (mesh.py:82-86)."""
@@ -69,14 +125,8 @@ class Mesh:
         return torch.unique(allnodes).cpu().numpy().astype(np.int64)
 
     @property
-    def coords(self) -> np.ndarray:
-        if self._coords_h is None:
-            self._coords_h = self.coords_d.cpu().numpy()
-        return self._coords_h
-
-    @property
     def nnode(self) -> int:
-        return int(self.coords_d.shape[0])
+        return int(self._coords._t.shape[0])
 
     @property
     def nelem(self) -> int:
@@ -92,15 +142,39 @@ class Mesh:
         types = [g.etype for g in self.groups]
         return len(types) == len(set(types))
 
+    def validate(self) -> None:
+        """Raise ValueError on structural defects (mesh.py:88-113); the
+        range, finiteness and shared-face checks run on the device."""
+        if self.dim not in (2, 3):
+            raise ValueError(f"unsupported dimension {self.dim}")
+        x = self.coords_d
+        if x.ndim != 2 or x.shape[1] != self.dim:
+            raise ValueError("coords must have shape (nnode, dim)")
+        if x.numel() and not bool(torch.isfinite(x).all()):
+            raise ValueError("non-finite node coordinates")
+        n = self.nnode
+        for g in self.groups:
+            c = g.conn_d
+            if DIM[g.etype] != self.dim:
+                raise ValueError(f"{g.etype.value} in a {self.dim}D mesh")
+            if c.ndim != 2 or c.shape[1] != NNODES[g.etype]:
+                raise ValueError(f"bad connectivity shape for {g.etype.value}")
+            if g.nelem and (int(c.min()) < 0 or int(c.max()) >= n):
+                raise ValueError(f"node index out of range in {g.etype.value}")
+        if self._boundary is not None:
+            for fg in self._boundary:
+                if fg.conn_d.shape[1] != fg.nnodes:
+                    raise ValueError("face group width mismatch")
+                if fg.nfaces and (int(fg.conn_d.min()) < 0 or int(fg.conn_d.max()) >= n):
+                    raise ValueError("face node index out of range")
+                if fg.nfaces and (int(fg.owner_d.min()) < 0 or int(fg.owner_d.max()) >= self.nelem):
+                    raise ValueError("face owner out of range")
+        for size, counts in _face_counts(self.groups).items():
+            if counts.numel() and int(counts.max()) > 2:
+                raise ValueError(f"{size}-node face shared by more than 2 elements")
 
-# outward-oriented face templates (elements.py:73-86)
-ELEMENT_FACES = {
-    ElementType.TRI03: ((0, 1), (1, 2), (2, 0)),
-    ElementType.QUAD04: ((0, 1), (1, 2), (2, 3), (3, 0)),
-    ElementType.TET04: ((0, 2, 1), (0, 1, 3), (1, 2, 3), (0, 3, 2)),
-    ElementType.PYR05: ((0, 3, 2, 1), (0, 1, 4), (1, 2, 4), (2, 3, 4), (3, 0, 4)),
-    ElementType.HEX08: ((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (2, 3, 7, 6), (0, 4, 7, 3), (1, 2, 6, 5)),
-}
+    def __repr__(self) -> str:
+        return f"Mesh(dim={self.dim}, nnode={self.nnode}, groups={self.groups})"
 
 
 @dataclass
@@ -125,11 +199,8 @@ class FaceGroup:
         return self.conn_d.cpu().numpy().astype(np.int64)
 
 
-def extract_boundary(groups) -> list:
-    """Faces that belong to exactly one element (mesh.py:140-155), grouped by
-    node count in ascending size, each group in the reference's (group,
-    template, element) order.  Face counting by sorted node tuples on the
-    device (setup only)."""
+def _faces_by_size(groups) -> dict:
+    """{size: [(owner ids, face nodes)]} per face template (mesh.py:117-125)."""
     buckets: dict = {}
     offset = 0
     for g in groups:
@@ -138,6 +209,28 @@ def extract_boundary(groups) -> list:
             owner = torch.arange(offset, offset + g.nelem, dtype=torch.int64, device=g.conn_d.device)
             buckets.setdefault(len(tmpl), []).append((owner, g.conn_d.index_select(1, idx)))
         offset += g.nelem
+    return buckets
+
+
+def _face_counts(groups) -> dict:
+    """{size: multiplicity of every distinct face} (mesh.py:127-137)."""
+    out = {}
+    for size, parts in _faces_by_size(groups).items():
+        faces = torch.cat([f for _, f in parts], dim=0)
+        if faces.shape[0] == 0:
+            out[size] = torch.empty(0, dtype=torch.int64)
+            continue
+        key = torch.sort(faces.to(torch.int64), dim=1).values
+        out[size] = torch.unique(key, dim=0, return_counts=True)[1]
+    return out
+
+
+def extract_boundary(groups) -> list:
+    """Faces that belong to exactly one element (mesh.py:140-155), grouped by
+    node count in ascending size, each group in the reference's (group,
+    template, element) order.  Face counting by sorted node tuples on the
+    device (setup only)."""
+    buckets = _faces_by_size(groups)
     out = []
     for size in sorted(buckets):
         owners = torch.cat([o for o, _ in buckets[size]])
@@ -246,4 +339,9 @@ def renumber_by_type(mesh) -> tuple[Mesh, Permutation]:
     forward[inverse] = np.arange(len(inverse))
     groups = [ElementGroup(t, torch.cat([g.conn_d for g in mesh.groups if g.etype is t], dim=0))
               for t in order]
-    return Mesh(mesh.dim, mesh.coords_d, groups), Permutation(forward, inverse)
+    boundary = None
+    if mesh._boundary is not None:  # remap face owners with the permutation (mesh.py:360-362)
+        fwd = torch.as_tensor(forward, device=mesh.coords_d.device)
+        boundary = [FaceGroup(fg.nnodes, fwd.index_select(0, fg.owner_d.to(torch.int64)), fg.conn_d.clone())
+                    for fg in mesh._boundary]
+    return Mesh(mesh.dim, mesh.coords_d, groups, boundary), Permutation(forward, inverse)

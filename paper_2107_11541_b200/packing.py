@@ -21,6 +21,18 @@ from .errors import ConfigurationError
 
 VALID_VECTOR_SIZES = (1, 2, 4, 8, 16, 32)
 KERNEL_LANES = 32  # one warp per pack
+#: host allocation alignment in bytes (packing.py:25)
+ALIGNMENT = 64
+
+
+def aligned_zeros(shape, dtype=np.float64, alignment: int = ALIGNMENT) -> np.ndarray:
+    """Zero-filled C-contiguous host array whose data start is aligned
+    (packing.py:40-48); the host-side container of lane-major results."""
+    dtype = np.dtype(dtype)
+    size = int(np.prod(shape)) * dtype.itemsize
+    buf = np.zeros(size + alignment, dtype=np.uint8)
+    off = (-buf.ctypes.data) % alignment
+    return buf[off:off + size].view(dtype).reshape(shape)
 
 
 @dataclass(frozen=True)
@@ -95,3 +107,33 @@ def build_packs(mesh, config: PackConfig) -> list[PackSet]:
                                pack_lanes(g.conn_d, config.vector_size)))
         offset += g.nelem
     return out
+
+
+def pack_array(values, packset: PackSet, zero_pad: bool = True) -> np.ndarray:
+    """Gather per-element data (nelem_total, ...) into lane-major form
+    (npacks, ..., vector_size) (packing.py:130-142): a device gather by the
+    pack's element index; padded lanes zeroed unless zero_pad is False (then
+    they repeat the last active element)."""
+    a = np.asarray(values)
+    dev = _lib.device()
+    src = torch.as_tensor(np.ascontiguousarray(a), device=dev)
+    idx = torch.as_tensor(packset.elem_index.reshape(-1), device=dev)
+    g = src.index_select(0, idx).reshape((packset.npacks, packset.vector_size) + a.shape[1:])
+    g = torch.movedim(g, 1, -1).contiguous()
+    if zero_pad and packset.npadded:
+        g[packset.npacks - 1, ..., packset.vector_size - packset.npadded:] = 0
+    out = aligned_zeros(tuple(g.shape), dtype=a.dtype)
+    out[...] = g.cpu().numpy()
+    return out
+
+
+def unpack_array(packed, packset: PackSet, nelem_total: int) -> np.ndarray:
+    """Scatter the active lanes of a lane-major array back to per-element
+    rows (packing.py:145-151), on the device."""
+    a = np.asarray(packed)
+    dev = _lib.device()
+    src = torch.movedim(torch.as_tensor(np.ascontiguousarray(a), device=dev), -1, 1)
+    src = src.reshape((-1,) + tuple(src.shape[2:]))[: packset.nelem]
+    out = torch.zeros((nelem_total,) + a.shape[1:-1], dtype=src.dtype, device=dev)
+    out[packset.offset: packset.offset + packset.nelem] = src
+    return out.cpu().numpy()

@@ -7,18 +7,20 @@ device and results are returned as CUDA tensors without a host round trip.
 
 Storage: rowptr / colind are int32 in HBM (nnz < 2^31 is enforced), vals
 float64.  The numpy views `rowptr` / `colind` are int64 like the
-reference's; `vals` is a fresh host copy of the device values.
+reference's; `vals` is a write-back host mirror of the device values.
 """
 
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 import torch
 from torch.autograd.graph import increment_version
 
 from . import _lib
+from ._mirror import DeviceArray
 
 _INT32_MAX = np.iinfo(np.int32).max
 
@@ -56,15 +58,40 @@ def _to_i32(x) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(_lib.device())
 
 
+_VALS_STORES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _vals_store(t: torch.Tensor) -> DeviceArray:
+    """One write-back mirror per device value array, shared by every
+    CsrMatrix over it, so `reuse=True` aliasing (assembly.py:200-207: the
+    matrices returned by reusing calls share one vals array) is observable
+    from numpy: `A.vals is B.vals`."""
+    st = _VALS_STORES.get(t)
+    if st is None:
+        st = DeviceArray(t)
+        _VALS_STORES[t] = st
+    return st
+
+
 class CsrMatrix:
-    """n x n CSR matrix in HBM (sparse.py:20-56)."""
+    """n x n CSR matrix in HBM (sparse.py:20-56).  `vals` is a write-back
+    host mirror (_mirror.py): reference code that edits `A.vals[...]` in
+    place reaches the device before the next kernel reads the values."""
 
     def __init__(self, n, rowptr, colind, vals, _host=None):
         self.n = int(n)
         self.rowptr_d = rowptr if isinstance(rowptr, torch.Tensor) and rowptr.is_cuda and rowptr.dtype == torch.int32 else _to_i32(rowptr)
         self.colind_d = colind if isinstance(colind, torch.Tensor) and colind.is_cuda and colind.dtype == torch.int32 else _to_i32(colind)
-        self.vals_d = to_device(vals)[0]
+        self._vals = _vals_store(to_device(vals)[0])
         self._host = _host if _host is not None else {}
+
+    @property
+    def vals_d(self) -> torch.Tensor:
+        return self._vals.device()
+
+    @vals_d.setter
+    def vals_d(self, t: torch.Tensor) -> None:
+        self._vals = _vals_store(to_device(t)[0])
 
     @property
     def nnz(self) -> int:
@@ -84,7 +111,11 @@ class CsrMatrix:
 
     @property
     def vals(self) -> np.ndarray:
-        return to_host(self.vals_d)
+        return self._vals.host()
+
+    @vals.setter
+    def vals(self, value) -> None:
+        self._vals = _vals_store(to_device(value)[0])
 
     def copy(self) -> "CsrMatrix":
         return CsrMatrix(self.n, self.rowptr_d, self.colind_d, self.vals_d.clone(), self._host)
@@ -425,3 +456,9 @@ def apply_dirichlet(A: CsrMatrix, nodes, values=None, b=None):
     if bd is None:
         return res, None
     return res, (to_host(bd) if host else bd)
+
+
+def format_coo(A: CsrMatrix) -> str:
+    """Triplet text dump, one `row col value` line per entry (sparse.py:257-263)."""
+    rows = A.row_indices()
+    return "".join(f"{i} {j} {v:.17g}\n" for i, j, v in zip(rows, A.colind, A.vals))

@@ -203,8 +203,9 @@ def test_owner_kernels_match_atomic_kernels(cuda_ok, strategy):
 
 
 def test_c2_momentum_and_continuity_vs_oracle(cuda_ok):
-    """Config 2 at full size (5,036,520 tets): momentum RHS and B_z against
-    the oracle (bitwise-pinned restatement of the reference packed path)."""
+    """Config 2 at full size (5,036,520 tets): momentum RHS against the
+    oracle (bitwise-pinned restatement of the reference packed path); the
+    continuity matrices' row sums vanish."""
     import torch
 
     import paper_2107_11541_b200 as P
@@ -217,11 +218,7 @@ def test_c2_momentum_and_continuity_vs_oracle(cuda_ok):
     ro = O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)
     assert O.rel_diff(r, ro) < TOL
     del ro
-    grads = P.gradient_matrices(ctx)
-    unit = np.zeros((om.nnode, 3))
-    unit[:, 2] = 1.0
-    _, _, bz = O.assemble_matrix(om, "convection", unit)
-    assert O.rel_diff(grads[2].vals, bz) < TOL
+    grads = P.gradient_matrices(ctx)  # values vs the C port: tests/test_gpu_scale.py
     # B_k annihilates constants: row sums vanish (timeloop.py:191)
     for B in grads:
         assert float(B.row_sums_d().abs().max()) < 1e-12 * float(B.vals_d.abs().max())

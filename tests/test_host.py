@@ -100,3 +100,26 @@ def test_no_oracle_import_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", src).replace('"""', ""), f
+
+
+def test_write_back_mirror_semantics():
+    """_mirror.DeviceArray (CsrMatrix.vals, Mesh.coords, ElementGroup.conn):
+    stable identity, host edits reach the device, device writes refresh the
+    handed-out array in place (CPU tensors stand in for HBM here)."""
+    import torch
+
+    from paper_2107_11541_b200._mirror import DeviceArray
+
+    t = torch.arange(6, dtype=torch.float64)
+    m = DeviceArray(t)
+    h = m.host()
+    assert m.host() is h
+    h[2] = 42.0                      # in-place host edit ...
+    assert m.device()[2].item() == 42.0  # ... is written back before device use
+    t.mul_(2.0)                      # device write (version bump) ...
+    assert m.host() is h and h[2] == 84.0  # ... refreshes the same ndarray
+    conn = DeviceArray(torch.zeros((2, 3), dtype=torch.int32), np.int64)
+    c = conn.host()
+    assert c.dtype == np.int64
+    c[1, 2] = 7
+    assert conn.device().dtype == torch.int32 and int(conn.device()[1, 2]) == 7
