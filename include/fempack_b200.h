@@ -135,6 +135,22 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
                  double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
                  void* stream);
 
+/* HEX08 continuity matrices B_x, B_y, B_z by node bricks (hexblock.cu):
+ * replaces the reference's 3 x CONVECTION(e_k) for gradient_matrices
+ * (timeloop.py:159-171, _kernels.py:238-266) with each element's geometry
+ * evaluated once per block.  Blocks of rows_per_block (64 | 128) rows:
+ * blk_rows[nblocks][R] (row id or -1), bloc[nblocks][maxinc][R] (uint16 local
+ * element index, 0xffff = none), bslot[nblocks][maxinc][R] (uint2 slot bytes,
+ * fpb_incidence_slots8 convention), blk_eptr[nblocks + 1] / blk_elems (the
+ * block's distinct elements).  out[k * nnz + j] = B_k (overwritten, or added
+ * when accumulate).  fpb_hex_blocks_smem gives the CTA's shared memory. */
+int64_t fpb_hex_blocks_smem(int rows_per_block, int emax, int rowcap);
+int fpb_assemble_hex_gradient_blocks(int nblocks, int rows_per_block, int maxinc, int rowcap, int emax,
+                                     const int32_t* blk_rows, const uint16_t* bloc, const uint32_t* bslot,
+                                     const int32_t* blk_eptr, const int32_t* blk_elems, const int32_t* conn,
+                                     const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
+                                     int accumulate, double* out, void* stream);
+
 /* Element-local contributions without a scatter, replacing the reference's
  * assemble_element_scalar / assemble_element_packed (assembly.py:296-380).
  * lane_conn[npacks][nn][vs] (vs = 1: conn[nelem][nn]); out in the reference's

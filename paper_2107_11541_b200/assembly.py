@@ -87,6 +87,8 @@ ROW_OWNED_GAUSS = ("QUAD04", "PYR05", "HEX08")  # Gauss-loop elements: row-owned
 # TET04 continuity matrices by column pairs (pairs.cu) instead of the
 # incidence-accumulating row kernel; module switch for A/B measurements
 GRADIENT_PAIRS = True
+# brick-blocked HEX08 continuity kernel (hexblock.cu); False = per-row rowsq.cu
+HEX_BRICKS = True
 
 
 class RowPlan:
@@ -154,6 +156,86 @@ class RowPlan:
         self.slots, self.rowcap = slots, int(cap[0])
 
 
+def _morton_order(coords_d: torch.Tensor) -> torch.Tensor:
+    """Node permutation in Morton (Z) order of the per-axis coordinate ranks:
+    consecutive nodes form spatially compact bricks on any mesh (on the box
+    meshes the ranks are exactly the (i, j, k) lattice indices)."""
+    n, dim = coords_d.shape
+    key = torch.zeros(n, dtype=torch.int64, device=coords_d.device)
+    ranks = [torch.unique(coords_d[:, d], return_inverse=True)[1].to(torch.int64) for d in range(dim)]
+    nbits = max(1, max(int(r.max()) for r in ranks).bit_length()) if n else 1
+    if nbits * dim > 62:
+        raise ConfigurationError("mesh too large for a 64-bit Morton key")
+    for bit in range(nbits):
+        for d in range(dim):
+            key |= ((ranks[d] >> bit) & 1) << (dim * bit + d)
+    return torch.argsort(key, stable=True)
+
+
+class HexBrickPlan:
+    """Row blocks for the brick-blocked HEX08 continuity kernel (hexblock.cu):
+    R Morton-consecutive rows per CTA, each block's distinct incident
+    elements, and per (block row, incidence) the local element index and the
+    row's slot bytes (RowPlan.slots, rowsq.cu convention).  Built on the
+    device once per mesh (setup)."""
+
+    def __init__(self, rows: RowPlan, coords_d: torch.Tensor, nelem: int, rowcap: int):
+        lib = _lib.load()
+        dev = coords_d.device
+        n = rows.n
+        self.ok = False
+        # incidences per row (dense [n, maxinc]) from the SELL-32 arrays
+        slc = torch.arange(n, device=dev, dtype=torch.int64)
+        sp = rows.slice_ptr.to(torch.int64)
+        m0 = sp[slc >> 5]
+        ln = sp[(slc >> 5) + 1] - m0
+        maxinc = int(ln.max()) if n else 0
+        j = torch.arange(maxinc, device=dev, dtype=torch.int64)
+        idx = (m0[:, None] + j[None, :]) * 32 + (slc & 31)[:, None]
+        valid = j[None, :] < ln[:, None]
+        idx = torch.where(valid, idx, torch.zeros_like(idx))
+        inc = rows.inc.to(torch.int64)[idx]
+        inc = torch.where(valid, inc, torch.full_like(inc, -1))
+        words = rows.slots.view(torch.int64)[idx]
+        for R in (128, 64):
+            nblocks = -(-n // R)
+            perm = _morton_order(coords_d)
+            blk_rows = torch.full((nblocks * R,), -1, dtype=torch.int64, device=dev)
+            blk_rows[:n] = perm
+            rowsafe = blk_rows.clamp(min=0)
+            e_bo = torch.where((blk_rows >= 0)[:, None], inc[rowsafe], torch.full_like(inc[rowsafe], -1))
+            w_bo = words[rowsafe]
+            bid = (torch.arange(nblocks * R, device=dev, dtype=torch.int64) // R)[:, None].expand_as(e_bo)
+            ok = e_bo >= 0
+            keys = bid[ok] * max(nelem, 1) + e_bo[ok]
+            uniq, inv = torch.unique(keys, sorted=True, return_inverse=True)
+            ublk = uniq // max(nelem, 1)
+            counts = torch.bincount(ublk, minlength=nblocks)
+            eptr = torch.zeros(nblocks + 1, dtype=torch.int64, device=dev)
+            eptr[1:] = torch.cumsum(counts, 0)
+            emax = int(counts.max()) if nblocks else 0
+            smem = int(lib.fpb_hex_blocks_smem(R, emax, rowcap))
+            if 0 <= smem <= 227 * 1024 and emax < 0xffff:
+                local = torch.full(e_bo.shape, -1, dtype=torch.int64, device=dev)
+                local[ok] = inv - eptr[bid[ok]]
+                # [nblocks][R][maxinc] -> [nblocks][maxinc][R]
+                self.bloc = local.view(nblocks, R, maxinc).permute(0, 2, 1).contiguous().to(torch.int16)
+                self.bslot = w_bo.view(nblocks, R, maxinc).permute(0, 2, 1).contiguous()
+                self.blk_rows = blk_rows.to(torch.int32)
+                self.blk_eptr = eptr.to(torch.int32)
+                self.blk_elems = (uniq % max(nelem, 1)).to(torch.int32)
+                self.R, self.nblocks, self.maxinc, self.emax, self.rowcap = R, nblocks, maxinc, emax, rowcap
+                self.smem = smem
+                self.ok = True
+                return
+
+    def run(self, conn_d, xyz4, pattern, accumulate: int, out: torch.Tensor) -> None:
+        _lib.call("fpb_assemble_hex_gradient_blocks", self.nblocks, self.R, self.maxinc, self.rowcap, self.emax,
+                  self.blk_rows.data_ptr(), self.bloc.data_ptr(), self.bslot.data_ptr(), self.blk_eptr.data_ptr(),
+                  self.blk_elems.data_ptr(), conn_d.data_ptr(), xyz4.data_ptr(), pattern.rowptr_d.data_ptr(),
+                  pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), _lib.stream())
+
+
 class BlockPlan:
     """Element blocks of one group for the deterministic two-phase RHS
     assembly (blocks.cu): per-block distinct nodes + sorted gather slots,
@@ -208,6 +290,7 @@ class GroupData:
     pattern: CsrMatrix
     rows: RowPlan | None = None
     blocks: BlockPlan | None = None
+    hexbricks: "HexBrickPlan | None | bool" = None  # built on first B_xyz use; False = not eligible
     _pos32: torch.Tensor | None = None
     _cache: dict = field(default_factory=dict)
 
@@ -406,6 +489,9 @@ class AssemblyContext:
                           bp.blk_lidx.data_ptr(), bp.maxnu,
                           bp.partial(nv, out.device).data_ptr(), n, n0, n1, bp.node_pptr.data_ptr(),
                           bp.node_plist.data_ptr(), 0 if single_rows else 1, out.data_ptr(), _lib.stream())
+            elif own and g.rows.gauss and kind_id == GRADIENT_XYZ and window is None and HEX_BRICKS \
+                    and g.etype_id == ETYPE_ID[ElementType.HEX08] and self._hexbricks(g) is not None:
+                g.hexbricks.run(g.conn_d, self.xyz4, self.pattern, 0 if single_rows else 1, out)
             elif own and g.rows.gauss:
                 r = g.rows
                 _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),
@@ -434,6 +520,12 @@ class AssemblyContext:
                           g.pos32.data_ptr() if matrix else None, nnz, out.data_ptr(), _lib.stream())
         mark_written(out)
         return out
+
+    def _hexbricks(self, g: GroupData):
+        if g.hexbricks is None:
+            plan = HexBrickPlan(g.rows, self.mesh.coords_d, g.nelem, g.rows.rowcap)
+            g.hexbricks = plan if plan.ok else False
+        return g.hexbricks or None
 
     def assemble_matrix_d(self, kind: KernelKind, velocity_d: torch.Tensor | None,
                           out: torch.Tensor) -> torch.Tensor:
