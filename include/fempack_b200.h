@@ -135,21 +135,27 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
                  double mu, double kappa, const int32_t* pos, int64_t nnz, double* out,
                  void* stream);
 
-/* HEX08 continuity matrices B_x, B_y, B_z by node bricks (hexblock.cu):
- * replaces the reference's 3 x CONVECTION(e_k) for gradient_matrices
- * (timeloop.py:159-171, _kernels.py:238-266) with each element's geometry
- * evaluated once per block.  Blocks of rows_per_block (64 | 128) rows:
- * blk_rows[nblocks][R] (row id or -1), bloc[nblocks][maxinc][R] (uint16 local
- * element index, 0xffff = none), bslot[nblocks][maxinc][R] (uint2 slot bytes,
- * fpb_incidence_slots8 convention), blk_eptr[nblocks + 1] / blk_elems (the
- * block's distinct elements).  out[k * nnz + j] = B_k (overwritten, or added
- * when accumulate).  fpb_hex_blocks_smem gives the CTA's shared memory. */
-int64_t fpb_hex_blocks_smem(int rows_per_block, int emax, int rowcap);
-int fpb_assemble_hex_gradient_blocks(int nblocks, int rows_per_block, int maxinc, int rowcap, int emax,
-                                     const int32_t* blk_rows, const uint16_t* bloc, const uint32_t* bslot,
-                                     const int32_t* blk_eptr, const int32_t* blk_elems, const int32_t* conn,
-                                     const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
-                                     int accumulate, double* out, void* stream);
+/* HEX08 continuity matrices B_x, B_y, B_z with each element's geometry
+ * evaluated once (hexblock.cu), replacing the reference's 3 x CONVECTION(e_k)
+ * of gradient_matrices (timeloop.py:159-171, _kernels.py:238-266).
+ * fpb_hex_gradient_h: H[72][nelem] (plane q = 24 k + 8 l + 4 s + U': the
+ *   Walsh-transformed adjugate columns, see hexblock.cu); conn[nelem][8]
+ *   16-byte aligned, xyz4 = fpb_pack4 records.
+ * fpb_hex_gradient_rows: out[k * nnz + j] = B_k (overwritten, or added when
+ *   accumulate) for the rows listed —
+ *   canonical rows (interior box pattern, fpb_hex_canon_slots[m][d] = CSR
+ *   offset of relative corner d of incidence m): canon_rows[ncanon],
+ *   canon_inc8[8][ncanon] element ids in incidence order;
+ *   generic rows in blocks of 32: gblk_rows[ngblocks][32] (row or -1),
+ *   ginc[ngblocks][maxinc][32] (element id or -1), gslot[ngblocks][maxinc][32]
+ *   (uint2 relative-corner slot bytes: byte 0 = corner sign bits p of the
+ *   row's node, byte d = off-diagonal slot of corner p ^ d). */
+int fpb_hex_canon_slots(int32_t* slots_h /* [8][8] */);
+int fpb_hex_gradient_h(int64_t nelem, const int32_t* conn, const double* xyz4, double* H, void* stream);
+int fpb_hex_gradient_rows(int32_t ncanon, const int32_t* canon_rows, const int32_t* canon_inc8, int32_t ngblocks,
+                          int maxinc, int rowcap, const int32_t* gblk_rows, const int32_t* ginc,
+                          const uint32_t* gslot, const double* H, int64_t nelem, const int32_t* rowptr,
+                          const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream);
 
 /* Element-local contributions without a scatter, replacing the reference's
  * assemble_element_scalar / assemble_element_packed (assembly.py:296-380).

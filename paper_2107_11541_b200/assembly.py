@@ -87,8 +87,9 @@ ROW_OWNED_GAUSS = ("QUAD04", "PYR05", "HEX08")  # Gauss-loop elements: row-owned
 # TET04 continuity matrices by column pairs (pairs.cu) instead of the
 # incidence-accumulating row kernel; module switch for A/B measurements
 GRADIENT_PAIRS = True
-# brick-blocked HEX08 continuity kernel (hexblock.cu); False = per-row rowsq.cu
-HEX_BRICKS = True
+# HEX08 continuity with element geometry evaluated once (hexblock.cu);
+# False = the per-row kernel (rowsq.cu)
+HEX_ONCE = True
 
 
 class RowPlan:
@@ -156,84 +157,85 @@ class RowPlan:
         self.slots, self.rowcap = slots, int(cap[0])
 
 
-def _morton_order(coords_d: torch.Tensor) -> torch.Tensor:
-    """Node permutation in Morton (Z) order of the per-axis coordinate ranks:
-    consecutive nodes form spatially compact bricks on any mesh (on the box
-    meshes the ranks are exactly the (i, j, k) lattice indices)."""
-    n, dim = coords_d.shape
-    key = torch.zeros(n, dtype=torch.int64, device=coords_d.device)
-    ranks = [torch.unique(coords_d[:, d], return_inverse=True)[1].to(torch.int64) for d in range(dim)]
-    nbits = max(1, max(int(r.max()) for r in ranks).bit_length()) if n else 1
-    if nbits * dim > 62:
-        raise ConfigurationError("mesh too large for a 64-bit Morton key")
-    for bit in range(nbits):
-        for d in range(dim):
-            key |= ((ranks[d] >> bit) & 1) << (dim * bit + d)
-    return torch.argsort(key, stable=True)
+class HexRowPlan:
+    """Row lists for the HEX08 continuity kernels (hexblock.cu): the element
+    pass writes each hex's 72-double H record once; the row pass reads them.
+    Rows whose incidences and slot bytes equal the interior box pattern
+    (hexblock.cu hb_canon_slot) go to the register kernel, with their 8
+    element ids; all other rows to the generic kernel, in blocks of 32 with
+    per-incidence element ids and relative-corner slot bytes (byte 0 = sign
+    bits p(a) of the row's own corner, byte d = off-diagonal slot of corner
+    p(a) ^ d).  Built on the device once per mesh (setup)."""
 
+    GEN_ROWS = 32
 
-class HexBrickPlan:
-    """Row blocks for the brick-blocked HEX08 continuity kernel (hexblock.cu):
-    R Morton-consecutive rows per CTA, each block's distinct incident
-    elements, and per (block row, incidence) the local element index and the
-    row's slot bytes (RowPlan.slots, rowsq.cu convention).  Built on the
-    device once per mesh (setup)."""
-
-    def __init__(self, rows: RowPlan, coords_d: torch.Tensor, nelem: int, rowcap: int):
+    def __init__(self, rows: RowPlan, nelem: int, rowcap: int):
         lib = _lib.load()
-        dev = coords_d.device
+        dev = rows.slice_ptr.device
         n = rows.n
-        self.ok = False
+        self.nelem, self.rowcap = nelem, rowcap
         # incidences per row (dense [n, maxinc]) from the SELL-32 arrays
         slc = torch.arange(n, device=dev, dtype=torch.int64)
         sp = rows.slice_ptr.to(torch.int64)
         m0 = sp[slc >> 5]
         ln = sp[(slc >> 5) + 1] - m0
         maxinc = int(ln.max()) if n else 0
+        self.maxinc = maxinc
         j = torch.arange(maxinc, device=dev, dtype=torch.int64)
         idx = (m0[:, None] + j[None, :]) * 32 + (slc & 31)[:, None]
         valid = j[None, :] < ln[:, None]
         idx = torch.where(valid, idx, torch.zeros_like(idx))
-        inc = rows.inc.to(torch.int64)[idx]
-        inc = torch.where(valid, inc, torch.full_like(inc, -1))
-        words = rows.slots.view(torch.int64)[idx]
-        for R in (128, 64):
-            nblocks = -(-n // R)
-            perm = _morton_order(coords_d)
-            blk_rows = torch.full((nblocks * R,), -1, dtype=torch.int64, device=dev)
-            blk_rows[:n] = perm
-            rowsafe = blk_rows.clamp(min=0)
-            e_bo = torch.where((blk_rows >= 0)[:, None], inc[rowsafe], torch.full_like(inc[rowsafe], -1))
-            w_bo = words[rowsafe]
-            bid = (torch.arange(nblocks * R, device=dev, dtype=torch.int64) // R)[:, None].expand_as(e_bo)
-            ok = e_bo >= 0
-            keys = bid[ok] * max(nelem, 1) + e_bo[ok]
-            uniq, inv = torch.unique(keys, sorted=True, return_inverse=True)
-            ublk = uniq // max(nelem, 1)
-            counts = torch.bincount(ublk, minlength=nblocks)
-            eptr = torch.zeros(nblocks + 1, dtype=torch.int64, device=dev)
-            eptr[1:] = torch.cumsum(counts, 0)
-            emax = int(counts.max()) if nblocks else 0
-            smem = int(lib.fpb_hex_blocks_smem(R, emax, rowcap))
-            if 0 <= smem <= 227 * 1024 and emax < 0xffff:
-                local = torch.full(e_bo.shape, -1, dtype=torch.int64, device=dev)
-                local[ok] = inv - eptr[bid[ok]]
-                # [nblocks][R][maxinc] -> [nblocks][maxinc][R]
-                self.bloc = local.view(nblocks, R, maxinc).permute(0, 2, 1).contiguous().to(torch.int16)
-                self.bslot = w_bo.view(nblocks, R, maxinc).permute(0, 2, 1).contiguous()
-                self.blk_rows = blk_rows.to(torch.int32)
-                self.blk_eptr = eptr.to(torch.int32)
-                self.blk_elems = (uniq % max(nelem, 1)).to(torch.int32)
-                self.R, self.nblocks, self.maxinc, self.emax, self.rowcap = R, nblocks, maxinc, emax, rowcap
-                self.smem = smem
-                self.ok = True
-                return
+        inc = torch.where(valid, rows.inc.to(torch.int64)[idx], torch.full_like(idx, -1))
+        by = rows.slots.view(torch.int64)[idx].view(torch.uint8).view(n, maxinc, 8).to(torch.int64)
+        a = torch.argmax((by == 0xff).to(torch.int64), dim=2)
+        pa = a ^ ((a >> 1) & 1)  # corner sign bits, elements.py corner order
+        rel = torch.empty_like(by)
+        rel[..., 0] = pa
+        for d in range(1, 8):
+            pb = pa ^ d
+            rel[..., d] = torch.gather(by, 2, (pb ^ ((pb >> 1) & 1)).unsqueeze(-1)).squeeze(-1)
+        words = rel.to(torch.uint8).view(torch.int64).view(n, maxinc)
+        canon = torch.zeros(n, dtype=torch.bool, device=dev)
+        if maxinc == 8 and os.environ.get("FPB_HEX_CANON", "1") != "0":
+            tab = np.zeros(64, dtype=np.int32)
+            _lib.check(lib.fpb_hex_canon_slots(tab.ctypes.data), "fpb_hex_canon_slots")
+            tab = tab.reshape(8, 8)
+            want = np.zeros((8, 8), dtype=np.uint8)
+            for m in range(8):
+                want[m, 0] = m ^ 7
+                for d in range(1, 8):
+                    want[m, d] = tab[m, d] - (tab[m, d] > 13)  # off-diagonal index (diagonal = 13)
+            want_w = torch.as_tensor(want.view(np.int64).reshape(8), device=dev)
+            canon = valid.all(dim=1) & (words == want_w[None, :]).all(dim=1)
+        # natural row order: a warp's lanes read consecutive elements' H (one
+        # 256-byte run per plane) and a CTA's rows are mostly one contiguous
+        # CSR range (Morton-brick order measured 1.7x slower, profiles/r02c_hex)
+        crow = torch.nonzero(canon).flatten()
+        self.ncanon = int(crow.numel())
+        self.canon_rows = crow.to(torch.int32).contiguous()
+        self.canon_inc8 = inc[crow].t().contiguous().to(torch.int32) if self.ncanon else \
+            torch.empty(8, dtype=torch.int32, device=dev)
+        grow = torch.nonzero(~canon).flatten()
+        R = self.GEN_ROWS
+        self.ngblocks = -(-int(grow.numel()) // R)
+        blk = torch.full((self.ngblocks * R,), -1, dtype=torch.int64, device=dev)
+        blk[: grow.numel()] = grow
+        safe = blk.clamp(min=0)
+        ginc = torch.where((blk >= 0)[:, None], inc[safe], torch.full_like(inc[safe], -1))
+        self.gblk_rows = blk.to(torch.int32).contiguous()
+        self.ginc = ginc.view(self.ngblocks, R, maxinc).permute(0, 2, 1).contiguous().to(torch.int32)
+        self.gslot = words[safe].view(self.ngblocks, R, maxinc).permute(0, 2, 1).contiguous()
+        self.H = None
 
     def run(self, conn_d, xyz4, pattern, accumulate: int, out: torch.Tensor) -> None:
-        _lib.call("fpb_assemble_hex_gradient_blocks", self.nblocks, self.R, self.maxinc, self.rowcap, self.emax,
-                  self.blk_rows.data_ptr(), self.bloc.data_ptr(), self.bslot.data_ptr(), self.blk_eptr.data_ptr(),
-                  self.blk_elems.data_ptr(), conn_d.data_ptr(), xyz4.data_ptr(), pattern.rowptr_d.data_ptr(),
-                  pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), _lib.stream())
+        if self.H is None:  # HBM scratch, 72 planes of nelem doubles (once per mesh)
+            self.H = torch.empty(max(self.nelem, 1) * 72, dtype=torch.float64, device=out.device)
+        s = _lib.stream()
+        _lib.call("fpb_hex_gradient_h", self.nelem, conn_d.data_ptr(), xyz4.data_ptr(), self.H.data_ptr(), s)
+        _lib.call("fpb_hex_gradient_rows", self.ncanon, self.canon_rows.data_ptr(), self.canon_inc8.data_ptr(),
+                  self.ngblocks, self.maxinc, self.rowcap, self.gblk_rows.data_ptr(), self.ginc.data_ptr(),
+                  self.gslot.data_ptr(), self.H.data_ptr(), self.nelem, pattern.rowptr_d.data_ptr(),
+                  pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), s)
 
 
 class BlockPlan:
@@ -290,7 +292,7 @@ class GroupData:
     pattern: CsrMatrix
     rows: RowPlan | None = None
     blocks: BlockPlan | None = None
-    hexbricks: "HexBrickPlan | None | bool" = None  # built on first B_xyz use; False = not eligible
+    hexrows: "HexRowPlan | None" = None  # built on first B_xyz use
     _pos32: torch.Tensor | None = None
     _cache: dict = field(default_factory=dict)
 
@@ -489,9 +491,9 @@ class AssemblyContext:
                           bp.blk_lidx.data_ptr(), bp.maxnu,
                           bp.partial(nv, out.device).data_ptr(), n, n0, n1, bp.node_pptr.data_ptr(),
                           bp.node_plist.data_ptr(), 0 if single_rows else 1, out.data_ptr(), _lib.stream())
-            elif own and g.rows.gauss and kind_id == GRADIENT_XYZ and window is None and HEX_BRICKS \
-                    and g.etype_id == ETYPE_ID[ElementType.HEX08] and self._hexbricks(g) is not None:
-                g.hexbricks.run(g.conn_d, self.xyz4, self.pattern, 0 if single_rows else 1, out)
+            elif own and g.rows.gauss and kind_id == GRADIENT_XYZ and window is None and HEX_ONCE \
+                    and g.etype_id == ETYPE_ID[ElementType.HEX08]:
+                self._hexrows(g).run(g.conn_d, self.xyz4, self.pattern, 0 if single_rows else 1, out)
             elif own and g.rows.gauss:
                 r = g.rows
                 _lib.call("fpb_assemble_rows_gl", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),
@@ -521,11 +523,10 @@ class AssemblyContext:
         mark_written(out)
         return out
 
-    def _hexbricks(self, g: GroupData):
-        if g.hexbricks is None:
-            plan = HexBrickPlan(g.rows, self.mesh.coords_d, g.nelem, g.rows.rowcap)
-            g.hexbricks = plan if plan.ok else False
-        return g.hexbricks or None
+    def _hexrows(self, g: GroupData) -> HexRowPlan:
+        if g.hexrows is None:
+            g.hexrows = HexRowPlan(g.rows, g.nelem, g.rows.rowcap)
+        return g.hexrows
 
     def assemble_matrix_d(self, kind: KernelKind, velocity_d: torch.Tensor | None,
                           out: torch.Tensor) -> torch.Tensor:

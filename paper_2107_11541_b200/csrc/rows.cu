@@ -42,6 +42,7 @@ constexpr int kRowsBlock = 128;
 #endif
 constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
 int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
+extern int g_tuning_hex_canon_rows;  // hexblock.cu
 
 
 template <int ET, int KIND>
@@ -826,6 +827,11 @@ extern "C" {
 int fpb_set_tuning(const char* name, int value) {
   if (name && strcmp(name, "rows_nb") == 0) {
     g_tuning_rows_nb = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "hex_canon_rows") == 0) {
+    FPB_REQUIRE(value == 32 || value == 64, "hex_canon_rows must be 32 or 64");
+    g_tuning_hex_canon_rows = value;
     return FPB_OK;
   }
   set_error("unknown tuning knob %s", name ? name : "(null)");

@@ -90,10 +90,10 @@ def test_rhs_on_distorted_mesh(case, kind):
 
 
 @pytest.mark.parametrize("dims", [(20, 17, 13), (9, 33, 5)])
-def test_hex_brick_gradients_match_row_kernel(cuda_ok, dims):
-    """hexblock.cu (element geometry once per Morton brick) against the
-    per-row kernel (rowsq.cu) and the oracle on a jittered HEX08 box whose
-    sides are not powers of two (irregular bricks); bitwise run-to-run."""
+def test_hex_once_gradients_match_row_kernel(cuda_ok, dims):
+    """hexblock.cu (element geometry once: element pass + canonical / generic
+    row passes) against the per-row kernel (rowsq.cu) and the oracle on a
+    jittered HEX08 box; bitwise run-to-run."""
     import paper_2107_11541_b200 as P
     from paper_2107_11541_b200 import assembly as A
 
@@ -106,16 +106,17 @@ def test_hex_brick_gradients_match_row_kernel(cuda_ok, dims):
     nnz = ctx.pattern.nnz
     brick = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
     ctx.assemble_gradients_d(brick)
-    assert ctx.groups[0].hexbricks, "brick plan not built"
+    plan = ctx.groups[0].hexrows
+    assert plan is not None and plan.ncanon > 0 and plan.ngblocks > 0, "both row kinds exercised"
     again = torch.empty_like(brick)
     ctx.assemble_gradients_d(again)
     assert torch.equal(brick, again)
-    A.HEX_BRICKS = False
+    A.HEX_ONCE = False
     try:
         rows = torch.empty_like(brick)
         ctx.assemble_gradients_d(rows)
     finally:
-        A.HEX_BRICKS = True
+        A.HEX_ONCE = True
     b, r = brick.cpu().numpy(), rows.cpu().numpy()
     assert O.rel_diff(b, r) < 1e-13
     for k in range(3):
