@@ -162,7 +162,7 @@ __host__ __device__ constexpr int hb_canon_slot(int m, int d) {
 }
 
 // ---- canonical rows: thread per (row, k), R rows per CTA ---------------------
-int g_tuning_hex_canon_rows = 64;  // fpb_set_tuning("hex_canon_rows", 32 | 64)
+int g_tuning_hex_canon_rows = 32;  // fpb_set_tuning("hex_canon_rows", 32 | 64)
 
 template <int R, bool ACC>
 __global__ void __launch_bounds__(3 * R, R == 32 ? 2 * FPB_HEXR_MINB : FPB_HEXR_MINB)
