@@ -518,18 +518,22 @@ def dist_bicgstab_block(sub, vel, dev, dist, iters=40):
     nglob = (L.nx + 1) * (L.ny + 1) * (L.nz + 1)
     b = torch.as_tensor(np.random.default_rng(1).standard_normal(nglob)[L.node_offset:L.node_offset + L.nnode],
                         device=dev)
-    bicgstab_slab(L, A, b, tol=0.0, max_iter=8, check_every=8)  # warm
+    ws: dict = {}
+    kw = dict(tol=0.0, max_iter=iters, check_every=8, native=sub.native, ws=ws)
+    bicgstab_slab(L, A, b, **kw)  # warm: with the compiled NCCL path, captures the 8-iteration graph
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    x, st = bicgstab_slab(L, A, b, tol=0.0, max_iter=iters, check_every=iters)
+    x, st = bicgstab_slab(L, A, b, **kw)
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     return {"workload": f"slab BiCGSTAB on M + 0.05 (C(u) + 1e-2 L), {L.nx}x{L.ny}x{L.nz} cells split {L.world} ways",
+            "halo": "compiled NCCL (fpb_halo_exchange / fpb_allreduce_sum), 8-iteration CUDA graphs"
+            if sub.native is not None else "torch.distributed (" + dist.get_backend() + "), eager",
             "iterations": st.iterations, "ms": ms, "ms_per_iter": ms / max(st.iterations, 1),
             "rows_per_rank": L.owned_rows[1] - L.owned_rows[0]}
 
@@ -658,13 +662,23 @@ def main():
         if ev:
             ev[2].record(stream)
 
+    graph = None
+    if sub is not None:
+        # the decomposed step replayed from CUDA graphs (distributed.
+        # SlabStepGraph): with the compiled NCCL halo one graph per step —
+        # interface windows, NCCL send/recv + add on a side stream, interior
+        from paper_2107_11541_b200.distributed import SlabStepGraph
+
+        graph = SlabStepGraph(sub, vel, rhs, mats, 1.0, 1e-2)
+
     def step(ev=None, phases=None):
         if sub is None:
             kernels(ev)
-        else:
-            # interface rows first, NCCL halo on a side stream overlapping the
-            # interior (distributed.assemble_step)
+        elif phases is not None:
+            # eager, with per-phase events (interface / halo / interior)
             sub.assemble_step(vel, rhs, mats, 1.0, 1e-2, overlap=True, side=side, events=phases)
+        else:
+            graph.replay()
 
     for _ in range(args.warmup):
         step()
@@ -853,6 +867,11 @@ def main():
             "step_roofline": step_roof,
             "kernels_ms": kern,
             "phases": phases,
+            "multi_gpu": None if sub is None else {
+                "halo": "compiled NCCL (halo.cu fpb_halo_exchange), one communicator per rank"
+                if sub.native is not None else f"torch.distributed ({dist.get_backend()}), host-staged",
+                "timed_step": "one CUDA graph per step (interface windows, NCCL halo on a side stream, interior)"
+                if graph.single_graph else "two CUDA graphs (interface / interior windows), eager halo between"},
             # per step: element-block momentum RHS (integrate + partial
             # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
             # launches (ncu launch list under profiles/); the halo (N > 1) is NCCL

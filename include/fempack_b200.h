@@ -157,6 +157,29 @@ int fpb_hex_gradient_rows(int32_t ncanon, const int32_t* canon_rows, const int32
                           const uint32_t* gslot, const double* H, int64_t nelem, const int32_t* rowptr,
                           const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream);
 
+/* ---- multi-GPU: NCCL halo sum and allreduce (halo.cu) ----
+ * The compiled entry points of the z-slab decomposition.  NCCL is loaded at
+ * run time (libnccl.so.2).  A caller creates one communicator per rank:
+ * rank 0 calls fpb_nccl_unique_id, broadcasts the 128 bytes out of band,
+ * every rank calls fpb_nccl_comm_init (device = its CUDA device).
+ * fpb_halo_sum: for each segment i, x[offsets[i] .. + counts[i]) is sent to
+ *   peers[i] and the peer's matching segment (same order on both sides) is
+ *   received and ADDED (scratch: sum(counts) doubles); nseg <= 16.  Replaces
+ *   distributed.halo_sum_nodes / halo_sum_rows's torch.distributed exchange.
+ * fpb_halo_exchange: general form — segment i sends x[send_off[i] ..) and
+ *   receives the peer's into x[recv_off[i] ..), added (add = 1, through
+ *   scratch) or copied in place (add = 0: distributed.refresh_ghosts).
+ * fpb_allreduce_sum: in-place SUM of count doubles across the ranks (dots).
+ * All stream-ordered and CUDA-graph capturable. */
+int fpb_nccl_unique_id(unsigned char* id128);
+int fpb_nccl_comm_init(int nranks, int rank, const unsigned char* id128, int device, void** comm);
+int fpb_nccl_comm_destroy(void* comm);
+int fpb_halo_sum(void* comm, int nseg, const int32_t* peers, const int64_t* offsets, const int64_t* counts,
+                 double* x, double* scratch, void* stream);
+int fpb_halo_exchange(void* comm, int nseg, const int32_t* peers, const int64_t* send_off, const int64_t* recv_off,
+                      const int64_t* counts, int add, double* x, double* scratch, void* stream);
+int fpb_allreduce_sum(void* comm, double* x, int64_t count, void* stream);
+
 /* Element-local contributions without a scatter, replacing the reference's
  * assemble_element_scalar / assemble_element_packed (assembly.py:296-380).
  * lane_conn[npacks][nn][vs] (vs = 1: conn[nelem][nn]); out in the reference's

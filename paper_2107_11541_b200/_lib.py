@@ -38,6 +38,12 @@ SIGNATURES = {
     "fpb_geometry": (_int, [_int, _i64, _int, _vp, _vp, _vp, _vp, _pi64, _pint, _vp]),
     "fpb_assemble": (_int, [_int, _int, _i64, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _i64, _vp, _vp]),
     "fpb_assemble_elements": (_int, [_int, _int, _i64, _int, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp]),
+    "fpb_nccl_unique_id": (_int, [_vp]),
+    "fpb_nccl_comm_init": (_int, [_int, _int, _vp, _int, _vp]),
+    "fpb_nccl_comm_destroy": (_int, [_vp]),
+    "fpb_halo_sum": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpb_halo_exchange": (_int, [_vp, _int, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp]),
+    "fpb_allreduce_sum": (_int, [_vp, _vp, _i64, _vp]),
     "fpb_hex_canon_slots": (_int, [_vp]),
     "fpb_hex_gradient_h": (_int, [_i64, _vp, _vp, _vp, _vp]),
     "fpb_hex_gradient_rows": (_int, [_i32, _vp, _vp, _i32, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _int,

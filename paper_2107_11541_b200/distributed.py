@@ -140,10 +140,90 @@ def _exchange(sends: list[tuple[int, torch.Tensor]], group=None) -> list[torch.T
     return [r.to(dev) for r in recvs] if staged else recvs
 
 
-def halo_sum_nodes(layout: SlabLayout, x: torch.Tensor, group=None) -> torch.Tensor:
+class NativeComm:
+    """The compiled NCCL path (halo.cu): one NCCL communicator per rank made
+    through the C ABI (fpb_nccl_unique_id on rank 0, broadcast over the
+    process group, fpb_nccl_comm_init), then fpb_halo_exchange /
+    fpb_allreduce_sum on the current stream.  Used whenever the process
+    group runs NCCL (FPB_NATIVE_HALO=0 selects torch.distributed instead);
+    every call is CUDA-graph capturable, and scratch buffers are allocated
+    once and reused, so captured graphs stay valid."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        from . import _lib
+
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            _lib.call("fpb_nccl_unique_id", ctypes.addressof(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        self._uid = (ctypes.c_ubyte * 128).from_buffer_copy(obj[0])
+        self.ptr = ctypes.c_void_p()
+        _lib.call("fpb_nccl_comm_init", self.world, self.rank, ctypes.addressof(self._uid),
+                  torch.cuda.current_device(), ctypes.byref(self.ptr))
+        self._scratch: torch.Tensor | None = None
+
+    def _scratch_for(self, n: int, dev) -> torch.Tensor:
+        if self._scratch is None or self._scratch.numel() < n:
+            self._scratch = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        return self._scratch
+
+    def exchange(self, segs, x: torch.Tensor, add: bool) -> torch.Tensor:
+        """segs: [(peer, send offset, receive offset, count)] in elements of
+        x's flat storage; add = sum into place, else copy into place."""
+        import numpy as np
+
+        from . import _lib
+
+        if not segs:
+            return x
+        peers = np.array([p for p, _, _, _ in segs], dtype=np.int32)
+        so = np.array([a for _, a, _, _ in segs], dtype=np.int64)
+        ro = np.array([b for _, _, b, _ in segs], dtype=np.int64)
+        cnt = np.array([c for _, _, _, c in segs], dtype=np.int64)
+        scratch = self._scratch_for(int(cnt.sum()), x.device) if add else None
+        _lib.call("fpb_halo_exchange", self.ptr, len(segs), peers.ctypes.data, so.ctypes.data, ro.ctypes.data,
+                  cnt.ctypes.data, int(add), x.data_ptr(), _lib.ptr(scratch), _lib.stream())
+        return x
+
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        from . import _lib
+
+        _lib.call("fpb_allreduce_sum", self.ptr, t.data_ptr(), t.numel(), _lib.stream())
+        return t
+
+    def close(self) -> None:
+        """Destroy the communicator (free any CUDA graph that captured its
+        work first: NCCL waits for it)."""
+        from . import _lib
+
+        if self.ptr:
+            _lib.call("fpb_nccl_comm_destroy", self.ptr)
+            self.ptr = None
+
+
+def native_comm(group=None):
+    """NativeComm for an NCCL process group (None for gloo, or when
+    FPB_NATIVE_HALO=0)."""
+    import os
+
+    if not dist.is_available() or not dist.is_initialized():
+        return None  # domains built outside a process group (single-process tests)
+    if dist.get_backend(group) != "nccl" or os.environ.get("FPB_NATIVE_HALO", "1") == "0":
+        return None
+    return NativeComm(group)
+
+
+def halo_sum_nodes(layout: SlabLayout, x: torch.Tensor, group=None, native: NativeComm | None = None) -> torch.Tensor:
     """Sum a node-major field (x[n] or x[n, c]) across every interface plane,
     in place: both copies of an interface row end up with mine + theirs."""
     segs = [(peer, layout.plane_rows(k)) for peer, k in layout.interfaces()]
+    if native is not None:
+        c = x[0].numel() if x.dim() > 1 else 1
+        return native.exchange([(p, lo * c, lo * c, (hi - lo) * c) for p, (lo, hi) in segs], x, True)
     sends = [(peer, x[lo:hi].contiguous()) for peer, (lo, hi) in segs]
     recvs = _exchange(sends, group)
     for (peer, (lo, hi)), r in zip(segs, recvs):
@@ -161,7 +241,7 @@ def interface_segments(layout: SlabLayout, rowptr) -> list[tuple[int, int, int]]
 
 
 def halo_sum_rows(layout: SlabLayout, rowptr: torch.Tensor, vals: torch.Tensor, nmat: int = 1,
-                  nnz: int | None = None, group=None, segs=None) -> torch.Tensor:
+                  nnz: int | None = None, group=None, segs=None, native: NativeComm | None = None) -> torch.Tensor:
     """Sum the CSR values of every interface-plane row across the interface,
     in place.  vals holds nmat matrices back to back (vals[m*nnz + k]); the
     interface rows are contiguous, and have identical global column lists on
@@ -170,6 +250,9 @@ def halo_sum_rows(layout: SlabLayout, rowptr: torch.Tensor, vals: torch.Tensor, 
         nnz = vals.numel() // nmat
     if segs is None:
         segs = interface_segments(layout, rowptr)
+    if native is not None:
+        return native.exchange([(p, m * nnz + a, m * nnz + a, b - a) for p, a, b in segs for m in range(nmat)],
+                               vals, True)
     sends = []
     for peer, a, b in segs:
         parts = [vals[m * nnz + a:m * nnz + b] for m in range(nmat)]
@@ -190,6 +273,7 @@ class SlabDomain:
     def __init__(self, layout: SlabLayout, mesh, ctx, group=None):
         self.layout, self.mesh, self.ctx, self.group = layout, mesh, ctx, group
         self.segs = interface_segments(layout, ctx.pattern.rowptr)  # host copy, once
+        self.native = native_comm(group) if layout.world > 1 else None
 
     @classmethod
     def build(cls, nx: int, ny: int, nz: int, rank: int, world: int,
@@ -217,11 +301,11 @@ class SlabDomain:
         return cls(L, own, ctx, group)
 
     def halo_sum_rhs(self, rhs: torch.Tensor) -> torch.Tensor:
-        return halo_sum_nodes(self.layout, rhs, self.group)
+        return halo_sum_nodes(self.layout, rhs, self.group, self.native)
 
     def halo_sum_matrix(self, vals: torch.Tensor, nmat: int = 1) -> torch.Tensor:
         return halo_sum_rows(self.layout, self.ctx.pattern.rowptr_d, vals, nmat, self.ctx.pattern.nnz,
-                             self.group, self.segs)
+                             self.group, self.segs, self.native)
 
     def assemble_step(self, vel, rhs, mats, rho: float = 1.0, mu: float = 1e-2, overlap: bool = True, side=None,
                       events: dict | None = None):
@@ -238,10 +322,12 @@ def _staged(t: torch.Tensor, group=None) -> bool:
     return t.is_cuda and dist.get_backend(group) != "nccl"
 
 
-def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+def allreduce_sum_(t: torch.Tensor, group=None, native: NativeComm | None = None) -> torch.Tensor:
     """In-place SUM over ranks (NCCL on device; gloo through the host)."""
     if dist.get_world_size(group) == 1:
         return t
+    if native is not None:
+        return native.allreduce(t)
     if _staged(t, group):
         h = t.cpu()
         dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
@@ -264,12 +350,18 @@ def ghost_planes(layout: SlabLayout) -> list[tuple[int, int, int]]:
     return out
 
 
-def refresh_ghosts(layout: SlabLayout, x: torch.Tensor, group=None) -> torch.Tensor:
+def refresh_ghosts(layout: SlabLayout, x: torch.Tensor, group=None, native: NativeComm | None = None) -> torch.Tensor:
     """Overwrite the ghost node planes of a node vector with the neighbours'
     values, so every local entry holds its global value again."""
     plan = ghost_planes(layout)
     if not plan:
         return x
+    if native is not None:
+        segs = []
+        for peer, ks, kg in plan:
+            (lo, hi), (glo, _) = layout.plane_rows(ks), layout.plane_rows(kg)
+            segs.append((peer, lo, glo, hi - lo))
+        return native.exchange(segs, x, False)
     sends = []
     for peer, ks, _ in plan:
         lo, hi = layout.plane_rows(ks)
@@ -282,7 +374,8 @@ def refresh_ghosts(layout: SlabLayout, x: torch.Tensor, group=None) -> torch.Ten
 
 
 def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 1e-8,
-                  max_iter: int | None = None, jacobi: bool = True, group=None, check_every: int = 8):
+                  max_iter: int | None = None, jacobi: bool = True, group=None, check_every: int = 8,
+                  native: NativeComm | None = None, graph: bool = True, ws: dict | None = None):
     """Jacobi-BiCGSTAB over the z-slab decomposition (config 5).
 
     A is this rank's extended-slab CSR with halo-summed values (rows of
@@ -293,7 +386,12 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     planes of v = A phat and t = A shat.
     Returns (x, SolverStats) with x consistent on every local plane; the
     iterates are those of krylov.bicgstab_solve on the global system up to
-    the order of the cross-rank sums.
+    the order of the cross-rank sums.  With the compiled NCCL path (native,
+    see NativeComm) each batch of check_every iterations — kernels, ghost
+    refreshes and allreduces — is captured once in a CUDA graph and
+    replayed; with gloo the iterations run eagerly (host-staged exchanges
+    cannot be captured).  ws (optional dict) keeps the vectors and the
+    captured graph for repeated solves with the same operator object.
     """
     import numpy as np
 
@@ -307,22 +405,36 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     own_lo, own_hi = layout.owned_rows
     if max_iter is None:  # 10 x the global unknown count, identical on every rank
         nglob = torch.tensor([float(own_hi - own_lo)], dtype=torch.float64, device=dev)
-        max_iter = 10 * int(allreduce_sum_(nglob, group).item())
+        max_iter = 10 * int(allreduce_sum_(nglob, group, native).item())
     d = None
     if jacobi:
         # ghost-plane rows are partial locally: their diagonal comes from the
         # neighbour, so phat = p / d and shat = s / d are global on every plane
-        d = refresh_ghosts(layout, A.diagonal_d(), group)
+        d = refresh_ghosts(layout, A.diagonal_d(), group, native)
         own_zero = (d[own_lo:own_hi] == 0.0).any().to(torch.float64).reshape(1)
-        if allreduce_sum_(own_zero, group).item() > 0:
+        if allreduce_sum_(own_zero, group, native).item() > 0:
             raise SolverBreakdownError("Jacobi preconditioner needs a nonzero diagonal")
-    x, r, rt, p, ph, v, sv, sh, t = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(9))
     lib = _lib.load()
-    state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
+    cap = max(1, min(64, max_iter))
+    key = (id(A), n, cap, check_every, jacobi)
+    if ws is not None and ws.get("key") == key:
+        # reuse the vectors (and the captured graph, which names them)
+        x, r, rt, p, ph, v, sv, sh, t = ws["vecs"]
+        state, hist_d = ws["state"], ws["hist"]
+        state.zero_()
+        hist_d.zero_()
+        if d is not None:
+            ws["d"].copy_(d)
+            d = ws["d"]
+    else:
+        x, r, rt, p, ph, v, sv, sh, t = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(9))
+        state = torch.zeros(int(lib.fpb_bicgstab_state_size()), dtype=torch.float64, device=dev)
+        hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
+        if ws is not None:
+            ws.clear()
+            ws.update(key=key, vecs=(x, r, rt, p, ph, v, sv, sh, t), state=state, hist=hist_d, d=d, graph=None)
     red = state[16:18]
     red3 = state[16:19]  # after K4: (t, s), (t, t) and the deferred ||s||^2
-    cap = max(1, min(64, max_iter))
-    hist_d = torch.zeros(cap, dtype=torch.float64, device=dev)
     work = dot_work()
     s = _lib.stream()
     rp, ci, va = A.rowptr_d.data_ptr(), A.colind_d.data_ptr(), A.vals_d.data_ptr()
@@ -337,9 +449,9 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
               rt.data_ptr(), p.data_ptr(), v.data_ptr(), state.data_ptr(), hist_d.data_ptr(), float(tol),
               own_lo, own_hi, 1, work.data_ptr(), s)
     if x0 is not None:  # r = b - A x0 is exact on computed rows only
-        refresh_ghosts(layout, r, group)
+        refresh_ghosts(layout, r, group, native)
         rt.copy_(r)
-    allreduce_sum_(red, group)
+    allreduce_sum_(red, group, native)
     _lib.call("fpb_bicgstab_finish", 0, state.data_ptr(), hist_d.data_ptr(), 1, float(tol), s)
     st = state.cpu().numpy()
     if st[B_BNORM] == 0.0:
@@ -352,25 +464,44 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
     args = (n, nnz, rp, ci, va, *sell, d.data_ptr() if d is not None else None, x.data_ptr(),
             r.data_ptr(), rt.data_ptr(), p.data_ptr(), ph.data_ptr(), v.data_ptr(), sv.data_ptr(), sh.data_ptr(),
             t.data_ptr(), state.data_ptr(), hist_d.data_ptr(), cap, own_lo, own_hi, 1, work.data_ptr(), s)
-    done = 0
-    while done < max_iter:
-        k = min(check_every, max_iter - done)
+
+    def iterations(k: int) -> None:
         for _ in range(k):
             # three cross-rank reductions per iteration: K2's (r~, v); K3's
             # ||s||^2 together with K4's (t, s), (t, t); K5's ||r||^2, (r~, r)
-            _lib.call("fpb_bicgstab_step", 1, *args)
-            refresh_ghosts(layout, v, group)
-            allreduce_sum_(red, group)
-            _lib.call("fpb_bicgstab_finish", 1, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
-            _lib.call("fpb_bicgstab_step", 2, *args)
-            _lib.call("fpb_bicgstab_step", 3, *args)
-            refresh_ghosts(layout, t, group)
-            allreduce_sum_(red3, group)
-            _lib.call("fpb_bicgstab_finish", 2, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
-            _lib.call("fpb_bicgstab_finish", 3, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
-            _lib.call("fpb_bicgstab_step", 4, *args)
-            allreduce_sum_(red, group)
-            _lib.call("fpb_bicgstab_finish", 4, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, s)
+            st_ = _lib.stream()
+            a_ = args[:-1] + (st_,)
+            _lib.call("fpb_bicgstab_step", 1, *a_)
+            refresh_ghosts(layout, v, group, native)
+            allreduce_sum_(red, group, native)
+            _lib.call("fpb_bicgstab_finish", 1, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, st_)
+            _lib.call("fpb_bicgstab_step", 2, *a_)
+            _lib.call("fpb_bicgstab_step", 3, *a_)
+            refresh_ghosts(layout, t, group, native)
+            allreduce_sum_(red3, group, native)
+            _lib.call("fpb_bicgstab_finish", 2, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, st_)
+            _lib.call("fpb_bicgstab_finish", 3, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, st_)
+            _lib.call("fpb_bicgstab_step", 4, *a_)
+            allreduce_sum_(red, group, native)
+            _lib.call("fpb_bicgstab_finish", 4, state.data_ptr(), hist_d.data_ptr(), cap, 0.0, st_)
+
+    captured = ws.get("graph") if ws is not None else None
+    done = 0
+    while done < max_iter:
+        k = min(check_every, max_iter - done)
+        if native is not None and graph and k == check_every:
+            if captured is None:
+                captured = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(captured, stream=side):
+                    iterations(k)
+                torch.cuda.current_stream().wait_stream(side)
+                if ws is not None:
+                    ws["graph"] = captured
+            captured.replay()
+        else:
+            iterations(k)
         st = state.cpu().numpy()
         it = int(st[B_IT])
         if it > done:
@@ -384,10 +515,10 @@ def bicgstab_slab(layout: SlabLayout, A, b: torch.Tensor, x0=None, tol: float = 
             break
     converged = bool(st[B_STATUS] == 1.0)
     # true residual over the owned rows, summed across ranks
-    refresh_ghosts(layout, x, group)
+    refresh_ghosts(layout, x, group, native)
     res = axpy_d(-1.0, spmv_d(A, x), b)
     rr = dot_d(res[own_lo:own_hi].contiguous(), res[own_lo:own_hi].contiguous()).reshape(1).clone()
-    allreduce_sum_(rr, group)
+    allreduce_sum_(rr, group, native)
     true_residual = float(np.sqrt(rr.item())) / float(st[B_BNORM])
     return x, SolverStats(done, converged, history, true_residual)
 
@@ -492,3 +623,67 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
         ev["interior_done"].record(main)
     main.wait_stream(side)
     return rhs, mats
+
+
+class SlabStepGraph:
+    """One decomposed NS step (assemble_step) replayed from CUDA graphs.
+
+    With the compiled NCCL path (dom.native) the whole overlapped step —
+    interface windows, the halo on the side stream, interior windows — is
+    one graph (NCCL send/recv are capturable), so a step costs one launch.
+    With gloo (CPU-staged exchanges, several ranks sharing a GPU) the device
+    work is captured in two graphs (interface windows, interior windows) and
+    the halo runs eagerly between them.  Inputs and outputs are the tensors
+    given here (replay reads vel and overwrites rhs / mats in place).
+    Results are bitwise those of assemble_step(overlap=False)."""
+
+    def __init__(self, dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats: torch.Tensor,
+                 rho: float = 1.0, mu: float = 1e-2):
+        from .assembly import KernelKind
+
+        self.dom, self.vel, self.rhs, self.mats = dom, vel, rhs, mats
+        self.side = torch.cuda.Stream()
+        # eager warm-up: plans, scratch buffers, geometry check
+        assemble_step(dom, vel, rhs, mats, rho, mu, overlap=True, side=self.side)
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        ctx, K, none = dom.ctx, KernelKind.MOMENTUM_RHS, (0, 0)
+        self.whole = self.phase_a = self.phase_b = None
+        if dom.native is not None or dom.layout.world == 1:
+            self.whole = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.whole, stream=cap):
+                assemble_step(dom, vel, rhs, mats, rho, mu, overlap=True, side=self.side)
+        else:
+            w = _step_windows(dom)
+            self.phase_a, self.phase_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.phase_a, stream=cap):
+                for b in w["blocks_A"]:
+                    if b[1] > b[0]:
+                        ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": b, "nodes": none})
+                for nd in w["nodes_A"]:
+                    ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": none, "nodes": nd})
+                for r in w["rows_A"]:
+                    if r[1] > r[0]:
+                        ctx.assemble_gradients_d(mats, {"rows": r})
+            with torch.cuda.graph(self.phase_b, stream=cap):
+                ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": w["blocks_B"], "nodes": none})
+                for nd in w["nodes_B"]:
+                    ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs, {"blocks": none, "nodes": nd})
+                if w["rows_B"][1] > w["rows_B"][0]:
+                    ctx.assemble_gradients_d(mats, {"rows": w["rows_B"]})
+        torch.cuda.current_stream().wait_stream(cap)
+
+    @property
+    def single_graph(self) -> bool:
+        return self.whole is not None
+
+    def replay(self):
+        if self.whole is not None:
+            self.whole.replay()
+        else:
+            self.phase_a.replay()
+            self.dom.halo_sum_rhs(self.rhs)
+            self.dom.halo_sum_matrix(self.mats, self.dom.ctx.mesh.dim)
+            self.phase_b.replay()
+        return self.rhs, self.mats

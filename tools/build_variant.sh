@@ -7,10 +7,10 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/build_variants/$name
 mkdir -p $out
 cd $root/paper_2107_11541_b200/csrc
-for f in setup assemble rows rowsq pairs blocks vector flow hexblock; do
+for f in setup assemble rows rowsq pairs blocks vector flow hexblock halo; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr -rdc=true "$@" -c $f.cu -o $out/$f.o &
 done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC $out/*.o -o $out/libfempack_b200.so -lcudart_static
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC $out/*.o -o $out/libfempack_b200.so -lcudart_static -ldl
 echo built $out
