@@ -87,9 +87,75 @@ ROW_OWNED_GAUSS = ("QUAD04", "PYR05", "HEX08")  # Gauss-loop elements: row-owned
 # TET04 continuity matrices by column pairs (pairs.cu) instead of the
 # incidence-accumulating row kernel; module switch for A/B measurements
 GRADIENT_PAIRS = True
+# TET04 continuity: slices whose rows share one pair stream read it from
+# constant memory (pairs.cu); False = every slice streams its own words
+PAIR_CANON = True
+KUHN_STREAM = True  # ... and the Kuhn box's stream compiled in (pairs.cu k_rows_pairs_kuhn)
+_PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # HEX08 continuity with element geometry evaluated once (hexblock.cu);
 # False = the per-row kernel (rowsq.cu)
 HEX_ONCE = True
+
+
+def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 15):
+    """Find the canonical pair stream (pairs.cu): among the slices of the
+    most common stream width, the most frequent row stream (a 64-bit
+    polynomial hash, then an exact word-by-word check).  Returns (words
+    uint16 numpy, canonical slice ids, other slice ids, kuhn) — slice ids as
+    int32 device tensors; kuhn = the stream is pairs.cu's compile-time Kuhn
+    table and every canonical row has its diagonal at CSR offset 7 — or None
+    when no full slice shares one stream.  Setup only."""
+    dev = ptr.device
+    nsl = ptr.numel() - 1
+    if nsl == 0:
+        return None
+    width = (ptr[1:] - ptr[:-1]).to(torch.int64)
+    full = torch.arange(nsl, device=dev) < (n // 32)  # complete 32-row slices only
+    vals, counts = torch.unique(width[full], return_counts=True) if bool(full.any()) else (None, None)
+    if vals is None or vals.numel() == 0:
+        return None
+    W = int(vals[torch.argmax(counts)])
+    if W == 0 or W > 512 or W % 2:
+        return None
+    cand = torch.nonzero(full & (width == W)).flatten()
+    w16 = words.view(torch.int16)
+    k = torch.arange(W, device=dev, dtype=torch.int64)
+    lane = torch.arange(32, device=dev, dtype=torch.int64)
+    coef = torch.randint(1, 1 << 62, (W,), generator=torch.Generator().manual_seed(1), dtype=torch.int64).to(dev)
+
+    def streams(sl):  # [len(sl), 32, W] int64 words of the slices' rows
+        base = (ptr[sl] // 2)[:, None, None]
+        idx = ((base + (k // 2)[None, None, :]) * 32 + lane[None, :, None]) * 2 + (k & 1)[None, None, :]
+        return w16[idx].to(torch.int64) & 0xffff
+
+    hashes = []
+    for c0 in range(0, cand.numel(), chunk):
+        hashes.append((streams(cand[c0:c0 + chunk]) * coef).sum(dim=2))  # wraps mod 2^64
+    h = torch.cat(hashes)  # [ncand, 32]
+    hv, hc = torch.unique(h.flatten(), return_counts=True)
+    top = hv[torch.argmax(hc)]
+    where = torch.nonzero(h == top)[0]
+    canon = streams(cand[where[0]:where[0] + 1])[0, int(where[1])]  # [W]
+    ok = []
+    for c0 in range(0, cand.numel(), chunk):
+        ok.append((streams(cand[c0:c0 + chunk]) == canon[None, None, :]).all(dim=2).all(dim=1))
+    csl = cand[torch.cat(ok)]
+    if csl.numel() == 0:
+        return None
+    is_c = torch.zeros(nsl, dtype=torch.bool, device=dev)
+    is_c[csl] = True
+    other = torch.nonzero(~is_c).flatten()
+    cw = canon.cpu().numpy().astype(np.uint16)
+    kuhn = False
+    if rowptr is not None and KUHN_STREAM:
+        tab = np.zeros(512, dtype=np.uint16)
+        nk = int(_lib.load().fpb_pair_kuhn_table(tab.ctypes.data))
+        if cw.size == nk and np.array_equal(cw, tab[:nk]):
+            rows = (csl.to(torch.int64)[:, None] * 32 + torch.arange(32, device=dev)).flatten()
+            rp = rowptr.to(torch.int64)
+            kuhn = bool(((rp[rows + 1] - rp[rows]) == 15).all()) and \
+                bool((colind[rp[rows] + 7].to(torch.int64) == rows).all())
+    return (cw, csl.to(torch.int32).contiguous(), other.to(torch.int32).contiguous(), kuhn)
 
 
 class RowPlan:
@@ -122,6 +188,7 @@ class RowPlan:
         self.slots = None
         self.rowcap = 0
         self.pairs = None  # TET04 continuity pair stream (pairs.cu); False = not eligible
+        self.pair_canon = None  # (canonical words, canonical slices, other slices), see _pair_canon
 
     def ensure_pairs(self, pattern: "CsrMatrix"):
         """(pair_ptr, words) of the TET04 continuity pair stream (pairs.cu),
@@ -141,6 +208,8 @@ class RowPlan:
                                                pattern.rowptr_d.data_ptr(), ptr.data_ptr(), words.data_ptr(),
                                                ctypes.byref(total), _lib.stream())
             self.pairs = (ptr, words) if rc == _lib.FPB_OK and words is not None else False
+            if self.pairs and PAIR_CANON:
+                self.pair_canon = _pair_canon(self.n, ptr, words, pattern.rowptr_d, pattern.colind_d)
         return self.pairs if self.pairs is not False else None
 
     def ensure_slots(self, conn_d: torch.Tensor, pattern: "CsrMatrix") -> None:
@@ -503,9 +572,28 @@ class AssemblyContext:
             elif own and kind_id == GRADIENT_XYZ and GRADIENT_PAIRS and g.etype_id == ETYPE_ID[ElementType.TET04] \
                     and g.rows.ensure_pairs(self.pattern) is not None:
                 r = g.rows
-                _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.pairs[0].data_ptr(), r.pairs[1].data_ptr(),
-                          xyz4, self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
-                          0 if single_rows else 1, out.data_ptr(), _lib.stream())
+                acc = 0 if single_rows else 1
+                if r.pair_canon is not None and window is None:
+                    cw, csl, osl, kuhn = r.pair_canon
+                    if kuhn:  # compile-time stream: edge vectors in registers
+                        _lib.call("fpb_assemble_gradient_pairs_kuhn", r.n, int(csl.numel()), csl.data_ptr(), xyz4,
+                                  self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, acc,
+                                  out.data_ptr(), _lib.stream())
+                    else:
+                        global _PAIR_CANON_LOADED
+                        if _PAIR_CANON_LOADED is not cw:  # constant memory: upload when the stream changes
+                            torch.cuda.current_stream().synchronize()
+                            _lib.call("fpb_pair_canon_set", cw.ctypes.data, int(cw.size))
+                            _PAIR_CANON_LOADED = cw
+                    for sl, clen in (((osl, 0),) if kuhn else ((csl, int(cw.size)), (osl, 0))):
+                        _lib.call("fpb_assemble_gradient_pairs_slices", r.n, int(sl.numel()), sl.data_ptr(), clen,
+                                  r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4,
+                                  self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
+                                  acc, out.data_ptr(), _lib.stream())
+                else:
+                    _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.pairs[0].data_ptr(),
+                              r.pairs[1].data_ptr(), xyz4, self.pattern.rowptr_d.data_ptr(),
+                              self.pattern.colind_d.data_ptr(), nnz, r.rowcap, acc, out.data_ptr(), _lib.stream())
             elif own:
                 r = g.rows
                 _lib.call("fpb_assemble_rows", kind_id, g.etype_id, r.n, r0, r1, r.slice_ptr.data_ptr(),

@@ -48,6 +48,16 @@ constexpr int kPairMaxInc = 64;      // incidences per row the setup sort handle
 // the hot loop needs no end-of-row test
 constexpr uint16_t kPairPad = 0;
 
+// Canonical stream: the pair stream shared by every interior row of a
+// structured mesh (on the Kuhn box all interior rows have the same 15
+// columns, 24 incidences and therefore the same 72 (q, r) words).  The host
+// finds it as the most frequent row stream, verifies rows against it word by
+// word, and slices whose 32 rows all match run the kernel with the stream
+// read from constant memory (uniform across the warp) instead of 2 bytes
+// per pair per row from HBM.
+constexpr int kPairCanonMax = 512;
+__constant__ uint16_t c_pair_canon[kPairCanonMax];
+
 // Pass FILL = false: per-slice stream width (the slice's longest row,
 // rounded up to even) into width[sl]; FILL = true: the words.
 template <bool FILL>
@@ -177,19 +187,23 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
 // off-diagonal slots ([s][field][thread], region X) and the warp's three
 // output row blocks (linear, one per matrix), where each finished column is
 // stored once at its CSR position.
+template <bool CANON>
 __global__ void __launch_bounds__(32, 1)
-k_rows_pairs(int32_t n, int32_t row0, const int64_t* __restrict__ pair_ptr, const uint16_t* __restrict__ words,
+k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, int canon_len,
+             const int64_t* __restrict__ pair_ptr, const uint16_t* __restrict__ words,
              const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
              int64_t nnz, int rowcap, int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, T = 32;
   constexpr int SS = DIM * T;  // doubles per slot in each region
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
-  const int row = row0 + blockIdx.x * T + tid;
+  // rows: the 32-row slice slist[block] (slice lists), else row0 + 32 block
+  const int row = (slist ? __ldg(slist + blockIdx.x) * T : row0 + blockIdx.x * T) + tid;
   const bool live = row < n;
   const int lane = row & 31;
-  const int64_t p0 = __ldg(pair_ptr + (row >> 5));
-  const int k1 = live ? (int)(__ldg(pair_ptr + (row >> 5) + 1) - p0) : 0;  // stream words of the slice
+  const int64_t p0 = CANON ? 0 : __ldg(pair_ptr + (row >> 5));
+  // stream words of the slice
+  const int k1 = !live ? 0 : CANON ? canon_len : (int)(__ldg(pair_ptr + (row >> 5) + 1) - p0);
   int rlo = 0, rlen = 0;
   double x0[DIM] = {0.0, 0.0, 0.0};
   if (live) {
@@ -217,8 +231,13 @@ k_rows_pairs(int32_t n, int32_t row0, const int64_t* __restrict__ pair_ptr, cons
   constexpr int kW = FPB_PAIR_W;
   uint16_t wc[kW], wn[kW];
 #if FPB_PAIR_PACK2
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(words) + (p0 >> 1) * 32 + lane;
+  const uint32_t* wp = CANON ? nullptr : reinterpret_cast<const uint32_t*>(words) + (p0 >> 1) * 32 + lane;
   auto ld_w = [&](int k, uint16_t (&w)[kW]) {
+    if constexpr (CANON) {  // uniform across the warp: constant-cache broadcast
+#pragma unroll
+      for (int j = 0; j < kW; ++j) w[j] = k + j < k1 ? c_pair_canon[k + j] : kPairPad;
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < kW; j += 2) {
       const uint32_t v = k + j < k1 ? __ldg(wp + (int64_t)((k + j) >> 1) * 32) : 0u;
@@ -340,6 +359,109 @@ k_rows_pairs(int32_t n, int32_t row0, const int64_t* __restrict__ pair_ptr, cons
   }
 }
 
+
+// ---- compile-time Kuhn stream --------------------------------------------
+// The canonical stream of an interior row of the generator's Kuhn TET04 box
+// (mesh.py:212-213, :268-282: 24 tets around every interior node, 14
+// neighbours, 72 pairs), as the stream builder above emits it (dumped with
+// tools/pair_canon_dump.py).  The host uses this kernel only when the
+// detected canonical stream equals this table word for word
+// (fpb_pair_kuhn_table), so rows are still verified against the real
+// pattern.  With the pairs known at compile time the 14 edge vectors live in
+// registers and the walk is straight-line FP64 (no stream loads, no
+// shared-memory edge fetches, no decode).
+constexpr int kKuhnWords = 72, kKuhnCols = 14, kKuhnDiag = 7;
+__host__ __device__ constexpr uint16_t kuhn_word(int i) {
+  constexpr uint16_t t[kKuhnWords] = {
+      0x0083, 0x8281, 0x8205, 0x8304, 0x8106, 0xc182, 0x0180, 0x8383, 0x8287, 0xc005, 0x0300, 0x8406,
+      0x8188, 0xc003, 0x0001, 0x8100, 0x8402, 0x8488, 0x8389, 0xc087, 0x0280, 0x8505, 0x830a, 0xc006,
+      0x0004, 0x8080, 0x8381, 0x8587, 0x850b, 0xc20a, 0x0002, 0x8200, 0x8504, 0x860a, 0x840c, 0xc108,
+      0x0181, 0x8483, 0x8689, 0x858d, 0x828b, 0xc085, 0x0302, 0x8606, 0x868c, 0x848d, 0x8189, 0xc103,
+      0x0187, 0x8403, 0x8688, 0xc38d, 0x0284, 0x8585, 0x868b, 0x860d, 0x830c, 0xc206, 0x028a, 0x8385,
+      0x8687, 0xc50d, 0x0308, 0x8506, 0x868a, 0xc40d, 0x0487, 0x8409, 0x8608, 0x850c, 0x858a, 0xc38b};
+  return t[i];
+}
+
+constexpr int kKuhnWarps = 2;  // warps (32-row slices) per CTA
+
+#ifndef FPB_KUHN_MINB
+#define FPB_KUHN_MINB 6
+#endif
+__global__ void __launch_bounds__(32 * kKuhnWarps, FPB_KUHN_MINB)
+k_rows_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* __restrict__ slist, const double* __restrict__ xyz4,
+                  const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz,
+                  int accumulate, double* __restrict__ out) {
+  constexpr int DIM = 3, R = kKuhnCols + 1;  // entries per row
+  __shared__ double Bo[kKuhnWarps][DIM][32 * R];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int si = blockIdx.x * kKuhnWarps + warp;
+  if (si >= nslices) return;
+  const int row = __ldg(slist + si) * 32 + lane;
+  const bool live = row < n;
+  const int rlo = live ? __ldg(rowptr + row) : 0;
+  const int base = __shfl_sync(0xffffffffu, rlo, 0);
+  // the diagonal sits at CSR offset kKuhnDiag of every canonical row (the
+  // host checks it with the stream): off-diagonal slot t is offset t + (t >= 7)
+  constexpr int dslot = kKuhnDiag;
+  double x0[DIM] = {0.0, 0.0, 0.0}, X[kKuhnCols][DIM];
+  if (live) {
+    double r4[4];
+    ld256(xyz4 + 4 * (int64_t)row, r4);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) x0[d] = r4[d];
+#pragma unroll
+    for (int t = 0; t < kKuhnCols; ++t) {
+      ld256(xyz4 + 4 * (int64_t)__ldg(colind + rlo + t + (t >= dslot)), r4);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) X[t][d] = r4[d] - x0[d];
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < kKuhnCols; ++t)
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) X[t][d] = 0.0;
+  }
+  const double mN0 = refmN<FPB_TET04>(0);
+  double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
+  double* const bo = &Bo[warp][0][0];
+  int target = 0;
+#pragma unroll
+  for (int i = 0; i < kKuhnWords; ++i) {
+    const int w = kuhn_word(i);
+    const int q = w & 0x7f, r = (w >> 7) & 0x7f;
+    acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
+    acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
+    acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+    if (w & (1 << 14)) {  // column finished
+      const int cpos = target + (target >= dslot);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        bo[d * 32 * R + lane * R + cpos] = mN0 * acc[d];
+        tot[d] += acc[d];
+        acc[d] = 0.0;
+      }
+      ++target;
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) bo[d * 32 * R + lane * R + dslot] = -(mN0 * tot[d]);
+  __syncwarp();
+  // the slice's 32 rows are consecutive with 15 entries each: one contiguous
+  // CSR range of 480 values per matrix
+  int nlive = live ? lane + 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nlive = max(nlive, __shfl_xor_sync(0xffffffffu, nlive, o));
+  const int span = nlive * R;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    double* o = out + d * nnz + base;
+    for (int j = lane; j < span; j += 32) {
+      const double v = bo[d * 32 * R + j];
+      o[j] = accumulate ? o[j] + v : v;
+    }
+  }
+}
+
 }  // namespace fpb
 
 using namespace fpb;
@@ -397,9 +519,59 @@ int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int
   // edge vectors [rowcap - 1][3][32] + output rows [3][32 rowcap]
   const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
   if (smem > 48 * 1024)
-    FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_rows_pairs<<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(row1, row0, pair_ptr, words, xyz4, rowptr,
-                                                                     colind, nnz, rowcap, accumulate, out);
+    FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_rows_pairs<false><<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(
+      row1, row0, nullptr, 0, pair_ptr, words, xyz4, rowptr, colind, nnz, rowcap, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_pair_kuhn_table(uint16_t* words_h) {
+  for (int i = 0; i < kKuhnWords; ++i) words_h[i] = kuhn_word(i);
+  return kKuhnWords;
+}
+
+int fpb_assemble_gradient_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* slist, const double* xyz4,
+                                     const int32_t* rowptr, const int32_t* colind, int64_t nnz, int accumulate,
+                                     double* out, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(slist && xyz4 && rowptr && colind && out, "missing arrays for the Kuhn-stream kernel");
+  if (nslices <= 0) return FPB_OK;
+  k_rows_pairs_kuhn<<<(unsigned)((nslices + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
+      n, nslices, slist, xyz4, rowptr, colind, nnz, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_pair_canon_set(const uint16_t* words_h, int len) {
+  FPB_REQUIRE(len >= 0 && len <= kPairCanonMax && len % 2 == 0, "canonical stream length %d out of range", len);
+  if (len) FPB_CUDA(cudaMemcpyToSymbol(c_pair_canon, words_h, (size_t)len * sizeof(uint16_t)));
+  return FPB_OK;
+}
+
+int fpb_assemble_gradient_pairs_slices(int32_t n, int32_t nslices, const int32_t* slist, int canon_len,
+                                       const int64_t* pair_ptr, const uint16_t* words, const double* xyz4,
+                                       const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap,
+                                       int accumulate, double* out, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(slist && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
+              "pair-stream gradient assembly needs the slice list, the CSR pattern and rows <= 129 entries");
+  FPB_REQUIRE(canon_len > 0 || (pair_ptr && words), "generic slices need the pair stream");
+  FPB_REQUIRE(canon_len <= kPairCanonMax, "canonical stream too long");
+  if (nslices <= 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
+  if (canon_len > 0) {
+    if (smem > 48 * 1024)
+      FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_rows_pairs<true><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, canon_len, nullptr, nullptr, xyz4, rowptr,
+                                                           colind, nnz, rowcap, accumulate, out);
+  } else {
+    if (smem > 48 * 1024)
+      FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_rows_pairs<false><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, 0, pair_ptr, words, xyz4, rowptr, colind,
+                                                            nnz, rowcap, accumulate, out);
+  }
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
