@@ -254,22 +254,29 @@ int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int
                                 void* stream);
 
 /* Slice-list form of the pair-stream kernel: rows of the 32-row slices
- * slist[nslices].  canon_len > 0: every row of those slices has the same
- * stream, uploaded once with fpb_pair_canon_set (even length <= 512) and
- * read from constant memory (pair_ptr / words unused); canon_len = 0: the
- * per-slice stream as in fpb_assemble_gradient_pairs. */
+ * slist[nslices].  canon_len > 0:
+ * every row of those slices has the same stream, uploaded once with
+ * fpb_pair_canon_set (even length <= 512) and read from constant memory
+ * (pair_ptr / words unused); canon_len = 0: the per-slice stream as in
+ * fpb_assemble_gradient_pairs. */
 int fpb_pair_canon_set(const uint16_t* words_h, int len);
-/* The compile-time stream of an interior Kuhn-box row (72 words; returns the
- * count) and the kernel that uses it: every row of the slices must have that
- * stream and its diagonal at CSR offset 7 (the caller verifies both). */
-int fpb_pair_kuhn_table(uint16_t* words_h);
-int fpb_assemble_gradient_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* slist, const double* xyz4,
-                                     const int32_t* rowptr, const int32_t* colind, int64_t nnz, int accumulate,
-                                     double* out, void* stream);
 int fpb_assemble_gradient_pairs_slices(int32_t n, int32_t nslices, const int32_t* slist, int canon_len,
-                                       const int64_t* pair_ptr, const uint16_t* words, const double* xyz4,
-                                       const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap,
-                                       int accumulate, double* out, void* stream);
+                                       const int64_t* pair_ptr, const uint16_t* words,
+                                       const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
+                                       int rowcap, int accumulate, double* out, void* stream);
+/* The compile-time stream of an interior Kuhn-box row (72 words; returns the
+ * count) and the kernel that uses it on the listed rows rows[nrows] (any
+ * order; 32 per warp): every listed row must have that stream and 15 entries
+ * with the diagonal at CSR offset 7 (the caller verifies both). */
+int fpb_pair_kuhn_table(uint16_t* words_h);
+/* The per-row stream for an arbitrary row list rows[nrows] (the rows the
+ * Kuhn kernel does not take): each row reads its own slice's stream. */
+int fpb_assemble_gradient_pairs_rows(int32_t n, int32_t nrows, const int32_t* rows, const int64_t* pair_ptr,
+                                     const uint16_t* words, const double* xyz4, const int32_t* rowptr,
+                                     const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
+                                     void* stream);
+int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const double* xyz4, const int32_t* rowptr,
+                                     const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream);
 
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices

@@ -97,65 +97,76 @@ _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 HEX_ONCE = True
 
 
-def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 15):
-    """Find the canonical pair stream (pairs.cu): among the slices of the
-    most common stream width, the most frequent row stream (a 64-bit
-    polynomial hash, then an exact word-by-word check).  Returns (words
-    uint16 numpy, canonical slice ids, other slice ids, kuhn) — slice ids as
-    int32 device tensors; kuhn = the stream is pairs.cu's compile-time Kuhn
-    table and every canonical row has its diagonal at CSR offset 7 — or None
-    when no full slice shares one stream.  Setup only."""
+def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 14):
+    """Find the canonical pair stream (pairs.cu): the most frequent row
+    stream (64-bit polynomial hash over every row's words, then an exact
+    word-by-word check of each row).  Returns a dict (setup only):
+      words     the canonical stream (uint16 numpy, even length)
+      kuhn      it is pairs.cu's compile-time Kuhn table and every canonical
+                row has 15 entries with the diagonal at CSR offset 7: then
+      rows      the canonical rows (int32, natural order) for the register
+                kernel, and
+      other     every other row (int32), for the row-list stream kernel;
+    otherwise (constant-memory stream, whole slices only)
+      cslices / oslices  fully canonical / other slices.
+    None when no row stream repeats."""
     dev = ptr.device
     nsl = ptr.numel() - 1
-    if nsl == 0:
+    if nsl == 0 or n == 0:
         return None
     width = (ptr[1:] - ptr[:-1]).to(torch.int64)
-    full = torch.arange(nsl, device=dev) < (n // 32)  # complete 32-row slices only
-    vals, counts = torch.unique(width[full], return_counts=True) if bool(full.any()) else (None, None)
-    if vals is None or vals.numel() == 0:
+    W = int(width.max())
+    if W == 0:
         return None
-    W = int(vals[torch.argmax(counts)])
-    if W == 0 or W > 512 or W % 2:
-        return None
-    cand = torch.nonzero(full & (width == W)).flatten()
     w16 = words.view(torch.int16)
     k = torch.arange(W, device=dev, dtype=torch.int64)
     lane = torch.arange(32, device=dev, dtype=torch.int64)
     coef = torch.randint(1, 1 << 62, (W,), generator=torch.Generator().manual_seed(1), dtype=torch.int64).to(dev)
 
-    def streams(sl):  # [len(sl), 32, W] int64 words of the slices' rows
+    def streams(s0, s1):  # [s1 - s0, 32, W] int64 words of the slices' rows (0 past each slice's width)
+        sl = torch.arange(s0, s1, device=dev)
         base = (ptr[sl] // 2)[:, None, None]
-        idx = ((base + (k // 2)[None, None, :]) * 32 + lane[None, :, None]) * 2 + (k & 1)[None, None, :]
-        return w16[idx].to(torch.int64) & 0xffff
+        kk = torch.minimum(k, (width[sl] - 1).clamp(min=0)[:, None])[:, None, :]
+        idx = ((base + kk // 2) * 32 + lane[None, :, None]) * 2 + (kk & 1)
+        v = w16[idx].to(torch.int64) & 0xffff
+        return torch.where(k[None, None, :] < width[sl][:, None, None], v, torch.zeros_like(v))
 
-    hashes = []
-    for c0 in range(0, cand.numel(), chunk):
-        hashes.append((streams(cand[c0:c0 + chunk]) * coef).sum(dim=2))  # wraps mod 2^64
-    h = torch.cat(hashes)  # [ncand, 32]
-    hv, hc = torch.unique(h.flatten(), return_counts=True)
-    top = hv[torch.argmax(hc)]
-    where = torch.nonzero(h == top)[0]
-    canon = streams(cand[where[0]:where[0] + 1])[0, int(where[1])]  # [W]
-    ok = []
-    for c0 in range(0, cand.numel(), chunk):
-        ok.append((streams(cand[c0:c0 + chunk]) == canon[None, None, :]).all(dim=2).all(dim=1))
-    csl = cand[torch.cat(ok)]
-    if csl.numel() == 0:
+    h = torch.cat([(streams(c, min(c + chunk, nsl)) * coef).sum(dim=2) for c in range(0, nsl, chunk)]).flatten()
+    h = h[:n]
+    hv, hc = torch.unique(h, return_counts=True)
+    if int(hc.max()) < 2:
         return None
-    is_c = torch.zeros(nsl, dtype=torch.bool, device=dev)
-    is_c[csl] = True
-    other = torch.nonzero(~is_c).flatten()
-    cw = canon.cpu().numpy().astype(np.uint16)
-    kuhn = False
+    top = int(torch.nonzero(h == hv[torch.argmax(hc)])[0])
+    canon = streams(top // 32, top // 32 + 1)[0, top % 32]
+    nz = torch.nonzero(canon).flatten()
+    K = (int(nz[-1]) + 2) & ~1 if nz.numel() else 0
+    if K == 0 or K > 512:
+        return None
+    canon_k = canon[:K]
+    is_c = torch.cat([(streams(c, min(c + chunk, nsl)) == torch.cat(
+        [canon_k, torch.zeros(W - K, dtype=torch.int64, device=dev)])[None, None, :]).all(dim=2).flatten()
+        for c in range(0, nsl, chunk)])[:n]
+    cw = canon_k.cpu().numpy().astype(np.uint16)
+    out = {"words": cw, "kuhn": False}
     if rowptr is not None and KUHN_STREAM:
         tab = np.zeros(512, dtype=np.uint16)
         nk = int(_lib.load().fpb_pair_kuhn_table(tab.ctypes.data))
         if cw.size == nk and np.array_equal(cw, tab[:nk]):
-            rows = (csl.to(torch.int64)[:, None] * 32 + torch.arange(32, device=dev)).flatten()
             rp = rowptr.to(torch.int64)
-            kuhn = bool(((rp[rows + 1] - rp[rows]) == 15).all()) and \
-                bool((colind[rp[rows] + 7].to(torch.int64) == rows).all())
-    return (cw, csl.to(torch.int32).contiguous(), other.to(torch.int32).contiguous(), kuhn)
+            rows = torch.arange(n, device=dev)
+            ok = (rp[1:] - rp[:-1]) == 15
+            ok &= colind[(rp[:-1] + 7).clamp(max=max(int(rp[-1]) - 1, 0))].to(torch.int64) == rows
+            is_c &= ok
+            crow = torch.nonzero(is_c).flatten()
+            grow = torch.nonzero(~is_c).flatten()
+            out.update(kuhn=True, rows=crow.to(torch.int32).contiguous(), other=grow.to(torch.int32).contiguous())
+            return out
+    full = torch.ones(nsl * 32, dtype=torch.bool, device=dev)
+    full[:n] = is_c
+    allc = full.view(nsl, 32).all(dim=1) & (torch.arange(nsl, device=dev) < n // 32)
+    out.update(cslices=torch.nonzero(allc).flatten().to(torch.int32).contiguous(),
+               oslices=torch.nonzero(~allc).flatten().to(torch.int32).contiguous())
+    return out
 
 
 class RowPlan:
@@ -574,22 +585,25 @@ class AssemblyContext:
                 r = g.rows
                 acc = 0 if single_rows else 1
                 if r.pair_canon is not None and window is None:
-                    cw, csl, osl, kuhn = r.pair_canon
-                    if kuhn:  # compile-time stream: edge vectors in registers
-                        _lib.call("fpb_assemble_gradient_pairs_kuhn", r.n, int(csl.numel()), csl.data_ptr(), xyz4,
-                                  self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, acc,
-                                  out.data_ptr(), _lib.stream())
+                    pc = r.pair_canon
+                    rp_, ci_ = self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr()
+                    if pc["kuhn"]:  # compile-time stream, edge vectors in registers; the rest masked
+                        _lib.call("fpb_assemble_gradient_pairs_kuhn", int(pc["rows"].numel()), pc["rows"].data_ptr(),
+                                  xyz4, rp_, ci_, nnz, acc, out.data_ptr(), _lib.stream())
+                        _lib.call("fpb_assemble_gradient_pairs_rows", r.n, int(pc["other"].numel()),
+                                  pc["other"].data_ptr(), r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4, rp_,
+                                  ci_, nnz, r.rowcap, acc, out.data_ptr(), _lib.stream())
                     else:
+                        cw = pc["words"]
                         global _PAIR_CANON_LOADED
                         if _PAIR_CANON_LOADED is not cw:  # constant memory: upload when the stream changes
                             torch.cuda.current_stream().synchronize()
                             _lib.call("fpb_pair_canon_set", cw.ctypes.data, int(cw.size))
                             _PAIR_CANON_LOADED = cw
-                    for sl, clen in (((osl, 0),) if kuhn else ((csl, int(cw.size)), (osl, 0))):
-                        _lib.call("fpb_assemble_gradient_pairs_slices", r.n, int(sl.numel()), sl.data_ptr(), clen,
-                                  r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4,
-                                  self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr(), nnz, r.rowcap,
-                                  acc, out.data_ptr(), _lib.stream())
+                        for sl, clen in ((pc["cslices"], int(cw.size)), (pc["oslices"], 0)):
+                            _lib.call("fpb_assemble_gradient_pairs_slices", r.n, int(sl.numel()), sl.data_ptr(),
+                                      clen, r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4, rp_, ci_, nnz,
+                                      r.rowcap, acc, out.data_ptr(), _lib.stream())
                 else:
                     _lib.call("fpb_assemble_gradient_pairs", r.n, r0, r1, r.pairs[0].data_ptr(),
                               r.pairs[1].data_ptr(), xyz4, self.pattern.rowptr_d.data_ptr(),

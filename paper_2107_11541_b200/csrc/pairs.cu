@@ -189,17 +189,28 @@ __global__ void k_pair_stream(int32_t n, const int32_t* __restrict__ slice_ptr, 
 // stored once at its CSR position.
 template <bool CANON>
 __global__ void __launch_bounds__(32, 1)
-k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, int canon_len,
-             const int64_t* __restrict__ pair_ptr, const uint16_t* __restrict__ words,
+k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, const int32_t* __restrict__ rlist,
+             int32_t nlist, int canon_len, const int64_t* __restrict__ pair_ptr, const uint16_t* __restrict__ words,
              const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
              int64_t nnz, int rowcap, int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, T = 32;
   constexpr int SS = DIM * T;  // doubles per slot in each region
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
-  // rows: the 32-row slice slist[block] (slice lists), else row0 + 32 block
-  const int row = (slist ? __ldg(slist + blockIdx.x) * T : row0 + blockIdx.x * T) + tid;
-  const bool live = row < n;
+  // rows: a row list (rlist: any rows, each reading its own stream; the
+  // generic rows next to the Kuhn kernel's), the 32-row slice slist[block],
+  // else row0 + 32 block
+  const bool listed = rlist != nullptr;
+  int row;
+  bool live;
+  if (listed) {
+    const int64_t i = (int64_t)blockIdx.x * T + tid;
+    live = i < nlist;
+    row = __ldg(rlist + (live ? i : 0));
+  } else {
+    row = (slist ? __ldg(slist + blockIdx.x) : row0 / T + blockIdx.x) * T + tid;
+    live = row < n;
+  }
   const int lane = row & 31;
   const int64_t p0 = CANON ? 0 : __ldg(pair_ptr + (row >> 5));
   // stream words of the slice
@@ -222,6 +233,7 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, int can
   double* __restrict__ Bo = sm + nslot * SS;          // [3][32 rowcap]
   const int bstride = 32 * rowcap;
   const int base = __shfl_sync(0xffffffffu, rlo, 0);
+  const int boff = listed ? tid * rowcap : rlo - base;  // this row's first entry in Bo
 
   // ---- pair stream: the first two batches are requested before staging so
   // their latency hides behind it ----
@@ -318,7 +330,7 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, int can
       if (w & (1u << 14)) {  // column finished: store once, fold into the diagonal
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          Bo[d * bstride + rlo - base + target + (target >= dslot)] = mN0 * acc[d];
+          Bo[d * bstride + boff + target + (target >= dslot)] = mN0 * acc[d];
           tot[d] += acc[d];
           acc[d] = 0.0;
         }
@@ -346,15 +358,29 @@ k_rows_pairs(int32_t n, int32_t row0, const int32_t* __restrict__ slist, int can
   const int span = wend - base;  // <= 32 rowcap
   if (live) {
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) Bo[k * bstride + rlo - base + dslot] = dacc[k];
+    for (int k = 0; k < DIM; ++k) Bo[k * bstride + boff + dslot] = dacc[k];
   }
   __syncwarp();
+  if (!listed) {
 #pragma unroll
-  for (int k = 0; k < DIM; ++k) {
-    double* o = out + k * nnz + base;
-    for (int q = wlane; q < span; q += 32) {
-      const double v = Bo[k * bstride + q];
-      o[q] = accumulate ? o[q] + v : v;
+    for (int k = 0; k < DIM; ++k) {
+      double* o = out + k * nnz + base;
+      for (int q = wlane; q < span; q += 32) {
+        const double v = Bo[k * bstride + q];
+        o[q] = accumulate ? o[q] + v : v;
+      }
+    }
+  } else {  // listed rows are not consecutive: row by row (Bo slot rr rowcap)
+    for (int rr = 0; rr < 32; ++rr) {
+      const int lo = __shfl_sync(0xffffffffu, rlo, rr), len = __shfl_sync(0xffffffffu, rlen, rr);
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        double* o = out + k * nnz + lo;
+        for (int q = wlane; q < len; q += 32) {  // len = 0 for padding lanes
+          const double v = Bo[k * bstride + rr * rowcap + q];
+          o[q] = accumulate ? o[q] + v : v;
+        }
+      }
     }
   }
 }
@@ -388,16 +414,16 @@ constexpr int kKuhnWarps = 2;  // warps (32-row slices) per CTA
 #define FPB_KUHN_MINB 6
 #endif
 __global__ void __launch_bounds__(32 * kKuhnWarps, FPB_KUHN_MINB)
-k_rows_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* __restrict__ slist, const double* __restrict__ xyz4,
+k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz,
                   int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, R = kKuhnCols + 1;  // entries per row
   __shared__ double Bo[kKuhnWarps][DIM][32 * R];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int si = blockIdx.x * kKuhnWarps + warp;
-  if (si >= nslices) return;
-  const int row = __ldg(slist + si) * 32 + lane;
-  const bool live = row < n;
+  const int64_t i0 = ((int64_t)blockIdx.x * kKuhnWarps + warp) * 32;  // the warp's 32 list entries
+  if (i0 >= nrows) return;
+  const bool live = i0 + lane < nrows;
+  const int row = live ? __ldg(rows + i0 + lane) : -1;
   const int rlo = live ? __ldg(rowptr + row) : 0;
   const int base = __shfl_sync(0xffffffffu, rlo, 0);
   // the diagonal sits at CSR offset kKuhnDiag of every canonical row (the
@@ -446,18 +472,35 @@ k_rows_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* __restrict__ slist,
 #pragma unroll
   for (int d = 0; d < DIM; ++d) bo[d * 32 * R + lane * R + dslot] = -(mN0 * tot[d]);
   __syncwarp();
-  // the slice's 32 rows are consecutive with 15 entries each: one contiguous
-  // CSR range of 480 values per matrix
   int nlive = live ? lane + 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nlive = max(nlive, __shfl_xor_sync(0xffffffffu, nlive, o));
-  const int span = nlive * R;
+  const int last = __shfl_sync(0xffffffffu, row, nlive - 1), first = __shfl_sync(0xffffffffu, row, 0);
+  if (last - first == nlive - 1) {
+    // consecutive rows (15 entries each): one contiguous CSR range per matrix
+    const int span = nlive * R;
 #pragma unroll
-  for (int d = 0; d < DIM; ++d) {
-    double* o = out + d * nnz + base;
-    for (int j = lane; j < span; j += 32) {
-      const double v = bo[d * 32 * R + j];
-      o[j] = accumulate ? o[j] + v : v;
+    for (int d = 0; d < DIM; ++d) {
+      double* o = out + d * nnz + base;
+      for (int j = lane; j < span; j += 32) {
+        const double v = bo[d * 32 * R + j];
+        o[j] = accumulate ? o[j] + v : v;
+      }
+    }
+  } else {
+    // gaps (boundary rows between): two 15-entry rows per warp instruction
+    const int half = lane >> 4, j = lane & 15;
+    for (int r0 = 0; r0 < nlive; r0 += 2) {  // warp-uniform trip count (the shuffle needs every lane)
+      const int rr = r0 + half;
+      const int lo = __shfl_sync(0xffffffffu, rlo, rr & 31);
+      if (rr < nlive && j < R) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          double* o = out + d * nnz + lo + j;
+          const double v = bo[d * 32 * R + rr * R + j];
+          *o = accumulate ? *o + v : v;
+        }
+      }
     }
   }
 }
@@ -521,7 +564,26 @@ int fpb_assemble_gradient_pairs(int32_t n, int32_t row0, int32_t row1, const int
   if (smem > 48 * 1024)
     FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_rows_pairs<false><<<(unsigned)((row1 - row0 + 31) / 32), 32, smem, s>>>(
-      row1, row0, nullptr, 0, pair_ptr, words, xyz4, rowptr, colind, nnz, rowcap, accumulate, out);
+      row1, row0, nullptr, nullptr, 0, 0, pair_ptr, words, xyz4, rowptr, colind, nnz, rowcap, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_assemble_gradient_pairs_rows(int32_t n, int32_t nrows, const int32_t* rows, const int64_t* pair_ptr,
+                                     const uint16_t* words, const double* xyz4, const int32_t* rowptr,
+                                     const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
+                                     void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(rows && pair_ptr && words && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
+              "pair-stream row-list assembly needs the stream, the CSR pattern and rows <= 129 entries");
+  if (nrows <= 0) return FPB_OK;
+  cudaStream_t s = as_stream(stream);
+  const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
+  if (smem > 48 * 1024)
+    FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_rows_pairs<false><<<(unsigned)((nrows + 31) / 32), 32, smem, s>>>(n, 0, nullptr, rows, nrows, 0, pair_ptr, words,
+                                                                      xyz4, rowptr, colind, nnz, rowcap, accumulate,
+                                                                      out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -531,14 +593,14 @@ int fpb_pair_kuhn_table(uint16_t* words_h) {
   return kKuhnWords;
 }
 
-int fpb_assemble_gradient_pairs_kuhn(int32_t n, int32_t nslices, const int32_t* slist, const double* xyz4,
-                                     const int32_t* rowptr, const int32_t* colind, int64_t nnz, int accumulate,
-                                     double* out, void* stream) {
+int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const double* xyz4, const int32_t* rowptr,
+                                     const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
-  FPB_REQUIRE(slist && xyz4 && rowptr && colind && out, "missing arrays for the Kuhn-stream kernel");
-  if (nslices <= 0) return FPB_OK;
-  k_rows_pairs_kuhn<<<(unsigned)((nslices + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
-      n, nslices, slist, xyz4, rowptr, colind, nnz, accumulate, out);
+  FPB_REQUIRE(rows && xyz4 && rowptr && colind && out, "missing arrays for the Kuhn-stream kernel");
+  if (nrows <= 0) return FPB_OK;
+  const int64_t warps = ((int64_t)nrows + 31) / 32;
+  k_rows_pairs_kuhn<<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
+      nrows, rows, xyz4, rowptr, colind, nnz, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -564,13 +626,13 @@ int fpb_assemble_gradient_pairs_slices(int32_t n, int32_t nslices, const int32_t
   if (canon_len > 0) {
     if (smem > 48 * 1024)
       FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_rows_pairs<true><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, canon_len, nullptr, nullptr, xyz4, rowptr,
-                                                           colind, nnz, rowcap, accumulate, out);
+    k_rows_pairs<true><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, nullptr, 0, canon_len, nullptr, nullptr,
+                                                           xyz4, rowptr, colind, nnz, rowcap, accumulate, out);
   } else {
     if (smem > 48 * 1024)
       FPB_CUDA(cudaFuncSetAttribute(k_rows_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_rows_pairs<false><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, 0, pair_ptr, words, xyz4, rowptr, colind,
-                                                            nnz, rowcap, accumulate, out);
+    k_rows_pairs<false><<<(unsigned)nslices, 32, smem, s>>>(n, 0, slist, nullptr, 0, 0, pair_ptr, words, xyz4,
+                                                            rowptr, colind, nnz, rowcap, accumulate, out);
   }
   FPB_LAUNCH_CHECK();
   return FPB_OK;

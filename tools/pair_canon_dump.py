@@ -14,6 +14,10 @@ for n in (40, 64):
     out = torch.empty(3 * ctx.pattern.nnz, dtype=torch.float64, device="cuda")
     ctx.assemble_gradients_d(out)
     r = ctx.groups[0].rows
-    cw, csl, osl = r.pair_canon
-    print(n, "len", cw.size, "canonical slices", csl.numel(), "other", osl.numel(), "rowcap", r.rowcap)
+    pc = r.pair_canon
+    cw = pc["words"]
+    if pc["kuhn"]:
+        print(n, "len", cw.size, "kuhn rows", pc["rows"].numel(), "of", r.n, "generic rows", pc["other"].numel())
+    else:
+        print(n, "len", cw.size, "canonical slices", pc["cslices"].numel(), "other", pc["oslices"].numel())
     print("words", ",".join(f"0x{int(w):04x}" for w in cw))
