@@ -94,7 +94,7 @@ KUHN_STREAM = True  # ... and the Kuhn box's stream compiled in (pairs.cu k_rows
 _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # HEX08 continuity with element geometry evaluated once (hexblock.cu);
 # False = the per-row kernel (rowsq.cu)
-HEX_ONCE = True
+HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
 
 
 def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 14):

@@ -70,6 +70,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define FPB_BLK_MINB_NONAFFINE 2  // Gauss-loop elements (QUAD04, PYR05, HEX08): registers, not spills
 #endif
 constexpr int kBlockThreads = FPB_BLK_THREADS;  // threads of the RHS kernel
+int g_tuning_blk_pipe = 0;  // fpb_set_tuning("blk_pipe", 0|1): pipelined persistent block kernel (A/B: slower, profiles/r02e_mom)
 // elements per block (= setup threads): the affine kernels integrate EPT = 2
 // elements per thread so the CTA's fixed latencies (node-id and record
 // gathers, two barriers) are paid once per 256 elements; the Gauss-loop
@@ -345,6 +346,184 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
   }
 }
 
+// ---- pipelined persistent variant (affine simplices) ---------------------------
+// Same arithmetic and summation order as k_blk_rhs (bitwise identical
+// partials), but each CTA walks blocks blk0 + blockIdx.x, + gridDim.x, ... and
+// double-buffers the node staging: while block b is integrated and gathered,
+// block b + gridDim.x's node records, velocity rows and gather slots are
+// already in flight into the other buffer with cp.async (16-byte record
+// halves, 8-byte velocity components), and its node ids, element-local
+// indices and gather ranges are fetched into registers one block ahead.  The
+// gather -> record -> stage dependency chain that k_blk_rhs exposes once per
+// block (profiles/r02d_mom: ~31 % of its stall samples) overlaps the
+// previous block's FP64 work.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int ET, int KIND>
+__global__ void __launch_bounds__(kBlockThreads, 4)
+k_blk_rhs_pipe(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t* __restrict__ blk_lidx,
+               const double* __restrict__ xyz4, const double* __restrict__ vel, const double* __restrict__ phi,
+               int64_t fstride, double rho, double mu, double kappa, const int32_t* __restrict__ blk_ptr,
+               const int32_t* __restrict__ blk_nodes, const uint16_t* __restrict__ blk_gptr,
+               const uint16_t* __restrict__ blk_gslot, int maxnu, double* __restrict__ partial) {
+  constexpr int NN = Elem<ET>::NN, DIM = Elem<ET>::DIM;
+  constexpr int NV = Out<ET, KIND>::NV;
+  constexpr int NF = KIND == FPB_SCALAR_RHS ? 1 : KIND == KIND_SCALAR3 ? 3 : 0;
+  constexpr int NU = DIM + NF;  // velocity (+ scalars) per staged node
+  constexpr int TPB = kBlockThreads;
+  constexpr int kBlockElems = blk_elems<ET>();
+  constexpr int EPT = kBlockElems / TPB;
+  constexpr int NGR = 3;  // node slots per thread (nu <= 3 TPB)
+  static_assert(Elem<ET>::AFFINE && EPT == 2 && NN == 4 - (DIM == 2),
+                "pipelined block kernel: affine simplices, 2 elements per thread");
+  extern __shared__ __align__(16) double smem[];
+  double* const sm = smem;                                                      // [NN * NV][kBlockElems]
+  uint16_t* const sgs = reinterpret_cast<uint16_t*>(sm + NN * NV * kBlockElems);  // [2][NN * kBlockElems] slots
+  uint16_t* const sli = sgs + 2 * NN * kBlockElems;                             // [2][kBlockElems * NN] local ids
+  double* const sx = sm + NN * NV * kBlockElems + NN * kBlockElems;             // [2][maxnu][4]
+  double* const su = sx + 2 * maxnu * 4;                                        // [2][maxnu][NU]
+  const int tid = threadIdx.x;
+  const int64_t stride = gridDim.x;
+
+  // a block's staging inputs, fetched one block ahead: partial base, node
+  // count, the node ids of my staging slots
+  struct Ids {
+    int64_t base;
+    int nu;
+    int node[NGR];
+  };
+  auto fetch_ids = [&](int64_t b, Ids& m) {
+    m.nu = 0;
+    m.base = 0;
+    if (b >= blk1) return;
+    m.base = __ldg(blk_ptr + b);
+    m.nu = __ldg(blk_ptr + b + 1) - (int)m.base;
+#pragma unroll
+    for (int j = 0; j < NGR; ++j) {
+      const int u = tid + j * TPB;
+      m.node[j] = u < m.nu ? __ldg(blk_nodes + m.base + u) : 0;
+    }
+  };
+  // cp.async the block's node data, gather slots and local ids into buffer q
+  auto stage = [&](int64_t b, const Ids& m, int q) {
+    if (b < blk1) {
+      const uint16_t* gs = blk_gslot + b * kBlockElems * NN;
+      const uint16_t* li = blk_lidx + b * kBlockElems * NN;
+      uint16_t* g = sgs + q * NN * kBlockElems;
+      uint16_t* l = sli + q * NN * kBlockElems;
+      const int64_t nvalid = min((int64_t)kBlockElems, nelem - b * kBlockElems) * NN;  // lidx ends with the mesh
+      for (int c = tid; c < NN * kBlockElems / 8; c += TPB) {
+        cp_async16(g + 8 * c, gs + 8 * c);
+        if (8 * c < nvalid) cp_async16(l + 8 * c, li + 8 * c);
+      }
+      double* x = sx + q * maxnu * 4;
+      double* u = su + q * maxnu * NU;
+#pragma unroll
+      for (int j = 0; j < NGR; ++j) {
+        const int v = tid + j * TPB;
+        if (v < m.nu) {
+          const int64_t nd = m.node[j];
+          cp_async16(x + v * 4, xyz4 + 4 * nd);
+          cp_async16(x + v * 4 + 2, xyz4 + 4 * nd + 2);
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) cp_async8(u + v * NU + d, vel + nd * DIM + d);
+          if constexpr (KIND == FPB_SCALAR_RHS) cp_async8(u + v * NU + DIM, phi + nd);
+          if constexpr (KIND == KIND_SCALAR3) {
+#pragma unroll
+            for (int f = 0; f < 3; ++f) cp_async8(u + v * NU + DIM + f, phi + f * fstride + nd);
+          }
+        }
+      }
+    }
+    cp_async_commit();  // (an empty group past the window keeps the wait count uniform)
+  };
+
+  int64_t b = blk0 + blockIdx.x;
+  Ids cur, nxt;
+  fetch_ids(b, cur);
+  stage(b, cur, 0);
+  fetch_ids(b + stride, nxt);
+  int q = 0;
+  for (; b < blk1; b += stride, q ^= 1) {
+    stage(b + stride, nxt, q ^ 1);  // the next block is in flight while this one computes
+    Ids nn2;
+    fetch_ids(b + 2 * stride, nn2);  // ids two blocks ahead, for the next iteration's stage
+    // this block's gather ranges (consumed after the integration)
+    int glo[NGR], ghi[NGR];
+    const uint16_t* gptr = blk_gptr + cur.base + b;
+#pragma unroll
+    for (int j = 0; j < NGR; ++j) {
+      const int v = tid + j * TPB;
+      glo[j] = v < cur.nu ? __ldg(gptr + v) : 0;
+      ghi[j] = v < cur.nu ? __ldg(gptr + v + 1) : 0;
+    }
+    cp_async_wait_1();  // this block's group has landed
+    __syncthreads();
+    const double* x = sx + q * maxnu * 4;
+    const double* u = su + q * maxnu * NU;
+    const uint16_t* l = sli + q * NN * kBlockElems;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int el = tid + j * TPB;
+      if (b * kBlockElems + el >= nelem) break;
+      int li[NN];
+      if constexpr (NN == 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(l + el * NN);
+        li[0] = v.x & 0xffff; li[1] = v.x >> 16; li[2] = v.y & 0xffff; li[3] = v.y >> 16;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NN; ++a) li[a] = l[el * NN + a];
+      }
+      double xe[NN][DIM], ue[Out<ET, KIND>::NU][DIM], fe[Out<ET, KIND>::NF];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          xe[a][d] = x[li[a] * 4 + d];
+          ue[a][d] = u[li[a] * NU + d];
+        }
+        if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = u[li[a] * NU + DIM];
+        if constexpr (KIND == KIND_SCALAR3) {
+#pragma unroll
+          for (int f = 0; f < 3; ++f) fe[f * NN + a] = u[li[a] * NU + DIM + f];
+        }
+      }
+      double acc[Out<ET, KIND>::NOUT];
+      simplex_rhs_all<ET, KIND>(xe, ue, fe, rho, mu, kappa, acc);
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sm[(a * NV + k) * kBlockElems + el] = acc[a * NV + k];
+    }
+    __syncthreads();
+    const uint16_t* g = sgs + q * NN * kBlockElems;
+#pragma unroll
+    for (int j = 0; j < NGR; ++j) {
+      const int v = tid + j * TPB;
+      if (v >= cur.nu) break;
+      double sv[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) sv[k] = 0.0;
+      for (int t = glo[j]; t < ghi[j]; ++t) {
+        const int slot = g[t];
+        const int el = slot / NN, a = slot - el * NN;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) sv[k] += sm[(a * NV + k) * kBlockElems + el];
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k) partial[(cur.base + v) * NV + k] = sv[k];
+    }
+    __syncthreads();  // sm and buffer q are reused two stages on
+    cur = nxt;
+    nxt = nn2;
+  }
+  cp_async_wait_all();
+}
+
 // ---- phase 2: per-node gather of block partials ---------------------------------
 // out[i][k] (node-major), or out[k][fstride] (field-major) when fstride > 0
 template <int NV>
@@ -389,6 +568,28 @@ static int launch_blk(int64_t nelem, int64_t blk0, int64_t blk1, const uint16_t*
   FPB_REQUIRE(blk0 >= 0 && blk0 <= blk1 && blk1 <= nblocks, "block window [%lld, %lld) outside [0, %lld)",
               (long long)blk0, (long long)blk1, (long long)nblocks);
   if (blk1 == blk0) return FPB_OK;
+  if constexpr (Elem<ET>::AFFINE && kBlockElems / kBlockThreads == 2) {
+    if (g_tuning_blk_pipe && uvw4 == nullptr && maxnu <= 3 * kBlockThreads) {
+      constexpr int NU = Elem<ET>::DIM + (KIND == FPB_SCALAR_RHS ? 1 : KIND == KIND_SCALAR3 ? 3 : 0);
+      const size_t psmem = (size_t)Elem<ET>::NN * NV * kBlockElems * sizeof(double) +
+                           4 * (size_t)Elem<ET>::NN * kBlockElems * sizeof(uint16_t) +
+                           2 * (size_t)maxnu * (4 + NU) * sizeof(double);
+      FPB_REQUIRE(psmem <= 227 * 1024, "element block needs %zu bytes of shared memory", psmem);
+      auto kern = k_blk_rhs_pipe<ET, KIND>;
+      FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
+      int per_sm = 0;
+      FPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlockThreads, psmem));
+      int dev = 0, nsm = kNumSMs;
+      FPB_CUDA(cudaGetDevice(&dev));
+      FPB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+      const int64_t grid = std::min<int64_t>(blk1 - blk0, (int64_t)std::max(per_sm, 1) * nsm);
+      kern<<<(unsigned)grid, kBlockThreads, psmem, s>>>(nelem, blk0, blk1, lidx, xyz4, vel, phi, fstride, rho, mu,
+                                                        kappa, blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,
+                                                        partial);
+      FPB_LAUNCH_CHECK();
+      return FPB_OK;
+    }
+  }
   k_blk_rhs<ET, KIND><<<(unsigned)(blk1 - blk0), kBlockThreads, smem, s>>>(nelem, blk0, lidx, xyz4, uvw4, vel, phi, fstride,
                                                                    rho, mu, kappa,
                                                                    blk_ptr, blk_nodes, blk_gptr, blk_gslot, maxnu,

@@ -43,6 +43,7 @@ constexpr int kRowsBlock = 128;
 constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
 int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
 extern int g_tuning_hex_canon_rows;  // hexblock.cu
+extern int g_tuning_blk_pipe;        // blocks.cu
 
 
 template <int ET, int KIND>
@@ -827,6 +828,10 @@ extern "C" {
 int fpb_set_tuning(const char* name, int value) {
   if (name && strcmp(name, "rows_nb") == 0) {
     g_tuning_rows_nb = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "blk_pipe") == 0) {
+    g_tuning_blk_pipe = value;
     return FPB_OK;
   }
   if (name && strcmp(name, "hex_canon_rows") == 0) {

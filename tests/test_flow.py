@@ -134,7 +134,12 @@ def test_two_steps_match_reference(case):
     st = _initial(P, name, mesh, g)
     for k in (1, 2):
         st, diag = solver.step(st)
-        assert abs(diag.solver.iterations - int(g[f"s{k}_iterations"])) <= 1
+        # iteration parity only for a well-posed pressure RHS: with a uniform
+        # velocity (hex_uniform) the predicted divergence is round-off, and
+        # the iteration count of a solve to tol on round-off measures how the
+        # continuity matrices' last bits fall, not the solver
+        if diag.div_star > 1e-12:
+            assert abs(diag.solver.iterations - int(g[f"s{k}_iterations"])) <= 1
         for f in ("velocity", "pressure", "heat", "species"):
             # the pressure solve runs to tol (1e-12 / 1e-13) on both sides
             assert _close(getattr(st, f), g[f"s{k}_{f}"]), (name, k, f)
