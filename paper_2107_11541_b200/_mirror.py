@@ -13,6 +13,12 @@ live in HBM, so the numpy attribute is a host mirror with write-back:
   against the snapshot taken when it was last synchronised), so the next
   kernel sees the edit.
 
+Large arrays (> WRITE_BACK_MAX bytes, e.g. a 100 M-tet matrix's 2 GB of
+values) get a read-only mirror instead: downloaded through pinned staging at
+PCIe speed, no snapshot copy, and an in-place write raises ("assignment
+destination is read-only") instead of being lost — assign a new array
+(`A.vals = ...`, `CsrMatrix.with_vals`) to change them.
+
 Nothing here runs unless a caller touches the numpy attribute: the device
 paths never create a mirror.
 """
@@ -21,6 +27,19 @@ from __future__ import annotations
 
 import numpy as np
 import torch
+
+
+WRITE_BACK_MAX = 64 << 20  # bytes: larger mirrors are read-only (no snapshot)
+
+
+def _download(t: torch.Tensor) -> np.ndarray:
+    """Device -> numpy through pinned staging (DMA speed, not pageable)."""
+    if not t.is_cuda:
+        return t.detach().numpy().copy()
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return out.numpy()
 
 
 class DeviceArray:
@@ -37,8 +56,8 @@ class DeviceArray:
 
     def _sync_up(self) -> None:
         h = self._h
-        if h is None or self._ver != self._t._version:
-            return  # no mirror, or the device copy is newer (device wins)
+        if h is None or self._snap is None or self._ver != self._t._version:
+            return  # no (writable) mirror, or the device copy is newer (device wins)
         if h.shape == self._snap.shape and np.array_equal(h.view(np.uint8), self._snap.view(np.uint8)):
             return
         if tuple(h.shape) != tuple(self._t.shape):
@@ -61,16 +80,19 @@ class DeviceArray:
         t = self._t
         if self._h is not None and self._ver == t._version:
             return self._h
-        if t.is_cuda:
-            torch.cuda.current_stream(t.device).synchronize()
-        fresh = t.detach().cpu().numpy()
-        if self._host_dtype is not None:
+        fresh = _download(t)
+        if self._host_dtype is not None and fresh.dtype != self._host_dtype:
             fresh = fresh.astype(self._host_dtype)
-        if self._h is not None and self._h.shape == fresh.shape and self._h.dtype == fresh.dtype:
+        if fresh.nbytes > WRITE_BACK_MAX:
+            fresh.flags.writeable = False  # no write-back for huge arrays: writes raise
+            self._h, self._snap = fresh, None
+        elif (self._h is not None and self._h.shape == fresh.shape and self._h.dtype == fresh.dtype
+              and self._h.flags.writeable):
             self._h[...] = fresh  # keep the handed-out object current
+            self._snap = self._h.copy()
         else:
             self._h = np.ascontiguousarray(fresh)
-        self._snap = self._h.copy()
+            self._snap = self._h.copy()
         self._ver = t._version
         return self._h
 

@@ -134,11 +134,14 @@ def test_two_steps_match_reference(case):
     st = _initial(P, name, mesh, g)
     for k in (1, 2):
         st, diag = solver.step(st)
-        # iteration parity only for a well-posed pressure RHS: with a uniform
-        # velocity (hex_uniform) the predicted divergence is round-off, and
-        # the iteration count of a solve to tol on round-off measures how the
-        # continuity matrices' last bits fall, not the solver
-        if diag.div_star > 1e-12:
+        if diag.solver.iterations == 0 and diag.solver.residual_history == [0.0]:
+            # exactly zero pressure RHS: a uniform velocity (hex_uniform) has
+            # zero interior divergence, which the continuity matrices here
+            # cancel exactly and the reference's to round-off — its solve
+            # then iterates on noise; the increment must be round-off there
+            prev = g["s0_pressure"] if k == 1 else g[f"s{k - 1}_pressure"]
+            assert np.abs(g[f"s{k}_pressure"] - prev).max() < 1e-10
+        else:
             assert abs(diag.solver.iterations - int(g[f"s{k}_iterations"])) <= 1
         for f in ("velocity", "pressure", "heat", "species"):
             # the pressure solve runs to tol (1e-12 / 1e-13) on both sides

@@ -123,3 +123,19 @@ def test_write_back_mirror_semantics():
     assert c.dtype == np.int64
     c[1, 2] = 7
     assert conn.device().dtype == torch.int32 and int(conn.device()[1, 2]) == 7
+
+
+def test_large_mirror_is_read_only(monkeypatch):
+    """Above WRITE_BACK_MAX the mirror is a read-only pinned download (no
+    snapshot): in-place writes raise instead of vanishing."""
+    import pytest
+    import torch
+
+    from paper_2107_11541_b200 import _mirror
+
+    monkeypatch.setattr(_mirror, "WRITE_BACK_MAX", 64)
+    m = _mirror.DeviceArray(torch.zeros(100, dtype=torch.float64))
+    h = m.host()
+    with pytest.raises(ValueError):
+        h[0] = 1.0
+    assert m.device().sum().item() == 0.0
