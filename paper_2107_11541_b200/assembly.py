@@ -95,6 +95,7 @@ _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # HEX08 continuity with element geometry evaluated once (hexblock.cu);
 # False = the per-row kernel (rowsq.cu)
 HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
+HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))  # y-band of canonical hex rows (0 = natural order)
 
 
 def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 14):
@@ -249,7 +250,7 @@ class HexRowPlan:
 
     GEN_ROWS = 32
 
-    def __init__(self, rows: RowPlan, nelem: int, rowcap: int):
+    def __init__(self, rows: RowPlan, nelem: int, rowcap: int, coords_d: torch.Tensor | None = None):
         lib = _lib.load()
         dev = rows.slice_ptr.device
         n = rows.n
@@ -287,10 +288,21 @@ class HexRowPlan:
                     want[m, d] = tab[m, d] - (tab[m, d] > 13)  # off-diagonal index (diagonal = 13)
             want_w = torch.as_tensor(want.view(np.int64).reshape(8), device=dev)
             canon = valid.all(dim=1) & (words == want_w[None, :]).all(dim=1)
-        # natural row order: a warp's lanes read consecutive elements' H (one
-        # 256-byte run per plane) and a CTA's rows are mostly one contiguous
-        # CSR range (Morton-brick order measured 1.7x slower, profiles/r02c_hex)
+        # row order: x-lines stay whole (a warp's lanes read consecutive
+        # elements' H, one 256-byte run per plane, and a CTA's rows are mostly
+        # one contiguous CSR range — Morton bricks measured 1.7x slower,
+        # profiles/r02c_hex), but lines are visited in y-bands of HEX_BAND
+        # lines, z inside the band: each element's 8 rows (2 lines x 2
+        # planes) then fall within a few lines of each other instead of a
+        # whole node plane apart, so H is read ~once from HBM, not ~1.6x
         crow = torch.nonzero(canon).flatten()
+        if coords_d is not None and HEX_BAND > 0 and crow.numel():
+            rk = [torch.unique(coords_d[:, d], return_inverse=True)[1].to(torch.int64) for d in range(3)]
+            rx, ry, rz = (r[crow] for r in rk)
+            nzr = int(rk[2].max()) + 1
+            nxr = int(rk[0].max()) + 1
+            key = (((ry // HEX_BAND) * nzr + rz) * HEX_BAND + ry % HEX_BAND) * nxr + rx
+            crow = crow[torch.argsort(key, stable=True)]
         self.ncanon = int(crow.numel())
         self.canon_rows = crow.to(torch.int32).contiguous()
         self.canon_inc8 = inc[crow].t().contiguous().to(torch.int32) if self.ncanon else \
@@ -627,7 +639,7 @@ class AssemblyContext:
 
     def _hexrows(self, g: GroupData) -> HexRowPlan:
         if g.hexrows is None:
-            g.hexrows = HexRowPlan(g.rows, g.nelem, g.rows.rowcap)
+            g.hexrows = HexRowPlan(g.rows, g.nelem, g.rows.rowcap, self.mesh.coords_d)
         return g.hexrows
 
     def assemble_matrix_d(self, kind: KernelKind, velocity_d: torch.Tensor | None,
