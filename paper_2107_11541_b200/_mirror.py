@@ -25,6 +25,8 @@ paths never create a mirror.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 import torch
 
@@ -45,10 +47,14 @@ def _download(t: torch.Tensor) -> np.ndarray:
 class DeviceArray:
     """A device tensor plus an optional write-back numpy mirror."""
 
-    __slots__ = ("_t", "_host_dtype", "_h", "_snap", "_ver")
+    __slots__ = ("_tt", "_weak", "_host_dtype", "_h", "_snap", "_ver")
 
-    def __init__(self, t: torch.Tensor, host_dtype=None):
-        self._t = t
+    def __init__(self, t: torch.Tensor, host_dtype=None, weak: bool = False):
+        """weak = True: hold the tensor by weak reference (a registry keyed by
+        the tensor — sparse._vals_store — must not keep its key alive; the
+        owners hold the tensor)."""
+        self._weak = weak
+        self._tt = weakref.ref(t) if weak else t
         self._host_dtype = np.dtype(host_dtype) if host_dtype is not None else None
         self._h = None
         self._snap = None
@@ -72,8 +78,12 @@ class DeviceArray:
         self._sync_up()
         return self._t
 
+    @property
+    def _t(self) -> torch.Tensor:
+        return self._tt() if self._weak else self._tt
+
     def set_device(self, t: torch.Tensor) -> None:
-        self._t = t
+        self._tt = weakref.ref(t) if self._weak else t
         self._h = self._snap = self._ver = None
 
     def host(self) -> np.ndarray:

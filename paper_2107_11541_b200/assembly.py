@@ -95,7 +95,10 @@ _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # HEX08 continuity with element geometry evaluated once (hexblock.cu);
 # False = the per-row kernel (rowsq.cu)
 HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
-HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))  # y-band of canonical hex rows (0 = natural order)
+HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))
+# element blocks of the RHS kernels over Morton-ordered elements (BlockPlan);
+# slab domains keep natural order (their interface windows are block ranges)
+BLOCK_MORTON = os.environ.get("FPB_BLOCK_MORTON", "0") != "0"  # measured slower (profiles/r02e_mom)  # y-band of canonical hex rows (0 = natural order)
 
 
 def _pair_canon(n: int, ptr: torch.Tensor, words: torch.Tensor, rowptr=None, colind=None, chunk: int = 1 << 14):
@@ -330,14 +333,37 @@ class HexRowPlan:
                   pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), s)
 
 
+def _centroid_morton(conn_d: torch.Tensor, coords_d: torch.Tensor) -> torch.Tensor:
+    """Element permutation in Morton order of the centroids (quantised to
+    2^20 levels per axis over the bounding box); setup only."""
+    dim = coords_d.shape[1]
+    c = coords_d.index_select(0, conn_d.reshape(-1).to(torch.int64)).reshape(conn_d.shape[0], conn_d.shape[1], dim)
+    c = c.mean(dim=1)
+    lo, hi = c.min(dim=0).values, c.max(dim=0).values
+    q = ((c - lo) / torch.clamp(hi - lo, min=1e-300) * ((1 << 20) - 1)).to(torch.int64)
+    key = torch.zeros(c.shape[0], dtype=torch.int64, device=c.device)
+    for bit in range(20):
+        for d in range(dim):
+            key |= ((q[:, d] >> bit) & 1) << (dim * bit + d)
+    return torch.argsort(key, stable=True)
+
+
 class BlockPlan:
     """Element blocks of one group for the deterministic two-phase RHS
     assembly (blocks.cu): per-block distinct nodes + sorted gather slots,
     and per-node lists of block partials."""
 
-    def __init__(self, conn_d: torch.Tensor, n: int, etype_id: int):
+    def __init__(self, conn_d: torch.Tensor, n: int, etype_id: int, coords_d: torch.Tensor | None = None):
         lib = _lib.load()
         ne, nn = int(conn_d.shape[0]), int(conn_d.shape[1])
+        if coords_d is not None and ne > 0:
+            # blocks of Morton-consecutive elements (by centroid): a block is
+            # a compact 3-D brick instead of a run of cells along x, so it
+            # touches fewer distinct nodes (staging) and leaves fewer
+            # per-(block, node) partials (the HBM round trip of phase 2).
+            # Only the blocks change — each element is still integrated once
+            # and every sum runs in a fixed order (bitwise reproducible).
+            conn_d = conn_d.index_select(0, _centroid_morton(conn_d, coords_d)).contiguous()
         be = int(lib.fpb_block_elems(etype_id))
         nblocks = -(-ne // be)
         dev = conn_d.device
@@ -442,13 +468,16 @@ class AssemblyContext:
 
     @classmethod
     def build(cls, mesh, vector_size: int = 8, scatter: str = "auto",
-              pattern: CsrMatrix | None = None) -> "AssemblyContext":
+              pattern: CsrMatrix | None = None, block_order: str = "morton") -> "AssemblyContext":
         """scatter selects the global-assembly strategy (scatter):
         "auto"   — matrices of affine simplices (TRI03, TET04): row-owned
                    kernels; RHS of every type: element blocks; matrices of
                    PYR05/HEX08/QUAD04: element kernels + FP64 reductions;
         "rows"   — row-owned kernels for every affine kind (RHS included);
         "atomic" — element kernels + FP64 reductions for everything.
+        block_order: "morton" (default) builds the RHS element blocks over
+            Morton-ordered elements; "natural" keeps the mesh order (slab
+            domains, whose interface-first windows are block ranges).
         pattern: an externally built CSR graph that contains every element
         node pair (e.g. a slab's graph including ghost elements,
         distributed.py); default: the mesh's own node graph."""
@@ -471,7 +500,8 @@ class AssemblyContext:
             lane32 = ps.lane_conn_d if cfg.vector_size == KERNEL_LANES else pack_lanes(g.conn_d, KERNEL_LANES)
             gd = GroupData(reference_element(g.etype), g.conn_d, offset, ps, lane32, pattern)
             if scatter == "auto":
-                gd.blocks = BlockPlan(g.conn_d, mesh.nnode, ETYPE_ID[g.etype])
+                gd.blocks = BlockPlan(g.conn_d, mesh.nnode, ETYPE_ID[g.etype],
+                                      mesh.coords_d if (block_order == "morton" and BLOCK_MORTON) else None)
             if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
                 gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time

@@ -297,7 +297,7 @@ class SlabDomain:
         ext = Mesh(3, coords, [ElementGroup(etype, conn)])
         pattern = build_node_pattern(ext)  # own + ghost elements
         own = Mesh(3, coords, [ElementGroup(etype, conn[e0:e1].contiguous())])
-        ctx = AssemblyContext.build(own, vector_size, pattern=pattern)
+        ctx = AssemblyContext.build(own, vector_size, pattern=pattern, block_order="natural")  # windows = block ranges
         return cls(L, own, ctx, group)
 
     def halo_sum_rhs(self, rhs: torch.Tensor) -> torch.Tensor:

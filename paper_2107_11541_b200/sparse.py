@@ -58,18 +58,23 @@ def _to_i32(x) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(_lib.device())
 
 
-_VALS_STORES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_VALS_STORES: dict = {}  # id(tensor) -> (weakref to the tensor, its DeviceArray)
 
 
 def _vals_store(t: torch.Tensor) -> DeviceArray:
     """One write-back mirror per device value array, shared by every
     CsrMatrix over it, so `reuse=True` aliasing (assembly.py:200-207: the
     matrices returned by reusing calls share one vals array) is observable
-    from numpy: `A.vals is B.vals`."""
-    st = _VALS_STORES.get(t)
-    if st is None:
-        st = DeviceArray(t)
-        _VALS_STORES[t] = st
+    from numpy: `A.vals is B.vals`.  Keyed by identity (a tensor's __eq__ is
+    elementwise, so no WeakKeyDictionary) and dropped with the tensor; the
+    mirror holds the tensor weakly, the CsrMatrix objects strongly."""
+    hit = _VALS_STORES.get(id(t))
+    if hit is not None and hit[0]() is t:
+        return hit[1]
+    st = DeviceArray(t, weak=True)
+    key = id(t)
+    _VALS_STORES[key] = (weakref.ref(t), st)
+    weakref.finalize(t, _VALS_STORES.pop, key, None)
     return st
 
 
@@ -82,7 +87,8 @@ class CsrMatrix:
         self.n = int(n)
         self.rowptr_d = rowptr if isinstance(rowptr, torch.Tensor) and rowptr.is_cuda and rowptr.dtype == torch.int32 else _to_i32(rowptr)
         self.colind_d = colind if isinstance(colind, torch.Tensor) and colind.is_cuda and colind.dtype == torch.int32 else _to_i32(colind)
-        self._vals = _vals_store(to_device(vals)[0])
+        self._vals_t = to_device(vals)[0]  # owns the device values
+        self._vals = _vals_store(self._vals_t)
         self._host = _host if _host is not None else {}
 
     @property
@@ -91,7 +97,8 @@ class CsrMatrix:
 
     @vals_d.setter
     def vals_d(self, t: torch.Tensor) -> None:
-        self._vals = _vals_store(to_device(t)[0])
+        self._vals_t = to_device(t)[0]
+        self._vals = _vals_store(self._vals_t)
 
     @property
     def nnz(self) -> int:
@@ -115,7 +122,8 @@ class CsrMatrix:
 
     @vals.setter
     def vals(self, value) -> None:
-        self._vals = _vals_store(to_device(value)[0])
+        self._vals_t = to_device(value)[0]
+        self._vals = _vals_store(self._vals_t)
 
     def copy(self) -> "CsrMatrix":
         return CsrMatrix(self.n, self.rowptr_d, self.colind_d, self.vals_d.clone(), self._host)

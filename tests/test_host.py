@@ -139,3 +139,22 @@ def test_large_mirror_is_read_only(monkeypatch):
     with pytest.raises(ValueError):
         h[0] = 1.0
     assert m.device().sum().item() == 0.0
+
+
+def test_vals_store_does_not_keep_tensors_alive():
+    """The per-tensor mirror registry (sparse._vals_store) holds its key
+    weakly: dropping every CsrMatrix over a value tensor frees it."""
+    import gc
+    import weakref
+
+    import torch
+
+    from paper_2107_11541_b200 import sparse
+
+    t = torch.zeros(8, dtype=torch.float64)
+    st = sparse._vals_store(t)
+    assert sparse._vals_store(t) is st
+    r = weakref.ref(t)
+    del t, st
+    gc.collect()
+    assert r() is None
