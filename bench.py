@@ -642,7 +642,15 @@ def main():
     stream = torch.cuda.current_stream()
 
     side = torch.cuda.Stream() if sub is not None else None
-    launches_per_step = 3  # element-block momentum RHS (integrate + node gather) + B_xyz rows
+    # element-block momentum RHS (integrate + node gather) + B_xyz (Kuhn rows
+    # from registers + the remaining rows' pair-stream kernel, when both exist)
+    # (the pair-stream plan is built on the first assembly: counted after warm-up)
+    def _gradient_launches():
+        g0 = ctx.groups[0]
+        pc = g0.rows.pair_canon if g0.rows is not None else None
+        return 2 if pc is not None and pc.get("kuhn") and pc["other"].numel() else 1
+
+    launches_per_step = None
     if sub is not None:  # windowed schedule: one launch per non-empty window
         from paper_2107_11541_b200.distributed import _step_windows
 
@@ -683,6 +691,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    grad_launches = _gradient_launches()
     clocks = ClockSampler(local)
     # soak (untimed) so the clock sampler sees the loaded state; every rank
     # must run the same number of steps (each step has halo exchanges), so
@@ -873,9 +882,10 @@ def main():
                 "timed_step": "one CUDA graph per step (interface windows, NCCL halo on a side stream, interior)"
                 if graph.single_graph else "two CUDA graphs (interface / interior windows), eager halo between"},
             # per step: element-block momentum RHS (integrate + partial
-            # gather; velocity read in place) and row-owned B_x,B_y,B_z — 3
-            # launches (ncu launch list under profiles/); the halo (N > 1) is NCCL
-            "gpu_launches": args.steps * launches_per_step,
+            # gather; velocity read in place) and B_x,B_y,B_z (Kuhn rows +
+            # the other rows) — 4 launches (ncu launch list under profiles/);
+            # N > 1: one launch per window, the halo is NCCL
+            "gpu_launches": args.steps * (launches_per_step or 2 + grad_launches),
             "clocks": clk,
             "e2e": e2e,
             "solver": solver,

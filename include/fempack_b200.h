@@ -267,7 +267,10 @@ int fpb_assemble_gradient_pairs_slices(int32_t n, int32_t nslices, const int32_t
 /* The compile-time stream of an interior Kuhn-box row (72 words; returns the
  * count) and the kernel that uses it on the listed rows rows[nrows] (any
  * order; 32 per warp): every listed row must have that stream and 15 entries
- * with the diagonal at CSR offset 7 (the caller verifies both). */
+ * with the diagonal at CSR offset 7 (the caller verifies both).  rlos[nrows]
+ * (row starts) and nbr[14][nrows] (off-diagonal columns in CSR order) are
+ * optional precomputed copies that shorten the load chain (NULL: read
+ * through rowptr / colind). */
 int fpb_pair_kuhn_table(uint16_t* words_h);
 /* The per-row stream for an arbitrary row list rows[nrows] (the rows the
  * Kuhn kernel does not take): each row reads its own slice's stream. */
@@ -275,8 +278,9 @@ int fpb_assemble_gradient_pairs_rows(int32_t n, int32_t nrows, const int32_t* ro
                                      const uint16_t* words, const double* xyz4, const int32_t* rowptr,
                                      const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
                                      void* stream);
-int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const double* xyz4, const int32_t* rowptr,
-                                     const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream);
+int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const int32_t* rlos, const int32_t* nbr,
+                                     const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
+                                     int accumulate, double* out, void* stream);
 
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices

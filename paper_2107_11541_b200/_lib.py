@@ -46,7 +46,7 @@ SIGNATURES = {
     "fpb_allreduce_sum": (_int, [_vp, _vp, _i64, _vp]),
     "fpb_pair_canon_set": (_int, [_vp, _int]),
     "fpb_pair_kuhn_table": (_int, [_vp]),
-    "fpb_assemble_gradient_pairs_kuhn": (_int, [_i32, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
+    "fpb_assemble_gradient_pairs_kuhn": (_int, [_i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp, _vp]),
     "fpb_assemble_gradient_pairs_slices": (_int, [_i32, _i32, _vp, _int, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int,
                                                   _vp, _vp]),
     "fpb_assemble_gradient_pairs_rows": (_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _int, _vp, _vp]),

@@ -414,7 +414,8 @@ constexpr int kKuhnWarps = 2;  // warps (32-row slices) per CTA
 #define FPB_KUHN_MINB 6
 #endif
 __global__ void __launch_bounds__(32 * kKuhnWarps, FPB_KUHN_MINB)
-k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const double* __restrict__ xyz4,
+k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ rlos,
+                  const int32_t* __restrict__ nbr, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz,
                   int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, R = kKuhnCols + 1;  // entries per row
@@ -424,7 +425,11 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const double*
   if (i0 >= nrows) return;
   const bool live = i0 + lane < nrows;
   const int row = live ? __ldg(rows + i0 + lane) : -1;
-  const int rlo = live ? __ldg(rowptr + row) : 0;
+  // rlos / nbr (per list entry, nullable): the row's CSR start and its 14
+  // neighbours ([14][nrows]) precomputed, so every load below is indexed by
+  // the list position alone — one dependent level (-> coordinates) instead
+  // of three (row -> rowptr -> colind -> coordinates)
+  const int rlo = !live ? 0 : rlos ? __ldg(rlos + i0 + lane) : __ldg(rowptr + row);
   const int base = __shfl_sync(0xffffffffu, rlo, 0);
   // the diagonal sits at CSR offset kKuhnDiag of every canonical row (the
   // host checks it with the stream): off-diagonal slot t is offset t + (t >= 7)
@@ -437,7 +442,8 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const double*
     for (int d = 0; d < DIM; ++d) x0[d] = r4[d];
 #pragma unroll
     for (int t = 0; t < kKuhnCols; ++t) {
-      ld256(xyz4 + 4 * (int64_t)__ldg(colind + rlo + t + (t >= dslot)), r4);
+      const int col = nbr ? __ldg(nbr + (int64_t)t * nrows + i0 + lane) : __ldg(colind + rlo + t + (t >= dslot));
+      ld256(xyz4 + 4 * (int64_t)col, r4);
 #pragma unroll
       for (int d = 0; d < DIM; ++d) X[t][d] = r4[d] - x0[d];
     }
@@ -593,14 +599,15 @@ int fpb_pair_kuhn_table(uint16_t* words_h) {
   return kKuhnWords;
 }
 
-int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const double* xyz4, const int32_t* rowptr,
-                                     const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream) {
+int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const int32_t* rlos, const int32_t* nbr,
+                                     const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
+                                     int accumulate, double* out, void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(rows && xyz4 && rowptr && colind && out, "missing arrays for the Kuhn-stream kernel");
   if (nrows <= 0) return FPB_OK;
   const int64_t warps = ((int64_t)nrows + 31) / 32;
   k_rows_pairs_kuhn<<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
-      nrows, rows, xyz4, rowptr, colind, nnz, accumulate, out);
+      nrows, rows, rlos, nbr, xyz4, rowptr, colind, nnz, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
