@@ -296,6 +296,8 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
     double acc[Out<ET, KIND>::NOUT];
     if constexpr (Elem<ET>::AFFINE) {
       simplex_rhs_all<ET, KIND>(xe, ue, fe, rho, mu, kappa, acc);
+    } else if constexpr (KIND == KIND_SCALAR3 && ET == FPB_HEX08) {  // one geometry, three fields (Walsh forms)
+      hex_rhs_integrate<KIND_SCALAR3>(xe, ue, fe, rho, mu, kappa, acc);
     } else if constexpr (KIND == KIND_SCALAR3) {  // Gauss loop per field (staging shared)
       const double kap[3] = {rho, mu, kappa};
 #pragma unroll 1

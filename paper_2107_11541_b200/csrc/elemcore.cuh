@@ -43,7 +43,8 @@ __device__ __forceinline__ void hex_rhs_integrate(const double (&xe)[8][3],
                                                   double mu, double kappa,
                                                   double (&acc)[Out<FPB_HEX08, KIND>::NOUT]) {
   constexpr int ET = FPB_HEX08;
-  constexpr int NV = KIND == FPB_MOMENTUM_RHS ? 3 : 1;
+  constexpr int NV = KIND == FPB_MOMENTUM_RHS || KIND == KIND_SCALAR3 ? 3 : 1;
+  constexpr int NFLD = KIND == KIND_SCALAR3 ? 3 : 1;  // scalar fields sharing the geometry
   HexCoef hc;
   hex_coeffs(xe, hc);
   double uh[3][8];
@@ -54,8 +55,17 @@ __device__ __forceinline__ void hex_rhs_integrate(const double (&xe)[8][3],
     for (int b = 0; b < 8; ++b) v[b] = ue[b][k];
     hex_walsh(v, uh[k]);
   }
-  double fh[8];
-  if constexpr (KIND == FPB_SCALAR_RHS) hex_walsh(fe, fh);
+  double fh[NFLD][8];
+  if constexpr (KIND == FPB_SCALAR_RHS) hex_walsh(fe, fh[0]);
+  if constexpr (KIND == KIND_SCALAR3) {  // fields fe[f * 8 + b], diffusivities (rho, mu, kappa)
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+      double v[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v[b] = fe[f * 8 + b];
+      hex_walsh(v, fh[f]);
+    }
+  }
   HexTest T[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) T[k].zero();
@@ -112,18 +122,22 @@ __device__ __forceinline__ void hex_rhs_integrate(const double (&xe)[8][3],
         for (int m = 0; m < 3; ++m) V[m] = sv * (A[m][0] * S[k][0] + A[m][1] * S[k][1] + A[m][2] * S[k][2]);
         T[k].add(g, -w * (rho * c[k]), V);
       }
-    } else {  // SCALAR_RHS, _kernels.py:420-461
-      double px[3], gphi[3];
+    } else {  // SCALAR_RHS (one field, or the three of KIND_SCALAR3 on one geometry), _kernels.py:420-461
 #pragma unroll
-      for (int m = 0; m < 3; ++m) px[m] = hex_dxi(fh, m, g);
+      for (int f = 0; f < NFLD; ++f) {
+        const double kap = KIND == KIND_SCALAR3 ? (f == 0 ? rho : f == 1 ? mu : kappa) : kappa;
+        double px[3], gphi[3];
 #pragma unroll
-      for (int l = 0; l < 3; ++l) gphi[l] = inv * (A[0][l] * px[0] + A[1][l] * px[1] + A[2][l] * px[2]);
-      const double adv = ug[0] * gphi[0] + ug[1] * gphi[1] + ug[2] * gphi[2];
-      const double sk = -kappa * refW<ET>(g);
-      double V[3];
+        for (int m = 0; m < 3; ++m) px[m] = hex_dxi(fh[f], m, g);
 #pragma unroll
-      for (int m = 0; m < 3; ++m) V[m] = sk * (A[m][0] * gphi[0] + A[m][1] * gphi[1] + A[m][2] * gphi[2]);
-      T[0].add(g, -w * adv, V);
+        for (int l = 0; l < 3; ++l) gphi[l] = inv * (A[0][l] * px[0] + A[1][l] * px[1] + A[2][l] * px[2]);
+        const double adv = ug[0] * gphi[0] + ug[1] * gphi[1] + ug[2] * gphi[2];
+        const double sk = -kap * refW<ET>(g);
+        double V[3];
+#pragma unroll
+        for (int m = 0; m < 3; ++m) V[m] = sk * (A[m][0] * gphi[0] + A[m][1] * gphi[1] + A[m][2] * gphi[2]);
+        T[f].add(g, -w * adv, V);
+      }
     }
   }
 #pragma unroll
