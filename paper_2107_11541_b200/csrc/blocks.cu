@@ -63,9 +63,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef FPB_BLK_MINB_SCALAR3
 #define FPB_BLK_MINB_SCALAR3 5
 #endif
-#ifndef FPB_BLK_VEC2
-#define FPB_BLK_VEC2 1  // 16-byte shared-memory reads of even-width node records
-#endif
 #ifndef FPB_BLK_INTERLEAVE
 #define FPB_BLK_INTERLEAVE 1  // the compiler interleaves a thread's two elements (ILP)
 #endif
@@ -285,25 +282,10 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
 #pragma unroll
     for (int a = 0; a < NN; ++a) {
       const int l = j == 0 ? li[0][a] : li[EPT - 1][a];
-      if constexpr (NDAT % 2 == 0 && FPB_BLK_VEC2) {  // 16-byte node-record reads (half the LDS issue)
-        double v[NDAT];
 #pragma unroll
-        for (int h = 0; h < NDAT / 2; ++h) {
-          const double2 t = *reinterpret_cast<const double2*>(snode + l * NDAT + 2 * h);
-          v[2 * h] = t.x;
-          v[2 * h + 1] = t.y;
-        }
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          xe[a][d] = v[d];
-          ue[a][d] = v[DIM + d];
-        }
-      } else {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) {
-          xe[a][d] = snode[l * NDAT + d];
-          ue[a][d] = snode[l * NDAT + DIM + d];
-        }
+      for (int d = 0; d < DIM; ++d) {
+        xe[a][d] = snode[l * NDAT + d];
+        ue[a][d] = snode[l * NDAT + DIM + d];
       }
       if constexpr (KIND == FPB_SCALAR_RHS) fe[a] = snode[l * NDAT + 2 * DIM];
       if constexpr (KIND == KIND_SCALAR3) {
