@@ -348,6 +348,20 @@ int fpb_assemble_blocks_scalar3(int etype, int64_t nelem, int64_t blk0, int64_t 
                                 int32_t n, int32_t node0, int32_t node1, const int32_t* node_pptr,
                                 const int32_t* node_plist, int accumulate, double* out3, void* stream);
 
+/* Momentum RHS of a Kuhn box mesh (reference momentum_rhs_packed,
+ * _kernels.py:320-382, + scatter_vector_dim_packed :511-519, as driven by
+ * AssemblyContext.assemble_rhs, assembly.py:235-270) when the TET04
+ * connectivity is exactly generate_box_mesh(TET04, nx, ny, nz)'s
+ * (mesh.py:258-282; the caller checks it, e.g. against fpb_box_conn).
+ * Coordinates (32-byte records, fpb_pack4) and vel[n][3] are read as given.
+ * Cell lines (0..nx-1, j) march the z-chunks of kchunk cell layers; out[n][3]
+ * is overwritten, every node written once in a fixed summation order.
+ * sync: fpb_kuhn_mom_sync_len(ny, nz, kchunk) int32 of scratch (zeroed by
+ * the call); pup: n * 3 doubles of scratch.  nx <= 256. */
+int fpb_kuhn_mom_sync_len(int ny, int nz, int kchunk);
+int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double* xyz4, const double* vel,
+                               double rho, double mu, int32_t* sync, double* pup, double* out, void* stream);
+
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 
 /* y = A x (sparse.py:78-84).  nnz = rowptr[n] sizes the lanes per row. */

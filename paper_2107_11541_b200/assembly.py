@@ -98,6 +98,9 @@ HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
 HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))
 # element blocks of the RHS kernels over Morton-ordered elements (BlockPlan);
 # slab domains keep natural order (their interface windows are block ranges)
+# TET04 momentum RHS on a Kuhn box mesh by z-marching cell lines (kmom.cu)
+KUHN_MOMENTUM = os.environ.get("FPB_KUHN_MOM", "1") != "0"
+KUHN_KCHUNK = int(os.environ.get("FPB_KUHN_KCHUNK", "0"))  # 0 = from the grid size
 BLOCK_MORTON = os.environ.get("FPB_BLOCK_MORTON", "0") != "0"  # measured slower (profiles/r02e_mom)  # y-band of canonical hex rows (0 = natural order)
 
 
@@ -350,6 +353,55 @@ def _centroid_morton(conn_d: torch.Tensor, coords_d: torch.Tensor) -> torch.Tens
     return torch.argsort(key, stable=True)
 
 
+class KuhnBox:
+    """A TET04 group whose connectivity is exactly generate_box_mesh(TET04,
+    nx, ny, nz)'s (mesh.py:258-282, cell-major, the six Kuhn tets per cell in
+    permutation order) — checked element by element against the device
+    generator at setup.  Node coordinates are NOT assumed: the kernel reads
+    them.  Then the momentum RHS runs as z-marching cell lines (kmom.cu)
+    with no per-element metadata."""
+
+    MAX_NX = 256
+
+    def __init__(self, nx: int, ny: int, nz: int, dev):
+        self.nx, self.ny, self.nz = nx, ny, nz
+        # z-chunks: about 8 CTA waves of 2 x 148 over the (chunk, row) grid,
+        # >= 8 cell layers per chunk (each chunk re-integrates one halo layer)
+        nchunk = max(1, min(nz // 8, -(-8 * 2 * 148 // ny)))
+        self.kchunk = min(KUHN_KCHUNK or -(-nz // nchunk), nz)
+        nsync = int(_lib.load().fpb_kuhn_mom_sync_len(ny, nz, self.kchunk))
+        self.sync = torch.zeros(nsync, dtype=torch.int32, device=dev)
+        self._pup = None
+
+    def pup(self, n: int, dev) -> torch.Tensor:
+        if self._pup is None:  # row partials of the y reduction (n x 3 doubles, once)
+            self._pup = torch.empty(max(n, 1) * 3, dtype=torch.float64, device=dev)
+        return self._pup
+
+    @staticmethod
+    def detect(conn_d: torch.Tensor, nnode: int) -> "KuhnBox | None":
+        ne = int(conn_d.shape[0])
+        if ne == 0 or conn_d.ndim != 2 or conn_d.shape[1] != 4:
+            return None
+        c0 = [int(v) for v in conn_d[0].tolist()]
+        if c0[0] != 0 or c0[1] != 1:
+            return None
+        nx = c0[2] - 2
+        if nx < 1 or nx > KuhnBox.MAX_NX or (c0[3] - c0[2]) % (nx + 1):
+            return None
+        ny = (c0[3] - c0[2]) // (nx + 1) - 1
+        if ny < 1 or ne % (6 * nx * ny):
+            return None
+        nz = ne // (6 * nx * ny)
+        if (nx + 1) * (ny + 1) * (nz + 1) != nnode:
+            return None
+        ref = torch.empty_like(conn_d)
+        _lib.call("fpb_box_conn", ETYPE_ID[ElementType.TET04], nx, ny, nz, ref.data_ptr(), _lib.stream())
+        if not torch.equal(ref, conn_d):
+            return None
+        return KuhnBox(nx, ny, nz, conn_d.device)
+
+
 class BlockPlan:
     """Element blocks of one group for the deterministic two-phase RHS
     assembly (blocks.cu): per-block distinct nodes + sorted gather slots,
@@ -412,6 +464,7 @@ class GroupData:
     pattern: CsrMatrix
     rows: RowPlan | None = None
     blocks: BlockPlan | None = None
+    kuhn: "KuhnBox | None" = None  # TET04 Kuhn box (momentum RHS by cell lines)
     hexrows: "HexRowPlan | None" = None  # built on first B_xyz use
     _pos32: torch.Tensor | None = None
     _cache: dict = field(default_factory=dict)
@@ -504,6 +557,8 @@ class AssemblyContext:
             if scatter == "auto":
                 gd.blocks = BlockPlan(g.conn_d, mesh.nnode, ETYPE_ID[g.etype],
                                       mesh.coords_d if (block_order == "morton" and BLOCK_MORTON) else None)
+                if g.etype is ElementType.TET04 and KUHN_MOMENTUM and len(mesh.groups) == 1:
+                    gd.kuhn = KuhnBox.detect(g.conn_d, mesh.nnode)
             if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
                 gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time
@@ -605,7 +660,13 @@ class AssemblyContext:
             uvw4 = self._uvw4.data_ptr()
         xyz4 = self.xyz4.data_ptr()
         for g, own in zip(self.groups, owner):
-            if own and not matrix and g.blocks is not None:
+            if own and single_rows and window is None and g.kuhn is not None \
+                    and kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] and KUHN_MOMENTUM:
+                kb = g.kuhn
+                _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kchunk, xyz4, vp, float(rho),
+                          float(mu), kb.sync.data_ptr(), kb.pup(n, out.device).data_ptr(), out.data_ptr(),
+                          _lib.stream())
+            elif own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
                 b0, b1 = window.get("blocks", (0, bp.nblocks)) if window else (0, bp.nblocks)

@@ -227,4 +227,77 @@ __device__ __forceinline__ void simplex_rhs_all(
   }
 }
 
+// P1 tetrahedron momentum residual in adjugate form (no J^-1 scaling, one
+// reciprocal).  x[b], u[b]: positions / velocities of the local nodes b =
+// 0..3 (reference order); res[b][k] -= the element residual of
+// _kernels.py:320-382 (momentum_rhs_packed), closed form:
+//   E_b = x_b - x_0, A = rows (E2 x E3, E3 x E1, E1 x E2) = det J^-1,
+//   Ga[l][k] = sum_b (u_b - u_0)[k] A[b-1][l]  (= det du_k/dx_l),
+//   convective part  rho sum_l ub_a[l] (Ga + div Ga I)[l][k]  with
+//     ub_a = sum_c M[a][c] u_c = (W/20) (U + u_a),  U = sum_c u_c,
+//   viscous part     (mu W / det) sum_l (Ga[k][l] + Ga[l][k]) dg[l][a],
+//     dg[.][a] = A[a-1] (a >= 1), dg[.][0] = -(A[0] + A[1] + A[2]).
+// r = rho W / 20 (= rho * M[0][1]); muW = mu * W.  The 4-point rule of the
+// reference integrates these polynomials exactly, so this agrees with its
+// Gauss loop to rounding (~190 FP64 instructions instead of ~285).
+template <class Sub>
+__device__ __forceinline__ void tet_mom_adj_f(const double (&x)[4][3], const double (&u)[4][3], double r, double muW,
+                                              Sub&& sub) {
+  double E[3][3], A[3][3], du[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      E[b][d] = x[b + 1][d] - x[0][d];
+      du[b][d] = u[b + 1][d] - u[0][d];
+    }
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const double* p = E[(b + 1) % 3];
+    const double* q = E[(b + 2) % 3];
+    A[b][0] = p[1] * q[2] - p[2] * q[1];
+    A[b][1] = p[2] * q[0] - p[0] * q[2];
+    A[b][2] = p[0] * q[1] - p[1] * q[0];
+  }
+  const double det = E[0][0] * A[0][0] + E[0][1] * A[0][1] + E[0][2] * A[0][2];
+  double G[3][3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) G[l][k] = du[0][k] * A[0][l] + du[1][k] * A[1][l] + du[2][k] * A[2][l];
+  const double divu = G[0][0] + G[1][1] + G[2][2];
+  const double f = muW / det;
+  double Mr[3][3], Sf[3][3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      Mr[l][k] = r * (l == k ? G[l][k] + divu : G[l][k]);
+      Sf[l][k] = l == k ? (2.0 * f) * G[l][l] : f * (G[l][k] + G[k][l]);
+    }
+  double vs[3][3];  // viscous part of nodes 1..3
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vs[a][k] = Sf[k][0] * A[a][0] + Sf[k][1] * A[a][1] + Sf[k][2] * A[a][2];
+  double U[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) U[d] = (u[0][d] + u[1][d]) + (u[2][d] + u[3][d]);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double w[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) w[d] = U[d] + u[a][d];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double v = a == 0 ? -((vs[0][k] + vs[1][k]) + vs[2][k]) : vs[a - 1][k];
+      sub(a, k, fma(w[0], Mr[0][k], fma(w[1], Mr[1][k], fma(w[2], Mr[2][k], v))));
+    }
+  }
+}
+__device__ __forceinline__ void tet_mom_adj(const double (&x)[4][3], const double (&u)[4][3], double r, double muW,
+                                            double (&res)[4][3]) {
+  tet_mom_adj_f(x, u, r, muW, [&](int a, int k, double v) { res[a][k] -= v; });
+}
+
 }  // namespace fpb

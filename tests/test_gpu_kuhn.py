@@ -1,0 +1,111 @@
+"""Momentum RHS on Kuhn box meshes by z-marching cell lines (kmom.cu).
+
+The default dispatch sends MOMENTUM_RHS of a TET04 mesh whose connectivity
+is exactly generate_box_mesh's (assembly.py KuhnBox.detect) to
+fpb_assemble_momentum_kuhn.  Checked here against the oracle (pinned to the
+reference, tests/test_oracle_golden.py) on unjittered and jittered
+coordinates, over z-chunk sizes that exercise the halo layer, the row
+chain and the top face, against the element-block path at a larger size,
+and for bitwise run-to-run determinism.  Bar: 1e-12 max-normalised."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fempack_np as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _ctx(P, nx, ny, nz, kchunk=0, coords=None):
+    import paper_2107_11541_b200.assembly as A
+
+    old = A.KUHN_KCHUNK
+    A.KUHN_KCHUNK = kchunk
+    try:
+        mesh = P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz)
+        if coords is not None:
+            mesh.coords = coords
+        ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    finally:
+        A.KUHN_KCHUNK = old
+    return mesh, ctx
+
+
+def _jitter(coords, nx, ny, nz, seed=3):
+    rng = np.random.default_rng(seed)
+    h = np.array([1.0 / nx, 1.0 / ny, 1.0 / nz])
+    return coords + rng.uniform(-0.15, 0.15, coords.shape) * h
+
+
+@pytest.mark.parametrize("dims,kchunk", [((5, 4, 7), 0), ((5, 4, 7), 1), ((5, 4, 7), 2), ((5, 4, 7), 3),
+                                         ((1, 1, 1), 0), ((1, 3, 2), 1), ((33, 3, 5), 2), ((64, 2, 3), 0),
+                                         ((7, 1, 9), 4)])
+@pytest.mark.parametrize("jitter", [False, True])
+def test_kuhn_momentum_matches_oracle(cuda_ok, dims, kchunk, jitter):
+    import paper_2107_11541_b200 as P
+
+    nx, ny, nz = dims
+    om = O.box(O.TET04, nx, ny, nz)
+    if jitter:
+        om.coords = _jitter(om.coords, nx, ny, nz)
+    mesh, ctx = _ctx(P, nx, ny, nz, kchunk, om.coords if jitter else None)
+    assert ctx.groups[0].kuhn is not None
+    if kchunk:
+        assert ctx.groups[0].kuhn.kchunk == min(kchunk, nz)
+    vel, _ = O.bench_fields(om.nnode, 3)
+    for rho, mu in ((1.0, 1e-2), (0.7, 0.0), (0.0, 0.3)):
+        r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, rho, mu, 0.0)
+        ro = O.assemble_rhs(om, "momentum_rhs", vel, None, rho, mu, 0.0)
+        assert O.rel_diff(r, ro) < TOL, (dims, kchunk, rho, mu, O.rel_diff(r, ro))
+
+
+def test_kuhn_nx_limit_and_detection(cuda_ok):
+    import paper_2107_11541_b200 as P
+
+    _, ctx = _ctx(P, 256, 1, 2)
+    assert ctx.groups[0].kuhn is not None  # widest supported line
+    om = O.box(O.TET04, 256, 1, 2)
+    vel, _ = O.bench_fields(om.nnode, 3)
+    r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
+    assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL
+    _, ctx = _ctx(P, 257, 1, 1)
+    assert ctx.groups[0].kuhn is None  # too wide: element blocks
+    # a permuted element order is not the generator's: element blocks
+    mesh = P.generate_box_mesh(P.ElementType.TET04, 4, 3, 2)
+    conn = mesh.groups[0].conn.copy()
+    conn[[5, 6]] = conn[[6, 5]]
+    m2 = P.Mesh(3, mesh.coords, [P.ElementGroup(P.ElementType.TET04, conn)])
+    ctx2 = P.AssemblyContext.build(m2, vector_size=8)
+    assert ctx2.groups[0].kuhn is None
+    om = O.box(O.TET04, 4, 3, 2)
+    vel, _ = O.bench_fields(om.nnode, 3)
+    r = ctx2.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
+    assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL
+
+
+def test_kuhn_matches_block_path_and_is_deterministic(cuda_ok):
+    import paper_2107_11541_b200 as P
+    import paper_2107_11541_b200.assembly as A
+
+    nx, ny, nz = 94, 40, 37
+    mesh, ctx = _ctx(P, nx, ny, nz)
+    kb = ctx.groups[0].kuhn
+    assert kb is not None and -(-nz // kb.kchunk) > 1
+    n = mesh.nnode
+    g = torch.Generator(device="cuda").manual_seed(5)
+    vel = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=g)
+    out1 = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    out2 = torch.empty_like(out1)
+    ref = torch.empty_like(out1)
+    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out1)
+    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out2)
+    assert torch.equal(out1, out2)
+    A.KUHN_MOMENTUM = False
+    try:
+        ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, ref)
+    finally:
+        A.KUHN_MOMENTUM = True
+    a, b = out1.cpu().numpy(), ref.cpu().numpy()
+    assert O.rel_diff(a, b) < TOL

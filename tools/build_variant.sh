@@ -7,7 +7,7 @@ root=$(cd "$(dirname "$0")/.." && pwd)
 out=$root/build_variants/$name
 mkdir -p $out
 cd $root/paper_2107_11541_b200/csrc
-for f in setup assemble rows rowsq pairs blocks vector flow hexblock halo; do
+for f in $(sed -n "s/^SRCS := //p" Makefile | sed "s/\.cu//g"); do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
     --expt-relaxed-constexpr -rdc=true "$@" -c $f.cu -o $out/$f.o &
 done

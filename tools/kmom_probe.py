@@ -1,0 +1,76 @@
+"""Momentum RHS timings: Kuhn cell-line kernel (kmom.cu) vs element blocks
+(blocks.cu) on the config-2 and config-5 meshes, L2 flushed between reps.
+
+    python tools/kmom_probe.py [--sizes 94x94x95,256x256x256] [--reps 10]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2107_11541_b200 as P  # noqa: E402
+import paper_2107_11541_b200.assembly as A  # noqa: E402
+
+
+def timeit(fn, reps, flush):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="94x94x95,256x256x256")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--kchunks", default="0")
+    ap.add_argument("--blocks", type=int, default=1)
+    args = ap.parse_args()
+    flush = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
+    res = {}
+    for sz in args.sizes.split(","):
+        nx, ny, nz = (int(v) for v in sz.split("x"))
+        mesh = P.generate_box_mesh(P.ElementType.TET04, nx, ny, nz)
+        n, ne = mesh.nnode, mesh.nelem
+        g = torch.Generator(device="cuda").manual_seed(0)
+        vel = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=g)
+        out = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+        ref = torch.empty_like(out)
+        for kc in (int(v) for v in args.kchunks.split(",")):
+            A.KUHN_KCHUNK = kc
+            ctx = P.AssemblyContext.build(mesh, vector_size=8)
+            kb = ctx.groups[0].kuhn
+            fn = lambda: ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out)  # noqa: E731
+            ms = timeit(fn, args.reps, flush)
+            res[f"{sz}/kuhn/kchunk{kb.kchunk if kb else None}"] = {"ms": round(ms, 4), "Gelem_s": round(ne / ms / 1e6, 2)}
+            if args.blocks:
+                A.KUHN_MOMENTUM = False
+                ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, ref)
+                msb = timeit(lambda: ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, ref),
+                             args.reps, flush)
+                A.KUHN_MOMENTUM = True
+                fn()
+                torch.cuda.synchronize()
+                d = float((out - ref).abs().max() / ref.abs().max())
+                res[f"{sz}/blocks"] = {"ms": round(msb, 4), "Gelem_s": round(ne / msb / 1e6, 2), "rel_diff": d}
+            del ctx
+            torch.cuda.empty_cache()
+        del mesh, vel, out, ref
+        torch.cuda.empty_cache()
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
