@@ -354,13 +354,12 @@ int fpb_assemble_blocks_scalar3(int etype, int64_t nelem, int64_t blk0, int64_t 
  * connectivity is exactly generate_box_mesh(TET04, nx, ny, nz)'s
  * (mesh.py:258-282; the caller checks it, e.g. against fpb_box_conn).
  * Coordinates (32-byte records, fpb_pack4) and vel[n][3] are read as given.
- * Cell lines (0..nx-1, j) march the z-chunks of kchunk cell layers; out[n][3]
- * is overwritten, every node written once in a fixed summation order.
- * sync: fpb_kuhn_mom_sync_len(ny, nz, kchunk) int32 of scratch (zeroed by
- * the call); pup: n * 3 doubles of scratch.  nx <= 256. */
-int fpb_kuhn_mom_sync_len(int ny, int nz, int kchunk);
+ * 32 x 8 cell pencils march z-chunks of kchunk cell layers; out[n][3] is
+ * overwritten in a fixed summation order (bitwise reproducible).  scratch:
+ * fpb_kuhn_mom_scratch_len(nx, ny, nz) doubles (CTA boundary partials). */
+int64_t fpb_kuhn_mom_scratch_len(int nx, int ny, int nz);
 int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double* xyz4, const double* vel,
-                               double rho, double mu, int32_t* sync, double* pup, double* out, void* stream);
+                               double rho, double mu, double* scratch, double* out, void* stream);
 
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 

@@ -361,22 +361,20 @@ class KuhnBox:
     them.  Then the momentum RHS runs as z-marching cell lines (kmom.cu)
     with no per-element metadata."""
 
-    MAX_NX = 256
-
     def __init__(self, nx: int, ny: int, nz: int, dev):
         self.nx, self.ny, self.nz = nx, ny, nz
-        # z-chunks: about 8 CTA waves of 2 x 148 over the (chunk, row) grid,
-        # >= 8 cell layers per chunk (each chunk re-integrates one halo layer)
-        nchunk = max(1, min(nz // 8, -(-8 * 2 * 148 // ny)))
+        # CTAs are 32 x 8 cell pencils; z-chunks for about 8 waves of 2 CTAs
+        # per SM, >= 8 cell layers each (a chunk re-integrates one halo layer)
+        pencils = -(-nx // 32) * -(-ny // 8)
+        nchunk = max(1, min(nz // 8, -(-8 * 2 * 148 // pencils)))
         self.kchunk = min(KUHN_KCHUNK or -(-nz // nchunk), nz)
-        nsync = int(_lib.load().fpb_kuhn_mom_sync_len(ny, nz, self.kchunk))
-        self.sync = torch.zeros(nsync, dtype=torch.int32, device=dev)
-        self._pup = None
+        self._scratch = None
 
-    def pup(self, n: int, dev) -> torch.Tensor:
-        if self._pup is None:  # row partials of the y reduction (n x 3 doubles, once)
-            self._pup = torch.empty(max(n, 1) * 3, dtype=torch.float64, device=dev)
-        return self._pup
+    def scratch(self, dev) -> torch.Tensor:
+        if self._scratch is None:  # CTA boundary partials (kmom.cu Px / Py), once
+            m = int(_lib.load().fpb_kuhn_mom_scratch_len(self.nx, self.ny, self.nz))
+            self._scratch = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+        return self._scratch
 
     @staticmethod
     def detect(conn_d: torch.Tensor, nnode: int) -> "KuhnBox | None":
@@ -387,7 +385,7 @@ class KuhnBox:
         if c0[0] != 0 or c0[1] != 1:
             return None
         nx = c0[2] - 2
-        if nx < 1 or nx > KuhnBox.MAX_NX or (c0[3] - c0[2]) % (nx + 1):
+        if nx < 1 or (c0[3] - c0[2]) % (nx + 1):
             return None
         ny = (c0[3] - c0[2]) // (nx + 1) - 1
         if ny < 1 or ne % (6 * nx * ny):
@@ -664,8 +662,7 @@ class AssemblyContext:
                     and kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] and KUHN_MOMENTUM:
                 kb = g.kuhn
                 _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kchunk, xyz4, vp, float(rho),
-                          float(mu), kb.sync.data_ptr(), kb.pup(n, out.device).data_ptr(), out.data_ptr(),
-                          _lib.stream())
+                          float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
             elif own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1

@@ -1,105 +1,127 @@
-// Momentum RHS on a Kuhn box mesh by z-marching cell lines (TET04).
+// Momentum RHS on a Kuhn box mesh by z-marching cell pencils (TET04).
 //
 // The reference's generate_box_mesh(TET04, nx, ny, nz) (mesh.py:258-282)
 // cuts every grid cell (i, j, k) into six tetrahedra that all contain the
 // cell origin v0 as local node 0 and the far corner v7.  When a mesh's
 // connectivity is exactly that (checked element by element on the device at
-// setup, assembly.py KuhnBox) the momentum RHS of _kernels.py:320-382 +
-// the scatter of :511-519 is assembled without any per-element metadata:
+// setup, assembly.py KuhnBox) the momentum RHS of _kernels.py:320-382 + the
+// scatter of :511-519 is assembled with no per-element metadata at all:
 //
-//   CTA (chunk c, cell row j) owns the x-line of cells (0..nx-1, j) and walks
-//   the cell layers k of its z-chunk, one thread per cell column i.  Node
-//   data of two node layers x two node rows are staged in shared memory
-//   (structure of arrays, cp.async one layer ahead); each thread integrates
-//   its cell's six tets (tet_mom_adj, simplex.cuh) into eight corner
-//   accumulators held in registers.  Reductions:
+//   CTA (x-block a, y-block b, z-chunk c) owns the 32 x kKmomTY cell
+//   columns (i0 + lane, j0 + warp) and walks the cell layers k of its
+//   z-chunk; one thread per cell column.  Each warp stages the node data it
+//   needs (two node layers x two node rows x 33 node columns, structure of
+//   arrays, cp.async two layers ahead) in its own shared-memory slice and
+//   integrates its cell's six tets (tet_mom_adj_f, simplex.cuh) into eight
+//   corner accumulators held in registers.  Reductions:
 //     z: the top-face accumulators become the next cell's bottom face;
-//     x: a thread's right-hand corners go through shared memory to the
-//        thread on its right;
-//     y: node row j+1 also receives row j+1's cells: this CTA publishes its
-//        partial of node row j+1 (pup, an n x 3 scratch) layer by layer
-//        with a release flag, and the CTA of row j+1 adds it when it writes
-//        node row j, one layer later (no chain waits in the steady state).
-//   z-chunks: a chunk first integrates the cell layer below it (halo) for
-//   the contributions to its lowest node layer, so chunks are independent.
-// CTAs take (chunk, row) tickets in launch order, so the CTA a row waits for
-// has always started: no deadlock whatever the residency.
-// Every node is written exactly once, each sum has a fixed order (bitwise
-// reproducible) and nothing is zero-filled.
+//     x: right-hand corners move one lane up by a warp shuffle;
+//     y: a warp's top node row goes to the warp above through a
+//        shared-memory ring (volatile full / consumed counters);
+//   the warps of a CTA never meet at a barrier.  Contributions that cross a
+//   CTA boundary — the right-edge node column and the CTA's top node row —
+//   go to small per-CTA partial buffers (Px, Py), and k_kuhn_fixup adds
+//   them to the boundary nodes afterwards (stream order; no inter-CTA
+//   synchronisation).  z-chunks integrate the cell layer below them (halo)
+//   for the contributions to their lowest node layer, so they are
+//   independent too.  Every sum has a fixed order: bitwise reproducible.
 #include "simplex.cuh"
 
 namespace fpb {
 
 // corner c = di + 2 dj + 4 dk of the cell; tets in the generator's
-// permutation order (mesh.py:212-213), odd ones with the last two swapped
+// permutation order (mesh.py:212-213), odd ones with the last two swapped:
 // {0,1,3,7} {0,2,6,7} {0,4,5,7} {0,1,7,5} {0,4,7,6} {0,2,7,3}, one nibble per node
 __host__ __device__ constexpr int kuhn_corner(int t, int a) {
   return (int)(((t == 0 ? 0x7310u : t == 1 ? 0x7620u : t == 2 ? 0x7540u : t == 3 ? 0x5710u : t == 4 ? 0x6740u : 0x3720u) >>
                 (4 * a)) & 15u);
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ void cp8(double* smem_dst, const double* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 #ifndef FPB_KMOM_MINB
 #define FPB_KMOM_MINB 2
 #endif
+#ifndef FPB_KMOM_TY
+#define FPB_KMOM_TY 8
+#endif
+constexpr int kKmomTY = FPB_KMOM_TY;            // cell rows (warps) per CTA
+constexpr int kKmomRing = 4;                    // y-forward slots per warp
+constexpr int kKmomStg = 3 * 2 * 6 * 33;        // staged doubles per warp: [layer][row][comp][33 nodes]
+constexpr int kKmomSlot = 33 * 3;               // one forwarded node row: [33][3]
+constexpr int kKmomWarpD = kKmomStg + kKmomRing * kKmomSlot;
+
+// boundary partials, per CTA (a, b) and node layer k:
+//   Px[a][b][k][lr][3], lr = 0..kKmomTY: node column i0 + 32 (the next x-block's
+//       first), local node row lr (lr = TY_b: the top-right corner)
+//   Py[a][b][k][l][3], l = 0..32: node row j0 + TY_b (the next y-block's first),
+//       node column i0 + l (l = 32 only when i0 + 32 == nx)
+struct KuhnGrid {
+  int nx, ny, nz, nxb, nyb;
+  __host__ __device__ int64_t px(int a, int b, int k, int lr) const {
+    return ((((int64_t)a * nyb + b) * (nz + 1) + k) * (kKmomTY + 1) + lr) * 3;
+  }
+  __host__ __device__ int64_t py(int a, int b, int k, int l) const {
+    return (int64_t)nxb * nyb * (nz + 1) * (kKmomTY + 1) * 3 + ((((int64_t)a * nyb + b) * (nz + 1) + k) * 33 + l) * 3;
+  }
+  __host__ __device__ int64_t scratch() const { return py(nxb, 0, 0, 0); }
+};
 
 template <int MAXT>
 __global__ void __launch_bounds__(MAXT, FPB_KMOM_MINB)
-k_kuhn_mom(int nx, int ny, int nz, int kchunk, const double* __restrict__ xyz4, const double* __restrict__ vel,
-           double rho, double mu, int* __restrict__ sync, double* __restrict__ pup, double* __restrict__ out) {
+k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double* __restrict__ vel, double rho,
+           double mu, double* __restrict__ part, double* __restrict__ out) {
   extern __shared__ __align__(16) double sm[];
-  const int NP = nx + 1;                      // nodes per node row
-  const int T = blockDim.x, tid = threadIdx.x;
-  double* const stg = sm;                     // [3 layers][2 rows][6 comps][NP]
-  double* const xl = stg + 36 * NP;           // [2 rows][3][NP]: corners di = 0 of thread i
-  double* const xr = xl + 6 * NP;             // [2 rows][3][NP]: corners di = 1 of thread i - 1
-  double* const own = xr + 6 * NP;            // [2 slots][3][NP]: node row j, thread-private
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int a = blockIdx.x, b = blockIdx.y, c = blockIdx.z;
+  const int i0 = 32 * a, j0 = kKmomTY * b;
+  const int tyb = min(kKmomTY, ny - j0);  // cell rows of this CTA
+  double* const stg = sm + (size_t)w * kKmomWarpD;
+  volatile double* const ring = stg + kKmomStg;                                   // my top rows [slot][33][3]
+  volatile double* const dring = sm + (size_t)(w - 1) * kKmomWarpD + kKmomStg;  // the warp below's
+  volatile int* const yc = reinterpret_cast<volatile int*>(sm + (size_t)kKmomTY * kKmomWarpD);  // [TY][2]
   const double r = rho * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
   const double muW = mu * c_ref[FPB_TET04].W;
-  __shared__ int s_ticket;
-  if (tid == 0) s_ticket = atomicAdd(sync, 1);
-  for (int i = tid; i < 6 * NP; i += T) {  // xr[.][.][0] and xl[.][.][nx] stay zero
-    xl[i] = 0.0;
-    xr[i] = 0.0;
-  }
+  if (threadIdx.x < 2 * kKmomTY) yc[threadIdx.x] = 0;
   __syncthreads();
-  const int ticket = s_ticket;
-  const int c = ticket / ny, j = ticket - c * ny;
+  if (w >= tyb) return;  // no barrier below
+  const int j = j0 + w;
   const int nchunk = (nz + kchunk - 1) / kchunk;
   const int kb = c * kchunk, ke = min(nz, kb + kchunk);
   const int kfirst = c > 0 ? kb - 1 : kb;          // halo cell layer below the chunk
   const int klast = c == nchunk - 1 ? nz : ke - 1;  // last node layer written (nz: the top face)
-  const int ktop = ke;                               // highest node layer staged
-  int* const flags = sync + 1 + (size_t)c * ny;      // layers of row j+1's partial published
-  const int64_t row = NP, layer = (int64_t)NP * (ny + 1);
+  const int64_t row = nx + 1, layer = (int64_t)(nx + 1) * (ny + 1);
+  const bool cell = i0 + lane < nx;
+  const bool last_x = i0 + 32 >= nx;
+  const bool node = i0 + lane <= nx;                 // my node column i0 + lane is written here
+  const bool xtra = i0 + 32 == nx && lane == 31;     // also owns node column nx
+  const bool redge = lane == 31 && !last_x;          // right edge -> the next x-block (Px)
+  const bool top_w = w == tyb - 1;                   // my top node row leaves the CTA
+  const bool top_final = top_w && j + 1 == ny;
 
-  auto stage = [&](int kl) {  // node layer kl, node rows j, j+1 -> stg[kl % 3]
-    double* s = stg + (kl % 3) * 12 * NP;
-    for (int i = tid; i < NP; i += T) {
+  auto stage = [&](int kl) {  // node layer kl, node rows j, j + 1, columns i0 .. i0 + 32
+    double* s = stg + (kl % 3) * 2 * 6 * 33;
+    for (int q = lane; q < 33; q += 32) {
+      const int ii = i0 + q;
+      if (ii <= nx) {
 #pragma unroll
-      for (int dj = 0; dj < 2; ++dj) {
-        const int64_t nd = i + (j + dj) * row + kl * layer;
-        double* t = s + dj * 6 * NP + i;
-        cp8(t, xyz4 + 4 * nd);
-        cp8(t + NP, xyz4 + 4 * nd + 1);
-        cp8(t + 2 * NP, xyz4 + 4 * nd + 2);
-        cp8(t + 3 * NP, vel + 3 * nd);
-        cp8(t + 4 * NP, vel + 3 * nd + 1);
-        cp8(t + 5 * NP, vel + 3 * nd + 2);
+        for (int dj = 0; dj < 2; ++dj) {
+          const int64_t nd = ii + (j + dj) * row + kl * layer;
+          double* t = s + dj * 6 * 33 + q;
+          cp8(t, xyz4 + 4 * nd);
+          cp8(t + 33, xyz4 + 4 * nd + 1);
+          cp8(t + 66, xyz4 + 4 * nd + 2);
+          cp8(t + 99, vel + 3 * nd);
+          cp8(t + 132, vel + 3 * nd + 1);
+          cp8(t + 165, vel + 3 * nd + 2);
+        }
       }
     }
     cp_commit();
@@ -107,117 +129,196 @@ k_kuhn_mom(int nx, int ny, int nz, int kchunk, const double* __restrict__ xyz4, 
 
   stage(kfirst);
   stage(kfirst + 1);
-  double bot[4][3];  // corners dk = 0: (di, dj) = c & 3
+  double bot[4][3];  // corners dk = 0, index di + 2 dj
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int d = 0; d < 3; ++d) bot[q][d] = 0.0;
-  const bool cell = tid < nx;
+  double R[3], X[3];  // node row j of layer t - 1 (B -> C): my column; column i0 + 32 (lane 31)
+#pragma unroll
+  for (int d = 0; d < 3; ++d) R[d] = X[d] = 0.0;
 
-  for (int k = kfirst; k <= klast; ++k) {
-    cp_wait_all();
-    // node row j of layer k - 1 is written below: row j - 1's partial of it
-    // must be published (it was, one layer ago, unless that CTA lags)
-    if (tid == 0 && j > 0 && k - 1 >= kb) {
-      const int need = k - kb;
-      while (ld_acquire(flags + j - 1) < need) __nanosleep(64);
-    }
-    __syncthreads();
-    if (tid == 0 && j + 1 < ny && k - 1 >= kb) st_release(flags + j, k - kb);  // layer k - 1 of row j + 1
-    if (k + 2 <= ktop) stage(k + 2);
-    if (k - 1 >= kb) {  // deferred write-out of node row j, layer k - 1
-      const int sl = (k - 1) & 1;
-      for (int i = tid; i < NP; i += T) {
-        const int64_t nd = i + j * row + (int64_t)(k - 1) * layer;
+  for (int t = kfirst; t <= klast + 1; ++t) {
+    // (C) node row j of layer t - 1: add the warp below's top row, write out
+    if (t - 1 >= kb) {
+      const int kk = t - 1;
+      if (w > 0) {
+        if (lane == 0)
+          while (yc[2 * (w - 1)] < kk - kb + 1) __nanosleep(20);
+        __syncwarp();
+        const volatile double* e = dring + (kk % kKmomRing) * kKmomSlot;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const double o = own[(sl * 3 + d) * NP + i];
-          out[3 * nd + d] = j > 0 ? __ldcg(pup + 3 * nd + d) + o : o;
+          R[d] += e[lane * 3 + d];
+          if (lane == 31) X[d] += e[32 * 3 + d];
         }
+        __syncwarp();
+        if (lane == 0) yc[2 * (w - 1) + 1] = kk - kb + 1;  // consumed
+      }
+      const int64_t nd = i0 + lane + j * row + (int64_t)kk * layer;
+      if (node) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) out[3 * nd + d] = R[d];
+      }
+      if (xtra) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) out[3 * (nd + 1) + d] = X[d];
+      } else if (redge) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) part[g.px(a, b, kk, w) + d] = X[d];
       }
     }
+    if (t > klast) break;
+    // (A) cell layer t
+    __syncwarp();
+    if (t + 2 <= ke) stage(t + 2);
+    else cp_commit();
+    cp_wait_1();
+    __syncwarp();
     double top[4][3];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int d = 0; d < 3; ++d) top[q][d] = 0.0;
-    if (cell && k < nz) {
-      const double* s0 = stg + (k % 3) * 12 * NP + tid;
-      const double* s1 = stg + ((k + 1) % 3) * 12 * NP + tid;
+    if (cell && t < nz) {
+      const double* s0 = stg + (t % 3) * 2 * 6 * 33 + lane;
+      const double* s1 = stg + ((t + 1) % 3) * 2 * 6 * 33 + lane;
 #pragma unroll
-      for (int t = 0; t < 6; ++t) {
+      for (int tt = 0; tt < 6; ++tt) {
         asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
         double xe[4][3], ue[4][3];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int cc = kuhn_corner(t, a);
-          const double* s = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * 6 * NP + (cc & 1);
+        for (int q = 0; q < 4; ++q) {
+          const int cc = kuhn_corner(tt, q);
+          const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * 6 * 33 + (cc & 1);
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            xe[a][d] = s[d * NP];
-            ue[a][d] = s[(3 + d) * NP];
+            xe[q][d] = sp[d * 33];
+            ue[q][d] = sp[(3 + d) * 33];
           }
         }
-        tet_mom_adj_f(xe, ue, r, muW, [&](int a, int d, double v) {
-          const int cc = kuhn_corner(t, a);
+        tet_mom_adj_f(xe, ue, r, muW, [&](int q, int d, double v) {
+          const int cc = kuhn_corner(tt, q);
           if (cc & 4) top[cc & 3][d] -= v;
           else bot[cc & 3][d] -= v;
         });
       }
     }
-    if (cell && k >= kb) {  // bottom face complete in z: split by x owner
+    // (B) layer t's bottom face is complete in z: x-shuffle; the right edge
+    // and the top node row leave the warp
+    if (t >= kb) {
+      double up[3], ex1[3];  // row j + 1 at my column; right edge of row j + 1 (lane 31)
 #pragma unroll
-      for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          xl[(dj * 3 + d) * NP + tid] = bot[2 * dj][d];
-          xr[(dj * 3 + d) * NP + tid + 1] = bot[2 * dj + 1][d];
-        }
-    }
-    __syncthreads();
-    if (k >= kb) {
-      const int sl = k & 1;
-      bool wrote = false;
-      for (int i = tid; i < NP; i += T) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          own[(sl * 3 + d) * NP + i] = xl[d * NP + i] + xr[d * NP + i];
-          const double s1v = xl[(3 + d) * NP + i] + xr[(3 + d) * NP + i];
-          const int64_t nd = i + (j + 1) * row + (int64_t)k * layer;
-          if (j + 1 < ny) pup[3 * nd + d] = s1v;
-          else out[3 * nd + d] = s1v;
-        }
-        wrote = true;
+      for (int d = 0; d < 3; ++d) {
+        const double l0 = __shfl_up_sync(0xffffffffu, bot[1][d], 1);
+        const double l1 = __shfl_up_sync(0xffffffffu, bot[3][d], 1);
+        R[d] = lane > 0 ? bot[0][d] + l0 : bot[0][d];
+        up[d] = lane > 0 ? bot[2][d] + l1 : bot[2][d];
+        X[d] = bot[1][d];
+        ex1[d] = bot[3][d];
       }
-      if (wrote && j + 1 < ny) __threadfence();
+      if (top_w) {  // row j + 1 leaves the CTA: final (top of the mesh) or Py / Px partials
+        const int64_t nd1 = i0 + lane + (j + 1) * row + (int64_t)t * layer;
+        if (top_final) {
+          if (node) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) out[3 * nd1 + d] = up[d];
+          }
+          if (xtra) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) out[3 * (nd1 + 1) + d] = ex1[d];
+          }
+        } else {
+          if (node) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) part[g.py(a, b, t, lane) + d] = up[d];
+          }
+          if (xtra) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) part[g.py(a, b, t, 32) + d] = ex1[d];
+          }
+        }
+        if (redge) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) part[g.px(a, b, t, tyb) + d] = ex1[d];
+        }
+      } else {  // to the warp above
+        if (lane == 0)
+          while (yc[2 * w + 1] < (t - kb + 1) - kKmomRing) __nanosleep(20);  // slot free
+        __syncwarp();
+        volatile double* slot = ring + (t % kKmomRing) * kKmomSlot;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          slot[lane * 3 + d] = up[d];
+          if (lane == 31) slot[32 * 3 + d] = ex1[d];
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) yc[2 * w] = t - kb + 1;  // full
+      }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int d = 0; d < 3; ++d) bot[q][d] = top[q][d];
   }
-  // last node layer of row j: publish ours first, then wait for row j - 1
-  __syncthreads();
-  if (tid == 0) {
-    if (j + 1 < ny) st_release(flags + j, klast - kb + 1);
-    if (j > 0)
-      while (ld_acquire(flags + j - 1) < klast - kb + 1) __nanosleep(64);
-  }
-  __syncthreads();
-  {
-    const int sl = klast & 1;
-    for (int i = tid; i < NP; i += T) {
-      const int64_t nd = i + j * row + (int64_t)klast * layer;
+  cp_wait_all();
+}
+
+// Boundary nodes: x-block edges (columns 32 a, 0 < a < nxb) over every node
+// row, then y-block edges (rows TY b, 0 < b < nyb) over the other columns.
+// out += Px(a - 1, b)[lr] (+ Py(a, b - 1)[0] + Px(a - 1, b - 1)[TY] at a
+// y-block edge), resp. out += Py(a, b - 1)[l] — a fixed order per node.
+__global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double* __restrict__ out) {
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int64_t row = nx + 1, layer = (int64_t)(nx + 1) * (ny + 1);
+  const int64_t nxe = (int64_t)(g.nxb - 1) * (ny + 1);                // x-edge nodes per layer
+  const int64_t cols = nx + 1 - (g.nxb - 1);                          // columns that are not x-edges
+  const int64_t per = nxe + (int64_t)(g.nyb - 1) * cols;
+  const int64_t total = per * (nz + 1);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(q / per);
+    int64_t u = q - (int64_t)k * per;
+    if (u < nxe) {
+      const int a = 1 + (int)(u / (ny + 1));
+      const int jn = (int)(u - (int64_t)(a - 1) * (ny + 1));
+      const int b = min(jn / kKmomTY, g.nyb - 1);
+      const int lr = jn - kKmomTY * b;
+      const int64_t nd = 32 * a + jn * row + (int64_t)k * layer;
+      double s[3];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double o = own[(sl * 3 + d) * NP + i];
-        out[3 * nd + d] = j > 0 ? __ldcg(pup + 3 * nd + d) + o : o;
+      for (int d = 0; d < 3; ++d) s[d] = out[3 * nd + d] + part[g.px(a - 1, b, k, lr) + d];
+      if (lr == 0 && b > 0) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          s[d] = (s[d] + part[g.py(a, b - 1, k, 0) + d]) + part[g.px(a - 1, b - 1, k, kKmomTY) + d];
       }
+#pragma unroll
+      for (int d = 0; d < 3; ++d) out[3 * nd + d] = s[d];
+    } else {
+      u -= nxe;
+      const int b = 1 + (int)(u / cols);
+      const int m = (int)(u - (int64_t)(b - 1) * cols);  // m-th column that is not an x-edge
+      const int i = m < 32 ? m : m + min((m - 32) / 31 + 1, g.nxb - 1);
+      const int a = min(i / 32, g.nxb - 1);
+      const int64_t nd = i + (int64_t)(kKmomTY * b) * row + (int64_t)k * layer;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) out[3 * nd + d] = out[3 * nd + d] + part[g.py(a, b - 1, k, i - 32 * a) + d];
     }
   }
 }
 
-inline size_t kmom_smem(int nx) { return (size_t)(36 + 6 + 6 + 6) * (nx + 1) * sizeof(double); }
+inline size_t kmom_smem() { return (size_t)kKmomTY * kKmomWarpD * sizeof(double) + 2 * kKmomTY * sizeof(int); }
+
+inline KuhnGrid kuhn_grid(int nx, int ny, int nz) {
+  KuhnGrid g;
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = nz;
+  g.nxb = (nx + 31) / 32;
+  g.nyb = (ny + kKmomTY - 1) / kKmomTY;
+  return g;
+}
 
 }  // namespace fpb
 
@@ -225,27 +326,31 @@ using namespace fpb;
 
 extern "C" {
 
-int fpb_kuhn_mom_sync_len(int ny, int nz, int kchunk) {
-  if (ny < 1 || nz < 1 || kchunk < 1) return 0;
-  return 1 + ny * ((nz + kchunk - 1) / kchunk);
+int64_t fpb_kuhn_mom_scratch_len(int nx, int ny, int nz) {
+  if (nx < 1 || ny < 1 || nz < 1) return 0;
+  return kuhn_grid(nx, ny, nz).scratch();
 }
 
 int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double* xyz4, const double* vel,
-                               double rho, double mu, int32_t* sync, double* pup, double* out, void* stream) {
+                               double rho, double mu, double* scratch, double* out, void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
-  FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1 && nx <= 256, "Kuhn box %d x %d x %d: need 1 <= nx <= 256", nx, ny, nz);
+  FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "Kuhn box %d x %d x %d", nx, ny, nz);
   FPB_REQUIRE(kchunk >= 1, "bad z chunk %d", kchunk);
-  FPB_REQUIRE(xyz4 && vel && sync && pup && out, "null argument");
+  FPB_REQUIRE(xyz4 && vel && scratch && out, "null argument");
   cudaStream_t s = as_stream(stream);
+  const KuhnGrid g = kuhn_grid(nx, ny, nz);
   const int nchunk = (nz + kchunk - 1) / kchunk;
-  const int nsync = 1 + ny * nchunk;
-  FPB_CUDA(cudaMemsetAsync(sync, 0, sizeof(int32_t) * nsync, s));
-  const size_t smem = kmom_smem(nx);
-  const int T = (nx + 31) / 32 * 32;
-  auto kern = k_kuhn_mom<256>;
+  FPB_REQUIRE(g.nyb <= 65535 && nchunk <= 65535, "grid too large");
+  const size_t smem = kmom_smem();
+  auto kern = k_kuhn_mom<32 * kKmomTY>;
   FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)(ny * nchunk), T, smem, s>>>(nx, ny, nz, kchunk, xyz4, vel, rho, mu, sync, pup, out);
+  kern<<<dim3(g.nxb, g.nyb, nchunk), 32 * kKmomTY, smem, s>>>(g, kchunk, xyz4, vel, rho, mu, scratch, out);
   FPB_LAUNCH_CHECK();
+  const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (nz + 1);
+  if (nb > 0) {
+    k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out);
+    FPB_LAUNCH_CHECK();
+  }
   return FPB_OK;
 }
 

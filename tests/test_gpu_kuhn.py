@@ -41,7 +41,8 @@ def _jitter(coords, nx, ny, nz, seed=3):
 
 @pytest.mark.parametrize("dims,kchunk", [((5, 4, 7), 0), ((5, 4, 7), 1), ((5, 4, 7), 2), ((5, 4, 7), 3),
                                          ((1, 1, 1), 0), ((1, 3, 2), 1), ((33, 3, 5), 2), ((64, 2, 3), 0),
-                                         ((7, 1, 9), 4)])
+                                         ((7, 1, 9), 4), ((65, 17, 4), 3), ((32, 8, 2), 0), ((70, 16, 5), 2),
+                                         ((31, 9, 3), 1), ((96, 24, 3), 0)])
 @pytest.mark.parametrize("jitter", [False, True])
 def test_kuhn_momentum_matches_oracle(cuda_ok, dims, kchunk, jitter):
     import paper_2107_11541_b200 as P
@@ -61,17 +62,16 @@ def test_kuhn_momentum_matches_oracle(cuda_ok, dims, kchunk, jitter):
         assert O.rel_diff(r, ro) < TOL, (dims, kchunk, rho, mu, O.rel_diff(r, ro))
 
 
-def test_kuhn_nx_limit_and_detection(cuda_ok):
+def test_kuhn_wide_and_detection(cuda_ok):
     import paper_2107_11541_b200 as P
 
-    _, ctx = _ctx(P, 256, 1, 2)
-    assert ctx.groups[0].kuhn is not None  # widest supported line
-    om = O.box(O.TET04, 256, 1, 2)
-    vel, _ = O.bench_fields(om.nnode, 3)
-    r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
-    assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL
-    _, ctx = _ctx(P, 257, 1, 1)
-    assert ctx.groups[0].kuhn is None  # too wide: element blocks
+    for dims in ((300, 1, 2), (257, 9, 1)):
+        _, ctx = _ctx(P, *dims)
+        assert ctx.groups[0].kuhn is not None
+        om = O.box(O.TET04, *dims)
+        vel, _ = O.bench_fields(om.nnode, 3)
+        r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
+        assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL, dims
     # a permuted element order is not the generator's: element blocks
     mesh = P.generate_box_mesh(P.ElementType.TET04, 4, 3, 2)
     conn = mesh.groups[0].conn.copy()
