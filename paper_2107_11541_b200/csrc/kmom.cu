@@ -55,7 +55,8 @@ constexpr int kKmomTY = FPB_KMOM_TY;            // cell rows (warps) per CTA
 constexpr int kKmomRing = 4;                    // y-forward slots per warp
 constexpr int kKmomStg = 3 * 2 * 6 * 33;        // staged doubles per warp: [layer][row][comp][33 nodes]
 constexpr int kKmomSlot = 33 * 3;               // one forwarded node row: [33][3]
-constexpr int kKmomWarpD = kKmomStg + kKmomRing * kKmomSlot;
+constexpr int kKmomHold = 2 * 3 * 33;           // node row j held two layers: [parity][comp][33]
+constexpr int kKmomWarpD = kKmomStg + kKmomRing * kKmomSlot + kKmomHold;
 
 // boundary partials, per CTA (a, b) and node layer k:
 //   Px[a][b][k][lr][3], lr = 0..kKmomTY: node column i0 + 32 (the next x-block's
@@ -86,6 +87,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   double* const stg = sm + (size_t)w * kKmomWarpD;
   volatile double* const ring = stg + kKmomStg;                                   // my top rows [slot][33][3]
   volatile double* const dring = sm + (size_t)(w - 1) * kKmomWarpD + kKmomStg;  // the warp below's
+  double* const hold = stg + kKmomStg + kKmomRing * kKmomSlot;                   // lane-private
   volatile int* const yc = reinterpret_cast<volatile int*>(sm + (size_t)kKmomTY * kKmomWarpD);  // [TY][2]
   const double r = rho * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
   const double muW = mu * c_ref[FPB_TET04].W;
@@ -134,14 +136,18 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   for (int q = 0; q < 4; ++q)
 #pragma unroll
     for (int d = 0; d < 3; ++d) bot[q][d] = 0.0;
-  double R[3], X[3];  // node row j of layer t - 1 (B -> C): my column; column i0 + 32 (lane 31)
+  for (int t = kfirst; t <= klast + 2; ++t) {
+    // (C) node row j of layer t - 2 (held in smem since (B), so the warp
+    // below had a whole iteration to forward it): add its top row, write out
+    if (t - 2 >= kb) {
+      const int kk = t - 2;
+      double R[3], X[3];  // my column; column i0 + 32 (lane 31)
+      const double* h = hold + (kk & 1) * 99;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) R[d] = X[d] = 0.0;
-
-  for (int t = kfirst; t <= klast + 1; ++t) {
-    // (C) node row j of layer t - 1: add the warp below's top row, write out
-    if (t - 1 >= kb) {
-      const int kk = t - 1;
+      for (int d = 0; d < 3; ++d) {
+        R[d] = h[d * 33 + lane];
+        X[d] = h[d * 33 + 32];
+      }
       if (w > 0) {
         if (lane == 0)
           while (yc[2 * (w - 1)] < kk - kb + 1) __nanosleep(20);
@@ -168,7 +174,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
         for (int d = 0; d < 3; ++d) part[g.px(a, b, kk, w) + d] = X[d];
       }
     }
-    if (t > klast) break;
+    if (t > klast) continue;
     // (A) cell layer t
     __syncwarp();
     if (t + 2 <= ke) stage(t + 2);
@@ -212,9 +218,10 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
       for (int d = 0; d < 3; ++d) {
         const double l0 = __shfl_up_sync(0xffffffffu, bot[1][d], 1);
         const double l1 = __shfl_up_sync(0xffffffffu, bot[3][d], 1);
-        R[d] = lane > 0 ? bot[0][d] + l0 : bot[0][d];
+        double* h = hold + (t & 1) * 99;
+        h[d * 33 + lane] = lane > 0 ? bot[0][d] + l0 : bot[0][d];
+        if (lane == 31) h[d * 33 + 32] = bot[1][d];
         up[d] = lane > 0 ? bot[2][d] + l1 : bot[2][d];
-        X[d] = bot[1][d];
         ex1[d] = bot[3][d];
       }
       if (top_w) {  // row j + 1 leaves the CTA: final (top of the mesh) or Py / Px partials

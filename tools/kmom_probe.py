@@ -69,7 +69,8 @@ def main():
             torch.cuda.empty_cache()
         del mesh, vel, out, ref
         torch.cuda.empty_cache()
-    print(json.dumps(res, indent=1))
+    for k, v in res.items():
+        print(k, json.dumps(v))
 
 
 if __name__ == "__main__":
