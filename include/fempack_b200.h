@@ -281,6 +281,13 @@ int fpb_assemble_gradient_pairs_rows(int32_t n, int32_t nrows, const int32_t* ro
 int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const int32_t* rlos, const int32_t* nbr,
                                      const double* xyz4, const int32_t* rowptr, const int32_t* colind, int64_t nnz,
                                      int accumulate, double* out, void* stream);
+/* Same rows on the generator's Kuhn box (nx x ny cells per layer; the
+ * connectivity checked equal to generate_box_mesh's, assembly.py KuhnBox):
+ * the 14 neighbours of an interior row are at fixed node offsets, so colind
+ * is not read.  rows: canonical (15-entry, interior) rows only. */
+int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
+                                         const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
+                                         void* stream);
 
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices

@@ -413,11 +413,22 @@ constexpr int kKuhnWarps = 2;  // warps (32-row slices) per CTA
 #ifndef FPB_KUHN_MINB
 #define FPB_KUHN_MINB 6
 #endif
+// BOX (R = nx + 1, L = (nx + 1)(ny + 1) > 0): the mesh is the generator's Kuhn
+// box (assembly.py KuhnBox), whose interior rows hold the node and its 14
+// neighbours at the offsets +-1, +-R, +-(1+R), +-L, +-(1+L), +-(R+L),
+// +-(1+R+L) in ascending order: the neighbour ids are computed, not read
+// from colind (one dependent load level and 4 B per entry less).
+__host__ __device__ __forceinline__ int64_t kuhn_box_off(int t, int64_t R, int64_t L) {
+  const int64_t o[7] = {1 + R + L, R + L, 1 + L, L, 1 + R, R, 1};
+  return t < 7 ? -o[t] : o[13 - t];
+}
+
+template <bool BOX>
 __global__ void __launch_bounds__(32 * kKuhnWarps, FPB_KUHN_MINB)
 k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ rlos,
                   const int32_t* __restrict__ nbr, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz,
-                  int accumulate, double* __restrict__ out) {
+                  int accumulate, double* __restrict__ out, int64_t boxR = 0, int64_t boxL = 0) {
   constexpr int DIM = 3, R = kKuhnCols + 1;  // entries per row
   __shared__ double Bo[kKuhnWarps][DIM][32 * R];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -442,7 +453,8 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
     for (int d = 0; d < DIM; ++d) x0[d] = r4[d];
 #pragma unroll
     for (int t = 0; t < kKuhnCols; ++t) {
-      const int col = nbr ? __ldg(nbr + (int64_t)t * nrows + i0 + lane) : __ldg(colind + rlo + t + (t >= dslot));
+      const int64_t col = BOX ? row + kuhn_box_off(t, boxR, boxL)
+                              : nbr ? __ldg(nbr + (int64_t)t * nrows + i0 + lane) : __ldg(colind + rlo + t + (t >= dslot));
       ld256(xyz4 + 4 * (int64_t)col, r4);
 #pragma unroll
       for (int d = 0; d < DIM; ++d) X[t][d] = r4[d] - x0[d];
@@ -606,8 +618,22 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
   FPB_REQUIRE(rows && xyz4 && rowptr && colind && out, "missing arrays for the Kuhn-stream kernel");
   if (nrows <= 0) return FPB_OK;
   const int64_t warps = ((int64_t)nrows + 31) / 32;
-  k_rows_pairs_kuhn<<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
+  k_rows_pairs_kuhn<false><<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
       nrows, rows, rlos, nbr, xyz4, rowptr, colind, nnz, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
+                                         const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
+                                         void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1, "bad Kuhn-box gradient arguments");
+  if (nrows <= 0) return FPB_OK;
+  const int64_t warps = ((int64_t)nrows + 31) / 32;
+  const int64_t R = nx + 1, L = R * (ny + 1);
+  k_rows_pairs_kuhn<true><<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
+      nrows, rows, nullptr, nullptr, xyz4, rowptr, nullptr, nnz, accumulate, out, R, L);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }

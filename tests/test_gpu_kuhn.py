@@ -109,3 +109,32 @@ def test_kuhn_matches_block_path_and_is_deterministic(cuda_ok):
         A.KUHN_MOMENTUM = True
     a, b = out1.cpu().numpy(), ref.cpu().numpy()
     assert O.rel_diff(a, b) < TOL
+
+
+def test_kuhn_box_gradients_bitwise_equal_colind_path(cuda_ok):
+    """Continuity B_x, B_y, B_z on a Kuhn box: neighbour ids by offset
+    (fpb_assemble_gradient_pairs_kuhn_box) give bitwise the colind path's
+    values (same arithmetic, same order), and match the oracle."""
+    import paper_2107_11541_b200 as P
+    import paper_2107_11541_b200.assembly as A
+
+    for dims in ((37, 21, 9), (6, 5, 4)):
+        om = O.box(O.TET04, *dims)
+        om.coords = _jitter(om.coords, *dims, seed=11)
+        mesh, ctx = _ctx(P, *dims, coords=om.coords)
+        assert ctx.groups[0].kuhn is not None
+        nnz = ctx.pattern.nnz
+        a = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
+        b = torch.empty_like(a)
+        ctx.assemble_gradients_d(a)
+        A.KUHN_BOX_GRADIENT = False
+        try:
+            ctx.assemble_gradients_d(b)
+        finally:
+            A.KUHN_BOX_GRADIENT = True
+        assert torch.equal(a, b), dims
+        for k in range(3):
+            e = np.zeros((om.nnode, 3))
+            e[:, k] = 1.0
+            _, _, vo = O.assemble_matrix(om, "convection", e)
+            assert O.rel_diff(a[k * nnz:(k + 1) * nnz].cpu().numpy(), vo) < TOL, (dims, k)

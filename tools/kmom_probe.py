@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--kchunks", default="0")
     ap.add_argument("--blocks", type=int, default=1)
+    ap.add_argument("--grad", type=int, default=0, help="also time B_x,B_y,B_z (Kuhn box vs colind path)")
     args = ap.parse_args()
     flush = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
     res = {}
@@ -65,6 +66,18 @@ def main():
                 torch.cuda.synchronize()
                 d = float((out - ref).abs().max() / ref.abs().max())
                 res[f"{sz}/blocks"] = {"ms": round(msb, 4), "Gelem_s": round(ne / msb / 1e6, 2), "rel_diff": d}
+            if args.grad:
+                nnz = ctx.pattern.nnz
+                ga = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
+                gb = torch.empty_like(ga)
+                msg = timeit(lambda: ctx.assemble_gradients_d(ga), args.reps, flush)
+                A.KUHN_BOX_GRADIENT = False
+                msc = timeit(lambda: ctx.assemble_gradients_d(gb), args.reps, flush)
+                A.KUHN_BOX_GRADIENT = True
+                res[f"{sz}/grad_box"] = {"ms": round(msg, 4), "Gelem_s": round(ne / msg / 1e6, 2),
+                                         "bitwise_equal": bool(torch.equal(ga, gb))}
+                res[f"{sz}/grad_colind"] = {"ms": round(msc, 4), "Gelem_s": round(ne / msc / 1e6, 2)}
+                del ga, gb
             del ctx
             torch.cuda.empty_cache()
         del mesh, vel, out, ref
