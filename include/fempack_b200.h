@@ -283,8 +283,9 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
                                      int accumulate, double* out, void* stream);
 /* Same rows on the generator's Kuhn box (nx x ny cells per layer; the
  * connectivity checked equal to generate_box_mesh's, assembly.py KuhnBox):
- * the 14 neighbours of an interior row are at fixed node offsets, so colind
- * is not read.  rows: canonical (15-entry, interior) rows only. */
+ * the canonical rows are exactly the interior nodes (nrows = (nx-1)(ny-1)
+ * (nz-1), the caller checks the count), so row ids and the 14 neighbours'
+ * ids are computed — neither rows nor colind is read (rows may be NULL). */
 int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
                                          const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
                                          void* stream);

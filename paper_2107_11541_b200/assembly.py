@@ -691,7 +691,10 @@ class AssemblyContext:
                 if r.pair_canon is not None and window is None:
                     pc = r.pair_canon
                     rp_, ci_ = self.pattern.rowptr_d.data_ptr(), self.pattern.colind_d.data_ptr()
-                    if pc["kuhn"] and g.kuhn is not None and KUHN_BOX_GRADIENT:  # neighbour ids computed
+                    kb_ = g.kuhn
+                    box = (pc["kuhn"] and kb_ is not None and KUHN_BOX_GRADIENT and kb_.nx > 1 and kb_.ny > 1
+                           and int(pc["rows"].numel()) == (kb_.nx - 1) * (kb_.ny - 1) * (kb_.nz - 1))
+                    if box:  # canonical rows = the interior nodes: row and neighbour ids computed
                         _lib.call("fpb_assemble_gradient_pairs_kuhn_box", int(pc["rows"].numel()),
                                   pc["rows"].data_ptr(), g.kuhn.nx, g.kuhn.ny, xyz4, rp_, nnz, acc, out.data_ptr(),
                                   _lib.stream())

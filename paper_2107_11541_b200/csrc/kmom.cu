@@ -25,6 +25,8 @@
 //   synchronisation).  z-chunks integrate the cell layer below them (halo)
 //   for the contributions to their lowest node layer, so they are
 //   independent too.  Every sum has a fixed order: bitwise reproducible.
+#include <algorithm>
+
 #include "simplex.cuh"
 
 namespace fpb {
@@ -315,6 +317,8 @@ __global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double
   }
 }
 
+int g_tuning_kmom_smem_kb = 0;  // fpb_set_tuning("kmom_smem_kb", KB): pad the CTA's shared memory (co-residency A/B)
+
 inline size_t kmom_smem() { return (size_t)kKmomTY * kKmomWarpD * sizeof(double) + 2 * kKmomTY * sizeof(int); }
 
 inline KuhnGrid kuhn_grid(int nx, int ny, int nz) {
@@ -348,7 +352,7 @@ int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double*
   const KuhnGrid g = kuhn_grid(nx, ny, nz);
   const int nchunk = (nz + kchunk - 1) / kchunk;
   FPB_REQUIRE(g.nyb <= 65535 && nchunk <= 65535, "grid too large");
-  const size_t smem = kmom_smem();
+  const size_t smem = std::max(kmom_smem(), (size_t)g_tuning_kmom_smem_kb * 1024);
   auto kern = k_kuhn_mom<32 * kKmomTY>;
   FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<dim3(g.nxb, g.nyb, nchunk), 32 * kKmomTY, smem, s>>>(g, kchunk, xyz4, vel, rho, mu, scratch, out);

@@ -31,6 +31,7 @@
 // columns go straight into the warp's linear output rows.  Config 2
 // (B200): 0.196 ms vs 0.264 ms for k_rows_nb (profiles/r01v_pairs ..
 // r01y_step); 24-word batches = one third of an interior row's 72 pairs.
+#include <algorithm>
 #include <cub/device/device_scan.cuh>
 
 #include "elemcore.cuh"
@@ -428,14 +429,30 @@ __global__ void __launch_bounds__(32 * kKuhnWarps, FPB_KUHN_MINB)
 k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ rlos,
                   const int32_t* __restrict__ nbr, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind, int64_t nnz,
-                  int accumulate, double* __restrict__ out, int64_t boxR = 0, int64_t boxL = 0) {
+                  int accumulate, double* __restrict__ out, int64_t boxR = 0, int64_t boxL = 0, int nxi = 0,
+                  int nyi = 0) {
   constexpr int DIM = 3, R = kKuhnCols + 1;  // entries per row
   __shared__ double Bo[kKuhnWarps][DIM][32 * R];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = ((int64_t)blockIdx.x * kKuhnWarps + warp) * 32;  // the warp's 32 list entries
-  if (i0 >= nrows) return;
-  const bool live = i0 + lane < nrows;
-  const int row = live ? __ldg(rows + i0 + lane) : -1;
+  bool live;
+  int row;
+  if constexpr (BOX) {
+    // interior node rows by arithmetic: warp -> (x segment, interior line
+    // (j, k)), lane -> i; nrows = the number of warps
+    const int64_t wg = i0 >> 5;
+    if (wg >= nrows) return;
+    const int segs = (nxi + 31) >> 5;
+    const int64_t line = wg / segs;
+    const int i = 1 + 32 * (int)(wg - line * segs) + lane;
+    const int64_t j = 1 + line % nyi, k = 1 + line / nyi;
+    live = i <= nxi;
+    row = live ? (int)(i + boxR * j + boxL * k) : -1;
+  } else {
+    if (i0 >= nrows) return;
+    live = i0 + lane < nrows;
+    row = live ? __ldg(rows + i0 + lane) : -1;
+  }
   // rlos / nbr (per list entry, nullable): the row's CSR start and its 14
   // neighbours ([14][nrows]) precomputed, so every load below is indexed by
   // the list position alone — one dependent level (-> coordinates) instead
@@ -523,6 +540,136 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
   }
 }
 
+
+// ---- Kuhn box, z-marching interior lines -----------------------------------
+// Same rows, values and order as k_rows_pairs_kuhn<true>, but each warp owns
+// a 32-node segment of one interior node line (j) and walks the interior
+// layers k of a z-chunk.  The coordinates of node rows j - 1 .. j + 1 over the
+// segment's 34 node columns are staged per layer in the warp's shared-memory
+// ring by cp.async two layers ahead, so the 14 edge vectors of every row
+// come from shared memory and no load latency is exposed; the row's CSR
+// start is one load per warp and layer.  Warps are independent (no
+// barriers).
+constexpr int kGradWarps = 2;
+int g_tuning_kgrad_march = 1;  // fpb_set_tuning("kgrad_march", 0|1): z-marching lines (1) or the row kernel (0)
+int g_tuning_kgrad_kchunk = 32;
+constexpr int kGradStg = 4 * 3 * 3 * 34 + 2;  // [layer slot][node row][comp][34 columns] + 4 CSR starts (int)
+__device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kGradWarps, FPB_KUHN_MINB)
+k_kuhn_grad_march(int nx, int ny, int nz, int kchunk, int64_t nwarps, const double* __restrict__ xyz4,
+                  const int32_t* __restrict__ rowptr, int64_t nnz, int accumulate, double* __restrict__ out) {
+  constexpr int DIM = 3, RE = kKuhnCols + 1;  // entries per row
+  extern __shared__ __align__(16) double gsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * kGradWarps + warp;
+  if (wg >= nwarps) return;
+  double* const stg = gsm + (size_t)warp * (kGradStg + DIM * 32 * RE);
+  double* const bo = stg + kGradStg;
+  const int nxi = nx - 1, nyi = ny - 1;
+  const int segs = (nxi + 31) >> 5;
+  const int64_t per_chunk = (int64_t)segs * nyi;
+  const int c = (int)(wg / per_chunk);
+  const int rem = (int)(wg - (int64_t)c * per_chunk);
+  const int j = 1 + rem / segs, s = rem - (rem / segs) * segs;
+  const int i = 1 + 32 * s + lane;
+  const int nlive = min(32, nxi - 32 * s);
+  const bool live = lane < nlive;
+  const int kb = 1 + c * kchunk, ke = min(nz, kb + kchunk);
+  const int64_t R = nx + 1, L = R * (ny + 1);
+
+  int* const rlo_s = reinterpret_cast<int*>(stg + 4 * 3 * 3 * 34);  // [layer slot]
+  auto stage = [&](int kl) {  // node layer kl, node rows j - 1 .. j + 1, columns 32 s .. 32 s + 33
+    double* t0 = stg + (kl & 3) * 3 * 3 * 34;
+    if (lane == 0 && kl >= kb && kl < ke) {  // the segment's CSR start in layer kl (4-byte cp.async)
+      const unsigned d = (unsigned)__cvta_generic_to_shared(rlo_s + (kl & 3));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(rowptr + (1 + 32 * s) + R * j + L * kl)
+                   : "memory");
+    }
+    for (int q = lane; q < 34; q += 32) {
+      const int col = 32 * s + q;
+      if (col <= nx) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double* src = xyz4 + 4 * (col + R * (j - 1 + r) + L * kl);
+          double* t = t0 + r * 3 * 34 + q;
+          g_cp8(t, src);
+          g_cp8(t + 34, src + 1);
+          g_cp8(t + 68, src + 2);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  stage(kb - 1);
+  stage(kb);
+  stage(kb + 1);
+  const double mN0 = refmN<FPB_TET04>(0);
+  constexpr int dslot = kKuhnDiag;
+  for (int k = kb; k < ke; ++k) {
+    if (k + 2 <= nz) stage(k + 2);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    double x0[DIM], X[kKuhnCols][DIM];
+    {
+      const double* c0 = stg + (k & 3) * 3 * 3 * 34 + 1 * 3 * 34 + lane + 1;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) x0[d] = c0[d * 34];
+#pragma unroll
+      for (int t = 0; t < kKuhnCols; ++t) {
+        // neighbour offsets in ascending node order (kuhn_box_off): (di, dj, dk)
+        constexpr int8_t off[14][3] = {{-1, -1, -1}, {0, -1, -1}, {-1, 0, -1}, {0, 0, -1}, {-1, -1, 0},
+                                       {0, -1, 0},   {-1, 0, 0},  {1, 0, 0},   {0, 1, 0},  {1, 1, 0},
+                                       {0, 0, 1},    {1, 0, 1},   {0, 1, 1},   {1, 1, 1}};
+        const double* cp = stg + ((k + off[t][2]) & 3) * 3 * 3 * 34 + (1 + off[t][1]) * 3 * 34 + lane + 1 + off[t][0];
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) X[t][d] = cp[d * 34] - x0[d];
+      }
+    }
+    double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
+    int target = 0;
+#pragma unroll
+    for (int q8 = 0; q8 < kKuhnWords; ++q8) {
+      const int w = kuhn_word(q8);
+      const int q = w & 0x7f, r = (w >> 7) & 0x7f;
+      acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
+      acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
+      acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+      if (w & (1 << 14)) {  // column finished
+        const int cpos = target + (target >= dslot);
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          bo[d * 32 * RE + lane * RE + cpos] = mN0 * acc[d];
+          tot[d] += acc[d];
+          acc[d] = 0.0;
+        }
+        ++target;
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) bo[d * 32 * RE + lane * RE + dslot] = -(mN0 * tot[d]);
+    __syncwarp();
+    // the segment's rows are consecutive (15 entries each): one contiguous CSR range per matrix
+    const int base = rlo_s[k & 3];
+    const int span = nlive * RE;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double* o = out + d * nnz + base;
+      for (int q = lane; q < span; q += 32) {
+        const double v = bo[d * 32 * RE + q];
+        o[q] = accumulate ? o[q] + v : v;
+      }
+    }
+    (void)live;
+    __syncwarp();
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
 }  // namespace fpb
 
 using namespace fpb;
@@ -627,13 +774,30 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
 int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
                                          const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
                                          void* stream) {
+  if (g_tuning_kgrad_march && nx >= 2 && ny >= 2 && nrows > 0) {
+    const int nxi = nx - 1, nyi = ny - 1;
+    FPB_REQUIRE((int64_t)nrows % ((int64_t)nxi * nyi) == 0, "%d interior rows: not whole interior planes", nrows);
+    const int nz = nrows / (nxi * nyi) + 1;
+    const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk, nz - 1));
+    const int nchunk = (nz - 1 + kchunk - 1) / kchunk;
+    const int64_t nwarps = (int64_t)((nxi + 31) / 32) * nyi * nchunk;
+    const size_t smem = (size_t)kGradWarps * (kGradStg + 3 * 32 * (kKuhnCols + 1)) * sizeof(double);
+    FPB_CUDA(cudaFuncSetAttribute(k_kuhn_grad_march, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_kuhn_grad_march<<<(unsigned)((nwarps + kGradWarps - 1) / kGradWarps), 32 * kGradWarps, smem,
+                        as_stream(stream)>>>(nx, ny, nz, kchunk, nwarps, xyz4, rowptr, nnz, accumulate, out);
+    FPB_LAUNCH_CHECK();
+    return FPB_OK;
+  }
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1, "bad Kuhn-box gradient arguments");
   if (nrows <= 0) return FPB_OK;
-  const int64_t warps = ((int64_t)nrows + 31) / 32;
   const int64_t R = nx + 1, L = R * (ny + 1);
+  const int nxi = nx - 1, nyi = ny - 1;
+  FPB_REQUIRE(nxi >= 1 && nyi >= 1 && (int64_t)nrows % ((int64_t)nxi * nyi) == 0,
+              "%d interior rows is not a whole number of interior node planes of %d x %d", nrows, nxi, nyi);
+  const int64_t warps = (int64_t)(nrows / nxi) * ((nxi + 31) / 32);  // interior lines x segments
   k_rows_pairs_kuhn<true><<<(unsigned)((warps + kKuhnWarps - 1) / kKuhnWarps), 32 * kKuhnWarps, 0, as_stream(stream)>>>(
-      nrows, rows, nullptr, nullptr, xyz4, rowptr, nullptr, nnz, accumulate, out, R, L);
+      (int32_t)warps, nullptr, nullptr, nullptr, xyz4, rowptr, nullptr, nnz, accumulate, out, R, L, nxi, nyi);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }

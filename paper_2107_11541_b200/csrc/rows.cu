@@ -43,7 +43,10 @@ constexpr int kRowsBlock = 128;
 constexpr int kOwnerSpan = 256;  // write-out chunk of a warp's CSR range (bytes of owner map)
 int g_tuning_rows_nb = 1;         // fpb_set_tuning("rows_nb", 0|1): neighbour-staged matrix kernel
 extern int g_tuning_hex_canon_rows;  // hexblock.cu
-extern int g_tuning_blk_pipe;        // blocks.cu
+extern int g_tuning_blk_pipe;
+extern int g_tuning_kmom_smem_kb;    // kmom.cu
+extern int g_tuning_kgrad_march;     // pairs.cu
+extern int g_tuning_kgrad_kchunk;    // pairs.cu
 
 
 template <int ET, int KIND>
@@ -832,6 +835,20 @@ int fpb_set_tuning(const char* name, int value) {
   }
   if (name && strcmp(name, "blk_pipe") == 0) {
     g_tuning_blk_pipe = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "kgrad_march") == 0) {
+    g_tuning_kgrad_march = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "kgrad_kchunk") == 0) {
+    FPB_REQUIRE(value >= 1, "kgrad_kchunk must be >= 1");
+    g_tuning_kgrad_kchunk = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "kmom_smem_kb") == 0) {
+    FPB_REQUIRE(value >= 0 && value <= 227, "kmom_smem_kb must be 0..227");
+    g_tuning_kmom_smem_kb = value;
     return FPB_OK;
   }
   if (name && strcmp(name, "hex_canon_rows") == 0) {

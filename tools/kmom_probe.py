@@ -38,7 +38,13 @@ def main():
     ap.add_argument("--kchunks", default="0")
     ap.add_argument("--blocks", type=int, default=1)
     ap.add_argument("--grad", type=int, default=0, help="also time B_x,B_y,B_z (Kuhn box vs colind path)")
+    ap.add_argument("--overlap", default="", help="kmom_smem_kb values: time momentum + B_xyz sequential vs on two streams")
+    ap.add_argument("--tune", default="", help="name=value[,name=value] passed to fpb_set_tuning")
     args = ap.parse_args()
+    from paper_2107_11541_b200 import _lib
+    for kv in filter(None, args.tune.split(",")):
+        name, val = kv.split("=")
+        _lib.check(_lib.load().fpb_set_tuning(name.encode(), int(val)))
     flush = torch.empty(128 << 20, dtype=torch.float32, device="cuda")
     res = {}
     for sz in args.sizes.split(","):
@@ -78,6 +84,38 @@ def main():
                                          "bitwise_equal": bool(torch.equal(ga, gb))}
                 res[f"{sz}/grad_colind"] = {"ms": round(msc, 4), "Gelem_s": round(ne / msc / 1e6, 2)}
                 del ga, gb
+            if args.overlap:
+                from paper_2107_11541_b200 import _lib
+                nnz = ctx.pattern.nnz
+                ga = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
+                side = torch.cuda.Stream()
+                main = torch.cuda.current_stream()
+
+                def seq():
+                    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out)
+                    ctx.assemble_gradients_d(ga)
+
+                def par():
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        ctx.assemble_gradients_d(ga)
+                    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out)
+                    main.wait_stream(side)
+
+                def par2():  # gradients first, momentum on the side stream
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, out)
+                    ctx.assemble_gradients_d(ga)
+                    main.wait_stream(side)
+
+                for kbv in (int(v) for v in args.overlap.split(",")):
+                    _lib.check(_lib.load().fpb_set_tuning(b"kmom_smem_kb", kbv))
+                    res[f"{sz}/seq/smem{kbv}"] = {"ms": round(timeit(seq, args.reps, flush), 4)}
+                    res[f"{sz}/par_grad_side/smem{kbv}"] = {"ms": round(timeit(par, args.reps, flush), 4)}
+                    res[f"{sz}/par_mom_side/smem{kbv}"] = {"ms": round(timeit(par2, args.reps, flush), 4)}
+                _lib.check(_lib.load().fpb_set_tuning(b"kmom_smem_kb", 0))
+                del ga
             del ctx
             torch.cuda.empty_cache()
         del mesh, vel, out, ref
