@@ -289,6 +289,13 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
 int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
                                          const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
                                          void* stream);
+/* The boundary (non-canonical) rows of the same Kuhn box (nx x ny x nz
+ * cells): each row keeps the interior stream's words whose tet lies in a
+ * cell inside the box; CSR slots by popcount of the present neighbours.
+ * rows: the boundary node ids (any order). */
+int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz,
+                                        const double* xyz4, const int32_t* rowptr, int64_t nnz, int accumulate,
+                                        double* out, void* stream);
 
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices

@@ -103,6 +103,7 @@ KUHN_MOMENTUM = os.environ.get("FPB_KUHN_MOM", "1") != "0"
 KUHN_KCHUNK = int(os.environ.get("FPB_KUHN_KCHUNK", "0"))  # 0 = from the grid size
 # TET04 continuity on a Kuhn box: neighbour ids by offset instead of colind (pairs.cu)
 KUHN_BOX_GRADIENT = os.environ.get("FPB_KUHN_BOX_GRAD", "1") != "0"
+KUHN_BOX_BOUNDARY = os.environ.get("FPB_KUHN_BOX_BOUNDARY", "1") != "0"  # ... and its boundary rows
 BLOCK_MORTON = os.environ.get("FPB_BLOCK_MORTON", "0") != "0"  # measured slower (profiles/r02e_mom)  # y-band of canonical hex rows (0 = natural order)
 
 
@@ -698,9 +699,14 @@ class AssemblyContext:
                         _lib.call("fpb_assemble_gradient_pairs_kuhn_box", int(pc["rows"].numel()),
                                   pc["rows"].data_ptr(), g.kuhn.nx, g.kuhn.ny, xyz4, rp_, nnz, acc, out.data_ptr(),
                                   _lib.stream())
-                        _lib.call("fpb_assemble_gradient_pairs_rows", r.n, int(pc["other"].numel()),
-                                  pc["other"].data_ptr(), r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4, rp_,
-                                  ci_, nnz, r.rowcap, acc, out.data_ptr(), _lib.stream())
+                        if KUHN_BOX_BOUNDARY:  # boundary rows: the interior stream masked by the box
+                            _lib.call("fpb_assemble_gradient_kuhn_boundary", int(pc["other"].numel()),
+                                      pc["other"].data_ptr(), kb_.nx, kb_.ny, kb_.nz, xyz4, rp_, nnz, acc,
+                                      out.data_ptr(), _lib.stream())
+                        else:
+                            _lib.call("fpb_assemble_gradient_pairs_rows", r.n, int(pc["other"].numel()),
+                                      pc["other"].data_ptr(), r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4,
+                                      rp_, ci_, nnz, r.rowcap, acc, out.data_ptr(), _lib.stream())
                     elif pc["kuhn"]:  # compile-time stream, edge vectors in registers; the rest masked
                         _lib.call("fpb_assemble_gradient_pairs_kuhn", int(pc["rows"].numel()), pc["rows"].data_ptr(),
                                   None, None, xyz4, rp_, ci_, nnz, acc, out.data_ptr(), _lib.stream())

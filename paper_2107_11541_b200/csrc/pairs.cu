@@ -552,7 +552,7 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
 // barriers).
 constexpr int kGradWarps = 2;
 int g_tuning_kgrad_march = 1;  // fpb_set_tuning("kgrad_march", 0|1): z-marching lines (1) or the row kernel (0)
-int g_tuning_kgrad_kchunk = 32;
+int g_tuning_kgrad_kchunk = 0;  // 0: from the grid size
 constexpr int kGradStg = 4 * 3 * 3 * 34 + 2;  // [layer slot][node row][comp][34 columns] + 4 CSR starts (int)
 __device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -670,6 +670,101 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kchunk, int64_t nwarps, const doub
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
+
+// ---- Kuhn box, boundary rows -----------------------------------------------
+// A boundary node of the Kuhn box keeps the subset of the interior stream
+// whose tets exist: word (target t, pair q, r) belongs to the tet {node, t,
+// q, r}, which lies in the cell at offset min(0, off_t, off_q, off_r) per
+// axis; the word counts iff that cell is inside the box.  The row's columns
+// are the neighbours with at least one counting word, in ascending order
+// (the t order), the diagonal among them — so the CSR slot of column t is a
+// popcount.  Values equal the generic pair-stream kernel's to rounding (the
+// summation order is the interior stream's).
+__host__ __device__ constexpr int kuhn_off3(int t, int d) {
+  // (di, dj, dk) of neighbour t in ascending node order (kuhn_box_off)
+  return d == 0 ? ((t == 0 || t == 2 || t == 4 || t == 6) ? -1 : (t == 7 || t == 9 || t == 11 || t == 13) ? 1 : 0)
+       : d == 1 ? ((t == 0 || t == 1 || t == 4 || t == 5) ? -1 : (t == 8 || t == 9 || t == 12 || t == 13) ? 1 : 0)
+                : ((t <= 3) ? -1 : (t >= 10) ? 1 : 0);
+}
+__host__ __device__ constexpr int cmin0(int a, int b, int c) { return (a < b ? (a < c ? a : c) : (b < c ? b : c)) < 0 ? -1 : 0; }
+
+__global__ void __launch_bounds__(128)
+k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, int ny, int nz,
+                     const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, int64_t nnz,
+                     int accumulate, double* __restrict__ out) {
+  constexpr int DIM = 3;
+  const int64_t R = nx + 1, L = R * (ny + 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nrows; e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = __ldg(rows + e);
+    const int k = (int)(row / L), rem = (int)(row - k * L), j = rem / (int)R, i = rem - j * (int)R;
+    // the 8 cells around the node: bit (cx + 1) + 2 (cy + 1) + 4 (cz + 1)
+    unsigned cells = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int ci = i + (b & 1) - 1, cj = j + ((b >> 1) & 1) - 1, ck = k + ((b >> 2) & 1) - 1;
+      if (ci >= 0 && ci < nx && cj >= 0 && cj < ny && ck >= 0 && ck < nz) cells |= 1u << b;
+    }
+    double x0[DIM], X[kKuhnCols][DIM];
+    {
+      double r4[4];
+      ld256(xyz4 + 4 * (int64_t)row, r4);
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) x0[d] = r4[d];
+#pragma unroll
+      for (int t = 0; t < kKuhnCols; ++t) {
+        const int ii = i + kuhn_off3(t, 0), jj = j + kuhn_off3(t, 1), kk = k + kuhn_off3(t, 2);
+        const bool ok = ii >= 0 && ii <= nx && jj >= 0 && jj <= ny && kk >= 0 && kk <= nz;
+        if (ok) ld256(xyz4 + 4 * (row + kuhn_box_off(t, R, L)), r4);
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) X[t][d] = ok ? r4[d] - x0[d] : 0.0;
+      }
+    }
+    const double mN0 = refmN<FPB_TET04>(0);
+    double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0}, col[kKuhnCols][DIM];
+    unsigned present = 0;
+    bool any = false;
+    int target = 0;
+#pragma unroll
+    for (int q8 = 0; q8 < kKuhnWords; ++q8) {
+      const int w = kuhn_word(q8);
+      const int q = w & 0x7f, r = (w >> 7) & 0x7f;
+      const int cb = (cmin0(kuhn_off3(target, 0), kuhn_off3(q, 0), kuhn_off3(r, 0)) + 1) +
+                     2 * (cmin0(kuhn_off3(target, 1), kuhn_off3(q, 1), kuhn_off3(r, 1)) + 1) +
+                     4 * (cmin0(kuhn_off3(target, 2), kuhn_off3(q, 2), kuhn_off3(r, 2)) + 1);
+      if ((cells >> cb) & 1u) {
+        acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
+        acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
+        acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+        any = true;
+      }
+      if (w & (1 << 14)) {  // column finished
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) {
+          col[target][d] = mN0 * acc[d];
+          tot[d] += acc[d];
+          acc[d] = 0.0;
+        }
+        if (any) present |= 1u << target;
+        any = false;
+        ++target;
+      }
+    }
+    const int lo = __ldg(rowptr + row);
+    const int dpos = __popc(present & 0x7fu);
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      double* o = out + d * nnz + lo;
+      const double dv = -(mN0 * tot[d]);
+      o[dpos] = accumulate ? o[dpos] + dv : dv;
+#pragma unroll
+      for (int t = 0; t < kKuhnCols; ++t)
+        if ((present >> t) & 1u) {
+          const int cp = __popc(present & ((1u << t) - 1u)) + (t >= kKuhnDiag ? 1 : 0);
+          o[cp] = accumulate ? o[cp] + col[t][d] : col[t][d];
+        }
+    }
+  }
+}
 }  // namespace fpb
 
 using namespace fpb;
@@ -739,9 +834,9 @@ int fpb_assemble_gradient_pairs_rows(int32_t n, int32_t nrows, const int32_t* ro
                                      const int32_t* colind, int64_t nnz, int rowcap, int accumulate, double* out,
                                      void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  if (nrows <= 0) return FPB_OK;
   FPB_REQUIRE(rows && pair_ptr && words && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
               "pair-stream row-list assembly needs the stream, the CSR pattern and rows <= 129 entries");
-  if (nrows <= 0) return FPB_OK;
   cudaStream_t s = as_stream(stream);
   const size_t smem = ((size_t)3 * (rowcap - 1) * 32 + (size_t)3 * 32 * rowcap) * sizeof(double);
   if (smem > 48 * 1024)
@@ -771,6 +866,18 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
   return FPB_OK;
 }
 
+int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz,
+                                        const double* xyz4, const int32_t* rowptr, int64_t nnz, int accumulate,
+                                        double* out, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1 && nz >= 1, "bad Kuhn-boundary arguments");
+  if (nrows <= 0) return FPB_OK;
+  k_kuhn_grad_boundary<<<grid_for(nrows, 128), 128, 0, as_stream(stream)>>>(nrows, rows, nx, ny, nz, xyz4, rowptr,
+                                                                          nnz, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
 int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int nx, int ny, const double* xyz4,
                                          const int32_t* rowptr, int64_t nnz, int accumulate, double* out,
                                          void* stream) {
@@ -778,7 +885,10 @@ int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int
     const int nxi = nx - 1, nyi = ny - 1;
     FPB_REQUIRE((int64_t)nrows % ((int64_t)nxi * nyi) == 0, "%d interior rows: not whole interior planes", nrows);
     const int nz = nrows / (nxi * nyi) + 1;
-    const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk, nz - 1));
+    // z-chunks: about four waves of 10 resident warps per SM, 4..32 layers each
+    const int64_t lines = (int64_t)((nxi + 31) / 32) * nyi;
+    const int kauto = (int)std::min<int64_t>(32, std::max<int64_t>(4, lines * (nz - 1) / (4 * 10 * kNumSMs)));
+    const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk > 0 ? g_tuning_kgrad_kchunk : kauto, nz - 1));
     const int nchunk = (nz - 1 + kchunk - 1) / kchunk;
     const int64_t nwarps = (int64_t)((nxi + 31) / 32) * nyi * nchunk;
     const size_t smem = (size_t)kGradWarps * (kGradStg + 3 * 32 * (kKuhnCols + 1)) * sizeof(double);
@@ -813,6 +923,7 @@ int fpb_assemble_gradient_pairs_slices(int32_t n, int32_t nslices, const int32_t
                                        const int32_t* rowptr, const int32_t* colind, int64_t nnz, int rowcap,
                                        int accumulate, double* out, void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  if (nslices <= 0) return FPB_OK;
   FPB_REQUIRE(slist && xyz4 && rowptr && colind && out && rowcap >= 2 && rowcap <= 129,
               "pair-stream gradient assembly needs the slice list, the CSR pattern and rows <= 129 entries");
   FPB_REQUIRE(canon_len > 0 || (pair_ptr && words), "generic slices need the pair stream");

@@ -842,7 +842,7 @@ int fpb_set_tuning(const char* name, int value) {
     return FPB_OK;
   }
   if (name && strcmp(name, "kgrad_kchunk") == 0) {
-    FPB_REQUIRE(value >= 1, "kgrad_kchunk must be >= 1");
+    FPB_REQUIRE(value >= 0, "kgrad_kchunk must be >= 0 (0: automatic)");
     g_tuning_kgrad_kchunk = value;
     return FPB_OK;
   }

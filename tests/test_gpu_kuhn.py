@@ -112,13 +112,15 @@ def test_kuhn_matches_block_path_and_is_deterministic(cuda_ok):
 
 
 def test_kuhn_box_gradients_bitwise_equal_colind_path(cuda_ok):
-    """Continuity B_x, B_y, B_z on a Kuhn box: neighbour ids by offset
-    (fpb_assemble_gradient_pairs_kuhn_box) give bitwise the colind path's
-    values (same arithmetic, same order), and match the oracle."""
+    """Continuity B_x, B_y, B_z on a Kuhn box: the interior rows by z-marching
+    lines (fpb_assemble_gradient_pairs_kuhn_box) give bitwise the colind
+    path's values (same arithmetic, same order); the boundary rows by the
+    box-masked interior stream (fpb_assemble_gradient_kuhn_boundary) agree
+    with the generic row-list kernel to rounding; all match the oracle."""
     import paper_2107_11541_b200 as P
     import paper_2107_11541_b200.assembly as A
 
-    for dims in ((37, 21, 9), (6, 5, 4)):
+    for dims in ((37, 21, 9), (6, 5, 4), (2, 2, 2), (33, 2, 3)):
         om = O.box(O.TET04, *dims)
         om.coords = _jitter(om.coords, *dims, seed=11)
         mesh, ctx = _ctx(P, *dims, coords=om.coords)
@@ -126,13 +128,20 @@ def test_kuhn_box_gradients_bitwise_equal_colind_path(cuda_ok):
         nnz = ctx.pattern.nnz
         a = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
         b = torch.empty_like(a)
-        ctx.assemble_gradients_d(a)
+        c = torch.empty_like(a)
+        ctx.assemble_gradients_d(a)  # interior lines + masked-stream boundary rows
+        A.KUHN_BOX_BOUNDARY = False
+        try:
+            ctx.assemble_gradients_d(c)  # interior lines + the generic row-list kernel
+        finally:
+            A.KUHN_BOX_BOUNDARY = True
         A.KUHN_BOX_GRADIENT = False
         try:
             ctx.assemble_gradients_d(b)
         finally:
             A.KUHN_BOX_GRADIENT = True
-        assert torch.equal(a, b), dims
+        assert torch.equal(c, b), dims
+        assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < 1e-14, dims
         for k in range(3):
             e = np.zeros((om.nnode, 3))
             e[:, k] = 1.0
