@@ -366,11 +366,11 @@ class KuhnBox:
 
     def __init__(self, nx: int, ny: int, nz: int, dev):
         self.nx, self.ny, self.nz = nx, ny, nz
-        # CTAs are 32 x 8 cell pencils; z-chunks for about 8 waves of 2 CTAs
-        # per SM, >= 8 cell layers each (a chunk re-integrates one halo layer)
+        # CTAs are 32 x 8 cell pencils, one per SM; z-chunks of 8..32 cell
+        # layers for about 14 waves (a chunk re-integrates one halo layer)
         pencils = -(-nx // 32) * -(-ny // 8)
-        nchunk = max(1, min(nz // 8, -(-8 * 2 * 148 // pencils)))
-        self.kchunk = min(KUHN_KCHUNK or -(-nz // nchunk), nz)
+        kc = max(8, min(32, nz * pencils // (14 * 148)))
+        self.kchunk = min(KUHN_KCHUNK or kc, nz)
         self._scratch = None
 
     def scratch(self, dev) -> torch.Tensor:

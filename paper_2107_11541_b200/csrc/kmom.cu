@@ -48,7 +48,7 @@ __device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 #ifndef FPB_KMOM_MINB
-#define FPB_KMOM_MINB 2
+#define FPB_KMOM_MINB 1  // one 8-warp CTA per SM at ~228 registers: no spills (2 CTAs at 128: spills, 13 % slower)
 #endif
 #ifndef FPB_KMOM_TY
 #define FPB_KMOM_TY 8
@@ -75,6 +75,164 @@ struct KuhnGrid {
   }
   __host__ __device__ int64_t scratch() const { return py(nxb, 0, 0, 0); }
 };
+
+#ifndef FPB_KMOM_SHARED
+#define FPB_KMOM_SHARED 1
+#endif
+#ifdef FPB_KMOM_TETBARRIER  // one tet's node loads at a time (A/B: tighter registers, slower without spills)
+#define FPB_KMOM_TETBAR() asm volatile("" ::: "memory")
+#else
+#define FPB_KMOM_TETBAR() ((void)0)
+#endif
+// One Kuhn cell, its six tets in the cycle T0 (0,1,3,7), T3 (0,1,7,5), T2
+// (0,4,5,7), T4 (0,4,7,6), T1 (0,2,6,7), T5 (0,2,7,3): consecutive tets share
+// the cell diagonal, one middle node and one cross product with the diagonal
+// edge e7, so each tet after the first loads one new node and forms two new
+// cross products.  Edges / velocity differences against corner 0 (e_c, d_c),
+// adjugate rows from the crosses (tet_mom_core, simplex.cuh).
+__device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double* s1, double r, double muW,
+                                                 double (&bot)[4][3], double (&top)[4][3]) {
+  auto ld = [&](int cc, double (&x)[3], double (&u)[3]) {
+    const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * 6 * 33 + (cc & 1);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      x[d] = sp[d * 33];
+      u[d] = sp[(3 + d) * 33];
+    }
+  };
+  double x0[3], u0[3], e7[3], d7[3], u05[3];
+  {
+    double x[3], u[3];
+    ld(0, x0, u0);
+    ld(7, x, u);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      e7[d] = x[d] - x0[d];
+      d7[d] = u[d] - u0[d];
+      u05[d] = 5.0 * u0[d];
+    }
+  }
+  auto edge = [&](int cc, double (&e)[3], double (&dv)[3]) {
+    double x[3], u[3];
+    ld(cc, x, u);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      e[d] = x[d] - x0[d];
+      dv[d] = u[d] - u0[d];
+    }
+  };
+  // corner of local node a for each tet: (0, p, q, 7) or (0, p, 7, q)
+  auto acc = [&](int cc, int k, double v) {
+    if (cc & 4) top[cc & 3][k] -= v;
+    else bot[cc & 3][k] -= v;
+  };
+  double e1[3], d1[3], e3[3], d3[3], c71[3], c75[3];
+  edge(1, e1, d1);
+  edge(3, e3, d3);
+  {  // T0 (0, 1, 3, 7): E = (e1, e3, e7)
+    double A[3][3], du[3][3];
+    cross3(e3, e7, A[0]);
+    cross3(e7, e1, A[1]);
+    cross3(e1, e3, A[2]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      c71[d] = A[1][d];
+      du[0][d] = d1[d];
+      du[1][d] = d3[d];
+      du[2][d] = d7[d];
+    }
+    const double det = dot3(e1, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 3 : 7, k, v); });
+  }
+  FPB_KMOM_TETBAR();
+  double e5[3], d5[3];
+  edge(5, e5, d5);
+  {  // T3 (0, 1, 7, 5): E = (e1, e7, e5)
+    double A[3][3], du[3][3];
+    cross3(e7, e5, A[0]);
+    cross3(e5, e1, A[1]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      c75[d] = A[0][d];
+      A[2][d] = -c71[d];
+      du[0][d] = d1[d];
+      du[1][d] = d7[d];
+      du[2][d] = d5[d];
+    }
+    const double det = dot3(e1, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 7 : 5, k, v); });
+  }
+  FPB_KMOM_TETBAR();
+  double e4[3], d4[3], c74[3];
+  edge(4, e4, d4);
+  {  // T2 (0, 4, 5, 7): E = (e4, e5, e7)
+    double A[3][3], du[3][3];
+    cross3(e7, e4, A[1]);
+    cross3(e4, e5, A[2]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      A[0][d] = -c75[d];
+      c74[d] = A[1][d];
+      du[0][d] = d4[d];
+      du[1][d] = d5[d];
+      du[2][d] = d7[d];
+    }
+    const double det = dot3(e4, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 5 : 7, k, v); });
+  }
+  FPB_KMOM_TETBAR();
+  double e6[3], d6[3], c76[3];
+  edge(6, e6, d6);
+  {  // T4 (0, 4, 7, 6): E = (e4, e7, e6)
+    double A[3][3], du[3][3];
+    cross3(e7, e6, A[0]);
+    cross3(e6, e4, A[1]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      c76[d] = A[0][d];
+      A[2][d] = -c74[d];
+      du[0][d] = d4[d];
+      du[1][d] = d7[d];
+      du[2][d] = d6[d];
+    }
+    const double det = dot3(e4, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 7 : 6, k, v); });
+  }
+  FPB_KMOM_TETBAR();
+  double e2[3], d2[3], c72[3];
+  edge(2, e2, d2);
+  {  // T1 (0, 2, 6, 7): E = (e2, e6, e7)
+    double A[3][3], du[3][3];
+    cross3(e7, e2, A[1]);
+    cross3(e2, e6, A[2]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      A[0][d] = -c76[d];
+      c72[d] = A[1][d];
+      du[0][d] = d2[d];
+      du[1][d] = d6[d];
+      du[2][d] = d7[d];
+    }
+    const double det = dot3(e2, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 6 : 7, k, v); });
+  }
+  FPB_KMOM_TETBAR();
+  edge(3, e3, d3);  // reloaded (not held across the cell)
+  {  // T5 (0, 2, 7, 3): E = (e2, e7, e3)
+    double A[3][3], du[3][3];
+    cross3(e7, e3, A[0]);
+    cross3(e3, e2, A[1]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      A[2][d] = -c72[d];
+      du[0][d] = d2[d];
+      du[1][d] = d7[d];
+      du[2][d] = d3[d];
+    }
+    const double det = dot3(e2, A[0]);
+    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 7 : 3, k, v); });
+  }
+}
 
 template <int MAXT>
 __global__ void __launch_bounds__(MAXT, FPB_KMOM_MINB)
@@ -191,6 +349,9 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
     if (cell && t < nz) {
       const double* s0 = stg + (t % 3) * 2 * 6 * 33 + lane;
       const double* s1 = stg + ((t + 1) % 3) * 2 * 6 * 33 + lane;
+#if FPB_KMOM_SHARED
+      kuhn_cell_shared(s0, s1, r, muW, bot, top);
+#else
 #pragma unroll
       for (int tt = 0; tt < 6; ++tt) {
         asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
@@ -211,6 +372,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
           else bot[cc & 3][d] -= v;
         });
       }
+#endif
     }
     // (B) layer t's bottom face is complete in z: x-shuffle; the right edge
     // and the top node row leave the warp

@@ -300,4 +300,57 @@ __device__ __forceinline__ void tet_mom_adj(const double (&x)[4][3], const doubl
   tet_mom_adj_f(x, u, r, muW, [&](int a, int k, double v) { res[a][k] -= v; });
 }
 
+// The same residual from precomputed adjugate rows A (= rows of det J^-1),
+// det, the velocity differences du[b] = u_{b+1} - u_0 and u05 = 5 u_0 (so
+// that U + u_0 = u05 + sum_b du[b], U + u_a = that + du[a-1]).  Used by the
+// Kuhn-cell kernel (kmom.cu), where the cross products and differences
+// against the cell's shared nodes are computed once per cell.
+template <class Sub>
+__device__ __forceinline__ void tet_mom_core(const double (&A)[3][3], double det, const double (&du)[3][3],
+                                             const double (&u05)[3], double r, double muW, Sub&& sub) {
+  double G[3][3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) G[l][k] = du[0][k] * A[0][l] + du[1][k] * A[1][l] + du[2][k] * A[2][l];
+  const double divu = G[0][0] + G[1][1] + G[2][2];
+  const double f = muW / det;
+  double Mr[3][3], Sf[3][3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      Mr[l][k] = r * (l == k ? G[l][k] + divu : G[l][k]);
+      Sf[l][k] = l == k ? (2.0 * f) * G[l][l] : f * (G[l][k] + G[k][l]);
+    }
+  double vs[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) vs[a][k] = Sf[k][0] * A[a][0] + Sf[k][1] * A[a][1] + Sf[k][2] * A[a][2];
+  double w0[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) w0[d] = u05[d] + ((du[0][d] + du[1][d]) + du[2][d]);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    double w[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) w[d] = a == 0 ? w0[d] : w0[d] + du[a - 1][d];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double v = a == 0 ? -((vs[0][k] + vs[1][k]) + vs[2][k]) : vs[a - 1][k];
+      sub(a, k, fma(w[0], Mr[0][k], fma(w[1], Mr[1][k], fma(w[2], Mr[2][k], v))));
+    }
+  }
+}
+
+__device__ __forceinline__ void cross3(const double (&p)[3], const double (&q)[3], double (&o)[3]) {
+  o[0] = p[1] * q[2] - p[2] * q[1];
+  o[1] = p[2] * q[0] - p[0] * q[2];
+  o[2] = p[0] * q[1] - p[1] * q[0];
+}
+__device__ __forceinline__ double dot3(const double (&p)[3], const double (&q)[3]) {
+  return p[0] * q[0] + p[1] * q[1] + p[2] * q[2];
+}
+
 }  // namespace fpb
