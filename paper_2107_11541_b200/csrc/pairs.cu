@@ -550,7 +550,13 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
 // come from shared memory and no load latency is exposed; the row's CSR
 // start is one load per warp and layer.  Warps are independent (no
 // barriers).
-constexpr int kGradWarps = 2;
+#ifndef FPB_KGRAD_WARPS
+#define FPB_KGRAD_WARPS 2
+#endif
+constexpr int kGradWarps = FPB_KGRAD_WARPS;
+#ifndef FPB_KGRAD_MINB
+#define FPB_KGRAD_MINB 4  // ~249 registers, 8 warps/SM: 1.40 ms at C5 vs 1.59 at 168 registers / 10 warps
+#endif
 int g_tuning_kgrad_march = 1;  // fpb_set_tuning("kgrad_march", 0|1): z-marching lines (1) or the row kernel (0)
 int g_tuning_kgrad_kchunk = 0;  // 0: from the grid size
 constexpr int kGradStg = 4 * 3 * 3 * 34 + 2;  // [layer slot][node row][comp][34 columns] + 4 CSR starts (int)
@@ -559,7 +565,7 @@ __device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
 }
 
-__global__ void __launch_bounds__(32 * kGradWarps, FPB_KUHN_MINB)
+__global__ void __launch_bounds__(32 * kGradWarps, FPB_KGRAD_MINB)
 k_kuhn_grad_march(int nx, int ny, int nz, int kchunk, int64_t nwarps, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, int64_t nnz, int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, RE = kKuhnCols + 1;  // entries per row
