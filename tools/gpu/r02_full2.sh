@@ -5,4 +5,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 1500 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; head -c 1200 gpurun_out/bench.json; echo; tail -2 gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err; head -c 300 gpurun_out/bench_ref.json; echo
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --soak 0 --no-cpu-baseline --e2e-steps 0 --no-solver --no-configs > gpurun_out/ncu_launch.log 2>&1; tail -1 gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kuhn|k_rows_pairs" -s 6 -c 4 -o gpurun_out/prof_c5 python bench.py --steps 1 --warmup 3 --soak 0 --no-cpu-baseline --e2e-steps 0 --no-solver --no-configs > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_kuhn" -s 6 -c 4 -o gpurun_out/prof_c5 python bench.py --steps 1 --warmup 3 --soak 0 --no-cpu-baseline --e2e-steps 0 --no-solver --no-configs > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
