@@ -642,22 +642,25 @@ def main():
     stream = torch.cuda.current_stream()
 
     side = torch.cuda.Stream() if sub is not None else None
-    # element-block momentum RHS (integrate + node gather) + B_xyz (Kuhn rows
-    # from registers + the remaining rows' pair-stream kernel, when both exist)
-    # (the pair-stream plan is built on the first assembly: counted after warm-up)
+    kb0 = ctx.groups[0].kuhn
+
+    # the step's kernels: momentum RHS (Kuhn-box cell pencils + CTA-edge
+    # fixup, or element blocks + node gather) and B_x, B_y, B_z (Kuhn
+    # interior lines + boundary rows, or canonical rows + the other rows)
     def _momentum_launches():
-        kb = ctx.groups[0].kuhn if sub is None else None
-        if kb is None:
+        if kb0 is None:
             return 2  # element blocks: integrate + node gather
-        return 1 + (kb.nx > 32 or kb.ny > 8)  # Kuhn pencils (+ CTA-boundary fixup)
+        return 1 + (kb0.nx > 32 or kb0.ny > 8)  # Kuhn pencils (+ CTA-boundary fixup)
 
     def _gradient_launches():
+        if kb0 is not None and kb0.pattern_ok and kb0.nx > 1 and kb0.ny > 1:
+            return 2  # interior lines + boundary rows (a slab's ghost ranges: torch fills)
         g0 = ctx.groups[0]
         pc = g0.rows.pair_canon if g0.rows is not None else None
         return 2 if pc is not None and pc.get("kuhn") and pc["other"].numel() else 1
 
     launches_per_step = None
-    if sub is not None:  # windowed schedule: one launch per non-empty window
+    if sub is not None and kb0 is None:  # windowed schedule: one launch per non-empty window
         from paper_2107_11541_b200.distributed import _step_windows
 
         w = _step_windows(sub)
@@ -665,6 +668,8 @@ def main():
         launches_per_step = (sum(map(nonempty, w["blocks_A"])) + sum(map(nonempty, w["nodes_A"]))
                              + sum(map(nonempty, w["rows_A"])) + nonempty(w["blocks_B"])
                              + sum(map(nonempty, w["nodes_B"])) + nonempty(w["rows_B"]))
+    elif sub is not None:  # Kuhn slab: the kernels + one halo add kernel per exchange (RHS, matrices)
+        launches_per_step = None  # counted after warm-up (plans are built lazily)
 
     def kernels(ev=None):
         if ev:
@@ -699,6 +704,8 @@ def main():
     torch.cuda.synchronize()
     grad_launches = _gradient_launches()
     mom_launches = _momentum_launches()
+    if sub is not None and kb0 is not None:
+        launches_per_step = mom_launches + grad_launches + (2 if sub.layout.interfaces() else 0)
     clocks = ClockSampler(local)
     # soak (untimed) so the clock sampler sees the loaded state; every rank
     # must run the same number of steps (each step has halo exchanges), so
@@ -762,7 +769,11 @@ def main():
         dist.all_reduce(loc, op=dist.ReduceOp.MAX)
         phases = dict(zip(acc.keys(), loc.tolist()))
         phases["note"] = ("max over ranks of each phase's median: interface windows first, halo (NCCL send/recv "
-                          "of interface RHS rows + CSR row segments) on a side stream, interior meanwhile")
+                          "of interface RHS rows + CSR row segments) on a side stream, interior meanwhile"
+                          if kb0 is None else
+                          "max over ranks of each phase's median: 'interface' = the whole-slab Kuhn-box kernels, "
+                          "then the halo (NCCL send/recv of interface RHS rows + CSR row segments); no interior "
+                          "phase (interior_ms includes the halo)")
         for _ in range(5):
             flush.fill_(1.0)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -901,8 +912,14 @@ def main():
             "multi_gpu": None if sub is None else {
                 "halo": "compiled NCCL (halo.cu fpb_halo_exchange), one communicator per rank"
                 if sub.native is not None else f"torch.distributed ({dist.get_backend()}), host-staged",
-                "timed_step": "one CUDA graph per step (interface windows, NCCL halo on a side stream, interior)"
-                if graph.single_graph else "two CUDA graphs (interface / interior windows), eager halo between"},
+                "timed_step": ("one CUDA graph per step (Kuhn-box slab kernels, then the NCCL halo)"
+                               if graph.single_graph and kb0 is not None else
+                               "one CUDA graph per step (interface windows, NCCL halo on a side stream, interior)"
+                               if graph.single_graph else
+                               "one CUDA graph (Kuhn-box slab kernels), eager halo after" if kb0 is not None else
+                               "two CUDA graphs (interface / interior windows), eager halo between"),
+                "kernels": "Kuhn-box slab kernels over the own cell layers (kmom.cu, pairs.cu)" if kb0 is not None
+                else "windowed element-block / row kernels"},
             # per step: momentum RHS (Kuhn-box cell pencils + CTA-boundary
             # fixup, or element blocks + node gather) and B_x,B_y,B_z (Kuhn
             # rows + the other rows) — 4 launches (ncu launch list under

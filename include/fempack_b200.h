@@ -292,10 +292,17 @@ int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int
 /* The boundary (non-canonical) rows of the same Kuhn box (nx x ny x nz
  * cells): each row keeps the interior stream's words whose tet lies in a
  * cell inside the box; CSR slots by popcount of the present neighbours.
- * rows: the boundary node ids (any order). */
-int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz,
-                                        const double* xyz4, const int32_t* rowptr, int64_t nnz, int accumulate,
-                                        double* out, void* stream);
+ * Only cells of layers [vk0, vk1) contribute values (a z-slab's own layers;
+ * 0, nz for the whole box).  rows: the node ids (any order). */
+int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz, int vk0,
+                                        int vk1, const double* xyz4, const int32_t* rowptr, int64_t nnz,
+                                        int accumulate, double* out, void* stream);
+/* Interior node lines (i in 1..nx-1, j in 1..ny-1) of node planes [kz0, kz1]
+ * (1 <= kz0, kz1 <= nz-1) of the Kuhn box: every incident tet is integrated
+ * (z-marching, staged coordinates); fpb_assemble_gradient_pairs_kuhn_box is
+ * this with planes [1, nz-1]. */
+int fpb_assemble_gradient_kuhn_lines(int nx, int ny, int nz, int kz0, int kz1, const double* xyz4,
+                                     const int32_t* rowptr, int64_t nnz, int accumulate, double* out, void* stream);
 
 /* ---- row-owned assembly for Gauss-loop elements (QUAD04, PYR05, HEX08) --
  * Matrix kinds only (rowsq.cu).  Incidence lists as for the simplices
@@ -370,11 +377,14 @@ int fpb_assemble_blocks_scalar3(int etype, int64_t nelem, int64_t blk0, int64_t 
  * (mesh.py:258-282; the caller checks it, e.g. against fpb_box_conn).
  * Coordinates (32-byte records, fpb_pack4) and vel[n][3] are read as given.
  * 32 x 8 cell pencils march z-chunks of kchunk cell layers; out[n][3] is
- * overwritten in a fixed summation order (bitwise reproducible).  scratch:
+ * overwritten in a fixed summation order (bitwise reproducible).  Only the
+ * cell layers [kc0, kc1) are integrated (a z-slab's own layers; 0, nz for
+ * the whole box); node planes outside [kc0, kc1] are zeroed.  scratch:
  * fpb_kuhn_mom_scratch_len(nx, ny, nz) doubles (CTA boundary partials). */
 int64_t fpb_kuhn_mom_scratch_len(int nx, int ny, int nz);
-int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double* xyz4, const double* vel,
-                               double rho, double mu, double* scratch, double* out, void* stream);
+int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                               const double* vel, double rho, double mu, double* scratch, double* out,
+                               void* stream);
 
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 

@@ -360,24 +360,68 @@ class KuhnBox:
     """A TET04 group whose connectivity is exactly generate_box_mesh(TET04,
     nx, ny, nz)'s (mesh.py:258-282, cell-major, the six Kuhn tets per cell in
     permutation order) — checked element by element against the device
-    generator at setup.  Node coordinates are NOT assumed: the kernel reads
-    them.  Then the momentum RHS runs as z-marching cell lines (kmom.cu)
-    with no per-element metadata."""
+    generator at setup (or, for a z-slab, the extended slab box generated by
+    fpb_box_conn with the own cell layers [kc0, kc1)).  Node coordinates are
+    NOT assumed: the kernels read them.  The momentum RHS then runs as
+    z-marching cell pencils (kmom.cu) and, when the context's CSR pattern is
+    the box's own (pattern_ok), B_x, B_y, B_z as z-marching interior lines
+    plus box-masked boundary rows (pairs.cu) — no per-element metadata."""
 
-    def __init__(self, nx: int, ny: int, nz: int, dev):
+    def __init__(self, nx: int, ny: int, nz: int, dev, kc0: int = 0, kc1: int | None = None,
+                 pattern_ok: bool = True):
         self.nx, self.ny, self.nz = nx, ny, nz
-        # CTAs are 32 x 8 cell pencils, one per SM; z-chunks of 8..32 cell
-        # layers for about 14 waves (a chunk re-integrates one halo layer)
+        self.kc0, self.kc1 = kc0, nz if kc1 is None else kc1
+        self.pattern_ok = pattern_ok
+        # CTAs are 32 x 8 cell pencils, one per SM; the z-chunk minimises
+        # waves x layers per CTA (a chunk re-integrates one halo layer)
         pencils = -(-nx // 32) * -(-ny // 8)
-        kc = max(8, min(32, nz * pencils // (14 * 148)))
-        self.kchunk = min(KUHN_KCHUNK or kc, nz)
+        nl = self.kc1 - self.kc0
+
+        def cost(k):
+            return -(-(-(-nl // k) * pencils) // 148) * (k + (1 if k < nl else 0))
+
+        kc = min(range(min(8, nl), min(64, nl) + 1), key=lambda k: (cost(k), k)) if nl > 0 else 1
+        self.kchunk = max(1, min(KUHN_KCHUNK or kc, nl))
         self._scratch = None
+        self._brows = None
+        self._zero = None
 
     def scratch(self, dev) -> torch.Tensor:
         if self._scratch is None:  # CTA boundary partials (kmom.cu Px / Py), once
             m = int(_lib.load().fpb_kuhn_mom_scratch_len(self.nx, self.ny, self.nz))
             self._scratch = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
         return self._scratch
+
+    def boundary_rows(self, dev) -> torch.Tensor:
+        """Rows the interior-line kernel does not cover: node planes kc0 and
+        kc1 whole, and the x / y boundary ring of the planes between."""
+        if self._brows is None:
+            nx, ny = self.nx, self.ny
+            plane = (nx + 1) * (ny + 1)
+            ij = torch.arange(plane, device=dev, dtype=torch.int64)
+            i, j = ij % (nx + 1), ij // (nx + 1)
+            ring = ij[(i == 0) | (i == nx) | (j == 0) | (j == ny)]
+            mid = torch.arange(self.kc0 + 1, self.kc1, device=dev, dtype=torch.int64)
+            parts = [ij + plane * self.kc0]
+            if mid.numel():
+                parts.append((ring[None, :] + plane * mid[:, None]).reshape(-1))
+            if self.kc1 > self.kc0:
+                parts.append(ij + plane * self.kc1)
+            self._brows = torch.cat(parts).to(torch.int32).contiguous()
+        return self._brows
+
+    def zero_ranges(self, rowptr_d: torch.Tensor) -> list:
+        """CSR value ranges of the node planes outside [kc0, kc1] (a slab's
+        ghost planes): no integrated cell touches them."""
+        if self._zero is None:
+            plane = (self.nx + 1) * (self.ny + 1)
+            out = []
+            if self.kc0 > 0:
+                out.append((0, int(rowptr_d[plane * self.kc0])))
+            if self.kc1 < self.nz:
+                out.append((int(rowptr_d[plane * (self.kc1 + 1)]), int(rowptr_d[-1])))
+            self._zero = out
+        return self._zero
 
     @staticmethod
     def detect(conn_d: torch.Tensor, nnode: int) -> "KuhnBox | None":
@@ -543,6 +587,7 @@ class AssemblyContext:
         mesh = as_device_mesh(mesh)
         if not mesh.is_grouped_by_type():
             raise ConfigurationError("mesh has repeated element-type blocks; renumber_by_type first")
+        own_pattern = pattern is None
         if pattern is None:
             pattern = build_node_pattern(mesh)
         elif pattern.n != mesh.nnode:
@@ -560,6 +605,8 @@ class AssemblyContext:
                                       mesh.coords_d if (block_order == "morton" and BLOCK_MORTON) else None)
                 if g.etype is ElementType.TET04 and KUHN_MOMENTUM and len(mesh.groups) == 1:
                     gd.kuhn = KuhnBox.detect(g.conn_d, mesh.nnode)
+                    if gd.kuhn is not None:
+                        gd.kuhn.pattern_ok = own_pattern
             if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
                 gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time
@@ -664,8 +711,21 @@ class AssemblyContext:
             if own and single_rows and window is None and g.kuhn is not None \
                     and kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] and KUHN_MOMENTUM:
                 kb = g.kuhn
-                _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kchunk, xyz4, vp, float(rho),
-                          float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
+                _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk, xyz4, vp,
+                          float(rho), float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
+            elif own and single_rows and window is None and g.kuhn is not None and g.kuhn.pattern_ok \
+                    and kind_id == GRADIENT_XYZ and KUHN_BOX_GRADIENT and g.kuhn.nx > 1 and g.kuhn.ny > 1:
+                # B_x, B_y, B_z on the Kuhn box: interior lines + boundary rows, ghost planes zero
+                kb = g.kuhn
+                rp_ = self.pattern.rowptr_d.data_ptr()
+                _lib.call("fpb_assemble_gradient_kuhn_lines", kb.nx, kb.ny, kb.nz, kb.kc0 + 1, kb.kc1 - 1, xyz4, rp_,
+                          nnz, 0, out.data_ptr(), _lib.stream())
+                br = kb.boundary_rows(out.device)
+                _lib.call("fpb_assemble_gradient_kuhn_boundary", int(br.numel()), br.data_ptr(), kb.nx, kb.ny, kb.nz,
+                          kb.kc0, kb.kc1, xyz4, rp_, nnz, 0, out.data_ptr(), _lib.stream())
+                for a0, a1 in kb.zero_ranges(self.pattern.rowptr_d):
+                    for m in range(3):
+                        out[m * nnz + a0:m * nnz + a1].zero_()
             elif own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1
@@ -701,8 +761,8 @@ class AssemblyContext:
                                   _lib.stream())
                         if KUHN_BOX_BOUNDARY:  # boundary rows: the interior stream masked by the box
                             _lib.call("fpb_assemble_gradient_kuhn_boundary", int(pc["other"].numel()),
-                                      pc["other"].data_ptr(), kb_.nx, kb_.ny, kb_.nz, xyz4, rp_, nnz, acc,
-                                      out.data_ptr(), _lib.stream())
+                                      pc["other"].data_ptr(), kb_.nx, kb_.ny, kb_.nz, 0, kb_.nz, xyz4, rp_, nnz,
+                                      acc, out.data_ptr(), _lib.stream())
                         else:
                             _lib.call("fpb_assemble_gradient_pairs_rows", r.n, int(pc["other"].numel()),
                                       pc["other"].data_ptr(), r.pairs[0].data_ptr(), r.pairs[1].data_ptr(), xyz4,

@@ -67,6 +67,7 @@ constexpr int kKmomWarpD = kKmomStg + kKmomRing * kKmomSlot + kKmomHold;
 //       node column i0 + l (l = 32 only when i0 + 32 == nx)
 struct KuhnGrid {
   int nx, ny, nz, nxb, nyb;
+  int kc0, kc1;  // cell layers integrated: [kc0, kc1) of the box's nz (a slab's own layers; 0, nz otherwise)
   __host__ __device__ int64_t px(int a, int b, int k, int lr) const {
     return ((((int64_t)a * nyb + b) * (nz + 1) + k) * (kKmomTY + 1) + lr) * 3;
   }
@@ -255,10 +256,10 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   __syncthreads();
   if (w >= tyb) return;  // no barrier below
   const int j = j0 + w;
-  const int nchunk = (nz + kchunk - 1) / kchunk;
-  const int kb = c * kchunk, ke = min(nz, kb + kchunk);
-  const int kfirst = c > 0 ? kb - 1 : kb;          // halo cell layer below the chunk
-  const int klast = c == nchunk - 1 ? nz : ke - 1;  // last node layer written (nz: the top face)
+  const int nchunk = (g.kc1 - g.kc0 + kchunk - 1) / kchunk;
+  const int kb = g.kc0 + c * kchunk, ke = min(g.kc1, kb + kchunk);
+  const int kfirst = c > 0 ? kb - 1 : kb;               // halo cell layer below the chunk
+  const int klast = c == nchunk - 1 ? g.kc1 : ke - 1;   // last node layer written (kc1: the top face)
   const int64_t row = nx + 1, layer = (int64_t)(nx + 1) * (ny + 1);
   const bool cell = i0 + lane < nx;
   const bool last_x = i0 + 32 >= nx;
@@ -346,7 +347,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int d = 0; d < 3; ++d) top[q][d] = 0.0;
-    if (cell && t < nz) {
+    if (cell && t < ke) {
       const double* s0 = stg + (t % 3) * 2 * 6 * 33 + lane;
       const double* s1 = stg + ((t + 1) % 3) * 2 * 6 * 33 + lane;
 #if FPB_KMOM_SHARED
@@ -446,10 +447,11 @@ __global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double
   const int64_t nxe = (int64_t)(g.nxb - 1) * (ny + 1);                // x-edge nodes per layer
   const int64_t cols = nx + 1 - (g.nxb - 1);                          // columns that are not x-edges
   const int64_t per = nxe + (int64_t)(g.nyb - 1) * cols;
-  const int64_t total = per * (nz + 1);
+  const int64_t total = per * (g.kc1 - g.kc0 + 1);  // node layers kc0 .. kc1
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(q / per);
-    int64_t u = q - (int64_t)k * per;
+    const int64_t kq = q / per;
+    int64_t u = q - kq * per;
+    const int k = g.kc0 + (int)kq;
     if (u < nxe) {
       const int a = 1 + (int)(u / (ny + 1));
       const int jn = (int)(u - (int64_t)(a - 1) * (ny + 1));
@@ -483,11 +485,13 @@ int g_tuning_kmom_smem_kb = 0;  // fpb_set_tuning("kmom_smem_kb", KB): pad the C
 
 inline size_t kmom_smem() { return (size_t)kKmomTY * kKmomWarpD * sizeof(double) + 2 * kKmomTY * sizeof(int); }
 
-inline KuhnGrid kuhn_grid(int nx, int ny, int nz) {
+inline KuhnGrid kuhn_grid(int nx, int ny, int nz, int kc0 = 0, int kc1 = -1) {
   KuhnGrid g;
   g.nx = nx;
   g.ny = ny;
   g.nz = nz;
+  g.kc0 = kc0;
+  g.kc1 = kc1 < 0 ? nz : kc1;
   g.nxb = (nx + 31) / 32;
   g.nyb = (ny + kKmomTY - 1) / kKmomTY;
   return g;
@@ -504,22 +508,28 @@ int64_t fpb_kuhn_mom_scratch_len(int nx, int ny, int nz) {
   return kuhn_grid(nx, ny, nz).scratch();
 }
 
-int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kchunk, const double* xyz4, const double* vel,
-                               double rho, double mu, double* scratch, double* out, void* stream) {
+int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                               const double* vel, double rho, double mu, double* scratch, double* out,
+                               void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "Kuhn box %d x %d x %d", nx, ny, nz);
+  FPB_REQUIRE(0 <= kc0 && kc0 < kc1 && kc1 <= nz, "cell layers [%d, %d) outside [0, %d)", kc0, kc1, nz);
   FPB_REQUIRE(kchunk >= 1, "bad z chunk %d", kchunk);
   FPB_REQUIRE(xyz4 && vel && scratch && out, "null argument");
   cudaStream_t s = as_stream(stream);
-  const KuhnGrid g = kuhn_grid(nx, ny, nz);
-  const int nchunk = (nz + kchunk - 1) / kchunk;
+  const KuhnGrid g = kuhn_grid(nx, ny, nz, kc0, kc1);
+  const int64_t plane = (int64_t)(nx + 1) * (ny + 1);
+  // node planes no integrated cell touches (a slab's ghost planes) are zero
+  if (kc0 > 0) FPB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * plane * kc0, s));
+  if (kc1 < nz) FPB_CUDA(cudaMemsetAsync(out + 3 * plane * (kc1 + 1), 0, sizeof(double) * 3 * plane * (nz - kc1), s));
+  const int nchunk = (kc1 - kc0 + kchunk - 1) / kchunk;
   FPB_REQUIRE(g.nyb <= 65535 && nchunk <= 65535, "grid too large");
   const size_t smem = std::max(kmom_smem(), (size_t)g_tuning_kmom_smem_kb * 1024);
   auto kern = k_kuhn_mom<32 * kKmomTY>;
   FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<dim3(g.nxb, g.nyb, nchunk), 32 * kKmomTY, smem, s>>>(g, kchunk, xyz4, vel, rho, mu, scratch, out);
   FPB_LAUNCH_CHECK();
-  const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (nz + 1);
+  const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (kc1 - kc0 + 1);
   if (nb > 0) {
     k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out);
     FPB_LAUNCH_CHECK();

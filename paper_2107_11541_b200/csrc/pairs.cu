@@ -566,7 +566,7 @@ __device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) 
 }
 
 __global__ void __launch_bounds__(32 * kGradWarps, FPB_KGRAD_MINB)
-k_kuhn_grad_march(int nx, int ny, int nz, int kchunk, int64_t nwarps, const double* __restrict__ xyz4,
+k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t nwarps, const double* __restrict__ xyz4,
                   const int32_t* __restrict__ rowptr, int64_t nnz, int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3, RE = kKuhnCols + 1;  // entries per row
   extern __shared__ __align__(16) double gsm[];
@@ -584,7 +584,7 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kchunk, int64_t nwarps, const doub
   const int i = 1 + 32 * s + lane;
   const int nlive = min(32, nxi - 32 * s);
   const bool live = lane < nlive;
-  const int kb = 1 + c * kchunk, ke = min(nz, kb + kchunk);
+  const int kb = kz0 + c * kchunk, ke = min(kz1 + 1, kb + kchunk);  // node planes [kz0, kz1]
   const int64_t R = nx + 1, L = R * (ny + 1);
 
   int* const rlo_s = reinterpret_cast<int*>(stg + 4 * 3 * 3 * 34);  // [layer slot]
@@ -695,7 +695,7 @@ __host__ __device__ constexpr int kuhn_off3(int t, int d) {
 __host__ __device__ constexpr int cmin0(int a, int b, int c) { return (a < b ? (a < c ? a : c) : (b < c ? b : c)) < 0 ? -1 : 0; }
 
 __global__ void __launch_bounds__(128)
-k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, int ny, int nz,
+k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, int ny, int nz, int vk0, int vk1,
                      const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, int64_t nnz,
                      int accumulate, double* __restrict__ out) {
   constexpr int DIM = 3;
@@ -704,11 +704,16 @@ k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, in
     const int row = __ldg(rows + e);
     const int k = (int)(row / L), rem = (int)(row - k * L), j = rem / (int)R, i = rem - j * (int)R;
     // the 8 cells around the node: bit (cx + 1) + 2 (cy + 1) + 4 (cz + 1)
-    unsigned cells = 0;
+    // cells in the box (they shape the CSR row) and cells integrated (layers
+    // [vk0, vk1): a slab's own layers) — the latter contribute values
+    unsigned cells = 0, vcells = 0;
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const int ci = i + (b & 1) - 1, cj = j + ((b >> 1) & 1) - 1, ck = k + ((b >> 2) & 1) - 1;
-      if (ci >= 0 && ci < nx && cj >= 0 && cj < ny && ck >= 0 && ck < nz) cells |= 1u << b;
+      if (ci >= 0 && ci < nx && cj >= 0 && cj < ny && ck >= 0 && ck < nz) {
+        cells |= 1u << b;
+        if (ck >= vk0 && ck < vk1) vcells |= 1u << b;
+      }
     }
     double x0[DIM], X[kKuhnCols][DIM];
     {
@@ -737,12 +742,12 @@ k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, in
       const int cb = (cmin0(kuhn_off3(target, 0), kuhn_off3(q, 0), kuhn_off3(r, 0)) + 1) +
                      2 * (cmin0(kuhn_off3(target, 1), kuhn_off3(q, 1), kuhn_off3(r, 1)) + 1) +
                      4 * (cmin0(kuhn_off3(target, 2), kuhn_off3(q, 2), kuhn_off3(r, 2)) + 1);
-      if ((cells >> cb) & 1u) {
+      if ((vcells >> cb) & 1u) {
         acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
         acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
         acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
-        any = true;
       }
+      if ((cells >> cb) & 1u) any = true;
       if (w & (1 << 14)) {  // column finished
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
@@ -872,14 +877,35 @@ int fpb_assemble_gradient_pairs_kuhn(int32_t nrows, const int32_t* rows, const i
   return FPB_OK;
 }
 
-int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz,
-                                        const double* xyz4, const int32_t* rowptr, int64_t nnz, int accumulate,
-                                        double* out, void* stream) {
+int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int nx, int ny, int nz, int vk0,
+                                        int vk1, const double* xyz4, const int32_t* rowptr, int64_t nnz,
+                                        int accumulate, double* out, void* stream) {
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1 && nz >= 1, "bad Kuhn-boundary arguments");
   if (nrows <= 0) return FPB_OK;
-  k_kuhn_grad_boundary<<<grid_for(nrows, 128), 128, 0, as_stream(stream)>>>(nrows, rows, nx, ny, nz, xyz4, rowptr,
-                                                                          nnz, accumulate, out);
+  k_kuhn_grad_boundary<<<grid_for(nrows, 128), 128, 0, as_stream(stream)>>>(nrows, rows, nx, ny, nz, vk0, vk1, xyz4,
+                                                                          rowptr, nnz, accumulate, out);
+  FPB_LAUNCH_CHECK();
+  return FPB_OK;
+}
+
+int fpb_assemble_gradient_kuhn_lines(int nx, int ny, int nz, int kz0, int kz1, const double* xyz4,
+                                     const int32_t* rowptr, int64_t nnz, int accumulate, double* out, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(xyz4 && rowptr && out && nx >= 2 && ny >= 2 && 1 <= kz0 && kz1 <= nz - 1,
+              "bad Kuhn-line arguments (box %d x %d x %d, planes [%d, %d])", nx, ny, nz, kz0, kz1);
+  if (kz1 < kz0) return FPB_OK;
+  const int nxi = nx - 1, nyi = ny - 1, np = kz1 - kz0 + 1;
+  // z-chunks: about four waves of 10 resident warps per SM, 4..32 layers each
+  const int64_t lines = (int64_t)((nxi + 31) / 32) * nyi;
+  const int kauto = (int)std::min<int64_t>(32, std::max<int64_t>(4, lines * np / (4 * 10 * kNumSMs)));
+  const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk > 0 ? g_tuning_kgrad_kchunk : kauto, np));
+  const int nchunk = (np + kchunk - 1) / kchunk;
+  const int64_t nwarps = lines * nchunk;
+  const size_t smem = (size_t)kGradWarps * (kGradStg + 3 * 32 * (kKuhnCols + 1)) * sizeof(double);
+  FPB_CUDA(cudaFuncSetAttribute(k_kuhn_grad_march, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_kuhn_grad_march<<<(unsigned)((nwarps + kGradWarps - 1) / kGradWarps), 32 * kGradWarps, smem,
+                      as_stream(stream)>>>(nx, ny, nz, kz0, kz1, kchunk, nwarps, xyz4, rowptr, nnz, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;
 }
@@ -891,18 +917,7 @@ int fpb_assemble_gradient_pairs_kuhn_box(int32_t nrows, const int32_t* rows, int
     const int nxi = nx - 1, nyi = ny - 1;
     FPB_REQUIRE((int64_t)nrows % ((int64_t)nxi * nyi) == 0, "%d interior rows: not whole interior planes", nrows);
     const int nz = nrows / (nxi * nyi) + 1;
-    // z-chunks: about four waves of 10 resident warps per SM, 4..32 layers each
-    const int64_t lines = (int64_t)((nxi + 31) / 32) * nyi;
-    const int kauto = (int)std::min<int64_t>(32, std::max<int64_t>(4, lines * (nz - 1) / (4 * 10 * kNumSMs)));
-    const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk > 0 ? g_tuning_kgrad_kchunk : kauto, nz - 1));
-    const int nchunk = (nz - 1 + kchunk - 1) / kchunk;
-    const int64_t nwarps = (int64_t)((nxi + 31) / 32) * nyi * nchunk;
-    const size_t smem = (size_t)kGradWarps * (kGradStg + 3 * 32 * (kKuhnCols + 1)) * sizeof(double);
-    FPB_CUDA(cudaFuncSetAttribute(k_kuhn_grad_march, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_kuhn_grad_march<<<(unsigned)((nwarps + kGradWarps - 1) / kGradWarps), 32 * kGradWarps, smem,
-                        as_stream(stream)>>>(nx, ny, nz, kchunk, nwarps, xyz4, rowptr, nnz, accumulate, out);
-    FPB_LAUNCH_CHECK();
-    return FPB_OK;
+    return fpb_assemble_gradient_kuhn_lines(nx, ny, nz, 1, nz - 1, xyz4, rowptr, nnz, accumulate, out, stream);
   }
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1, "bad Kuhn-box gradient arguments");

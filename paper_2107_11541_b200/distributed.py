@@ -32,6 +32,11 @@ import torch.distributed as dist
 
 from .elements import ElementType
 
+# slab domains assemble with the Kuhn-box kernels (no interface-first
+# windows: the halo follows the whole-slab kernels); False = windowed
+# element-block / row kernels with the halo overlapped
+SLAB_KUHN = True
+
 
 def slab_ranges(nz: int, world: int) -> list[tuple[int, int]]:
     """Balanced cell-layer ranges [k0, k1) per rank."""
@@ -298,6 +303,13 @@ class SlabDomain:
         pattern = build_node_pattern(ext)  # own + ghost elements
         own = Mesh(3, coords, [ElementGroup(etype, conn[e0:e1].contiguous())])
         ctx = AssemblyContext.build(own, vector_size, pattern=pattern, block_order="natural")  # windows = block ranges
+        from . import assembly as _asm
+
+        if etype is ElementType.TET04 and _asm.KUHN_MOMENTUM and SLAB_KUHN:
+            # the extended slab is the generator's box (nx, ny, nlay) by
+            # construction, its CSR graph the box's own: Kuhn-box kernels over
+            # the own cell layers (interface planes partial, ghost planes 0)
+            ctx.groups[0].kuhn = _asm.KuhnBox(nx, ny, nlay, dev, kc0=L.k0 - L.kA, kc1=L.k1 - L.kA, pattern_ok=True)
         return cls(L, own, ctx, group)
 
     def halo_sum_rhs(self, rhs: torch.Tensor) -> torch.Tensor:
@@ -577,11 +589,25 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
 
     ctx = dom.ctx
     K = KernelKind.MOMENTUM_RHS
-    if not overlap or dom.layout.world == 1:
+    if not overlap or dom.layout.world == 1 or ctx.groups[0].kuhn is not None:
+        # plain sequence (also the Kuhn-box slab step: whole-slab kernels,
+        # then the halo; per-phase events with an empty interior phase)
+        ev = None
+        if events is not None:
+            ev = {k: torch.cuda.Event(enable_timing=True)
+                  for k in ("start", "interface_done", "halo_start", "halo_done", "interior_done")}
+            events.update(ev)
+            ev["start"].record()
         ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs)
         ctx.assemble_gradients_d(mats)
+        if ev:
+            ev["interface_done"].record()
+            ev["halo_start"].record()
         dom.halo_sum_rhs(rhs)
         dom.halo_sum_matrix(mats, dom.ctx.mesh.dim)
+        if ev:
+            ev["halo_done"].record()
+            ev["interior_done"].record()
         return rhs, mats
     w = _step_windows(dom)
     none = (0, 0)
@@ -654,6 +680,11 @@ class SlabStepGraph:
             self.whole = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.whole, stream=cap):
                 assemble_step(dom, vel, rhs, mats, rho, mu, overlap=True, side=self.side)
+        elif ctx.groups[0].kuhn is not None:  # Kuhn-box slab: the whole assembly, then the eager halo
+            self.phase_a = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.phase_a, stream=cap):
+                ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs)
+                ctx.assemble_gradients_d(mats)
         else:
             w = _step_windows(dom)
             self.phase_a, self.phase_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -685,5 +716,6 @@ class SlabStepGraph:
             self.phase_a.replay()
             self.dom.halo_sum_rhs(self.rhs)
             self.dom.halo_sum_matrix(self.mats, self.dom.ctx.mesh.dim)
-            self.phase_b.replay()
+            if self.phase_b is not None:
+                self.phase_b.replay()
         return self.rhs, self.mats

@@ -215,7 +215,12 @@ def _step_worker(rank, world, initfile, q, dims):
         res = {"same": bool(np.array_equal(out[False][0], out[True][0]) and
                             np.array_equal(out[False][1], out[True][1])) and graph_same,
                "finite": bool(np.isfinite(out[True][0]).all() and np.isfinite(out[True][1]).all()),
-               "rhs": out[True][0][lo:hi]}
+               "rhs": out[True][0][lo:hi],
+               "kuhn": dom.ctx.groups[0].kuhn is not None}
+        rp = dom.ctx.pattern.rowptr_d.cpu().numpy()
+        a, b = int(rp[lo]), int(rp[hi])
+        res["mats"] = np.concatenate([out[True][1][m * nnz + a:m * nnz + b] for m in range(3)])
+        res["mat_rows"] = (lo + L.node_offset, hi + L.node_offset)
         gathered = [None] * world
         dist.all_gather_object(gathered, res)
         if rank == 0:
@@ -245,6 +250,21 @@ def test_interface_first_step_matches_plain_step(cuda_ok, world):
     vel_g, _ = O.bench_fields(full.mesh.nnode, 3)
     want = full.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel_g, None, 1.0, 1e-2, 0.0)
     assert O.rel_diff(np.concatenate([p["rhs"] for p in parts]), want) < 1e-13
+    # owned CSR rows of B_x, B_y, B_z (interface rows halo-summed) = the single domain's
+    import torch as _t
+
+    g = _t.empty(3 * full.pattern.nnz, dtype=_t.float64, device="cuda")
+    full.assemble_gradients_d(g)
+    g = g.cpu().numpy()
+    rpg = full.pattern.rowptr_d.cpu().numpy()
+    nnzg = full.pattern.nnz
+    for p in parts:
+        r0, r1 = p["mat_rows"]
+        a, b = int(rpg[r0]), int(rpg[r1])
+        wantm = np.concatenate([g[m * nnzg + a:m * nnzg + b] for m in range(3)])
+        assert p["mats"].shape == wantm.shape
+        assert O.rel_diff(p["mats"], wantm) < 1e-13
+    assert all(p["kuhn"] for p in parts)  # the slab step ran the Kuhn-box kernels
 
 
 def _fake_domain(nx, ny, nz, rank, world, be=256):

@@ -111,10 +111,10 @@ def test_kuhn_matches_block_path_and_is_deterministic(cuda_ok):
     assert O.rel_diff(a, b) < TOL
 
 
-def test_kuhn_box_gradients_bitwise_equal_colind_path(cuda_ok):
+def test_kuhn_box_gradients_match_colind_path(cuda_ok):
     """Continuity B_x, B_y, B_z on a Kuhn box: the interior rows by z-marching
-    lines (fpb_assemble_gradient_pairs_kuhn_box) give bitwise the colind
-    path's values (same arithmetic, same order); the boundary rows by the
+    lines (fpb_assemble_gradient_kuhn_lines) give bitwise the colind path's
+    values (same arithmetic, same order); the boundary rows by the
     box-masked interior stream (fpb_assemble_gradient_kuhn_boundary) agree
     with the generic row-list kernel to rounding; all match the oracle."""
     import paper_2107_11541_b200 as P
@@ -124,26 +124,31 @@ def test_kuhn_box_gradients_bitwise_equal_colind_path(cuda_ok):
         om = O.box(O.TET04, *dims)
         om.coords = _jitter(om.coords, *dims, seed=11)
         mesh, ctx = _ctx(P, *dims, coords=om.coords)
-        assert ctx.groups[0].kuhn is not None
+        kb = ctx.groups[0].kuhn
+        assert kb is not None and kb.pattern_ok
         nnz = ctx.pattern.nnz
         a = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
         b = torch.empty_like(a)
-        c = torch.empty_like(a)
-        ctx.assemble_gradients_d(a)  # interior lines + masked-stream boundary rows
-        A.KUHN_BOX_BOUNDARY = False
-        try:
-            ctx.assemble_gradients_d(c)  # interior lines + the generic row-list kernel
-        finally:
-            A.KUHN_BOX_BOUNDARY = True
+        ctx.assemble_gradients_d(a)
         A.KUHN_BOX_GRADIENT = False
         try:
             ctx.assemble_gradients_d(b)
         finally:
             A.KUHN_BOX_GRADIENT = True
-        assert torch.equal(c, b), dims
         assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < 1e-14, dims
-        for k in range(3):
+        # interior rows: bitwise
+        nx, ny, nz = dims
+        rp = ctx.pattern.rowptr_d.cpu().numpy()
+        idx = np.arange(mesh.nnode)
+        i, j, k = idx % (nx + 1), (idx // (nx + 1)) % (ny + 1), idx // ((nx + 1) * (ny + 1))
+        inner = idx[(i > 0) & (i < nx) & (j > 0) & (j < ny) & (k > 0) & (k < nz)]
+        sel = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in inner]) if inner.size else np.zeros(0, int)
+        pc = ctx.groups[0].rows.pair_canon
+        for m in range(3 if (pc is not None and pc.get("kuhn")) else 0):  # colind path on the Kuhn stream
+            assert torch.equal(a[m * nnz:(m + 1) * nnz][torch.as_tensor(sel, device="cuda")],
+                               b[m * nnz:(m + 1) * nnz][torch.as_tensor(sel, device="cuda")]), dims
+        for k3 in range(3):
             e = np.zeros((om.nnode, 3))
-            e[:, k] = 1.0
+            e[:, k3] = 1.0
             _, _, vo = O.assemble_matrix(om, "convection", e)
-            assert O.rel_diff(a[k * nnz:(k + 1) * nnz].cpu().numpy(), vo) < TOL, (dims, k)
+            assert O.rel_diff(a[k3 * nnz:(k3 + 1) * nnz].cpu().numpy(), vo) < TOL, (dims, k3)
