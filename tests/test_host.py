@@ -158,3 +158,28 @@ def test_vals_store_does_not_keep_tensors_alive():
     del t, st
     gc.collect()
     assert r() is None
+
+
+@pytest.mark.parametrize("dims,own", [((4, 3, 5), None), ((37, 21, 9), None), ((6, 5, 7), (1, 6)),
+                                      ((2, 2, 4), (0, 3))])
+def test_kuhn_box_row_split_covers_every_row_once(dims, own):
+    """KuhnBox (assembly.py): the interior-line kernel's rows (i, j in the
+    interior, node planes kc0+1 .. kc1-1) and boundary_rows() partition the
+    node planes kc0 .. kc1 exactly; the z-chunk model stays within the
+    integrated layers.  Host logic only (torch on the CPU)."""
+    import torch
+
+    from paper_2107_11541_b200.assembly import KuhnBox
+
+    nx, ny, nz = dims
+    kc0, kc1 = own if own else (0, nz)
+    kb = KuhnBox(nx, ny, nz, "cpu", kc0=kc0, kc1=kc1)
+    assert 1 <= kb.kchunk <= kc1 - kc0
+    br = kb.boundary_rows(torch.device("cpu")).numpy().astype(np.int64)
+    assert np.all(np.diff(br) > 0)  # ascending, no duplicates
+    plane = (nx + 1) * (ny + 1)
+    i, j = np.arange(plane) % (nx + 1), np.arange(plane) // (nx + 1)
+    inner = np.arange(plane)[(i > 0) & (i < nx) & (j > 0) & (j < ny)]
+    lines = np.concatenate([inner + plane * k for k in range(kc0 + 1, kc1)]) if kc1 - kc0 > 1 else np.zeros(0, int)
+    allrows = np.sort(np.concatenate([br, lines]))
+    assert np.array_equal(allrows, np.arange(plane * kc0, plane * (kc1 + 1)))
