@@ -385,6 +385,13 @@ int64_t fpb_kuhn_mom_scratch_len(int nx, int ny, int nz);
 int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
                                const double* vel, double rho, double mu, double* scratch, double* out,
                                void* stream);
+/* The three scalar-transport RHS of config 3 (enthalpy + two species,
+ * scalar_rhs_packed, _kernels.py:420-461, one velocity) on the same Kuhn box
+ * in one pass: phi3 / out3 are [3][fstride] (field-major), kappa_f the
+ * diffusivity of field f; same pencils, layer range and scratch. */
+int fpb_assemble_scalar3_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                              const double* vel, const double* phi3, int64_t fstride, double kappa0, double kappa1,
+                              double kappa2, double* scratch, double* out3, void* stream);
 
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 

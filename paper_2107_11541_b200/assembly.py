@@ -843,6 +843,13 @@ class AssemblyContext:
         if phi3.shape != (3, n) or out3.shape != (3, n) or not out3.is_contiguous():
             raise ConfigurationError("phi3 and out3 must be (3, nnode); out3 contiguous")
         g = self.groups[0] if len(self.groups) == 1 else None
+        if g is not None and g.kuhn is not None and window is None and KUHN_MOMENTUM:
+            kb = g.kuhn  # Kuhn box: z-marching cell pencils (kmom.cu), three fields per node
+            _lib.call("fpb_assemble_scalar3_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk,
+                      self.xyz4.data_ptr(), vel.data_ptr(), phi3.data_ptr(), n, k0, k1, k2,
+                      kb.scratch(out3.device).data_ptr(), out3.data_ptr(), _lib.stream())
+            mark_written(out3)
+            return out3
         if g is None or g.blocks is None:
             if window is not None:
                 raise ConfigurationError("assembly windows need a single owner-writes element group")

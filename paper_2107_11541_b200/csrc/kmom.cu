@@ -55,10 +55,13 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 #endif
 constexpr int kKmomTY = FPB_KMOM_TY;            // cell rows (warps) per CTA
 constexpr int kKmomRing = 4;                    // y-forward slots per warp
-constexpr int kKmomStg = 3 * 2 * 6 * 33;        // staged doubles per warp: [layer][row][comp][33 nodes]
 constexpr int kKmomSlot = 33 * 3;               // one forwarded node row: [33][3]
 constexpr int kKmomHold = 2 * 3 * 33;           // node row j held two layers: [parity][comp][33]
-constexpr int kKmomWarpD = kKmomStg + kKmomRing * kKmomSlot + kKmomHold;
+// KIND 0: momentum RHS (x, y, z, u, v, w staged per node); KIND 1: three
+// scalar RHS sharing the velocity (+ phi_0, phi_1, phi_2)
+template <int KIND> constexpr int kmom_nc() { return KIND ? 9 : 6; }
+template <int KIND> constexpr int kmom_stg() { return 3 * 2 * kmom_nc<KIND>() * 33; }  // [layer][row][comp][33]
+template <int KIND> constexpr int kmom_warp_d() { return kmom_stg<KIND>() + kKmomRing * kKmomSlot + kKmomHold; }
 
 // boundary partials, per CTA (a, b) and node layer k:
 //   Px[a][b][k][lr][3], lr = 0..kKmomTY: node column i0 + 32 (the next x-block's
@@ -94,7 +97,7 @@ struct KuhnGrid {
 __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double* s1, double r, double muW,
                                                  double (&bot)[4][3], double (&top)[4][3]) {
   auto ld = [&](int cc, double (&x)[3], double (&u)[3]) {
-    const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * 6 * 33 + (cc & 1);
+    const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * kmom_nc<0>() * 33 + (cc & 1);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       x[d] = sp[d * 33];
@@ -235,10 +238,14 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
   }
 }
 
-template <int MAXT>
+template <int MAXT, int KIND>
 __global__ void __launch_bounds__(MAXT, FPB_KMOM_MINB)
-k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double* __restrict__ vel, double rho,
-           double mu, double* __restrict__ part, double* __restrict__ out) {
+k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double* __restrict__ vel,
+           const double* __restrict__ phi, int64_t fstride, double rho, double mu, double kappa,
+           double* __restrict__ part, double* __restrict__ out) {
+  constexpr int NC = kmom_nc<KIND>(), kKmomStg = kmom_stg<KIND>(), kKmomWarpD = kmom_warp_d<KIND>();
+  // output slot of (node, component): [n][3] (momentum) or [3][fstride] (scalars)
+  auto oi = [&](int64_t nd, int d) -> int64_t { return KIND ? d * fstride + nd : 3 * nd + d; };
   extern __shared__ __align__(16) double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
@@ -250,8 +257,9 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   volatile double* const dring = sm + (size_t)(w - 1) * kKmomWarpD + kKmomStg;  // the warp below's
   double* const hold = stg + kKmomStg + kKmomRing * kKmomSlot;                   // lane-private
   volatile int* const yc = reinterpret_cast<volatile int*>(sm + (size_t)kKmomTY * kKmomWarpD);  // [TY][2]
-  const double r = rho * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
+  const double r = (KIND ? 1.0 : rho) * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
   const double muW = mu * c_ref[FPB_TET04].W;
+  const double kW[3] = {rho * c_ref[FPB_TET04].W, muW, kappa * c_ref[FPB_TET04].W};  // scalars: kappa_f W
   if (threadIdx.x < 2 * kKmomTY) yc[threadIdx.x] = 0;
   __syncthreads();
   if (w >= tyb) return;  // no barrier below
@@ -270,20 +278,24 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   const bool top_final = top_w && j + 1 == ny;
 
   auto stage = [&](int kl) {  // node layer kl, node rows j, j + 1, columns i0 .. i0 + 32
-    double* s = stg + (kl % 3) * 2 * 6 * 33;
+    double* s = stg + (kl % 3) * 2 * NC * 33;
     for (int q = lane; q < 33; q += 32) {
       const int ii = i0 + q;
       if (ii <= nx) {
 #pragma unroll
         for (int dj = 0; dj < 2; ++dj) {
           const int64_t nd = ii + (j + dj) * row + kl * layer;
-          double* t = s + dj * 6 * 33 + q;
+          double* t = s + dj * NC * 33 + q;
           cp8(t, xyz4 + 4 * nd);
           cp8(t + 33, xyz4 + 4 * nd + 1);
           cp8(t + 66, xyz4 + 4 * nd + 2);
           cp8(t + 99, vel + 3 * nd);
           cp8(t + 132, vel + 3 * nd + 1);
           cp8(t + 165, vel + 3 * nd + 2);
+          if constexpr (KIND) {
+#pragma unroll
+            for (int f = 0; f < 3; ++f) cp8(t + (6 + f) * 33, phi + f * fstride + nd);
+          }
         }
       }
     }
@@ -325,11 +337,11 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
       const int64_t nd = i0 + lane + j * row + (int64_t)kk * layer;
       if (node) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) out[3 * nd + d] = R[d];
+        for (int d = 0; d < 3; ++d) out[oi(nd, d)] = R[d];
       }
       if (xtra) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) out[3 * (nd + 1) + d] = X[d];
+        for (int d = 0; d < 3; ++d) out[oi(nd + 1, d)] = X[d];
       } else if (redge) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) part[g.px(a, b, kk, w) + d] = X[d];
@@ -348,32 +360,56 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
 #pragma unroll
       for (int d = 0; d < 3; ++d) top[q][d] = 0.0;
     if (cell && t < ke) {
-      const double* s0 = stg + (t % 3) * 2 * 6 * 33 + lane;
-      const double* s1 = stg + ((t + 1) % 3) * 2 * 6 * 33 + lane;
+      const double* s0 = stg + (t % 3) * 2 * NC * 33 + lane;
+      const double* s1 = stg + ((t + 1) % 3) * 2 * NC * 33 + lane;
+      if constexpr (KIND) {  // three scalars: tet by tet
+#pragma unroll
+        for (int tt = 0; tt < 6; ++tt) {
+          asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
+          double xe[4][3], ue[4][3], pe[3][4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int cc = kuhn_corner(tt, q);
+            const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * NC * 33 + (cc & 1);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              xe[q][d] = sp[d * 33];
+              ue[q][d] = sp[(3 + d) * 33];
+              pe[d][q] = sp[(6 + d) * 33];
+            }
+          }
+          tet_s3_adj(xe, ue, pe, r, kW, [&](int q, int f, double v) {
+            const int cc = kuhn_corner(tt, q);
+            if (cc & 4) top[cc & 3][f] -= v;
+            else bot[cc & 3][f] -= v;
+          });
+        }
+      } else {
 #if FPB_KMOM_SHARED
-      kuhn_cell_shared(s0, s1, r, muW, bot, top);
+        kuhn_cell_shared(s0, s1, r, muW, bot, top);
 #else
 #pragma unroll
-      for (int tt = 0; tt < 6; ++tt) {
-        asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
-        double xe[4][3], ue[4][3];
+        for (int tt = 0; tt < 6; ++tt) {
+          asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
+          double xe[4][3], ue[4][3];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int cc = kuhn_corner(tt, q);
-          const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * 6 * 33 + (cc & 1);
+          for (int q = 0; q < 4; ++q) {
+            const int cc = kuhn_corner(tt, q);
+            const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * NC * 33 + (cc & 1);
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            xe[q][d] = sp[d * 33];
-            ue[q][d] = sp[(3 + d) * 33];
+            for (int d = 0; d < 3; ++d) {
+              xe[q][d] = sp[d * 33];
+              ue[q][d] = sp[(3 + d) * 33];
+            }
           }
+          tet_mom_adj_f(xe, ue, r, muW, [&](int q, int d, double v) {
+            const int cc = kuhn_corner(tt, q);
+            if (cc & 4) top[cc & 3][d] -= v;
+            else bot[cc & 3][d] -= v;
+          });
         }
-        tet_mom_adj_f(xe, ue, r, muW, [&](int q, int d, double v) {
-          const int cc = kuhn_corner(tt, q);
-          if (cc & 4) top[cc & 3][d] -= v;
-          else bot[cc & 3][d] -= v;
-        });
-      }
 #endif
+      }
     }
     // (B) layer t's bottom face is complete in z: x-shuffle; the right edge
     // and the top node row leave the warp
@@ -394,11 +430,11 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
         if (top_final) {
           if (node) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) out[3 * nd1 + d] = up[d];
+            for (int d = 0; d < 3; ++d) out[oi(nd1, d)] = up[d];
           }
           if (xtra) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) out[3 * (nd1 + 1) + d] = ex1[d];
+            for (int d = 0; d < 3; ++d) out[oi(nd1 + 1, d)] = ex1[d];
           }
         } else {
           if (node) {
@@ -441,7 +477,8 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
 // row, then y-block edges (rows TY b, 0 < b < nyb) over the other columns.
 // out += Px(a - 1, b)[lr] (+ Py(a, b - 1)[0] + Px(a - 1, b - 1)[TY] at a
 // y-block edge), resp. out += Py(a, b - 1)[l] — a fixed order per node.
-__global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double* __restrict__ out) {
+__global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double* __restrict__ out, int64_t fstride) {
+  auto oi = [&](int64_t nd, int d) -> int64_t { return fstride ? d * fstride + nd : 3 * nd + d; };
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const int64_t row = nx + 1, layer = (int64_t)(nx + 1) * (ny + 1);
   const int64_t nxe = (int64_t)(g.nxb - 1) * (ny + 1);                // x-edge nodes per layer
@@ -460,14 +497,14 @@ __global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double
       const int64_t nd = 32 * a + jn * row + (int64_t)k * layer;
       double s[3];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) s[d] = out[3 * nd + d] + part[g.px(a - 1, b, k, lr) + d];
+      for (int d = 0; d < 3; ++d) s[d] = out[oi(nd, d)] + part[g.px(a - 1, b, k, lr) + d];
       if (lr == 0 && b > 0) {
 #pragma unroll
         for (int d = 0; d < 3; ++d)
           s[d] = (s[d] + part[g.py(a, b - 1, k, 0) + d]) + part[g.px(a - 1, b - 1, k, kKmomTY) + d];
       }
 #pragma unroll
-      for (int d = 0; d < 3; ++d) out[3 * nd + d] = s[d];
+      for (int d = 0; d < 3; ++d) out[oi(nd, d)] = s[d];
     } else {
       u -= nxe;
       const int b = 1 + (int)(u / cols);
@@ -476,14 +513,15 @@ __global__ void k_kuhn_fixup(KuhnGrid g, const double* __restrict__ part, double
       const int a = min(i / 32, g.nxb - 1);
       const int64_t nd = i + (int64_t)(kKmomTY * b) * row + (int64_t)k * layer;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) out[3 * nd + d] = out[3 * nd + d] + part[g.py(a, b - 1, k, i - 32 * a) + d];
+      for (int d = 0; d < 3; ++d) out[oi(nd, d)] = out[oi(nd, d)] + part[g.py(a, b - 1, k, i - 32 * a) + d];
     }
   }
 }
 
 int g_tuning_kmom_smem_kb = 0;  // fpb_set_tuning("kmom_smem_kb", KB): pad the CTA's shared memory (co-residency A/B)
 
-inline size_t kmom_smem() { return (size_t)kKmomTY * kKmomWarpD * sizeof(double) + 2 * kKmomTY * sizeof(int); }
+template <int KIND>
+inline size_t kmom_smem() { return (size_t)kKmomTY * kmom_warp_d<KIND>() * sizeof(double) + 2 * kKmomTY * sizeof(int); }
 
 inline KuhnGrid kuhn_grid(int nx, int ny, int nz, int kc0 = 0, int kc1 = -1) {
   KuhnGrid g;
@@ -495,6 +533,39 @@ inline KuhnGrid kuhn_grid(int nx, int ny, int nz, int kc0 = 0, int kc1 = -1) {
   g.nxb = (nx + 31) / 32;
   g.nyb = (ny + kKmomTY - 1) / kKmomTY;
   return g;
+}
+
+template <int KIND>
+static int launch_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4, const double* vel,
+                       const double* phi, int64_t fstride, double rho, double mu, double kappa, double* scratch,
+                       double* out, cudaStream_t s) {
+  const KuhnGrid g = kuhn_grid(nx, ny, nz, kc0, kc1);
+  const int64_t plane = (int64_t)(nx + 1) * (ny + 1);
+  // node planes no integrated cell touches (a slab's ghost planes) are zero
+  const int64_t lo = plane * kc0, hi = plane * (kc1 + 1), n = plane * (nz + 1);
+  if (KIND) {
+    for (int f = 0; f < 3; ++f) {
+      if (lo > 0) FPB_CUDA(cudaMemsetAsync(out + f * fstride, 0, sizeof(double) * lo, s));
+      if (hi < n) FPB_CUDA(cudaMemsetAsync(out + f * fstride + hi, 0, sizeof(double) * (n - hi), s));
+    }
+  } else {
+    if (lo > 0) FPB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * lo, s));
+    if (hi < n) FPB_CUDA(cudaMemsetAsync(out + 3 * hi, 0, sizeof(double) * 3 * (n - hi), s));
+  }
+  const int nchunk = (kc1 - kc0 + kchunk - 1) / kchunk;
+  FPB_REQUIRE(g.nyb <= 65535 && nchunk <= 65535, "grid too large");
+  const size_t smem = std::max(kmom_smem<KIND>(), (size_t)g_tuning_kmom_smem_kb * 1024);
+  auto kern = k_kuhn_mom<32 * kKmomTY, KIND>;
+  FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(g.nxb, g.nyb, nchunk), 32 * kKmomTY, smem, s>>>(g, kchunk, xyz4, vel, phi, fstride, rho, mu, kappa,
+                                                               scratch, out);
+  FPB_LAUNCH_CHECK();
+  const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (kc1 - kc0 + 1);
+  if (nb > 0) {
+    k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out, KIND ? fstride : 0);
+    FPB_LAUNCH_CHECK();
+  }
+  return FPB_OK;
 }
 
 }  // namespace fpb
@@ -516,25 +587,22 @@ int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kch
   FPB_REQUIRE(0 <= kc0 && kc0 < kc1 && kc1 <= nz, "cell layers [%d, %d) outside [0, %d)", kc0, kc1, nz);
   FPB_REQUIRE(kchunk >= 1, "bad z chunk %d", kchunk);
   FPB_REQUIRE(xyz4 && vel && scratch && out, "null argument");
-  cudaStream_t s = as_stream(stream);
-  const KuhnGrid g = kuhn_grid(nx, ny, nz, kc0, kc1);
-  const int64_t plane = (int64_t)(nx + 1) * (ny + 1);
-  // node planes no integrated cell touches (a slab's ghost planes) are zero
-  if (kc0 > 0) FPB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * plane * kc0, s));
-  if (kc1 < nz) FPB_CUDA(cudaMemsetAsync(out + 3 * plane * (kc1 + 1), 0, sizeof(double) * 3 * plane * (nz - kc1), s));
-  const int nchunk = (kc1 - kc0 + kchunk - 1) / kchunk;
-  FPB_REQUIRE(g.nyb <= 65535 && nchunk <= 65535, "grid too large");
-  const size_t smem = std::max(kmom_smem(), (size_t)g_tuning_kmom_smem_kb * 1024);
-  auto kern = k_kuhn_mom<32 * kKmomTY>;
-  FPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<dim3(g.nxb, g.nyb, nchunk), 32 * kKmomTY, smem, s>>>(g, kchunk, xyz4, vel, rho, mu, scratch, out);
-  FPB_LAUNCH_CHECK();
-  const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (kc1 - kc0 + 1);
-  if (nb > 0) {
-    k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out);
-    FPB_LAUNCH_CHECK();
-  }
-  return FPB_OK;
+  return launch_kuhn<0>(nx, ny, nz, kc0, kc1, kchunk, xyz4, vel, nullptr, 0, rho, mu, 0.0, scratch, out,
+                        as_stream(stream));
+}
+
+int fpb_assemble_scalar3_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                              const double* vel, const double* phi3, int64_t fstride, double kappa0, double kappa1,
+                              double kappa2, double* scratch, double* out3, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
+  FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "Kuhn box %d x %d x %d", nx, ny, nz);
+  FPB_REQUIRE(0 <= kc0 && kc0 < kc1 && kc1 <= nz, "cell layers [%d, %d) outside [0, %d)", kc0, kc1, nz);
+  FPB_REQUIRE(kchunk >= 1, "bad z chunk %d", kchunk);
+  FPB_REQUIRE(xyz4 && vel && phi3 && scratch && out3, "null argument");
+  FPB_REQUIRE(fstride >= (int64_t)(nx + 1) * (ny + 1) * (nz + 1), "field stride %lld below the node count",
+              (long long)fstride);
+  return launch_kuhn<1>(nx, ny, nz, kc0, kc1, kchunk, xyz4, vel, phi3, fstride, kappa0, kappa1, kappa2, scratch,
+                        out3, as_stream(stream));
 }
 
 }  // extern "C"

@@ -353,4 +353,48 @@ __device__ __forceinline__ double dot3(const double (&p)[3], const double (&q)[3
   return p[0] * q[0] + p[1] * q[1] + p[2] * q[2];
 }
 
+// Three scalar-transport residuals of one P1 tet sharing the velocity
+// (_kernels.py:420-461 for each field; enthalpy + two species), adjugate
+// form: with A the adjugate rows and gp_f = sum_b (phi_f,b+1 - phi_f,0) A[b]
+// (= det grad phi_f), sub(a, f, v) subtracts
+//   v = r (U + u_a) . gp_f + (kW_f / det) gp_f . dg_a,   r = W / 20,
+// dg_a = A[a-1] (a >= 1), -(A[0] + A[1] + A[2]) (a = 0) — the reference's
+// det ubar_a . grad phi + kappa det W grad phi . gradN_a to rounding.
+template <class Sub>
+__device__ __forceinline__ void tet_s3_adj(const double (&x)[4][3], const double (&u)[4][3], const double (&ph)[3][4],
+                                           double r, const double (&kW)[3], Sub&& sub) {
+  double E[3][3], A[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) E[b][d] = x[b + 1][d] - x[0][d];
+  cross3(E[1], E[2], A[0]);
+  cross3(E[2], E[0], A[1]);
+  cross3(E[0], E[1], A[2]);
+  const double det = dot3(E[0], A[0]);
+  const double inv = 1.0 / det;
+  double U[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) U[d] = (u[0][d] + u[1][d]) + (u[2][d] + u[3][d]);
+  double dg0[3];
+#pragma unroll
+  for (int l = 0; l < 3; ++l) dg0[l] = -((A[0][l] + A[1][l]) + A[2][l]);
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double gp[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+      gp[l] = (ph[f][1] - ph[f][0]) * A[0][l] + (ph[f][2] - ph[f][0]) * A[1][l] + (ph[f][3] - ph[f][0]) * A[2][l];
+    const double fk = kW[f] * inv;
+    const double ug = U[0] * gp[0] + U[1] * gp[1] + U[2] * gp[2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double* dg = a == 0 ? dg0 : A[a - 1];
+      const double adv = ug + (u[a][0] * gp[0] + u[a][1] * gp[1] + u[a][2] * gp[2]);
+      const double dif = gp[0] * dg[0] + gp[1] * dg[1] + gp[2] * dg[2];
+      sub(a, f, fma(r, adv, fk * dif));
+    }
+  }
+}
+
 }  // namespace fpb

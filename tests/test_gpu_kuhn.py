@@ -152,3 +152,52 @@ def test_kuhn_box_gradients_match_colind_path(cuda_ok):
             e[:, k3] = 1.0
             _, _, vo = O.assemble_matrix(om, "convection", e)
             assert O.rel_diff(a[k3 * nnz:(k3 + 1) * nnz].cpu().numpy(), vo) < TOL, (dims, k3)
+
+
+@pytest.mark.parametrize("dims,kchunk", [((5, 4, 7), 0), ((5, 4, 7), 2), ((33, 9, 5), 3), ((64, 2, 3), 0),
+                                         ((1, 1, 1), 0)])
+@pytest.mark.parametrize("jitter", [False, True])
+def test_kuhn_scalar3_matches_oracle(cuda_ok, dims, kchunk, jitter):
+    """Three scalar RHS (enthalpy + 2 species, one velocity) on the Kuhn box
+    (fpb_assemble_scalar3_kuhn): each field equals the oracle's SCALAR_RHS
+    with its own diffusivity."""
+    import paper_2107_11541_b200 as P
+
+    nx, ny, nz = dims
+    om = O.box(O.TET04, nx, ny, nz)
+    if jitter:
+        om.coords = _jitter(om.coords, nx, ny, nz, seed=7)
+    mesh, ctx = _ctx(P, nx, ny, nz, kchunk, om.coords if jitter else None)
+    assert ctx.groups[0].kuhn is not None
+    vel, sc = O.bench_fields(om.nnode, 3)
+    kap = (1e-2, 3e-2, 0.0)
+    phi3 = torch.as_tensor(np.stack(sc[:3]), device="cuda").contiguous()
+    out3 = torch.full((3, om.nnode), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.assemble_scalar_rhs3_d(torch.as_tensor(vel, device="cuda"), phi3, kap, out3)
+    got = out3.cpu().numpy()
+    for f in range(3):
+        want = O.assemble_rhs(om, "scalar_rhs", vel, sc[f], 1.0, 0.0, kap[f])
+        assert O.rel_diff(got[f], want) < TOL, (dims, kchunk, f)
+
+
+def test_kuhn_scalar3_matches_block_path(cuda_ok):
+    import paper_2107_11541_b200 as P
+    import paper_2107_11541_b200.assembly as A
+
+    mesh, ctx = _ctx(P, 94, 40, 37)
+    n = mesh.nnode
+    g = torch.Generator(device="cuda").manual_seed(9)
+    vel = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=g)
+    phi3 = torch.randn((3, n), dtype=torch.float64, device="cuda", generator=g)
+    a = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 2e-2, 3e-2), a)
+    c = torch.empty_like(a)
+    ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 2e-2, 3e-2), c)
+    assert torch.equal(a, c)
+    A.KUHN_MOMENTUM = False
+    try:
+        ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 2e-2, 3e-2), b)
+    finally:
+        A.KUHN_MOMENTUM = True
+    assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < TOL

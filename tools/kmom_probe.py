@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--kchunks", default="0")
     ap.add_argument("--blocks", type=int, default=1)
     ap.add_argument("--grad", type=int, default=0, help="also time B_x,B_y,B_z (Kuhn box vs colind path)")
+    ap.add_argument("--s3", type=int, default=0, help="also time the three-scalar RHS (Kuhn vs element blocks)")
     ap.add_argument("--overlap", default="", help="kmom_smem_kb values: time momentum + B_xyz sequential vs on two streams")
     ap.add_argument("--tune", default="", help="name=value[,name=value] passed to fpb_set_tuning")
     args = ap.parse_args()
@@ -84,6 +85,20 @@ def main():
                                          "bitwise_equal": bool(torch.equal(ga, gb))}
                 res[f"{sz}/grad_colind"] = {"ms": round(msc, 4), "Gelem_s": round(ne / msc / 1e6, 2)}
                 del ga, gb
+            if args.s3:
+                phi3 = torch.randn((3, n), dtype=torch.float64, device="cuda", generator=g)
+                o3 = torch.empty((3, n), dtype=torch.float64, device="cuda")
+                r3 = torch.empty_like(o3)
+                f3 = lambda: ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 1e-2, 1e-2), o3)  # noqa: E731
+                ms3 = timeit(f3, args.reps, flush)
+                A.KUHN_MOMENTUM = False
+                msb3 = timeit(lambda: ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 1e-2, 1e-2), r3), args.reps, flush)
+                A.KUHN_MOMENTUM = True
+                f3()
+                torch.cuda.synchronize()
+                res[f"{sz}/s3_kuhn"] = {"ms": round(ms3, 4), "rel_diff": float((o3 - r3).abs().max() / r3.abs().max())}
+                res[f"{sz}/s3_blocks"] = {"ms": round(msb3, 4)}
+                del phi3, o3, r3
             if args.overlap:
                 from paper_2107_11541_b200 import _lib
                 nnz = ctx.pattern.nnz
