@@ -300,6 +300,17 @@ __device__ __forceinline__ void tet_mom_adj(const double (&x)[4][3], const doubl
   tet_mom_adj_f(x, u, r, muW, [&](int a, int k, double v) { res[a][k] -= v; });
 }
 
+// 1/x from the hardware approximation plus two Newton steps (~2^-100 from the
+// ~2^-23 start, i.e. the FP64 result to within an ulp; no slow-path branch)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // The same residual from precomputed adjugate rows A (= rows of det J^-1),
 // det, the velocity differences du[b] = u_{b+1} - u_0 and u05 = 5 u_0 (so
 // that U + u_0 = u05 + sum_b du[b], U + u_a = that + du[a-1]).  Used by the
@@ -314,7 +325,7 @@ __device__ __forceinline__ void tet_mom_core(const double (&A)[3][3], double det
 #pragma unroll
     for (int k = 0; k < 3; ++k) G[l][k] = du[0][k] * A[0][l] + du[1][k] * A[1][l] + du[2][k] * A[2][l];
   const double divu = G[0][0] + G[1][1] + G[2][2];
-  const double f = muW / det;
+  const double f = muW * rcp_nr(det);
   double Mr[3][3], Sf[3][3];
 #pragma unroll
   for (int l = 0; l < 3; ++l)
@@ -372,7 +383,7 @@ __device__ __forceinline__ void tet_s3_adj(const double (&x)[4][3], const double
   cross3(E[2], E[0], A[1]);
   cross3(E[0], E[1], A[2]);
   const double det = dot3(E[0], A[0]);
-  const double inv = 1.0 / det;
+  const double inv = rcp_nr(det);
   double U[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) U[d] = (u[0][d] + u[1][d]) + (u[2][d] + u[3][d]);
