@@ -409,6 +409,28 @@ __host__ __device__ constexpr uint16_t kuhn_word(int i) {
   return t[i];
 }
 
+
+// acc += X[q] x X[r] with the pair taken in ascending order (the interior
+// stream holds every face pair twice, once per adjacent tet and in opposite
+// orders): the 36 distinct cross products become common subexpressions
+// the compiler evaluates once.  Used by every Kuhn-stream kernel, so they
+// stay bitwise equal to each other.
+__device__ __forceinline__ void kuhn_pair_acc(const double (&X)[kKuhnCols][3], int q, int r, double (&acc)[3]) {
+  const int a = q < r ? q : r, b = q < r ? r : q;  // compile-time after unrolling
+  const double c0 = X[a][1] * X[b][2] - X[a][2] * X[b][1];
+  const double c1 = X[a][2] * X[b][0] - X[a][0] * X[b][2];
+  const double c2 = X[a][0] * X[b][1] - X[a][1] * X[b][0];
+  if (q < r) {
+    acc[0] += c0;
+    acc[1] += c1;
+    acc[2] += c2;
+  } else {
+    acc[0] -= c0;
+    acc[1] -= c1;
+    acc[2] -= c2;
+  }
+}
+
 constexpr int kKuhnWarps = 2;  // warps (32-row slices) per CTA
 
 #ifndef FPB_KUHN_MINB
@@ -490,9 +512,7 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
   for (int i = 0; i < kKuhnWords; ++i) {
     const int w = kuhn_word(i);
     const int q = w & 0x7f, r = (w >> 7) & 0x7f;
-    acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
-    acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
-    acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+    kuhn_pair_acc(X, q, r, acc);
     if (w & (1 << 14)) {  // column finished
       const int cpos = target + (target >= dslot);
 #pragma unroll
@@ -643,9 +663,7 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
     for (int q8 = 0; q8 < kKuhnWords; ++q8) {
       const int w = kuhn_word(q8);
       const int q = w & 0x7f, r = (w >> 7) & 0x7f;
-      acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
-      acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
-      acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+      kuhn_pair_acc(X, q, r, acc);
       if (w & (1 << 14)) {  // column finished
         const int cpos = target + (target >= dslot);
 #pragma unroll
@@ -743,9 +761,7 @@ k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, in
                      2 * (cmin0(kuhn_off3(target, 1), kuhn_off3(q, 1), kuhn_off3(r, 1)) + 1) +
                      4 * (cmin0(kuhn_off3(target, 2), kuhn_off3(q, 2), kuhn_off3(r, 2)) + 1);
       if ((vcells >> cb) & 1u) {
-        acc[0] += X[q][1] * X[r][2] - X[q][2] * X[r][1];
-        acc[1] += X[q][2] * X[r][0] - X[q][0] * X[r][2];
-        acc[2] += X[q][0] * X[r][1] - X[q][1] * X[r][0];
+        kuhn_pair_acc(X, q, r, acc);
       }
       if ((cells >> cb) & 1u) any = true;
       if (w & (1 << 14)) {  // column finished
