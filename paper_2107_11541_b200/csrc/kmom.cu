@@ -113,7 +113,7 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
     for (int d = 0; d < 3; ++d) {
       e7[d] = x[d] - x0[d];
       d7[d] = u[d] - u0[d];
-      u05[d] = 5.0 * u0[d];
+      u05[d] = 5.0 * u0[d] + d7[d];  // 5 u_0 + (u_7 - u_0): the part of U + u_0 every tet shares
     }
   }
   auto edge = [&](int cc, double (&e)[3], double (&dv)[3]) {
@@ -145,8 +145,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d3[d];
       du[2][d] = d7[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d1[d] + d3[d]);
     const double det = dot3(e1, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 3 : 7, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 3 : 7, k, v); });
   }
   FPB_KMOM_TETBAR();
   double e5[3], d5[3];
@@ -163,8 +166,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d7[d];
       du[2][d] = d5[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d1[d] + d5[d]);
     const double det = dot3(e1, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 7 : 5, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 7 : 5, k, v); });
   }
   FPB_KMOM_TETBAR();
   double e4[3], d4[3], c74[3];
@@ -181,8 +187,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d5[d];
       du[2][d] = d7[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d4[d] + d5[d]);
     const double det = dot3(e4, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 5 : 7, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 5 : 7, k, v); });
   }
   FPB_KMOM_TETBAR();
   double e6[3], d6[3], c76[3];
@@ -199,8 +208,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d7[d];
       du[2][d] = d6[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d4[d] + d6[d]);
     const double det = dot3(e4, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 7 : 6, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 7 : 6, k, v); });
   }
   FPB_KMOM_TETBAR();
   double e2[3], d2[3], c72[3];
@@ -217,8 +229,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d6[d];
       du[2][d] = d7[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d2[d] + d6[d]);
     const double det = dot3(e2, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 6 : 7, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 6 : 7, k, v); });
   }
   FPB_KMOM_TETBAR();
   edge(3, e3, d3);  // reloaded (not held across the cell)
@@ -233,8 +248,11 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
       du[1][d] = d7[d];
       du[2][d] = d3[d];
     }
+    double w0[3];
+    #pragma unroll
+    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d2[d] + d3[d]);
     const double det = dot3(e2, A[0]);
-    tet_mom_core(A, det, du, u05, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 7 : 3, k, v); });
+    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 7 : 3, k, v); });
   }
 }
 

@@ -312,13 +312,13 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // The same residual from precomputed adjugate rows A (= rows of det J^-1),
-// det, the velocity differences du[b] = u_{b+1} - u_0 and u05 = 5 u_0 (so
-// that U + u_0 = u05 + sum_b du[b], U + u_a = that + du[a-1]).  Used by the
+// det, the velocity differences du[b] = u_{b+1} - u_0 and w0 = U + u_0 =
+// 5 u_0 + sum_b du[b] (so that U + u_a = w0 + du[a-1]).  Used by the
 // Kuhn-cell kernel (kmom.cu), where the cross products and differences
 // against the cell's shared nodes are computed once per cell.
 template <class Sub>
 __device__ __forceinline__ void tet_mom_core(const double (&A)[3][3], double det, const double (&du)[3][3],
-                                             const double (&u05)[3], double r, double muW, Sub&& sub) {
+                                             const double (&w0)[3], double r, double muW, Sub&& sub) {
   double G[3][3];
 #pragma unroll
   for (int l = 0; l < 3; ++l)
@@ -339,9 +339,6 @@ __device__ __forceinline__ void tet_mom_core(const double (&A)[3][3], double det
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int k = 0; k < 3; ++k) vs[a][k] = Sf[k][0] * A[a][0] + Sf[k][1] * A[a][1] + Sf[k][2] * A[a][2];
-  double w0[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) w0[d] = u05[d] + ((du[0][d] + du[1][d]) + du[2][d]);
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     double w[3];
