@@ -47,7 +47,7 @@ constexpr int kHbRec = 72;  // H planes per element: q = [k][l][s][4]
 #define FPB_HEXH_MINB 4
 #endif
 #ifndef FPB_HEXR_MINB
-#define FPB_HEXR_MINB 3
+#define FPB_HEXR_MINB 4  // 8 CTAs of 96 threads at 80 registers: C4 B_xyz 8.78 -> 8.53 ms (5: 64 registers, 11.4 ms)
 #endif
 __global__ void __launch_bounds__(128, FPB_HEXH_MINB)
 k_hex_h(int64_t nelem, const int32_t* __restrict__ conn, const double* __restrict__ xyz4, double* __restrict__ H) {
