@@ -83,6 +83,9 @@ struct KuhnGrid {
 #ifndef FPB_KMOM_SHARED
 #define FPB_KMOM_SHARED 1
 #endif
+#ifndef FPB_KMOM_S3_SHARED
+#define FPB_KMOM_S3_SHARED 1
+#endif
 #ifdef FPB_KMOM_TETBARRIER  // one tet's node loads at a time (A/B: tighter registers, slower without spills)
 #define FPB_KMOM_TETBAR() asm volatile("" ::: "memory")
 #else
@@ -94,165 +97,146 @@ struct KuhnGrid {
 // edge e7, so each tet after the first loads one new node and forms two new
 // cross products.  Edges / velocity differences against corner 0 (e_c, d_c),
 // adjugate rows from the crosses (tet_mom_core, simplex.cuh).
+template <int KIND>
 __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double* s1, double r, double muW,
-                                                 double (&bot)[4][3], double (&top)[4][3]) {
-  auto ld = [&](int cc, double (&x)[3], double (&u)[3]) {
-    const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * kmom_nc<0>() * 33 + (cc & 1);
+                                                 const double (&kW)[3], double (&bot)[4][3], double (&top)[4][3]) {
+  constexpr int NC = kmom_nc<KIND>();
+  struct Nd {  // differences of one corner against corner 0
+    double e[3], du[3], dp[3];
+  };
+  double x0[3], u0[3], p0[3], u05[3];
+  auto ldc = [&](int cc, double (&x)[3], double (&u)[3], double (&ph)[3]) {
+    const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * NC * 33 + (cc & 1);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       x[d] = sp[d * 33];
       u[d] = sp[(3 + d) * 33];
+      ph[d] = KIND ? sp[(6 + d) * 33] : 0.0;
     }
   };
-  double x0[3], u0[3], e7[3], d7[3], u05[3];
-  {
-    double x[3], u[3];
-    ld(0, x0, u0);
-    ld(7, x, u);
+  auto node = [&](int cc, Nd& n) {
+    double x[3], u[3], ph[3];
+    ldc(cc, x, u, ph);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      e7[d] = x[d] - x0[d];
-      d7[d] = u[d] - u0[d];
-      u05[d] = 5.0 * u0[d] + d7[d];  // 5 u_0 + (u_7 - u_0): the part of U + u_0 every tet shares
-    }
-  }
-  auto edge = [&](int cc, double (&e)[3], double (&dv)[3]) {
-    double x[3], u[3];
-    ld(cc, x, u);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      e[d] = x[d] - x0[d];
-      dv[d] = u[d] - u0[d];
+      n.e[d] = x[d] - x0[d];
+      n.du[d] = u[d] - u0[d];
+      n.dp[d] = KIND ? ph[d] - p0[d] : 0.0;
     }
   };
-  // corner of local node a for each tet: (0, p, q, 7) or (0, p, 7, q)
+  Nd n7;
+  ldc(0, x0, u0, p0);
+  node(7, n7);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) u05[d] = 5.0 * u0[d] + n7.du[d];  // 5 u_0 + (u_7 - u_0): shared by every tet's U + u_0
   auto acc = [&](int cc, int k, double v) {
     if (cc & 4) top[cc & 3][k] -= v;
     else bot[cc & 3][k] -= v;
   };
-  double e1[3], d1[3], e3[3], d3[3], c71[3], c75[3];
-  edge(1, e1, d1);
-  edge(3, e3, d3);
-  {  // T0 (0, 1, 3, 7): E = (e1, e3, e7)
-    double A[3][3], du[3][3];
-    cross3(e3, e7, A[0]);
-    cross3(e7, e1, A[1]);
-    cross3(e1, e3, A[2]);
+  // one tet: local nodes 1..3 = (na, nb, nc) at corners (ca, cb, cc); the two
+  // that are not corner 7 are (p, q) in local order
+  auto tet = [&](const double (&A)[3][3], double det, const Nd& na, const Nd& nb, const Nd& nc, const Nd& np,
+                 const Nd& nq, int ca, int cb, int cc) {
+    double du[3][3], w0[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      c71[d] = A[1][d];
-      du[0][d] = d1[d];
-      du[1][d] = d3[d];
-      du[2][d] = d7[d];
+      du[0][d] = na.du[d];
+      du[1][d] = nb.du[d];
+      du[2][d] = nc.du[d];
+      w0[d] = u05[d] + (np.du[d] + nq.du[d]);
     }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d1[d] + d3[d]);
-    const double det = dot3(e1, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 3 : 7, k, v); });
+    auto sub = [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? ca : a == 2 ? cb : cc, k, v); };
+    if constexpr (KIND) {
+      double dp[3][3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        dp[f][0] = na.dp[f];
+        dp[f][1] = nb.dp[f];
+        dp[f][2] = nc.dp[f];
+      }
+      tet_s3_core(A, det, du, dp, w0, r, kW, sub);
+    } else {
+      tet_mom_core(A, det, du, w0, r, muW, sub);
+    }
+  };
+  Nd n1, n3;
+  double c71[3], c75[3], c74[3], c76[3], c72[3];
+  node(1, n1);
+  node(3, n3);
+  {  // T0 (0, 1, 3, 7): E = (e1, e3, e7)
+    double A[3][3];
+    cross3(n3.e, n7.e, A[0]);
+    cross3(n7.e, n1.e, A[1]);
+    cross3(n1.e, n3.e, A[2]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) c71[d] = A[1][d];
+    tet(A, dot3(n1.e, A[0]), n1, n3, n7, n1, n3, 1, 3, 7);
   }
   FPB_KMOM_TETBAR();
-  double e5[3], d5[3];
-  edge(5, e5, d5);
+  Nd n5;
+  node(5, n5);
   {  // T3 (0, 1, 7, 5): E = (e1, e7, e5)
-    double A[3][3], du[3][3];
-    cross3(e7, e5, A[0]);
-    cross3(e5, e1, A[1]);
+    double A[3][3];
+    cross3(n7.e, n5.e, A[0]);
+    cross3(n5.e, n1.e, A[1]);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       c75[d] = A[0][d];
       A[2][d] = -c71[d];
-      du[0][d] = d1[d];
-      du[1][d] = d7[d];
-      du[2][d] = d5[d];
     }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d1[d] + d5[d]);
-    const double det = dot3(e1, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 1 : a == 2 ? 7 : 5, k, v); });
+    tet(A, dot3(n1.e, A[0]), n1, n7, n5, n1, n5, 1, 7, 5);
   }
   FPB_KMOM_TETBAR();
-  double e4[3], d4[3], c74[3];
-  edge(4, e4, d4);
+  Nd n4;
+  node(4, n4);
   {  // T2 (0, 4, 5, 7): E = (e4, e5, e7)
-    double A[3][3], du[3][3];
-    cross3(e7, e4, A[1]);
-    cross3(e4, e5, A[2]);
+    double A[3][3];
+    cross3(n7.e, n4.e, A[1]);
+    cross3(n4.e, n5.e, A[2]);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       A[0][d] = -c75[d];
       c74[d] = A[1][d];
-      du[0][d] = d4[d];
-      du[1][d] = d5[d];
-      du[2][d] = d7[d];
     }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d4[d] + d5[d]);
-    const double det = dot3(e4, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 5 : 7, k, v); });
+    tet(A, dot3(n4.e, A[0]), n4, n5, n7, n4, n5, 4, 5, 7);
   }
   FPB_KMOM_TETBAR();
-  double e6[3], d6[3], c76[3];
-  edge(6, e6, d6);
+  Nd n6;
+  node(6, n6);
   {  // T4 (0, 4, 7, 6): E = (e4, e7, e6)
-    double A[3][3], du[3][3];
-    cross3(e7, e6, A[0]);
-    cross3(e6, e4, A[1]);
+    double A[3][3];
+    cross3(n7.e, n6.e, A[0]);
+    cross3(n6.e, n4.e, A[1]);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       c76[d] = A[0][d];
       A[2][d] = -c74[d];
-      du[0][d] = d4[d];
-      du[1][d] = d7[d];
-      du[2][d] = d6[d];
     }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d4[d] + d6[d]);
-    const double det = dot3(e4, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 4 : a == 2 ? 7 : 6, k, v); });
+    tet(A, dot3(n4.e, A[0]), n4, n7, n6, n4, n6, 4, 7, 6);
   }
   FPB_KMOM_TETBAR();
-  double e2[3], d2[3], c72[3];
-  edge(2, e2, d2);
+  Nd n2;
+  node(2, n2);
   {  // T1 (0, 2, 6, 7): E = (e2, e6, e7)
-    double A[3][3], du[3][3];
-    cross3(e7, e2, A[1]);
-    cross3(e2, e6, A[2]);
+    double A[3][3];
+    cross3(n7.e, n2.e, A[1]);
+    cross3(n2.e, n6.e, A[2]);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       A[0][d] = -c76[d];
       c72[d] = A[1][d];
-      du[0][d] = d2[d];
-      du[1][d] = d6[d];
-      du[2][d] = d7[d];
     }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d2[d] + d6[d]);
-    const double det = dot3(e2, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 6 : 7, k, v); });
+    tet(A, dot3(n2.e, A[0]), n2, n6, n7, n2, n6, 2, 6, 7);
   }
   FPB_KMOM_TETBAR();
-  edge(3, e3, d3);  // reloaded (not held across the cell)
+  node(3, n3);  // reloaded (not held across the cell)
   {  // T5 (0, 2, 7, 3): E = (e2, e7, e3)
-    double A[3][3], du[3][3];
-    cross3(e7, e3, A[0]);
-    cross3(e3, e2, A[1]);
+    double A[3][3];
+    cross3(n7.e, n3.e, A[0]);
+    cross3(n3.e, n2.e, A[1]);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      A[2][d] = -c72[d];
-      du[0][d] = d2[d];
-      du[1][d] = d7[d];
-      du[2][d] = d3[d];
-    }
-    double w0[3];
-    #pragma unroll
-    for (int d = 0; d < 3; ++d) w0[d] = u05[d] + (d2[d] + d3[d]);
-    const double det = dot3(e2, A[0]);
-    tet_mom_core(A, det, du, w0, r, muW, [&](int a, int k, double v) { acc(a == 0 ? 0 : a == 1 ? 2 : a == 2 ? 7 : 3, k, v); });
+    for (int d = 0; d < 3; ++d) A[2][d] = -c72[d];
+    tet(A, dot3(n2.e, A[0]), n2, n7, n3, n2, n3, 2, 7, 3);
   }
 }
 
@@ -388,7 +372,9 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
     if (cell && t < ke) {
       const double* s0 = stg + (t % 3) * 2 * NC * 33 + lane;
       const double* s1 = stg + ((t + 1) % 3) * 2 * NC * 33 + lane;
-      if constexpr (KIND) {  // three scalars: tet by tet
+      if constexpr (KIND && FPB_KMOM_S3_SHARED) {  // three scalars, shared-node cell cycle
+        kuhn_cell_shared<1>(s0, s1, r, muW, kW, bot, top);
+      } else if constexpr (KIND) {  // three scalars: tet by tet
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt) {
           asm volatile("" ::: "memory");  // one tet's node loads at a time (register pressure)
@@ -412,7 +398,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
         }
       } else {
 #if FPB_KMOM_SHARED
-        kuhn_cell_shared(s0, s1, r, muW, bot, top);
+        kuhn_cell_shared<0>(s0, s1, r, muW, kW, bot, top);
 #else
 #pragma unroll
         for (int tt = 0; tt < 6; ++tt) {

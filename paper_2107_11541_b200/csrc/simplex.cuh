@@ -405,4 +405,32 @@ __device__ __forceinline__ void tet_s3_adj(const double (&x)[4][3], const double
   }
 }
 
+// Three scalar residuals from precomputed adjugate rows A, det, the
+// differences du[b] = u_{b+1} - u_0 and dp[f][b] = phi_f,b+1 - phi_f,0, and
+// w0 = U + u_0 (the Kuhn-cell form of tet_s3_adj: same terms, shared
+// differences and crosses).  sub(a, f, v) subtracts v from node a, field f.
+template <class Sub>
+__device__ __forceinline__ void tet_s3_core(const double (&A)[3][3], double det, const double (&du)[3][3],
+                                            const double (&dp)[3][3], const double (&w0)[3], double r,
+                                            const double (&kW)[3], Sub&& sub) {
+  const double inv = rcp_nr(det);
+#pragma unroll
+  for (int f = 0; f < 3; ++f) {
+    double gp[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) gp[l] = dp[f][0] * A[0][l] + dp[f][1] * A[1][l] + dp[f][2] * A[2][l];
+    const double fk = kW[f] * inv;
+    const double wg = w0[0] * gp[0] + w0[1] * gp[1] + w0[2] * gp[2];
+    double dif[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) dif[b] = gp[0] * A[b][0] + gp[1] * A[b][1] + gp[2] * A[b][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double adv = a == 0 ? wg : wg + (du[a - 1][0] * gp[0] + du[a - 1][1] * gp[1] + du[a - 1][2] * gp[2]);
+      const double df = a == 0 ? -((dif[0] + dif[1]) + dif[2]) : dif[a - 1];
+      sub(a, f, fma(r, adv, fk * df));
+    }
+  }
+}
+
 }  // namespace fpb
