@@ -149,13 +149,18 @@ int fpb_assemble(int kind, int etype, int64_t nelem, const int32_t* lane_conn,
  *   generic rows in blocks of 32: gblk_rows[ngblocks][32] (row or -1),
  *   ginc[ngblocks][maxinc][32] (element id or -1), gslot[ngblocks][maxinc][32]
  *   (uint2 relative-corner slot bytes: byte 0 = corner sign bits p of the
- *   row's node, byte d = off-diagonal slot of corner p ^ d). */
+ *   row's node, byte d = off-diagonal slot of corner p ^ d).
+ *   box_nx, box_ny > 0: the mesh is the generator's hex box with nx x ny
+ *   cells per layer and every canonical row's canon_inc8 equals
+ *   (i-1+mx) + nx ((j-1+my) + ny (k-1+mz)) (the caller verified it): the
+ *   kernel computes the element ids instead of reading canon_inc8. */
 int fpb_hex_canon_slots(int32_t* slots_h /* [8][8] */);
 int fpb_hex_gradient_h(int64_t nelem, const int32_t* conn, const double* xyz4, double* H, void* stream);
 int fpb_hex_gradient_rows(int32_t ncanon, const int32_t* canon_rows, const int32_t* canon_inc8, int32_t ngblocks,
                           int maxinc, int rowcap, const int32_t* gblk_rows, const int32_t* ginc,
                           const uint32_t* gslot, const double* H, int64_t nelem, const int32_t* rowptr,
-                          const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream);
+                          const int32_t* colind, int64_t nnz, int accumulate, double* out, int box_nx, int box_ny,
+                          void* stream);
 
 /* ---- multi-GPU: NCCL halo sum and allreduce (halo.cu) ----
  * The compiled entry points of the z-slab decomposition.  NCCL is loaded at

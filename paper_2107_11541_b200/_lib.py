@@ -61,7 +61,7 @@ SIGNATURES = {
     "fpb_hex_canon_slots": (_int, [_vp]),
     "fpb_hex_gradient_h": (_int, [_i64, _vp, _vp, _vp, _vp]),
     "fpb_hex_gradient_rows": (_int, [_i32, _vp, _vp, _i32, _int, _int, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _int,
-                                     _vp, _vp]),
+                                     _vp, _int, _int, _vp]),
     "fpb_incidence_build": (_int, [_i32, _i64, _int, _vp, _vp, _vp, _pi64, _vp]),
     "fpb_incidence_slots": (_int, [_i32, _int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp]),
     "fpb_pack4": (_int, [_i64, _int, _vp, _vp, _vp, _vp]),

@@ -96,6 +96,7 @@ _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # False = the per-row kernel (rowsq.cu)
 HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
 HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))
+HEX_BOX_IDS = os.environ.get("FPB_HEX_BOX_IDS", "1") != "0"  # hex box: canonical rows' element ids computed
 # element blocks of the RHS kernels over Morton-ordered elements (BlockPlan);
 # slab domains keep natural order (their interface windows are block ranges)
 # TET04 momentum RHS on a Kuhn box mesh by z-marching cell lines (kmom.cu)
@@ -318,6 +319,23 @@ class HexRowPlan:
         self.canon_rows = crow.to(torch.int32).contiguous()
         self.canon_inc8 = inc[crow].t().contiguous().to(torch.int32) if self.ncanon else \
             torch.empty(8, dtype=torch.int32, device=dev)
+        # the generator's hex box: every canonical row's 8 element ids are
+        # (i-1+mx) + nx ((j-1+my) + ny (k-1+mz)) of its node (i, j, k) —
+        # verified here for every canonical row; then the kernel computes
+        # them instead of reading canon_inc8
+        self.box = (0, 0)
+        if self.ncanon and HEX_BOX_IDS:
+            c8 = self.canon_inc8.to(torch.int64)
+            bnx = int(c8[2, 0] - c8[0, 0])
+            nxny = int(c8[4, 0] - c8[0, 0])
+            if bnx >= 1 and nxny % bnx == 0 and nxny // bnx >= 1:
+                bny = nxny // bnx
+                r64 = crow.to(torch.int64)
+                ii, jj, kk = r64 % (bnx + 1), (r64 // (bnx + 1)) % (bny + 1), r64 // ((bnx + 1) * (bny + 1))
+                m = torch.arange(8, device=dev, dtype=torch.int64)[:, None]
+                want = (ii - 1 + (m & 1)) + bnx * ((jj - 1 + ((m >> 1) & 1)) + bny * (kk - 1 + (m >> 2)))
+                if torch.equal(want, c8):
+                    self.box = (bnx, bny)
         grow = torch.nonzero(~canon).flatten()
         R = self.GEN_ROWS
         self.ngblocks = -(-int(grow.numel()) // R)
@@ -338,7 +356,8 @@ class HexRowPlan:
         _lib.call("fpb_hex_gradient_rows", self.ncanon, self.canon_rows.data_ptr(), self.canon_inc8.data_ptr(),
                   self.ngblocks, self.maxinc, self.rowcap, self.gblk_rows.data_ptr(), self.ginc.data_ptr(),
                   self.gslot.data_ptr(), self.H.data_ptr(), self.nelem, pattern.rowptr_d.data_ptr(),
-                  pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), s)
+                  pattern.colind_d.data_ptr(), pattern.nnz, accumulate, out.data_ptr(), self.box[0],
+                  self.box[1], s)
 
 
 def _centroid_morton(conn_d: torch.Tensor, coords_d: torch.Tensor) -> torch.Tensor:

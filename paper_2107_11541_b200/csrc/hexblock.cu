@@ -164,11 +164,11 @@ __host__ __device__ constexpr int hb_canon_slot(int m, int d) {
 // ---- canonical rows: thread per (row, k), R rows per CTA ---------------------
 int g_tuning_hex_canon_rows = 32;  // fpb_set_tuning("hex_canon_rows", 32 | 64)
 
-template <int R, bool ACC>
+template <int R, bool ACC, bool BOX>
 __global__ void __launch_bounds__(3 * R, R == 32 ? 2 * FPB_HEXR_MINB : FPB_HEXR_MINB)
 k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ inc8,
                  const double* __restrict__ H, int64_t nelem, const int32_t* __restrict__ rowptr, int64_t nnz,
-                 double* __restrict__ out) {
+                 double* __restrict__ out, int bnx = 0, int bny = 0) {
   constexpr int NT = 3 * R;
   __shared__ double stage[3][R][27];  // the CTA's output rows, for coalesced stores
   __shared__ int rlo_s[R];
@@ -177,9 +177,17 @@ k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t*
   const int nr = min(R, nrows - i0);
   if (r < nr) {
     int el[8];
+    const int row = __ldg(rows + i);
+    if constexpr (BOX) {  // element ids of the generator's hex box (verified by the caller)
+      const int ii = row % (bnx + 1), rj = row / (bnx + 1), jj = rj % (bny + 1), kk = rj / (bny + 1);
+      const int e0 = (ii - 1) + bnx * ((jj - 1) + bny * (kk - 1));
 #pragma unroll
-    for (int m = 0; m < 8; ++m) el[m] = __ldg(inc8 + (int64_t)m * nrows + i);
-    if (k == 0) rlo_s[r] = __ldg(rowptr + __ldg(rows + i));
+      for (int m = 0; m < 8; ++m) el[m] = e0 + (m & 1) + bnx * (((m >> 1) & 1) + bny * (m >> 2));
+    } else {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) el[m] = __ldg(inc8 + (int64_t)m * nrows + i);
+    }
+    if (k == 0) rlo_s[r] = __ldg(rowptr + row);
     double a27[27];
 #pragma unroll
     for (int j = 0; j < 27; ++j) a27[j] = 0.0;
@@ -322,18 +330,25 @@ int fpb_hex_gradient_h(int64_t nelem, const int32_t* conn, const double* xyz4, d
 int fpb_hex_gradient_rows(int32_t ncanon, const int32_t* canon_rows, const int32_t* canon_inc8, int32_t ngblocks,
                           int maxinc, int rowcap, const int32_t* gblk_rows, const int32_t* ginc,
                           const uint32_t* gslot, const double* H, int64_t nelem, const int32_t* rowptr,
-                          const int32_t* colind, int64_t nnz, int accumulate, double* out, void* stream) {
+                          const int32_t* colind, int64_t nnz, int accumulate, double* out, int box_nx, int box_ny,
+                          void* stream) {
   FPB_REQUIRE(ngblocks == 0 || (rowcap >= 2 && rowcap <= 256), "row length %d out of range", rowcap);
   cudaStream_t s = as_stream(stream);
   if (ncanon > 0) {
     const int R = g_tuning_hex_canon_rows == 32 ? 32 : 64;
     const unsigned grid = (unsigned)((ncanon + R - 1) / R);
-#define FPB_HC(RR, AA) \
-  k_hex_rows_canon<RR, AA><<<grid, 3 * RR, 0, s>>>(ncanon, canon_rows, canon_inc8, H, nelem, rowptr, nnz, out)
+#define FPB_HC(RR, AA, BB)                                                                                  \
+  k_hex_rows_canon<RR, AA, BB><<<grid, 3 * RR, 0, s>>>(ncanon, canon_rows, canon_inc8, H, nelem, rowptr, nnz, out, \
+                                                       box_nx, box_ny)
+    const bool box = box_nx > 0 && box_ny > 0;
     if (R == 32) {
-      if (accumulate) FPB_HC(32, true); else FPB_HC(32, false);
+      if (box) {
+        if (accumulate) FPB_HC(32, true, true); else FPB_HC(32, false, true);
+      } else {
+        if (accumulate) FPB_HC(32, true, false); else FPB_HC(32, false, false);
+      }
     } else {
-      if (accumulate) FPB_HC(64, true); else FPB_HC(64, false);
+      if (accumulate) FPB_HC(64, true, false); else FPB_HC(64, false, false);
     }
 #undef FPB_HC
     FPB_LAUNCH_CHECK();

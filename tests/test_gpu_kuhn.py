@@ -201,3 +201,36 @@ def test_kuhn_scalar3_matches_block_path(cuda_ok):
     finally:
         A.KUHN_MOMENTUM = True
     assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < TOL
+
+
+def test_hex_box_element_ids_bitwise_equal_listed_ids(cuda_ok):
+    """HEX08 continuity on the generator's hex box: the canonical-row kernel
+    with element ids computed from the node (HexRowPlan.box) gives bitwise
+    the values of the kernel reading them from canon_inc8, and the oracle's
+    (jittered coordinates)."""
+    import paper_2107_11541_b200 as P
+    import paper_2107_11541_b200.assembly as A
+
+    dims = (12, 9, 7)
+    om = O.box(O.HEX08, *dims)
+    om.coords = _jitter(om.coords, *dims, seed=5)
+    mesh = P.generate_box_mesh(P.ElementType.HEX08, *dims)
+    mesh.coords = om.coords
+    res = {}
+    for flag in (True, False):
+        A.HEX_BOX_IDS = flag
+        try:
+            ctx = P.AssemblyContext.build(mesh, vector_size=8)
+            out = torch.empty(3 * ctx.pattern.nnz, dtype=torch.float64, device="cuda")
+            ctx.assemble_gradients_d(out)
+            res[flag] = (out.cpu().numpy(), ctx.groups[0].hexrows.box)
+        finally:
+            A.HEX_BOX_IDS = True
+    assert res[True][1] == (12, 9) and res[False][1] == (0, 0)
+    assert np.array_equal(res[True][0], res[False][0])
+    nnz = res[True][0].size // 3
+    for k in range(3):
+        e = np.zeros((om.nnode, 3))
+        e[:, k] = 1.0
+        _, _, vo = O.assemble_matrix(om, "convection", e)
+        assert O.rel_diff(res[True][0][k * nnz:(k + 1) * nnz], vo) < TOL
