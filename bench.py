@@ -771,9 +771,10 @@ def main():
         phases["note"] = ("max over ranks of each phase's median: interface windows first, halo (NCCL send/recv "
                           "of interface RHS rows + CSR row segments) on a side stream, interior meanwhile"
                           if kb0 is None else
-                          "max over ranks of each phase's median: 'interface' = the whole-slab Kuhn-box kernels, "
-                          "then the halo (NCCL send/recv of interface RHS rows + CSR row segments); no interior "
-                          "phase (interior_ms includes the halo)")
+                          "max over ranks of each phase's median: 'interface' = the Kuhn-box momentum kernel + "
+                          "the B_xyz surface rows (which hold the interface planes), then the halo (NCCL send/recv "
+                          "of interface RHS rows + CSR row segments) on a side stream while the interior B_xyz "
+                          "lines run")
         for _ in range(5):
             flush.fill_(1.0)
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -912,11 +913,13 @@ def main():
             "multi_gpu": None if sub is None else {
                 "halo": "compiled NCCL (halo.cu fpb_halo_exchange), one communicator per rank"
                 if sub.native is not None else f"torch.distributed ({dist.get_backend()}), host-staged",
-                "timed_step": ("one CUDA graph per step (Kuhn-box slab kernels, then the NCCL halo)"
+                "timed_step": ("one CUDA graph per step (Kuhn-box slab kernels: momentum + B_xyz surface rows, "
+                               "then the NCCL halo on a side stream while the interior lines run)"
                                if graph.single_graph and kb0 is not None else
                                "one CUDA graph per step (interface windows, NCCL halo on a side stream, interior)"
                                if graph.single_graph else
-                               "one CUDA graph (Kuhn-box slab kernels), eager halo after" if kb0 is not None else
+                               "two CUDA graphs (Kuhn-box momentum + surface rows / interior lines), eager halo "
+                               "between" if kb0 is not None else
                                "two CUDA graphs (interface / interior windows), eager halo between"),
                 "kernels": "Kuhn-box slab kernels over the own cell layers (kmom.cu, pairs.cu)" if kb0 is not None
                 else "windowed element-block / row kernels"},

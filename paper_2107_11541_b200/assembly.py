@@ -732,19 +732,26 @@ class AssemblyContext:
                 kb = g.kuhn
                 _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk, xyz4, vp,
                           float(rho), float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
-            elif own and single_rows and window is None and g.kuhn is not None and g.kuhn.pattern_ok \
-                    and kind_id == GRADIENT_XYZ and KUHN_BOX_GRADIENT and g.kuhn.nx > 1 and g.kuhn.ny > 1:
-                # B_x, B_y, B_z on the Kuhn box: interior lines + boundary rows, ghost planes zero
+            elif own and single_rows and (window is None or "kuhn_part" in window) and g.kuhn is not None \
+                    and g.kuhn.pattern_ok and kind_id == GRADIENT_XYZ and KUHN_BOX_GRADIENT and g.kuhn.nx > 1 \
+                    and g.kuhn.ny > 1:
+                # B_x, B_y, B_z on the Kuhn box: interior lines + the surface rows
+                # (boundary ring and the kc0 / kc1 planes; ghost planes zero);
+                # window {"kuhn_part": "lines" | "surface"} runs one of the two
+                # (the slab step sums the interface planes while the lines run)
                 kb = g.kuhn
+                part = window.get("kuhn_part") if window else None
                 rp_ = self.pattern.rowptr_d.data_ptr()
-                _lib.call("fpb_assemble_gradient_kuhn_lines", kb.nx, kb.ny, kb.nz, kb.kc0 + 1, kb.kc1 - 1, xyz4, rp_,
-                          nnz, 0, out.data_ptr(), _lib.stream())
-                br = kb.boundary_rows(out.device)
-                _lib.call("fpb_assemble_gradient_kuhn_boundary", int(br.numel()), br.data_ptr(), kb.nx, kb.ny, kb.nz,
-                          kb.kc0, kb.kc1, xyz4, rp_, nnz, 0, out.data_ptr(), _lib.stream())
-                for a0, a1 in kb.zero_ranges(self.pattern.rowptr_d):
-                    for m in range(3):
-                        out[m * nnz + a0:m * nnz + a1].zero_()
+                if part in (None, "lines"):
+                    _lib.call("fpb_assemble_gradient_kuhn_lines", kb.nx, kb.ny, kb.nz, kb.kc0 + 1, kb.kc1 - 1, xyz4,
+                              rp_, nnz, 0, out.data_ptr(), _lib.stream())
+                if part in (None, "surface"):
+                    br = kb.boundary_rows(out.device)
+                    _lib.call("fpb_assemble_gradient_kuhn_boundary", int(br.numel()), br.data_ptr(), kb.nx, kb.ny,
+                              kb.nz, kb.kc0, kb.kc1, xyz4, rp_, nnz, 0, out.data_ptr(), _lib.stream())
+                    for a0, a1 in kb.zero_ranges(self.pattern.rowptr_d):
+                        for m in range(3):
+                            out[m * nnz + a0:m * nnz + a1].zero_()
             elif own and not matrix and g.blocks is not None:
                 bp = g.blocks
                 nv = self.mesh.dim if kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] else 1

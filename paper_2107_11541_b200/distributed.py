@@ -589,9 +589,10 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
 
     ctx = dom.ctx
     K = KernelKind.MOMENTUM_RHS
+    if overlap and dom.layout.world > 1 and ctx.groups[0].kuhn is not None:
+        return _kuhn_slab_step(dom, vel, rhs, mats, rho, mu, side, events)
     if not overlap or dom.layout.world == 1 or ctx.groups[0].kuhn is not None:
-        # plain sequence (also the Kuhn-box slab step: whole-slab kernels,
-        # then the halo; per-phase events with an empty interior phase)
+        # plain sequence (per-phase events with an empty interior phase)
         ev = None
         if events is not None:
             ev = {k: torch.cuda.Event(enable_timing=True)
@@ -651,6 +652,41 @@ def assemble_step(dom: "SlabDomain", vel: torch.Tensor, rhs: torch.Tensor, mats:
     return rhs, mats
 
 
+def _kuhn_slab_step(dom, vel, rhs, mats, rho, mu, side=None, events=None):
+    """Kuhn-box slab step: momentum (whole slab), the B_xyz surface rows
+    (which hold the interface planes), then the halo sums on a side stream
+    while the interior lines run.  Bitwise the plain sequence's result (the
+    halo touches interface rows only, the lines kernel never does)."""
+    from .assembly import KernelKind
+
+    ctx = dom.ctx
+    main = torch.cuda.current_stream()
+    ev = None
+    if events is not None:
+        ev = {k: torch.cuda.Event(enable_timing=True)
+              for k in ("start", "interface_done", "halo_start", "halo_done", "interior_done")}
+        events.update(ev)
+        ev["start"].record(main)
+    ctx.assemble_rhs_d(KernelKind.MOMENTUM_RHS, vel, None, rho, mu, 0.0, rhs)
+    ctx.assemble_gradients_d(mats, {"kuhn_part": "surface"})
+    if ev:
+        ev["interface_done"].record(main)
+    side = side or torch.cuda.Stream()
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        if ev:
+            ev["halo_start"].record(side)
+        dom.halo_sum_rhs(rhs)
+        dom.halo_sum_matrix(mats, ctx.mesh.dim)
+        if ev:
+            ev["halo_done"].record(side)
+    ctx.assemble_gradients_d(mats, {"kuhn_part": "lines"})
+    if ev:
+        ev["interior_done"].record(main)
+    main.wait_stream(side)
+    return rhs, mats
+
+
 class SlabStepGraph:
     """One decomposed NS step (assemble_step) replayed from CUDA graphs.
 
@@ -680,11 +716,13 @@ class SlabStepGraph:
             self.whole = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.whole, stream=cap):
                 assemble_step(dom, vel, rhs, mats, rho, mu, overlap=True, side=self.side)
-        elif ctx.groups[0].kuhn is not None:  # Kuhn-box slab: the whole assembly, then the eager halo
-            self.phase_a = torch.cuda.CUDAGraph()
+        elif ctx.groups[0].kuhn is not None:  # Kuhn-box slab: momentum + surface rows, eager halo, lines
+            self.phase_a, self.phase_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.phase_a, stream=cap):
                 ctx.assemble_rhs_d(K, vel, None, rho, mu, 0.0, rhs)
-                ctx.assemble_gradients_d(mats)
+                ctx.assemble_gradients_d(mats, {"kuhn_part": "surface"})
+            with torch.cuda.graph(self.phase_b, stream=cap):
+                ctx.assemble_gradients_d(mats, {"kuhn_part": "lines"})
         else:
             w = _step_windows(dom)
             self.phase_a, self.phase_b = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
