@@ -397,6 +397,15 @@ int fpb_assemble_momentum_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kch
 int fpb_assemble_scalar3_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
                               const double* vel, const double* phi3, int64_t fstride, double kappa0, double kappa1,
                               double kappa2, double* scratch, double* out3, void* stream);
+/* The same pencils on the generator's HEX08 box (one Q1 hex per cell,
+ * generate_box_mesh(HEX08, nx, ny, nz), mesh.py:265-267; the caller checks
+ * the connectivity against fpb_box_conn): kind FPB_MOMENTUM_RHS (out[n][3],
+ * rho, mu; phi3 NULL) or 101 = the three scalars (phi3 / out[3][fstride],
+ * diffusivities rho, mu, kappa), momentum_rhs_packed / scalar_rhs_packed
+ * (_kernels.py:320-382, :420-461) through the Walsh forms of elemcore.cuh. */
+int fpb_assemble_rhs_hexbox(int kind, int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                            const double* vel, const double* phi3, int64_t fstride, double rho, double mu,
+                            double kappa, double* scratch, double* out, void* stream);
 
 /* ---- solver vector kernels (sparse.py:78-130, krylov.py) -------------- */
 

@@ -46,6 +46,8 @@ SIGNATURES = {
     "fpb_allreduce_sum": (_int, [_vp, _vp, _i64, _vp]),
     "fpb_pair_canon_set": (_int, [_vp, _int]),
     "fpb_kuhn_mom_scratch_len": (_i64, [_int, _int, _int]),
+    "fpb_assemble_rhs_hexbox": (_int, [_int, _int, _int, _int, _int, _int, _int, _vp, _vp, _vp, _i64, _dbl, _dbl, _dbl,
+                                       _vp, _vp, _vp]),
     "fpb_assemble_scalar3_kuhn": (_int, [_int, _int, _int, _int, _int, _int, _vp, _vp, _vp, _i64, _dbl, _dbl, _dbl, _vp,
                                          _vp, _vp]),
     "fpb_assemble_momentum_kuhn": (_int, [_int, _int, _int, _int, _int, _int, _vp, _vp, _dbl, _dbl, _vp, _vp, _vp]),

@@ -96,7 +96,8 @@ _PAIR_CANON_LOADED = None  # the canonical stream currently in constant memory
 # False = the per-row kernel (rowsq.cu)
 HEX_ONCE = os.environ.get("FPB_HEX_ONCE", "1") != "0"
 HEX_BAND = int(os.environ.get("FPB_HEX_BAND", "32"))
-HEX_BOX_IDS = os.environ.get("FPB_HEX_BOX_IDS", "1") != "0"  # hex box: canonical rows' element ids computed
+HEX_BOX_IDS = os.environ.get("FPB_HEX_BOX_IDS", "1") != "0"
+HEX_BOX_RHS = os.environ.get("FPB_HEX_BOX_RHS", "1") != "0"  # HEX08 box: RHS kinds by z-marching cell pencils  # hex box: canonical rows' element ids computed
 # element blocks of the RHS kernels over Morton-ordered elements (BlockPlan);
 # slab domains keep natural order (their interface windows are block ranges)
 # TET04 momentum RHS on a Kuhn box mesh by z-marching cell lines (kmom.cu)
@@ -387,8 +388,9 @@ class KuhnBox:
     plus box-masked boundary rows (pairs.cu) — no per-element metadata."""
 
     def __init__(self, nx: int, ny: int, nz: int, dev, kc0: int = 0, kc1: int | None = None,
-                 pattern_ok: bool = True):
+                 pattern_ok: bool = True, etype: "ElementType | None" = None):
         self.nx, self.ny, self.nz = nx, ny, nz
+        self.etype = etype or ElementType.TET04  # TET04: Kuhn box; HEX08: one Q1 hex per cell
         self.kc0, self.kc1 = kc0, nz if kc1 is None else kc1
         self.pattern_ok = pattern_ok
         # CTAs are 32 x 8 cell pencils, one per SM; the z-chunk minimises
@@ -441,6 +443,30 @@ class KuhnBox:
                 out.append((int(rowptr_d[plane * (self.kc1 + 1)]), int(rowptr_d[-1])))
             self._zero = out
         return self._zero
+
+    @staticmethod
+    def detect_hex(conn_d: torch.Tensor, nnode: int) -> "KuhnBox | None":
+        """generate_box_mesh(HEX08, nx, ny, nz)'s connectivity (mesh.py:265-267,
+        corner order (0,0,0) (1,0,0) (1,1,0) (0,1,0) then z + 1), checked element
+        by element against the device generator."""
+        ne = int(conn_d.shape[0])
+        if ne == 0 or conn_d.ndim != 2 or conn_d.shape[1] != 8:
+            return None
+        c0 = [int(v) for v in conn_d[0].tolist()]
+        nx = c0[3] - 1
+        if nx < 1 or c0[0] != 0 or c0[1] != 1 or c0[4] % (nx + 1):
+            return None
+        ny = c0[4] // (nx + 1) - 1
+        if ny < 1 or ne % (nx * ny):
+            return None
+        nz = ne // (nx * ny)
+        if (nx + 1) * (ny + 1) * (nz + 1) != nnode:
+            return None
+        ref = torch.empty_like(conn_d)
+        _lib.call("fpb_box_conn", ETYPE_ID[ElementType.HEX08], nx, ny, nz, ref.data_ptr(), _lib.stream())
+        if not torch.equal(ref, conn_d):
+            return None
+        return KuhnBox(nx, ny, nz, conn_d.device, etype=ElementType.HEX08)
 
     @staticmethod
     def detect(conn_d: torch.Tensor, nnode: int) -> "KuhnBox | None":
@@ -626,6 +652,8 @@ class AssemblyContext:
                     gd.kuhn = KuhnBox.detect(g.conn_d, mesh.nnode)
                     if gd.kuhn is not None:
                         gd.kuhn.pattern_ok = own_pattern
+                elif g.etype is ElementType.HEX08 and HEX_BOX_RHS and len(mesh.groups) == 1:
+                    gd.kuhn = KuhnBox.detect_hex(g.conn_d, mesh.nnode)  # RHS kinds only (pencils)
             if scatter in ("auto", "rows") and g.etype.value in ROW_OWNED + ROW_OWNED_GAUSS:
                 gd.rows = RowPlan(g.conn_d, mesh.nnode, gauss=g.etype.value in ROW_OWNED_GAUSS)
                 gd.rows.ensure_slots(g.conn_d, pattern)  # ScatterPatternError at build time
@@ -730,10 +758,16 @@ class AssemblyContext:
             if own and single_rows and window is None and g.kuhn is not None \
                     and kind_id == KIND_ID[KernelKind.MOMENTUM_RHS] and KUHN_MOMENTUM:
                 kb = g.kuhn
-                _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk, xyz4, vp,
-                          float(rho), float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
+                if kb.etype is ElementType.HEX08:
+                    _lib.call("fpb_assemble_rhs_hexbox", KIND_ID[KernelKind.MOMENTUM_RHS], kb.nx, kb.ny, kb.nz,
+                              kb.kc0, kb.kc1, kb.kchunk, xyz4, vp, None, 0, float(rho), float(mu), 0.0,
+                              kb.scratch(out.device).data_ptr(), out.data_ptr(), _lib.stream())
+                else:
+                    _lib.call("fpb_assemble_momentum_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk, xyz4,
+                              vp, float(rho), float(mu), kb.scratch(out.device).data_ptr(), out.data_ptr(),
+                              _lib.stream())
             elif own and single_rows and (window is None or "kuhn_part" in window) and g.kuhn is not None \
-                    and g.kuhn.pattern_ok and kind_id == GRADIENT_XYZ and KUHN_BOX_GRADIENT and g.kuhn.nx > 1 \
+                    and g.kuhn.etype is ElementType.TET04 and g.kuhn.pattern_ok and kind_id == GRADIENT_XYZ and KUHN_BOX_GRADIENT and g.kuhn.nx > 1 \
                     and g.kuhn.ny > 1:
                 # B_x, B_y, B_z on the Kuhn box: interior lines + the surface rows
                 # (boundary ring and the kc0 / kc1 planes; ghost planes zero);
@@ -870,10 +904,15 @@ class AssemblyContext:
             raise ConfigurationError("phi3 and out3 must be (3, nnode); out3 contiguous")
         g = self.groups[0] if len(self.groups) == 1 else None
         if g is not None and g.kuhn is not None and window is None and KUHN_MOMENTUM:
-            kb = g.kuhn  # Kuhn box: z-marching cell pencils (kmom.cu), three fields per node
-            _lib.call("fpb_assemble_scalar3_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk,
-                      self.xyz4.data_ptr(), vel.data_ptr(), phi3.data_ptr(), n, k0, k1, k2,
-                      kb.scratch(out3.device).data_ptr(), out3.data_ptr(), _lib.stream())
+            kb = g.kuhn  # Kuhn / hex box: z-marching cell pencils (kmom.cu), three fields per node
+            if kb.etype is ElementType.HEX08:
+                _lib.call("fpb_assemble_rhs_hexbox", 101, kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk,
+                          self.xyz4.data_ptr(), vel.data_ptr(), phi3.data_ptr(), n, k0, k1, k2,
+                          kb.scratch(out3.device).data_ptr(), out3.data_ptr(), _lib.stream())
+            else:
+                _lib.call("fpb_assemble_scalar3_kuhn", kb.nx, kb.ny, kb.nz, kb.kc0, kb.kc1, kb.kchunk,
+                          self.xyz4.data_ptr(), vel.data_ptr(), phi3.data_ptr(), n, k0, k1, k2,
+                          kb.scratch(out3.device).data_ptr(), out3.data_ptr(), _lib.stream())
             mark_written(out3)
             return out3
         if g is None or g.blocks is None:

@@ -59,7 +59,8 @@ constexpr int kKmomSlot = 33 * 3;               // one forwarded node row: [33][
 constexpr int kKmomHold = 2 * 3 * 33;           // node row j held two layers: [parity][comp][33]
 // KIND 0: momentum RHS (x, y, z, u, v, w staged per node); KIND 1: three
 // scalar RHS sharing the velocity (+ phi_0, phi_1, phi_2)
-template <int KIND> constexpr int kmom_nc() { return KIND ? 9 : 6; }
+// KIND 2 / 3: the same for a HEX08 box (one Q1 hex per cell, hex_rhs_integrate)
+template <int KIND> constexpr int kmom_nc() { return (KIND & 1) ? 9 : 6; }
 template <int KIND> constexpr int kmom_stg() { return 3 * 2 * kmom_nc<KIND>() * 33; }  // [layer][row][comp][33]
 template <int KIND> constexpr int kmom_warp_d() { return kmom_stg<KIND>() + kKmomRing * kKmomSlot + kKmomHold; }
 
@@ -247,7 +248,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
            double* __restrict__ part, double* __restrict__ out) {
   constexpr int NC = kmom_nc<KIND>(), kKmomStg = kmom_stg<KIND>(), kKmomWarpD = kmom_warp_d<KIND>();
   // output slot of (node, component): [n][3] (momentum) or [3][fstride] (scalars)
-  auto oi = [&](int64_t nd, int d) -> int64_t { return KIND ? d * fstride + nd : 3 * nd + d; };
+  auto oi = [&](int64_t nd, int d) -> int64_t { return (KIND & 1) ? d * fstride + nd : 3 * nd + d; };
   extern __shared__ __align__(16) double sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
@@ -259,7 +260,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
   volatile double* const dring = sm + (size_t)(w - 1) * kKmomWarpD + kKmomStg;  // the warp below's
   double* const hold = stg + kKmomStg + kKmomRing * kKmomSlot;                   // lane-private
   volatile int* const yc = reinterpret_cast<volatile int*>(sm + (size_t)kKmomTY * kKmomWarpD);  // [TY][2]
-  const double r = (KIND ? 1.0 : rho) * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
+  const double r = ((KIND & 1) ? 1.0 : rho) * c_ref[FPB_TET04].M[1];  // M[0][1] = W / 20
   const double muW = mu * c_ref[FPB_TET04].W;
   const double kW[3] = {rho * c_ref[FPB_TET04].W, muW, kappa * c_ref[FPB_TET04].W};  // scalars: kappa_f W
   if (threadIdx.x < 2 * kKmomTY) yc[threadIdx.x] = 0;
@@ -294,7 +295,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
           cp8(t + 99, vel + 3 * nd);
           cp8(t + 132, vel + 3 * nd + 1);
           cp8(t + 165, vel + 3 * nd + 2);
-          if constexpr (KIND) {
+          if constexpr (KIND & 1) {
 #pragma unroll
             for (int f = 0; f < 3; ++f) cp8(t + (6 + f) * 33, phi + f * fstride + nd);
           }
@@ -372,7 +373,32 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
     if (cell && t < ke) {
       const double* s0 = stg + (t % 3) * 2 * NC * 33 + lane;
       const double* s1 = stg + ((t + 1) % 3) * 2 * NC * 33 + lane;
-      if constexpr (KIND && FPB_KMOM_S3_SHARED) {  // three scalars, shared-node cell cycle
+      if constexpr (KIND >= 2) {  // one Q1 hex per cell: local node b at corner c = {0,1,3,2,4,5,7,6}[b]
+        constexpr int HK = KIND == 2 ? FPB_MOMENTUM_RHS : KIND_SCALAR3;
+        double xe[8][3], ue[8][3], fe[Out<FPB_HEX08, HK>::NF], ae[Out<FPB_HEX08, HK>::NOUT];
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) {
+          const int cc = bb ^ ((bb >> 1) & 1);
+          const double* sp = ((cc & 4) ? s1 : s0) + ((cc >> 1) & 1) * NC * 33 + (cc & 1);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            xe[bb][d] = sp[d * 33];
+            ue[bb][d] = sp[(3 + d) * 33];
+            if constexpr (KIND == 3) fe[d * 8 + bb] = sp[(6 + d) * 33];
+          }
+        }
+        if constexpr (KIND == 2) fe[0] = 0.0;
+        hex_rhs_integrate<HK>(xe, ue, fe, rho, mu, kappa, ae);
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) {
+          const int cc = bb ^ ((bb >> 1) & 1);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if (cc & 4) top[cc & 3][d] += ae[bb * 3 + d];
+            else bot[cc & 3][d] += ae[bb * 3 + d];
+          }
+        }
+      } else if constexpr (KIND && FPB_KMOM_S3_SHARED) {  // three scalars, shared-node cell cycle
         kuhn_cell_shared<1>(s0, s1, r, muW, kW, bot, top);
       } else if constexpr (KIND) {  // three scalars: tet by tet
 #pragma unroll
@@ -555,7 +581,7 @@ static int launch_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, con
   const int64_t plane = (int64_t)(nx + 1) * (ny + 1);
   // node planes no integrated cell touches (a slab's ghost planes) are zero
   const int64_t lo = plane * kc0, hi = plane * (kc1 + 1), n = plane * (nz + 1);
-  if (KIND) {
+  if (KIND & 1) {
     for (int f = 0; f < 3; ++f) {
       if (lo > 0) FPB_CUDA(cudaMemsetAsync(out + f * fstride, 0, sizeof(double) * lo, s));
       if (hi < n) FPB_CUDA(cudaMemsetAsync(out + f * fstride + hi, 0, sizeof(double) * (n - hi), s));
@@ -574,7 +600,7 @@ static int launch_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchunk, con
   FPB_LAUNCH_CHECK();
   const int64_t nb = ((int64_t)(g.nxb - 1) * (ny + 1) + (int64_t)(g.nyb - 1) * (nx + 1 - (g.nxb - 1))) * (kc1 - kc0 + 1);
   if (nb > 0) {
-    k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out, KIND ? fstride : 0);
+    k_kuhn_fixup<<<grid_for(nb, 256), 256, 0, s>>>(g, scratch, out, (KIND & 1) ? fstride : 0);
     FPB_LAUNCH_CHECK();
   }
   return FPB_OK;
@@ -615,6 +641,23 @@ int fpb_assemble_scalar3_kuhn(int nx, int ny, int nz, int kc0, int kc1, int kchu
               (long long)fstride);
   return launch_kuhn<1>(nx, ny, nz, kc0, kc1, kchunk, xyz4, vel, phi3, fstride, kappa0, kappa1, kappa2, scratch,
                         out3, as_stream(stream));
+}
+
+int fpb_assemble_rhs_hexbox(int kind, int nx, int ny, int nz, int kc0, int kc1, int kchunk, const double* xyz4,
+                            const double* vel, const double* phi3, int64_t fstride, double rho, double mu,
+                            double kappa, double* scratch, double* out, void* stream) {
+  FPB_REQUIRE(g_ref_loaded[FPB_HEX08], "reference tables for HEX08 not uploaded");
+  FPB_REQUIRE(kind == FPB_MOMENTUM_RHS || kind == KIND_SCALAR3, "hex box RHS: MOMENTUM_RHS or the three scalars");
+  FPB_REQUIRE(nx >= 1 && ny >= 1 && nz >= 1, "hex box %d x %d x %d", nx, ny, nz);
+  FPB_REQUIRE(0 <= kc0 && kc0 < kc1 && kc1 <= nz, "cell layers [%d, %d) outside [0, %d)", kc0, kc1, nz);
+  FPB_REQUIRE(kchunk >= 1, "bad z chunk %d", kchunk);
+  FPB_REQUIRE(xyz4 && vel && scratch && out && (kind == FPB_MOMENTUM_RHS || phi3), "null argument");
+  if (kind == FPB_MOMENTUM_RHS)
+    return launch_kuhn<2>(nx, ny, nz, kc0, kc1, kchunk, xyz4, vel, nullptr, 0, rho, mu, 0.0, scratch, out,
+                          as_stream(stream));
+  FPB_REQUIRE(fstride >= (int64_t)(nx + 1) * (ny + 1) * (nz + 1), "field stride below the node count");
+  return launch_kuhn<3>(nx, ny, nz, kc0, kc1, kchunk, xyz4, vel, phi3, fstride, rho, mu, kappa, scratch, out,
+                        as_stream(stream));
 }
 
 }  // extern "C"

@@ -234,3 +234,68 @@ def test_hex_box_element_ids_bitwise_equal_listed_ids(cuda_ok):
         e[:, k] = 1.0
         _, _, vo = O.assemble_matrix(om, "convection", e)
         assert O.rel_diff(res[True][0][k * nnz:(k + 1) * nnz], vo) < TOL
+
+
+def _hex_ctx(P, dims, kchunk=0, coords=None):
+    import paper_2107_11541_b200.assembly as A
+
+    old = A.KUHN_KCHUNK
+    A.KUHN_KCHUNK = kchunk
+    try:
+        mesh = P.generate_box_mesh(P.ElementType.HEX08, *dims)
+        if coords is not None:
+            mesh.coords = coords
+        ctx = P.AssemblyContext.build(mesh, vector_size=8)
+    finally:
+        A.KUHN_KCHUNK = old
+    return mesh, ctx
+
+
+@pytest.mark.parametrize("dims,kchunk", [((5, 4, 7), 0), ((5, 4, 7), 2), ((33, 9, 4), 3), ((32, 8, 2), 0),
+                                         ((1, 1, 1), 0)])
+def test_hex_box_rhs_matches_oracle(cuda_ok, dims, kchunk):
+    """HEX08 box: momentum RHS and the three scalar RHS by the cell pencils
+    (fpb_assemble_rhs_hexbox) against the oracle, jittered coordinates."""
+    import paper_2107_11541_b200 as P
+
+    om = O.box(O.HEX08, *dims)
+    om.coords = _jitter(om.coords, *dims, seed=13)
+    mesh, ctx = _hex_ctx(P, dims, kchunk, om.coords)
+    kb = ctx.groups[0].kuhn
+    assert kb is not None and kb.etype is P.ElementType.HEX08
+    vel, sc = O.bench_fields(om.nnode, 3)
+    r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
+    assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL, dims
+    kap = (1e-2, 3e-2, 0.0)
+    phi3 = torch.as_tensor(np.stack(sc[:3]), device="cuda").contiguous()
+    out3 = torch.full((3, om.nnode), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.assemble_scalar_rhs3_d(torch.as_tensor(vel, device="cuda"), phi3, kap, out3)
+    got = out3.cpu().numpy()
+    for f in range(3):
+        want = O.assemble_rhs(om, "scalar_rhs", vel, sc[f], 1.0, 0.0, kap[f])
+        assert O.rel_diff(got[f], want) < TOL, (dims, f)
+
+
+def test_hex_box_rhs_matches_block_path(cuda_ok):
+    import paper_2107_11541_b200 as P
+    import paper_2107_11541_b200.assembly as A
+
+    mesh, ctx = _hex_ctx(P, (40, 24, 19))
+    n = mesh.nnode
+    g = torch.Generator(device="cuda").manual_seed(3)
+    vel = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=g)
+    phi3 = torch.randn((3, n), dtype=torch.float64, device="cuda", generator=g)
+    a, b = torch.empty((n, 3), dtype=torch.float64, device="cuda"), torch.empty((n, 3), dtype=torch.float64,
+                                                                                 device="cuda")
+    a3, b3 = torch.empty((3, n), dtype=torch.float64, device="cuda"), torch.empty((3, n), dtype=torch.float64,
+                                                                                  device="cuda")
+    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, a)
+    ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 2e-2, 3e-2), a3)
+    A.KUHN_MOMENTUM = False
+    try:
+        ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, b)
+        ctx.assemble_scalar_rhs3_d(vel, phi3, (1e-2, 2e-2, 3e-2), b3)
+    finally:
+        A.KUHN_MOMENTUM = True
+    assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < TOL
+    assert O.rel_diff(a3.cpu().numpy(), b3.cpu().numpy()) < TOL
