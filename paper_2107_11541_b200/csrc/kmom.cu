@@ -47,6 +47,18 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 __device__ __forceinline__ void cp_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// y-ring counters: acquire / release at CTA scope on shared memory
+__device__ __forceinline__ int yc_acquire(volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared((const void*)p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void yc_release(volatile int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;"
+               ::"r"((unsigned)__cvta_generic_to_shared((const void*)p)), "r"(v) : "memory");
+}
+
 #ifndef FPB_KMOM_MINB
 #define FPB_KMOM_MINB 1  // one 8-warp CTA per SM at ~228 registers: no spills (2 CTAs at 128: spills, 13 % slower)
 #endif
@@ -325,16 +337,15 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
         X[d] = h[d * 33 + 32];
       }
       if (w > 0) {
-        // flag protocol: the producer's slot stores are fenced (CTA scope)
-        // before its volatile full count; the slot is read with volatile
-        // loads issued after this warp observed the count (and the consumed
-        // count is published after them).  An acquire fence here measured
-        // 5 % slower (it also waits for the warp's in-flight global traffic)
-        // and shared-memory accesses of a warp are performed in order.
-        // compute-sanitizer racecheck does not model flag synchronisation
-        // and lists these slot accesses as hazards (profiles/r02m_sanitizer).
+        // flag protocol (CTA scope, shared memory): the producer's slot
+        // stores, __syncwarp, then lane 0's st.release of the full count; here
+        // lane 0's ld.acquire of it, __syncwarp, then the slot loads; the
+        // consumed count is released after them (and acquired by the
+        // producer before it reuses the slot).  compute-sanitizer racecheck
+        // does not model flag synchronisation and lists these slot accesses
+        // as hazards (profiles/r02m_sanitizer).
         if (lane == 0)
-          while (yc[2 * (w - 1)] < kk - kb + 1) __nanosleep(20);
+          while (yc_acquire(yc + 2 * (w - 1)) < kk - kb + 1) __nanosleep(20);
         __syncwarp();
         const volatile double* e = dring + (kk % kKmomRing) * kKmomSlot;
 #pragma unroll
@@ -343,7 +354,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
           if (lane == 31) X[d] += e[32 * 3 + d];
         }
         __syncwarp();
-        if (lane == 0) yc[2 * (w - 1) + 1] = kk - kb + 1;  // consumed
+        if (lane == 0) yc_release(yc + 2 * (w - 1) + 1, kk - kb + 1);  // consumed
       }
       const int64_t nd = i0 + lane + j * row + (int64_t)kk * layer;
       if (node) {
@@ -490,7 +501,7 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
         }
       } else {  // to the warp above
         if (lane == 0)
-          while (yc[2 * w + 1] < (t - kb + 1) - kKmomRing) __nanosleep(20);  // slot free
+          while (yc_acquire(yc + 2 * w + 1) < (t - kb + 1) - kKmomRing) __nanosleep(20);  // slot free
         __syncwarp();
         volatile double* slot = ring + (t % kKmomRing) * kKmomSlot;
 #pragma unroll
@@ -498,9 +509,8 @@ k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double
           slot[lane * 3 + d] = up[d];
           if (lane == 31) slot[32 * 3 + d] = ex1[d];
         }
-        __threadfence_block();
-        __syncwarp();
-        if (lane == 0) yc[2 * w] = t - kb + 1;  // full
+        __syncwarp();  // orders the warp's slot stores before lane 0's release
+        if (lane == 0) yc_release(yc + 2 * w, t - kb + 1);  // full
       }
     }
 #pragma unroll
