@@ -25,6 +25,12 @@
 //   synchronisation).  z-chunks integrate the cell layer below them (halo)
 //   for the contributions to their lowest node layer, so they are
 //   independent too.  Every sum has a fixed order: bitwise reproducible.
+//
+// The same pencils run four per-cell integrands (template KIND): 0 = TET04
+// momentum (six Kuhn tets, shared-node cycle, tet_mom_core), 1 = TET04 three
+// scalars (tet_s3_core), 2 / 3 = HEX08 momentum / three scalars (one Q1 hex
+// per cell of the generator's hex box, hex_rhs_integrate).  A cell-layer
+// range [kc0, kc1) restricts the integration to a z-slab's own layers.
 #include <algorithm>
 
 #include "simplex.cuh"
