@@ -888,6 +888,25 @@ class AssemblyContext:
         phi = scalar_d.contiguous() if scalar_d is not None else None
         return self._run(KIND_ID[kind], vel, phi, rho, mu, kappa, out, window)
 
+    def assemble_ns_d(self, velocity_d: torch.Tensor, rho: float, mu: float, rhs: torch.Tensor,
+                      mats: torch.Tensor) -> tuple:
+        """One NS assembly step on the device: the momentum RHS into rhs
+        (n, dim) and the continuity matrices B_x, B_y, B_z into mats (3 nnz),
+        the two on separate streams — they share no data, so the momentum
+        kernel's last wave overlaps the continuity kernels.  Joined before
+        returning (stream-ordered on the current stream); results equal the
+        two calls in sequence bitwise."""
+        main = torch.cuda.current_stream()
+        side = getattr(self, "_ns_side", None)
+        if side is None:
+            side = self._ns_side = torch.cuda.Stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            self.assemble_rhs_d(KernelKind.MOMENTUM_RHS, velocity_d, None, rho, mu, 0.0, rhs)
+        self.assemble_gradients_d(mats)
+        main.wait_stream(side)
+        return rhs, mats
+
     def assemble_scalar_rhs3_d(self, velocity_d: torch.Tensor, phi3_d: torch.Tensor, kappas, out3: torch.Tensor,
                                window: dict | None = None) -> torch.Tensor:
         """Three SCALAR_RHS sharing one velocity (enthalpy + two species,

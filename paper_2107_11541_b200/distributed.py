@@ -667,14 +667,20 @@ def _kuhn_slab_step(dom, vel, rhs, mats, rho, mu, side=None, events=None):
               for k in ("start", "interface_done", "halo_start", "halo_done", "interior_done")}
         events.update(ev)
         ev["start"].record(main)
-    ctx.assemble_rhs_d(KernelKind.MOMENTUM_RHS, vel, None, rho, mu, 0.0, rhs)
+    # momentum on its own stream (its last wave overlaps the B_xyz kernels)
+    mom = getattr(dom, "_mom_stream", None)
+    if mom is None:
+        mom = dom._mom_stream = torch.cuda.Stream()
+    mom.wait_stream(main)
+    with torch.cuda.stream(mom):
+        ctx.assemble_rhs_d(KernelKind.MOMENTUM_RHS, vel, None, rho, mu, 0.0, rhs)
     ctx.assemble_gradients_d(mats, {"kuhn_part": "surface"})
-    if ev:
-        ev["interface_done"].record(main)
     side = side or torch.cuda.Stream()
     side.wait_stream(main)
+    side.wait_stream(mom)
     with torch.cuda.stream(side):
         if ev:
+            ev["interface_done"].record(side)
             ev["halo_start"].record(side)
         dom.halo_sum_rhs(rhs)
         dom.halo_sum_matrix(mats, ctx.mesh.dim)
@@ -684,6 +690,7 @@ def _kuhn_slab_step(dom, vel, rhs, mats, rho, mu, side=None, events=None):
     if ev:
         ev["interior_done"].record(main)
     main.wait_stream(side)
+    main.wait_stream(mom)
     return rhs, mats
 
 

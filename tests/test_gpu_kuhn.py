@@ -299,3 +299,21 @@ def test_hex_box_rhs_matches_block_path(cuda_ok):
         A.KUHN_MOMENTUM = True
     assert O.rel_diff(a.cpu().numpy(), b.cpu().numpy()) < TOL
     assert O.rel_diff(a3.cpu().numpy(), b3.cpu().numpy()) < TOL
+
+
+def test_assemble_ns_d_equals_sequence(cuda_ok):
+    """assemble_ns_d (momentum and B_xyz on two streams) equals the two calls
+    in sequence bitwise."""
+    import paper_2107_11541_b200 as P
+
+    mesh, ctx = _ctx(P, 40, 21, 13)
+    n, nnz = mesh.nnode, ctx.pattern.nnz
+    g = torch.Generator(device="cuda").manual_seed(11)
+    vel = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=g)
+    r1, r2 = (torch.empty((n, 3), dtype=torch.float64, device="cuda") for _ in range(2))
+    m1, m2 = (torch.empty(3 * nnz, dtype=torch.float64, device="cuda") for _ in range(2))
+    ctx.assemble_ns_d(vel, 1.0, 1e-2, r1, m1)
+    ctx.assemble_rhs_d(P.KernelKind.MOMENTUM_RHS, vel, None, 1.0, 1e-2, 0.0, r2)
+    ctx.assemble_gradients_d(m2)
+    torch.cuda.synchronize()
+    assert torch.equal(r1, r2) and torch.equal(m1, m2)
