@@ -63,6 +63,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef FPB_BLK_MINB_SCALAR3
 #define FPB_BLK_MINB_SCALAR3 5
 #endif
+#ifndef FPB_BLK_TET_ADJ
+#define FPB_BLK_TET_ADJ 1  // TET04 momentum in the adjugate closed form (fewer FP64 operations)
+#endif
 #ifndef FPB_BLK_INTERLEAVE
 #define FPB_BLK_INTERLEAVE 1  // the compiler interleaves a thread's two elements (ILP)
 #endif
@@ -294,7 +297,15 @@ k_blk_rhs(int64_t nelem, int64_t blk0, const uint16_t* __restrict__ blk_lidx, co
       }
     }
     double acc[Out<ET, KIND>::NOUT];
-    if constexpr (Elem<ET>::AFFINE) {
+    if constexpr (ET == FPB_TET04 && KIND == FPB_MOMENTUM_RHS && FPB_BLK_TET_ADJ) {
+      // adjugate closed form (simplex.cuh tet_mom_adj, the Kuhn kernels' residual)
+      double res[4][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+      tet_mom_adj(xe, ue, rho * refM<ET>(0, 1), mu * refWsum<ET>(), res);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[a * 3 + k] = res[a][k];
+    } else if constexpr (Elem<ET>::AFFINE) {
       simplex_rhs_all<ET, KIND>(xe, ue, fe, rho, mu, kappa, acc);
     } else if constexpr (KIND == KIND_SCALAR3 && ET == FPB_HEX08) {  // one geometry, three fields (Walsh forms)
       hex_rhs_integrate<KIND_SCALAR3>(xe, ue, fe, rho, mu, kappa, acc);
