@@ -317,3 +317,33 @@ def test_assemble_ns_d_equals_sequence(cuda_ok):
     ctx.assemble_gradients_d(m2)
     torch.cuda.synchronize()
     assert torch.equal(r1, r2) and torch.equal(m1, m2)
+
+
+def test_kuhn_anisotropic_offset_box(cuda_ok):
+    """Kuhn-box kernels on a stretched, shifted box (lengths 2 x 0.5 x 3,
+    coordinates + 10): momentum, three scalars and B_xyz against the oracle."""
+    import paper_2107_11541_b200 as P
+
+    dims = (9, 7, 6)
+    om = O.box(O.TET04, *dims)
+    om.coords = om.coords * np.array([2.0, 0.5, 3.0]) + 10.0
+    om.coords = _jitter(om.coords, *dims, seed=23)
+    mesh, ctx = _ctx(P, *dims, coords=om.coords)
+    assert ctx.groups[0].kuhn is not None
+    vel, sc = O.bench_fields(om.nnode, 3)
+    r = ctx.assemble_rhs(P.KernelKind.MOMENTUM_RHS, "packed", vel, None, 1.0, 1e-2, 0.0)
+    assert O.rel_diff(r, O.assemble_rhs(om, "momentum_rhs", vel, None, 1.0, 1e-2, 0.0)) < TOL
+    phi3 = torch.as_tensor(np.stack(sc[:3]), device="cuda").contiguous()
+    out3 = torch.empty((3, om.nnode), dtype=torch.float64, device="cuda")
+    ctx.assemble_scalar_rhs3_d(torch.as_tensor(vel, device="cuda"), phi3, (1e-2, 1e-2, 1e-2), out3)
+    for f in range(3):
+        want = O.assemble_rhs(om, "scalar_rhs", vel, sc[f], 1.0, 0.0, 1e-2)
+        assert O.rel_diff(out3[f].cpu().numpy(), want) < TOL
+    nnz = ctx.pattern.nnz
+    mats = torch.empty(3 * nnz, dtype=torch.float64, device="cuda")
+    ctx.assemble_gradients_d(mats)
+    for k in range(3):
+        e = np.zeros((om.nnode, 3))
+        e[:, k] = 1.0
+        _, _, vo = O.assemble_matrix(om, "convection", e)
+        assert O.rel_diff(mats[k * nnz:(k + 1) * nnz].cpu().numpy(), vo) < TOL
