@@ -604,11 +604,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        from paper_2107_11541_b200.distributed import init_process_group
+
         backend = os.environ.get("FPB_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        init_process_group(backend, torch.device("cuda", local))
 
     import paper_2107_11541_b200 as P
 

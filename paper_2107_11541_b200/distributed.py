@@ -38,6 +38,31 @@ from .elements import ElementType
 SLAB_KUHN = True
 
 
+def init_process_group(backend: str = "nccl", device: torch.device | None = None,
+                       timeout_s: float | None = None, **kw) -> None:
+    """`dist.init_process_group` with the failure detection the slab path relies on.
+
+    * A bounded collective timeout (FPB_DIST_TIMEOUT_S, default 300 s): a rank
+      that dies or hangs mid-halo turns into an exception on its peers
+      instead of an indefinite wait.
+    * NCCL async error handling on (TORCH_NCCL_ASYNC_ERROR_HANDLING=1 unless
+      the caller set it): the watchdog aborts the communicator on a timeout or
+      a remote failure, so the process exits non-zero.
+    * The NCCL group is bound to this rank's device (eager init, the
+      communicator exists before the first halo).
+    """
+    import datetime
+    import os
+
+    if timeout_s is None:
+        timeout_s = float(os.environ.get("FPB_DIST_TIMEOUT_S", "300"))
+    if backend == "nccl":
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        if device is not None:
+            kw.setdefault("device_id", device)
+    dist.init_process_group(backend, timeout=datetime.timedelta(seconds=timeout_s), **kw)
+
+
 def slab_ranges(nz: int, world: int) -> list[tuple[int, int]]:
     """Balanced cell-layer ranges [k0, k1) per rank."""
     if world < 1 or nz < world:

@@ -146,6 +146,45 @@ def test_halo_sum_reproduces_single_domain(world):
     assert faces and all(len(v) == 2 and v[0] == v[1] for v in faces.values())
 
 
+def _timeout_worker(rank, world, initfile, out, done):
+    import time
+
+    from paper_2107_11541_b200.distributed import init_process_group
+
+    init_process_group("gloo", timeout_s=3.0, init_method=f"file://{initfile}", rank=rank, world_size=world)
+    if rank == 0:
+        t = torch.ones(4)
+        t0 = time.perf_counter()
+        try:
+            dist.all_reduce(t)  # rank 1 never joins: a dead neighbour
+            out.put(("returned", time.perf_counter() - t0))
+        except RuntimeError as e:
+            out.put(("raised", time.perf_counter() - t0, type(e).__name__))
+        done.set()
+    else:
+        done.wait(60)
+
+
+def test_collective_timeout_detects_missing_rank():
+    """Failure detection: with the bounded timeout of
+    distributed.init_process_group, a collective whose peer never arrives
+    raises on the waiting rank within seconds instead of hanging."""
+    ctx = mp.get_context("spawn")
+    q, done = ctx.Queue(), ctx.Event()
+    with tempfile.TemporaryDirectory() as d:
+        initfile = os.path.join(d, "init")
+        procs = [ctx.Process(target=_timeout_worker, args=(r, 2, initfile, q, done)) for r in range(2)]
+        for p in procs:
+            p.start()
+        res = q.get(timeout=120)
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert res[0] == "raised", res
+    assert 2.0 < res[1] < 30.0, res
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
 def test_device_slabs_reproduce_single_domain(cuda_ok, world):
