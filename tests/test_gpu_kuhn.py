@@ -120,7 +120,7 @@ def test_kuhn_box_gradients_match_colind_path(cuda_ok):
     import paper_2107_11541_b200 as P
     import paper_2107_11541_b200.assembly as A
 
-    for dims in ((37, 21, 9), (6, 5, 4), (2, 2, 2), (33, 2, 3)):
+    for dims in ((37, 21, 9), (6, 5, 4), (2, 2, 2), (33, 2, 3), (1, 1, 1), (1, 4, 3), (40, 1, 2), (3, 3, 1)):
         om = O.box(O.TET04, *dims)
         om.coords = _jitter(om.coords, *dims, seed=11)
         mesh, ctx = _ctx(P, *dims, coords=om.coords)
