@@ -718,7 +718,10 @@ __host__ __device__ constexpr int kuhn_off3(int t, int d) {
 }
 __host__ __device__ constexpr int cmin0(int a, int b, int c) { return (a < b ? (a < c ? a : c) : (b < c ? b : c)) < 0 ? -1 : 0; }
 
-__global__ void __launch_bounds__(128)
+#ifndef FPB_KGRAD_BMINB
+#define FPB_KGRAD_BMINB 4
+#endif
+__global__ void __launch_bounds__(128, FPB_KGRAD_BMINB)
 k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, int ny, int nz, int vk0, int vk1,
                      const double* __restrict__ xyz4, const int32_t* __restrict__ rowptr, int64_t nnz,
                      int accumulate, double* __restrict__ out) {
@@ -754,8 +757,12 @@ k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, in
         for (int d = 0; d < DIM; ++d) X[t][d] = ok ? r4[d] - x0[d] : 0.0;
       }
     }
+    // columns are stored as they finish (their CSR slot is known by then:
+    // the present columns before them, +1 past the diagonal), so no
+    // per-column register copy is kept — 195 -> ~120 registers
     const double mN0 = refmN<FPB_TET04>(0);
-    double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0}, col[kKuhnCols][DIM];
+    const int lo = __ldg(rowptr + row);
+    double acc[DIM] = {0.0, 0.0, 0.0}, tot[DIM] = {0.0, 0.0, 0.0};
     unsigned present = 0;
     bool any = false;
     int target = 0;
@@ -771,30 +778,31 @@ k_kuhn_grad_boundary(int32_t nrows, const int32_t* __restrict__ rows, int nx, in
       }
       if ((cells >> cb) & 1u) any = true;
       if (w & (1 << 14)) {  // column finished
+        if (any) {
+          const int cp = __popc(present) + (target >= kKuhnDiag ? 1 : 0);
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) {
+            double* o = out + d * nnz + lo + cp;
+            const double v = mN0 * acc[d];
+            *o = accumulate ? *o + v : v;
+          }
+          present |= 1u << target;
+        }
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          col[target][d] = mN0 * acc[d];
           tot[d] += acc[d];
           acc[d] = 0.0;
         }
-        if (any) present |= 1u << target;
         any = false;
         ++target;
       }
     }
-    const int lo = __ldg(rowptr + row);
     const int dpos = __popc(present & 0x7fu);
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-      double* o = out + d * nnz + lo;
+      double* o = out + d * nnz + lo + dpos;
       const double dv = -(mN0 * tot[d]);
-      o[dpos] = accumulate ? o[dpos] + dv : dv;
-#pragma unroll
-      for (int t = 0; t < kKuhnCols; ++t)
-        if ((present >> t) & 1u) {
-          const int cp = __popc(present & ((1u << t) - 1u)) + (t >= kKuhnDiag ? 1 : 0);
-          o[cp] = accumulate ? o[cp] + col[t][d] : col[t][d];
-        }
+      *o = accumulate ? *o + dv : dv;
     }
   }
 }
