@@ -46,6 +46,9 @@ constexpr int kHbRec = 72;  // H planes per element: q = [k][l][s][4]
 #ifndef FPB_HEXH_MINB
 #define FPB_HEXH_MINB 4
 #endif
+#ifndef FPB_HEXR_PFM
+#define FPB_HEXR_PFM 4  // cell lines L2-prefetched by the box row pass (bit my + 2 mz; 0 = off): C4 B_xyz 8.50 -> 7.93 ms (3, 12, 15: 8.51, 8.37, 9.70)
+#endif
 #ifndef FPB_HEXR_MINB
 #define FPB_HEXR_MINB 4  // 8 CTAs of 96 threads at 80 registers: C4 B_xyz 8.78 -> 8.53 ms (5: 64 registers, 11.4 ms)
 #endif
@@ -183,6 +186,23 @@ k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t*
       const int e0 = (ii - 1) + bnx * ((jj - 1) + bny * (kk - 1));
 #pragma unroll
       for (int m = 0; m < 8; ++m) el[m] = e0 + (m & 1) + bnx * (((m >> 1) & 1) + bny * (m >> 2));
+#if FPB_HEXR_PFM
+      // L2 prefetch of the H planes (this thread's matrix k) of the row's
+      // own cell lines before the loads: bit (my + 2 mz) of FPB_HEXR_PFM
+      // selects cell line (j-1+my, k-1+mz).  Fire-and-forget, no registers:
+      // the whole batch of 128-byte runs is in flight at once instead of
+      // one cell's twelve loads at a time.  Lanes 0 / 16 cover the warp's
+      // two runs per plane.
+      if ((r & 15) == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if ((FPB_HEXR_PFM >> c) & 1) {
+            const double* hp = H + e0 + (int64_t)bnx * ((c & 1) + (int64_t)bny * (c >> 1)) + (int64_t)k * 24 * nelem;
+#pragma unroll
+            for (int q = 0; q < 24; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(hp + (int64_t)q * nelem));
+          }
+      }
+#endif
     } else {
 #pragma unroll
       for (int m = 0; m < 8; ++m) el[m] = __ldg(inc8 + (int64_t)m * nrows + i);

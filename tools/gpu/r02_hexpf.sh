@@ -1,0 +1,7 @@
+# L2-prefetch distance sweep for the HEX08 box row pass (C4 B_xyz)
+for rep in 1 2; do
+echo "== default"; timeout 600 python tools/hexprobe.py --reps 7 2>&1 | tail -1 | grep -o '"once_ms.*'
+for v in m4 m12 m15 m3; do
+  echo "== $v"; FPB_LIB_PATH=$PWD/vtmp/$v/libfempack_b200.so timeout 600 python tools/hexprobe.py --reps 7 2>&1 | tail -1 | grep -o '"once_ms.*'
+done
+done
