@@ -1,3 +1,5 @@
+# Kuhn boundary-row kernel occupancy variants; build them first:
+#   for m in 2 3; do bash tools/build_variant.sh bminb$m -DFPB_KGRAD_BMINB=$m; mkdir -p vtmp/b$m; cp build_variants/bminb$m/libfempack_b200.so vtmp/b$m/; done
 mkdir -p gpurun_out
 for v in default b2 b3; do
   if [ $v = default ]; then unset FPB_LIB_PATH; else export FPB_LIB_PATH=$PWD/vtmp/$v/libfempack_b200.so; fi

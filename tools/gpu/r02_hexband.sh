@@ -1,4 +1,5 @@
-mkdir -p gpurun_out
-
-for B in 64 128 280; do FPB_HEX_BAND=$B timeout 600 python tools/hexprobe.py > gpurun_out/hexprobe_b$B.json 2>&1; echo band $B; cat gpurun_out/hexprobe_b$B.json | tail -1; done
-FPB_HEX_BAND=64 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:k_hex_rows_canon -c 1 python tools/hexprobe.py --reps 1 2>&1 | grep -E "dram__|duration" 
+# HEX08 box row pass with the L2 prefetch: band width / rows-per-CTA sweep (C4 B_xyz)
+for b in 32 16 64 8; do
+  echo "== band $b"; FPB_HEX_BAND=$b timeout 600 python tools/hexprobe.py --reps 7 2>&1 | tail -1 | grep -o '"once_ms.*'
+done
+echo "== band 32 canon64"; timeout 600 python tools/hexprobe.py --reps 7 --canon-rows 64 2>&1 | tail -1 | grep -o '"once_ms.*'
