@@ -128,6 +128,12 @@ def load(require_gpu: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        # FPB_TUNE_<KNOB>=<int> presets fpb_set_tuning(knob, value) (A/B timing aid)
+        for key, val in os.environ.items():
+            if key.startswith("FPB_TUNE_"):
+                knob = key[len("FPB_TUNE_"):].lower()
+                if lib.fpb_set_tuning(knob.encode(), int(val)) != 0:
+                    raise RuntimeError(f"{key}: {lib.fpb_last_error().decode()}")
         _lib = lib
     if require_gpu and not torch.cuda.is_available():
         raise RuntimeError("fempack_b200 needs a CUDA device (sm_100a); there is no CPU fallback")

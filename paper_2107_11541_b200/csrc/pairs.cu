@@ -584,6 +584,7 @@ constexpr int kGradWarps = FPB_KGRAD_WARPS;
 #endif
 int g_tuning_kgrad_march = 1;  // fpb_set_tuning("kgrad_march", 0|1): z-marching lines (1) or the row kernel (0)
 int g_tuning_kgrad_kchunk = 0;  // 0: from the grid size
+int g_tuning_kgrad_bthreads = 128;  // threads per CTA of the Kuhn boundary-row kernel
 constexpr int kGradStg = 4 * 3 * 3 * 34 + 2;  // [layer slot][node row][comp][34 columns] + 4 CSR starts (int)
 __device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -913,7 +914,8 @@ int fpb_assemble_gradient_kuhn_boundary(int32_t nrows, const int32_t* rows, int 
   FPB_REQUIRE(g_ref_loaded[FPB_TET04], "reference tables for TET04 not uploaded");
   FPB_REQUIRE(rows && xyz4 && rowptr && out && nx >= 1 && ny >= 1 && nz >= 1, "bad Kuhn-boundary arguments");
   if (nrows <= 0) return FPB_OK;
-  k_kuhn_grad_boundary<<<grid_for(nrows, 128), 128, 0, as_stream(stream)>>>(nrows, rows, nx, ny, nz, vk0, vk1, xyz4,
+  const int bt = g_tuning_kgrad_bthreads;
+  k_kuhn_grad_boundary<<<grid_for(nrows, bt), bt, 0, as_stream(stream)>>>(nrows, rows, nx, ny, nz, vk0, vk1, xyz4,
                                                                           rowptr, nnz, accumulate, out);
   FPB_LAUNCH_CHECK();
   return FPB_OK;

@@ -47,6 +47,7 @@ extern int g_tuning_blk_pipe;
 extern int g_tuning_kmom_smem_kb;    // kmom.cu
 extern int g_tuning_kgrad_march;     // pairs.cu
 extern int g_tuning_kgrad_kchunk;    // pairs.cu
+extern int g_tuning_kgrad_bthreads;  // pairs.cu
 
 
 template <int ET, int KIND>
@@ -844,6 +845,11 @@ int fpb_set_tuning(const char* name, int value) {
   if (name && strcmp(name, "kgrad_kchunk") == 0) {
     FPB_REQUIRE(value >= 0, "kgrad_kchunk must be >= 0 (0: automatic)");
     g_tuning_kgrad_kchunk = value;
+    return FPB_OK;
+  }
+  if (name && strcmp(name, "kgrad_bthreads") == 0) {
+    FPB_REQUIRE(value == 32 || value == 64 || value == 128, "kgrad_bthreads must be 32, 64 or 128");
+    g_tuning_kgrad_bthreads = value;
     return FPB_OK;
   }
   if (name && strcmp(name, "kmom_smem_kb") == 0) {
