@@ -571,7 +571,7 @@ k_rows_pairs_kuhn(int32_t nrows, const int32_t* __restrict__ rows, const int32_t
 // start is one load per warp and layer.  Warps are independent (no
 // barriers).
 #ifndef FPB_KGRAD_WARPS
-#define FPB_KGRAD_WARPS 2
+#define FPB_KGRAD_WARPS 1  // one warp per CTA, 6 CTAs/SM (33 KB of staging each)
 #endif
 constexpr int kGradWarps = FPB_KGRAD_WARPS;
 #ifdef FPB_KGRAD_STCS  // streaming (evict-first) stores of the output runs: A/B only, 1.92 vs 1.36 ms at C5
@@ -580,12 +580,26 @@ constexpr int kGradWarps = FPB_KGRAD_WARPS;
 #define FPB_KGRAD_STORE(p, v) (*(p) = (v))
 #endif
 #ifndef FPB_KGRAD_MINB
-#define FPB_KGRAD_MINB 4  // ~249 registers, 8 warps/SM: 1.40 ms at C5 vs 1.59 at 168 registers / 10 warps
+// CTAs per SM: 6 one-warp CTAs with the double-buffered TMA output staging
+// (plain stores: 4 two-warp CTAs, ~249 registers, 8 warps/SM: 1.40 ms at C5
+// vs 1.59 at 168 registers / 10 warps)
+#define FPB_KGRAD_MINB 6
 #endif
 int g_tuning_kgrad_march = 1;  // fpb_set_tuning("kgrad_march", 0|1): z-marching lines (1) or the row kernel (0)
 int g_tuning_kgrad_kchunk = 0;  // 0: from the grid size
 int g_tuning_kgrad_bthreads = 128;  // threads per CTA of the Kuhn boundary-row kernel
 constexpr int kGradStg = 4 * 3 * 3 * 34 + 2;  // [layer slot][node row][comp][34 columns] + 4 CSR starts (int)
+// output staging per matrix: 32 rows x 15 entries + 2 doubles of padding, so
+// the block can be shifted by one double to match the 16-byte phase of its
+// CSR destination (TMA bulk stores need 16-byte aligned ends)
+constexpr int kGradOut = 32 * (kKuhnCols + 1) + 2;
+// output path: 0 = coalesced st.global from the staging buffer; 1 = one TMA
+// bulk store per matrix and plane (single buffer: the next plane waits for
+// the store to drain, C5 B_xyz 1.35 -> 1.44 ms); 2 = the same, double
+// buffered (1.35 -> 1.29 ms; L1 wavefronts 80 -> 48 % of peak)
+#ifndef FPB_KGRAD_TMA
+#define FPB_KGRAD_TMA 2
+#endif
 __device__ __forceinline__ void g_cp8(double* smem_dst, const double* gmem_src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
@@ -599,8 +613,8 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wg = (int64_t)blockIdx.x * kGradWarps + warp;
   if (wg >= nwarps) return;
-  double* const stg = gsm + (size_t)warp * (kGradStg + DIM * 32 * RE);
-  double* const bo = stg + kGradStg;
+  constexpr int NBUF = FPB_KGRAD_TMA == 2 ? 2 : 1;  // TMA 2: double-buffered output staging
+  double* const stg = gsm + (size_t)warp * (kGradStg + NBUF * DIM * kGradOut);
   const int nxi = nx - 1, nyi = ny - 1;
   const int segs = (nxi + 31) >> 5;
   const int64_t per_chunk = (int64_t)segs * nyi;
@@ -646,7 +660,22 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
     if (k + 2 <= nz) stage(k + 2);
     else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
+#if FPB_KGRAD_TMA
+    // the previous plane's bulk stores must have read the staging buffer
+    if (lane == 0) {
+      if (NBUF == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+#endif
     __syncwarp();
+    double* const bo0 = stg + kGradStg + (NBUF == 2 ? (k & 1) * DIM * kGradOut : 0);
+    const int base = rlo_s[k & 3];
+    // per matrix d: staging block at bo0 + d kGradOut, shifted by the CSR
+    // destination's 16-byte phase (one double when its address is odd in doubles)
+    int sh[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d)
+      sh[d] = FPB_KGRAD_TMA && !accumulate ? (int)((reinterpret_cast<uintptr_t>(out + d * nnz + base) >> 3) & 1) : 0;
     double x0[DIM], X[kKuhnCols][DIM];
     {
       const double* c0 = stg + (k & 3) * 3 * 3 * 34 + 1 * 3 * 34 + lane + 1;
@@ -674,7 +703,7 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
         const int cpos = target + (target >= dslot);
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
-          bo[d * 32 * RE + lane * RE + cpos] = mN0 * acc[d];
+          bo0[d * kGradOut + sh[d] + lane * RE + cpos] = mN0 * acc[d];
           tot[d] += acc[d];
           acc[d] = 0.0;
         }
@@ -682,24 +711,50 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
       }
     }
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) bo[d * 32 * RE + lane * RE + dslot] = -(mN0 * tot[d]);
+    for (int d = 0; d < DIM; ++d) bo0[d * kGradOut + sh[d] + lane * RE + dslot] = -(mN0 * tot[d]);
     __syncwarp();
     // the segment's rows are consecutive (15 entries each): one contiguous CSR range per matrix
-    const int base = rlo_s[k & 3];
     const int span = nlive * RE;
+    if (FPB_KGRAD_TMA && !accumulate) {
+      // one TMA bulk store per matrix for the 16-byte aligned middle of the
+      // range; an unaligned first / last double by plain stores (lane 0)
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      double* o = out + d * nnz + base;
-      for (int q = lane; q < span; q += 32) {
-        const double v = bo[d * 32 * RE + q];
-        if (accumulate) o[q] += v;
-        else FPB_KGRAD_STORE(o + q, v);
+        for (int d = 0; d < DIM; ++d) {
+          double* o = out + d * nnz + base;
+          const double* b = bo0 + d * kGradOut + sh[d];
+          const int h = sh[d];                 // 0 or 1 leading double
+          const int nb = ((span - h) >> 1) << 1;  // doubles in the bulk part
+          if (h) o[0] = b[0];
+          if (h + nb < span) o[span - 1] = b[span - 1];
+          if (nb > 0) {
+            const unsigned src = (unsigned)__cvta_generic_to_shared(b + h);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o + h), "r"(src),
+                         "r"(nb * 8)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        double* o = out + d * nnz + base;
+        for (int q = lane; q < span; q += 32) {
+          const double v = bo0[d * kGradOut + q];
+          if (accumulate) o[q] += v;
+          else FPB_KGRAD_STORE(o + q, v);
+        }
       }
     }
     (void)live;
     __syncwarp();
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+#if FPB_KGRAD_TMA
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
 }
 
 // ---- Kuhn box, boundary rows -----------------------------------------------
@@ -934,7 +989,7 @@ int fpb_assemble_gradient_kuhn_lines(int nx, int ny, int nz, int kz0, int kz1, c
   const int kchunk = std::max(1, std::min(g_tuning_kgrad_kchunk > 0 ? g_tuning_kgrad_kchunk : kauto, np));
   const int nchunk = (np + kchunk - 1) / kchunk;
   const int64_t nwarps = lines * nchunk;
-  const size_t smem = (size_t)kGradWarps * (kGradStg + 3 * 32 * (kKuhnCols + 1)) * sizeof(double);
+  const size_t smem = (size_t)kGradWarps * (kGradStg + (FPB_KGRAD_TMA == 2 ? 2 : 1) * 3 * kGradOut) * sizeof(double);
   FPB_CUDA(cudaFuncSetAttribute(k_kuhn_grad_march, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_kuhn_grad_march<<<(unsigned)((nwarps + kGradWarps - 1) / kGradWarps), 32 * kGradWarps, smem,
                       as_stream(stream)>>>(nx, ny, nz, kz0, kz1, kchunk, nwarps, xyz4, rowptr, nnz, accumulate, out);
