@@ -65,9 +65,6 @@ __device__ __forceinline__ void yc_release(volatile int* p, int v) {
                ::"r"((unsigned)__cvta_generic_to_shared((const void*)p)), "r"(v) : "memory");
 }
 
-#ifndef FPB_KMOM_MINB
-#define FPB_KMOM_MINB 1  // one 8-warp CTA per SM at ~228 registers: no spills (2 CTAs at 128: spills, 13 % slower)
-#endif
 #ifndef FPB_KMOM_TY
 #define FPB_KMOM_TY 8
 #endif
@@ -259,8 +256,18 @@ __device__ __forceinline__ void kuhn_cell_shared(const double* s0, const double*
   }
 }
 
+// Register cap of the TET04 momentum kind: 184 leaves room next to the 8 momentum
+// warps (47 K registers, 114 KB of shared memory) for two one-warp CTAs of
+// the B_xyz lines kernel, so the two-stream NS step overlaps them from the
+// start (C5 step 2.808 -> 2.786 ms; momentum alone unchanged: 1.56 ms, no
+// spills; 176 measured 1.66 ms).  The other kinds keep 255 (the three-scalar
+// tet kind would spill at 184).  One 8-warp CTA per SM either way (2 CTAs
+// at 128 registers: spills, 13 % slower).
+#ifndef FPB_KMOM_MAXNREG
+#define FPB_KMOM_MAXNREG 184
+#endif
 template <int MAXT, int KIND>
-__global__ void __launch_bounds__(MAXT, FPB_KMOM_MINB)
+__global__ void __maxnreg__(KIND == 0 ? FPB_KMOM_MAXNREG : 255)
 k_kuhn_mom(KuhnGrid g, int kchunk, const double* __restrict__ xyz4, const double* __restrict__ vel,
            const double* __restrict__ phi, int64_t fstride, double rho, double mu, double kappa,
            double* __restrict__ part, double* __restrict__ out) {
