@@ -69,6 +69,8 @@ __device__ __forceinline__ void yc_release(volatile int* p, int v) {
 #define FPB_KMOM_TY 8
 #endif
 constexpr int kKmomTY = FPB_KMOM_TY;            // cell rows (warps) per CTA
+static_assert(kKmomTY >= 1 && 32 * kKmomTY * 255 <= 65536,
+              "the uncapped kinds (up to 255 registers) must fit one CTA of 32 x TY threads per SM");
 constexpr int kKmomRing = 4;                    // y-forward slots per warp
 constexpr int kKmomSlot = 33 * 3;               // one forwarded node row: [33][3]
 constexpr int kKmomHold = 2 * 3 * 33;           // node row j held two layers: [parity][comp][33]
