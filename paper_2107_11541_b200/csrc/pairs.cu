@@ -712,6 +712,11 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
     }
 #pragma unroll
     for (int d = 0; d < DIM; ++d) bo0[d * kGradOut + sh[d] + lane * RE + dslot] = -(mN0 * tot[d]);
+#if FPB_KGRAD_TMA
+    // every writer makes its staging stores visible to the async proxy
+    // before lane 0 hands the block to the TMA unit
+    if (!accumulate) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     __syncwarp();
     // the segment's rows are consecutive (15 entries each): one contiguous CSR range per matrix
     const int span = nlive * RE;
@@ -719,7 +724,6 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
       // one TMA bulk store per matrix for the 16-byte aligned middle of the
       // range; an unaligned first / last double by plain stores (lane 0)
       if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
         for (int d = 0; d < DIM; ++d) {
           double* o = out + d * nnz + base;
