@@ -347,3 +347,40 @@ def test_kuhn_anisotropic_offset_box(cuda_ok):
         e[:, k] = 1.0
         _, _, vo = O.assemble_matrix(om, "convection", e)
         assert O.rel_diff(mats[k * nnz:(k + 1) * nnz].cpu().numpy(), vo) < TOL
+
+
+def test_kuhn_lines_accumulate_and_window(cuda_ok):
+    """fpb_assemble_gradient_kuhn_lines through the C ABI: accumulate = 1
+    (plain read-modify-write stores) adds bitwise the values the default
+    path (TMA bulk stores, accumulate = 0) writes, only in the interior
+    rows of the node-plane window [kz0, kz1]; rows outside stay untouched."""
+    import paper_2107_11541_b200 as P
+    from paper_2107_11541_b200 import _lib
+
+    nx, ny, nz = 37, 21, 9
+    om = O.box(O.TET04, nx, ny, nz)
+    om.coords = _jitter(om.coords, nx, ny, nz, seed=5)
+    mesh, ctx = _ctx(P, nx, ny, nz, coords=om.coords)
+    ctx.assemble_gradients_d(torch.empty(3 * ctx.pattern.nnz, dtype=torch.float64, device="cuda"))  # xyz4 staged
+    nnz = ctx.pattern.nnz
+    rp = ctx.pattern.rowptr_d
+    idx = np.arange(mesh.nnode)
+    i, j, k = idx % (nx + 1), (idx // (nx + 1)) % (ny + 1), idx // ((nx + 1) * (ny + 1))
+    for kz0, kz1 in ((1, nz - 1), (3, 5), (4, 4)):
+        inner = idx[(i > 0) & (i < nx) & (j > 0) & (j < ny) & (k >= kz0) & (k <= kz1)]
+        rpc = rp.cpu().numpy()
+        sel = torch.as_tensor(np.concatenate([np.arange(rpc[r], rpc[r + 1]) for r in inner]), device="cuda")
+        mask = torch.zeros(nnz, dtype=torch.bool, device="cuda")
+        mask[sel] = True
+        g = torch.Generator(device="cuda").manual_seed(kz0)
+        base = torch.randn(3 * nnz, dtype=torch.float64, device="cuda", generator=g)
+        a = base.clone()
+        _lib.call("fpb_assemble_gradient_kuhn_lines", nx, ny, nz, kz0, kz1, ctx.xyz4.data_ptr(), rp.data_ptr(), nnz,
+                  0, a.data_ptr(), _lib.stream())
+        b = base.clone()
+        _lib.call("fpb_assemble_gradient_kuhn_lines", nx, ny, nz, kz0, kz1, ctx.xyz4.data_ptr(), rp.data_ptr(), nnz,
+                  1, b.data_ptr(), _lib.stream())
+        for m in range(3):
+            am, bm, vm = a[m * nnz:(m + 1) * nnz], b[m * nnz:(m + 1) * nnz], base[m * nnz:(m + 1) * nnz]
+            assert torch.equal(am[~mask], vm[~mask]) and torch.equal(bm[~mask], vm[~mask]), (kz0, kz1, m)
+            assert torch.equal(bm[mask], vm[mask] + am[mask]), (kz0, kz1, m)
