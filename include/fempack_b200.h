@@ -54,7 +54,14 @@ const char* fpb_last_error(void);
 int fpb_version(void);
 /* Performance knobs with no effect beyond rounding (for measured design
  * choices, profiles/): "rows_nb" = 0 assembles simplex matrices with the
- * incidence-walking row kernel instead of the neighbour-staged one. */
+ * incidence-walking row kernel instead of the neighbour-staged one;
+ * "blk_pipe" element-block pipelining; "kgrad_march" = 0 runs Kuhn-box B_xyz
+ * interior rows by the row kernel instead of the z-marching lines;
+ * "kgrad_kchunk" planes per z-chunk of the lines (0 = from the grid);
+ * "kgrad_bthreads" threads per CTA of the Kuhn boundary rows (32/64/128);
+ * "kmom_smem_kb" pads the Kuhn momentum CTA's shared memory (co-residency
+ * experiments); "hex_canon_rows" rows per CTA of the hex row pass (32/64).
+ * Python presets any of them from FPB_TUNE_<NAME>=<int> at library load. */
 int fpb_set_tuning(const char* name, int value);
 
 /* Upload one reference element's tables (host pointers) to device constant
