@@ -661,7 +661,8 @@ k_kuhn_grad_march(int nx, int ny, int nz, int kz0, int kz1, int kchunk, int64_t 
     else asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");
 #if FPB_KGRAD_TMA
-    // the previous plane's bulk stores must have read the staging buffer
+    // the bulk stores that last used this plane's staging buffer (two planes
+    // back when double-buffered, the previous plane otherwise) must have read it
     if (lane == 0) {
       if (NBUF == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
