@@ -167,20 +167,39 @@ __host__ __device__ constexpr int hb_canon_slot(int m, int d) {
 // ---- canonical rows: thread per (row, k), R rows per CTA ---------------------
 int g_tuning_hex_canon_rows = 32;  // fpb_set_tuning("hex_canon_rows", 32 | 64)
 
+// FPB_HEXR_TMA: CTAs loop over row blocks (grid = resident CTAs); a block
+// of consecutive rows leaves by one TMA bulk store per matrix
+// (cp.async.bulk.global.shared::cta) from the staging buffer, shifted to the
+// destination's 16-byte phase, instead of ld.shared + st.global per value;
+// the buffer's next writes wait for the bulk read after the next block's
+// H loads and arithmetic.  Measured (profiles/r02y_hextma): 11.9 ms for C4
+// B_xyz against 7.84 with plain stores — the looping CTAs and their block
+// barriers cost this latency-bound kernel far more than the LSU work the
+// bulk stores save; off.
+#ifndef FPB_HEXR_TMA
+#define FPB_HEXR_TMA 0
+#endif
 template <int R, bool ACC, bool BOX>
 __global__ void __launch_bounds__(3 * R, R == 32 ? 2 * FPB_HEXR_MINB : FPB_HEXR_MINB)
 k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t* __restrict__ inc8,
                  const double* __restrict__ H, int64_t nelem, const int32_t* __restrict__ rowptr, int64_t nnz,
                  double* __restrict__ out, int bnx = 0, int bny = 0) {
   constexpr int NT = 3 * R;
-  __shared__ double stage[3][R][27];  // the CTA's output rows, for coalesced stores
+  constexpr bool TMA = FPB_HEXR_TMA && !ACC;
+  constexpr int KS = R * 27 + 2;  // per-matrix stage stride (+2: phase shift room, 16-byte multiple)
+  __shared__ __align__(16) double stage[3 * KS];  // the CTA's output rows, for coalesced / bulk stores
   __shared__ int rlo_s[R];
   const int k = threadIdx.x / R, r = threadIdx.x - k * R;
-  const int32_t i0 = blockIdx.x * R, i = i0 + r;
+  bool pending = false;  // a bulk store still reads the stage (thread 0)
+  for (int32_t i0 = (TMA ? blockIdx.x : blockIdx.x) * R; i0 < nrows; i0 += (TMA ? gridDim.x * R : nrows)) {
+  const int32_t i = i0 + r;
   const int nr = min(R, nrows - i0);
+  const bool cons = __ldg(rows + i0 + nr - 1) - __ldg(rows + i0) == nr - 1;
+  double a27[27];
+  int row = 0;
   if (r < nr) {
     int el[8];
-    const int row = __ldg(rows + i);
+    row = __ldg(rows + i);
     if constexpr (BOX) {  // element ids of the generator's hex box (verified by the caller)
       const int ii = row % (bnx + 1), rj = row / (bnx + 1), jj = rj % (bny + 1), kk = rj / (bny + 1);
       const int e0 = (ii - 1) + bnx * ((jj - 1) + bny * (kk - 1));
@@ -207,8 +226,6 @@ k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t*
 #pragma unroll
       for (int m = 0; m < 8; ++m) el[m] = __ldg(inc8 + (int64_t)m * nrows + i);
     }
-    if (k == 0) rlo_s[r] = __ldg(rowptr + row);
-    double a27[27];
 #pragma unroll
     for (int j = 0; j < 27; ++j) a27[j] = 0.0;
 #pragma unroll
@@ -218,20 +235,53 @@ k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t*
 #pragma unroll
       for (int d = 0; d < 8; ++d) a27[hb_canon_slot(m, d)] += hb_value(V, d);
     }
-#pragma unroll
-    for (int j = 0; j < 27; ++j) stage[k][r][j] = a27[j];
   }
+  if constexpr (TMA) {  // the previous block's stage readers (bulk or plain) are done
+    if (threadIdx.x == 0 && pending) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
+  }
+  const int base0 = __ldg(rowptr + __ldg(rows + i0));
+  int sh = 0;  // this thread's matrix: stage shift matching the destination's 16-byte phase
+  if (TMA && cons) sh = (int)((reinterpret_cast<uintptr_t>(out + k * nnz + base0) >> 3) & 1);
+  if (r < nr) {
+    if (k == 0) rlo_s[r] = __ldg(rowptr + row);
+#pragma unroll
+    for (int j = 0; j < 27; ++j) stage[k * KS + sh + r * 27 + j] = a27[j];
+  }
+  if constexpr (TMA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (__ldg(rows + i0 + nr - 1) - __ldg(rows + i0) == nr - 1) {
+  if (cons) {
     // consecutive rows: each matrix's block is one contiguous CSR range of
-    // 27 nr values (the stage's [r][27] order) — flat, fully coalesced
-    const double* st = &stage[0][0][0];
+    // 27 nr values (the stage's [r][27] order)
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        const int span = 27 * nr;
 #pragma unroll
-    for (int kk = 0; kk < 3; ++kk) {
-      double* o = out + kk * nnz + rlo_s[0];
-      const double* sk = st + kk * R * 27;
-      for (int j = threadIdx.x; j < 27 * nr; j += NT) o[j] = ACC ? o[j] + sk[j] : sk[j];
+        for (int kk = 0; kk < 3; ++kk) {
+          double* o = out + kk * nnz + base0;
+          const int h = (int)((reinterpret_cast<uintptr_t>(o) >> 3) & 1);
+          const double* b = stage + kk * KS + h;
+          const int nb = ((span - h) >> 1) << 1;
+          if (h) o[0] = b[0];
+          if (h + nb < span) o[span - 1] = b[span - 1];
+          if (nb > 0) {
+            const unsigned src = (unsigned)__cvta_generic_to_shared(b + h);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o + h), "r"(src),
+                         "r"(nb * 8)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        pending = true;
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        double* o = out + kk * nnz + base0;
+        const double* sk = stage + kk * KS;
+        for (int j = threadIdx.x; j < 27 * nr; j += NT) o[j] = ACC ? o[j] + sk[j] : sk[j];
+      }
     }
   } else {
     // brick (Morton) order or boundary gaps: one 27-lane store per (row, k)
@@ -241,13 +291,18 @@ k_hex_rows_canon(int32_t nrows, const int32_t* __restrict__ rows, const int32_t*
     for (int kk = 0; kk < 3; ++kk)
       for (int rr = 2 * warp + half; rr < nr; rr += NT / 16) {
         double* o = out + kk * nnz + rlo_s[rr];
-        const double v0 = stage[kk][rr][j];
+        const double v0 = stage[kk * KS + rr * 27 + j];
         o[j] = ACC ? o[j] + v0 : v0;
         if (j < 11) {
-          const double v1 = stage[kk][rr][16 + j];
+          const double v1 = stage[kk * KS + rr * 27 + 16 + j];
           o[16 + j] = ACC ? o[16 + j] + v1 : v1;
         }
       }
+  }
+  if constexpr (!TMA) break;
+  }
+  if constexpr (TMA) {
+    if (threadIdx.x == 0 && pending) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
 
@@ -356,7 +411,9 @@ int fpb_hex_gradient_rows(int32_t ncanon, const int32_t* canon_rows, const int32
   cudaStream_t s = as_stream(stream);
   if (ncanon > 0) {
     const int R = g_tuning_hex_canon_rows == 32 ? 32 : 64;
-    const unsigned grid = (unsigned)((ncanon + R - 1) / R);
+    unsigned grid = (unsigned)((ncanon + R - 1) / R);
+    // TMA variant: CTAs loop over row blocks, one resident wave
+    if (FPB_HEXR_TMA && !accumulate) grid = std::min<unsigned>(grid, kNumSMs * (R == 32 ? 2 * FPB_HEXR_MINB : FPB_HEXR_MINB));
 #define FPB_HC(RR, AA, BB)                                                                                  \
   k_hex_rows_canon<RR, AA, BB><<<grid, 3 * RR, 0, s>>>(ncanon, canon_rows, canon_inc8, H, nelem, rowptr, nnz, out, \
                                                        box_nx, box_ny)
